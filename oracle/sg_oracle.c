@@ -1,0 +1,428 @@
+/*
+ * ORACLE — test infrastructure only.  Plain, slow, obviously-correct CPU evaluation of the Smolyak
+ * combination formula (Eq 2.6 with the tensor rule PAPER.md:69-71 Eq 2.7) on
+ * [0,1]^d in __float128 arithmetic.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code with the CUDA
+ * path (paper_2210_14313_b200/): it builds its own 1-D rule tables and evaluates f directly.
+ *
+ * Arithmetic: every node/weight is the double nearest to the quad value of the paper's formula
+ * (readings R2-R5); sums, products and the integrand are evaluated in __float128 with
+ * libquadmath (expq, cosq).  Multi-indices are visited in lexicographic order of their sparse form
+ * (list of (k, l_k >= 2)), the tensor points of one multi-index by an odometer with the LAST
+ * active coordinate fastest; OpenMP distributes whole top-level items (k1, l1), whose
+ * quad partial sums are then added in item order, so results do not depend on the thread count.
+ *
+ * Pins (tests/test_oracle_pins.py): Tables 5.6-5.8 of the paper; closed forms; weight sum = 1;
+ * polynomial exactness; d = 1 and L = 0 special cases; odd symmetry; brute-force tensor
+ * enumeration at tiny d; the 40-digit generating-function value of Eq 2.6 for product integrands.
+ */
+#include <math.h>
+#include <omp.h>
+#include <quadmath.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+typedef __float128 quad;
+
+enum { SGO_RULE_CC = 2, SGO_RULE_GL = 4 };
+enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_MONOMIAL = 4 };
+#define SGO_MAX_LEVEL 20
+#define SGO_MAX_GL 64
+
+/* ---------------------------------------------------------------------------------------------
+ * 1-D rules on [0,1]
+ * ------------------------------------------------------------------------------------------- */
+
+/* n_l: CC n_1 = 1, n_l = 2^{l-1} + 1 (Eq 2.11); GL n_l = l. */
+int sgo_node_count(int rule, int l) {
+    if (l < 1) return -1;
+    if (rule == SGO_RULE_CC) return l == 1 ? 1 : (1 << (l - 1)) + 1;
+    if (rule == SGO_RULE_GL) return l;
+    return -1;
+}
+
+/* Clenshaw-Curtis (Eq 2.11) mapped from [-1,1] to [0,1] by x' = (x+1)/2,
+ * w' = w/2 (reading R2).  Level 1 is the midpoint with weight 1 (reading R3).
+ *   x_j = -cos(pi (j-1)/(n-1)),   w_1 = w_n = 1/(n(n-2)),
+ *   w_j = 2/(n-1) * (1 + 2 sum'_{k=1}^{(n-1)/2} cos(2 pi (j-1) k/(n-1)) / (1 - 4k^2)),
+ * sum' = last term halved.  Evaluated in quad and rounded once to double. */
+static void cc_rule(int n, double *x, double *w) {
+    if (n == 1) { x[0] = 0.5; w[0] = 1.0; return; }
+    const quad pi = M_PIq;
+    const int m = n - 1;
+    for (int j = 1; j <= n; ++j) {
+        quad xj = -cosq(pi * (quad)(j - 1) / (quad)m);
+        x[j - 1] = (double)((xj + 1) / 2);
+        quad wj;
+        if (j == 1 || j == n) {
+            wj = (quad)1 / ((quad)n * (quad)(n - 2));
+        } else {
+            quad s = 0;
+            for (int k = 1; k <= m / 2; ++k) {
+                quad term = cosq(2 * pi * (quad)(j - 1) * (quad)k / (quad)m) / (quad)(1 - 4 * k * k);
+                if (k == m / 2) term /= 2;
+                s += term;
+            }
+            wj = (quad)2 / (quad)m * (1 + 2 * s);
+        }
+        w[j - 1] = (double)(wj / 2);
+    }
+}
+
+/* Legendre P_n and P_n' at t by the three-term recurrence, in quad. */
+static void legendre(int n, quad t, quad *p, quad *dp) {
+    quad p0 = 1, p1 = t;
+    if (n == 0) { *p = 1; *dp = 0; return; }
+    for (int k = 2; k <= n; ++k) {
+        quad p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k;
+        p0 = p1; p1 = p2;
+    }
+    *p = p1;
+    *dp = n * (t * p1 - p0) / (t * t - 1);
+}
+
+/* Gauss-Legendre (Eq 2.13): zeros of P_n, weights 2/((1-t^2) P_n'(t)^2),
+ * by Newton's method in quad; mapped to [0,1] (reading R2), ascending nodes. */
+static void gl_rule(int n, double *x, double *w) {
+    if (n == 1) { x[0] = 0.5; w[0] = 1.0; return; }
+    for (int i = 1; i <= n; ++i) {
+        quad t = cosq(M_PIq * ((quad)i - 0.25Q) / ((quad)n + 0.5Q));
+        quad p, dp;
+        for (int it = 0; it < 200; ++it) {
+            legendre(n, t, &p, &dp);
+            quad dt = p / dp;
+            t -= dt;
+            if (fabsq(dt) < 1e-33Q) break;
+        }
+        legendre(n, t, &p, &dp);
+        quad wt = 2 / ((1 - t * t) * dp * dp);
+        /* t_i descends with i; store ascending */
+        x[n - i] = (double)((1 + t) / 2);
+        w[n - i] = (double)(wt / 2);
+    }
+}
+
+/* Public: fill nodes/weights of level l, return n_l (or -1). */
+int sgo_rule(int rule, int l, double *x, double *w) {
+    int n = sgo_node_count(rule, l);
+    if (n < 0) return -1;
+    if (rule == SGO_RULE_CC) {
+        if (l > SGO_MAX_LEVEL) return -1;
+        cc_rule(n, x, w);
+    } else {
+        if (n > SGO_MAX_GL) return -1;
+        gl_rule(n, x, w);
+    }
+    return n;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * Integrand (BASELINE.json configs; PAPER.md:619 Test 8 kinds), evaluated at a full point x.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+    int d, kind;
+    const double *c, *w;
+    double u;
+    quad two_pi_u;     /* 2 pi u, quad */
+    quad *cinv2;       /* c_k^-2, quad (peak) */
+    quad s_mid;        /* sum_k c_k / 2 (exp/osc) or sum_k c_k^2 (1/2 - w_k)^2 (gauss) */
+    quad peak_mid;     /* prod_k 1/(c_k^-2 + (1/2 - w_k)^2) */
+} integrand;
+
+/* Plain O(d) evaluation: f(x_1..x_d) exactly as written in BASELINE.json. */
+static quad f_plain(const integrand *F, const double *x) {
+    const int d = F->d;
+    quad s = 0, p = 1;
+    switch (F->kind) {
+    case SGO_EXP:
+        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
+        return expq(s);
+    case SGO_OSC:
+        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
+        return cosq(F->two_pi_u + s);
+    case SGO_PEAK:
+        for (int k = 0; k < d; ++k) {
+            quad t = (quad)x[k] - (quad)F->w[k];
+            p *= 1 / (F->cinv2[k] + t * t);
+        }
+        return p;
+    case SGO_GAUSS:
+        for (int k = 0; k < d; ++k) {
+            quad t = (quad)x[k] - (quad)F->w[k];
+            s += (quad)F->c[k] * (quad)F->c[k] * t * t;
+        }
+        return expq(-s);
+    case SGO_MONOMIAL: /* test-only: prod x_k^{alpha_k}, alpha_k = (int) w[k] */
+        for (int k = 0; k < d; ++k) {
+            int a = (int)F->w[k];
+            for (int e = 0; e < a; ++e) p *= (quad)x[k];
+        }
+        return p;
+    }
+    return nanq("");
+}
+
+/* "Active" evaluation: the same f, using that every inactive coordinate sits at the midpoint 1/2
+ * (level 1, reading R3), so sum_k c_k x_k = sum_k c_k/2 + sum_active c_k (x_k - 1/2) exactly in
+ * real arithmetic (and the analogues for gauss/peak).  O(#active) per point; cross-checked
+ * against f_plain in tests. */
+static quad f_active(const integrand *F, int t, const int *ak, const double *ax) {
+    quad s = 0, p;
+    switch (F->kind) {
+    case SGO_EXP:
+        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
+        return expq(F->s_mid + s);
+    case SGO_OSC:
+        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
+        return cosq(F->two_pi_u + F->s_mid + s);
+    case SGO_GAUSS:
+        for (int m = 0; m < t; ++m) {
+            int k = ak[m];
+            quad c2 = (quad)F->c[k] * (quad)F->c[k];
+            quad a = (quad)ax[m] - (quad)F->w[k], b = 0.5Q - (quad)F->w[k];
+            s += c2 * (a * a - b * b);
+        }
+        return expq(-(F->s_mid + s));
+    case SGO_PEAK:
+        p = F->peak_mid;
+        for (int m = 0; m < t; ++m) {
+            int k = ak[m];
+            quad a = (quad)ax[m] - (quad)F->w[k], b = 0.5Q - (quad)F->w[k];
+            p *= (F->cinv2[k] + b * b) / (F->cinv2[k] + a * a);
+        }
+        return p;
+    }
+    return nanq("");
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * Combination formula, Eq 2.6 with q = d + L:  |l| = d + e, e in [max(0, L-d+1), L],
+ * coefficient (-1)^{q-|l|} C(d-1, q-|l|) = (-1)^{L-e} C(d-1, L-e).
+ * ------------------------------------------------------------------------------------------- */
+static quad binom_q(int n, int k) {
+    if (k < 0 || k > n) return 0;
+    quad r = 1;
+    for (int i = 1; i <= k; ++i) r = r * (quad)(n - k + i) / (quad)i;
+    return rintq(r);
+}
+
+typedef struct {
+    int d, L, rule, eval_mode, emin;
+    const integrand *F;
+    int nl[SGO_MAX_LEVEL + 2];
+    double *X[SGO_MAX_LEVEL + 2], *W[SGO_MAX_LEVEL + 2];
+    quad coef[SGO_MAX_LEVEL + 2];
+    int64_t M0;                      /* number of depth-1 (k1,l1,j1) triples per coordinate */
+    int64_t lo, hi;                  /* shard: depth-1 lexicographic range [lo, hi) */
+} problem;
+
+typedef struct {
+    int t;                           /* number of active coordinates */
+    int ak[SGO_MAX_LEVEL + 2], al[SGO_MAX_LEVEL + 2];
+    double *xfull;                   /* full point for the plain evaluator */
+    quad sum;
+    int64_t npoints;
+} walker;
+
+/* Lexicographic rank of a depth-1 triple (k1, l1, j1): k1 * M0 + sum_{l<l1} n_l + j1. */
+static int64_t depth1_rank(const problem *P, int k1, int l1, int j1) {
+    int64_t r = (int64_t)k1 * P->M0;
+    for (int l = 2; l < l1; ++l) r += P->nl[l];
+    return r + j1;
+}
+
+/* Tensor rule of one multi-index (Eq 2.7): odometer over the nodes of the active coordinates. */
+static void tensor_sum(const problem *P, walker *Wk, int e) {
+    const int t = Wk->t;
+    int j[SGO_MAX_LEVEL + 2];
+    double ax[SGO_MAX_LEVEL + 2];
+    int jlo0 = 0, jhi0 = t > 0 ? P->nl[Wk->al[0]] : 1;
+    if (t > 0) {   /* shard restriction on the first active coordinate's node */
+        int64_t base = depth1_rank(P, Wk->ak[0], Wk->al[0], 0);
+        int64_t a = P->lo - base, b = P->hi - base;
+        if (a > jlo0) jlo0 = (int)(a < jhi0 ? a : jhi0);
+        if (b < jhi0) jhi0 = (int)(b > jlo0 ? b : jlo0);
+        if (jlo0 >= jhi0) return;
+    }
+    for (int m = 0; m < t; ++m) j[m] = 0;
+    if (t > 0) j[0] = jlo0;
+    quad acc = 0;
+    for (;;) {
+        quad wprod = 1;
+        for (int m = 0; m < t; ++m) {
+            wprod *= (quad)P->W[Wk->al[m]][j[m]];
+            ax[m] = P->X[Wk->al[m]][j[m]];
+        }
+        quad fx;
+        if (P->eval_mode == 0) {
+            for (int m = 0; m < t; ++m) Wk->xfull[Wk->ak[m]] = ax[m];
+            fx = f_plain(P->F, Wk->xfull);
+        } else {
+            fx = f_active(P->F, t, Wk->ak, ax);
+        }
+        acc += wprod * fx;
+        Wk->npoints++;
+        /* advance odometer, last active coordinate fastest */
+        int m = t - 1;
+        while (m >= 0) {
+            int lim = (m == 0) ? jhi0 : P->nl[Wk->al[m]];
+            if (++j[m] < lim) break;
+            j[m] = (m == 0) ? jlo0 : 0;
+            --m;
+        }
+        if (m < 0) break;
+    }
+    if (P->eval_mode == 0)
+        for (int m = 0; m < t; ++m) Wk->xfull[Wk->ak[m]] = 0.5;
+    Wk->sum += P->coef[e] * acc;
+}
+
+/* Depth-first walk over sparse multi-indices in lexicographic order. */
+static void walk(const problem *P, walker *Wk, int kstart, int e) {
+    if (e >= P->emin) tensor_sum(P, Wk, e);
+    for (int k = kstart; k < P->d; ++k) {
+        for (int l = 2; l <= P->L + 1 - e; ++l) {
+            Wk->ak[Wk->t] = k; Wk->al[Wk->t] = l; Wk->t++;
+            walk(P, Wk, k + 1, e + l - 1);
+            Wk->t--;
+        }
+    }
+}
+
+/*
+ * sgo_integrate: A(q = d + L, d) f on [0,1]^d, restricted to the points whose first active
+ * coordinate triple (k1, l1, j1) has depth-1 lexicographic rank in [lo, hi), plus the all-midpoint
+ * point when include_root != 0 (lo = 0, hi = -1 means "everything").
+ * eval_mode: 0 = plain O(d) integrand, 1 = active-coordinate identity (see f_active).
+ * Outputs: out_hilo[0] + out_hilo[1] = quad result rounded to a double pair; out_str = "%.36Qe";
+ * out_npoints = tensor points evaluated; out_seconds = wall time of the summation.
+ * Returns 0, or -1 on bad arguments.
+ */
+int sgo_integrate(int d, int L, int rule, int kind, const double *c, const double *w, double u,
+                  long long lo, long long hi, int include_root, int eval_mode, int nthreads,
+                  double *out_hilo, char *out_str, long long *out_npoints, double *out_seconds) {
+    if (d < 1 || L < 0 || L + 1 > SGO_MAX_LEVEL || !c) return -1;
+    if ((kind == SGO_PEAK || kind == SGO_GAUSS || kind == SGO_MONOMIAL) && !w) return -1;
+    if (kind == SGO_MONOMIAL && eval_mode != 0) return -1;
+    problem P;
+    memset(&P, 0, sizeof P);
+    P.d = d; P.L = L; P.rule = rule; P.eval_mode = eval_mode;
+    P.emin = L - d + 1 > 0 ? L - d + 1 : 0;
+    for (int l = 1; l <= L + 1; ++l) {
+        int n = sgo_node_count(rule, l);
+        if (n < 0 || (rule == SGO_RULE_GL && n > SGO_MAX_GL)) return -1;
+        P.nl[l] = n;
+        P.X[l] = (double *)malloc(sizeof(double) * n);
+        P.W[l] = (double *)malloc(sizeof(double) * n);
+        sgo_rule(rule, l, P.X[l], P.W[l]);
+    }
+    for (int e = 0; e <= L; ++e) {
+        quad b = binom_q(d - 1, L - e);
+        P.coef[e] = ((L - e) % 2 ? -b : b);
+    }
+    P.M0 = 0;
+    for (int l = 2; l <= L + 1; ++l) P.M0 += P.nl[l];
+    P.lo = lo; P.hi = hi < 0 ? (int64_t)d * P.M0 + 1 : hi;
+
+    integrand F;
+    memset(&F, 0, sizeof F);
+    F.d = d; F.kind = kind; F.c = c; F.w = w; F.u = u;
+    F.two_pi_u = 2 * M_PIq * (quad)u;
+    F.cinv2 = (quad *)malloc(sizeof(quad) * d);
+    F.s_mid = 0; F.peak_mid = 1;
+    for (int k = 0; k < d; ++k) {
+        F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
+        if (kind == SGO_EXP || kind == SGO_OSC) F.s_mid += (quad)c[k] / 2;
+        if (kind == SGO_GAUSS) {
+            quad b = 0.5Q - (quad)w[k];
+            F.s_mid += (quad)c[k] * (quad)c[k] * b * b;
+        }
+        if (kind == SGO_PEAK) {
+            quad b = 0.5Q - (quad)w[k];
+            F.peak_mid *= 1 / (F.cinv2[k] + b * b);
+        }
+    }
+    P.F = &F;
+
+    /* top-level items: (k1, l1) for k1 in [0,d), l1 in [2, L+1]; item sums added in order */
+    const int nitems = d * L;
+    quad *item_sum = (quad *)calloc(nitems > 0 ? nitems : 1, sizeof(quad));
+    int64_t *item_pts = (int64_t *)calloc(nitems > 0 ? nitems : 1, sizeof(int64_t));
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+
+    quad root_sum = 0;
+    int64_t root_pts = 0;
+    if (include_root && P.emin == 0) {
+        walker Wk;
+        memset(&Wk, 0, sizeof Wk);
+        Wk.xfull = (double *)malloc(sizeof(double) * d);
+        for (int k = 0; k < d; ++k) Wk.xfull[k] = 0.5;
+        tensor_sum(&P, &Wk, 0);
+        root_sum = Wk.sum; root_pts = Wk.npoints;
+        free(Wk.xfull);
+    }
+
+#pragma omp parallel
+    {
+        walker Wk;
+        memset(&Wk, 0, sizeof Wk);
+        Wk.xfull = (double *)malloc(sizeof(double) * d);
+        for (int k = 0; k < d; ++k) Wk.xfull[k] = 0.5;
+#pragma omp for schedule(dynamic, 1)
+        for (int it = 0; it < nitems; ++it) {
+            int k1 = it / L, l1 = 2 + it % L;
+            int64_t r0 = depth1_rank(&P, k1, l1, 0), r1 = r0 + P.nl[l1];
+            if (r1 <= P.lo || r0 >= P.hi) continue;
+            Wk.sum = 0; Wk.npoints = 0; Wk.t = 1;
+            Wk.ak[0] = k1; Wk.al[0] = l1;
+            walk(&P, &Wk, k1 + 1, l1 - 1);
+            item_sum[it] = Wk.sum; item_pts[it] = Wk.npoints;
+        }
+        free(Wk.xfull);
+    }
+    quad total = root_sum;
+    int64_t npts = root_pts;
+    for (int it = 0; it < nitems; ++it) { total += item_sum[it]; npts += item_pts[it]; }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+
+    double hi_d = (double)total;
+    double lo_d = (double)(total - (quad)hi_d);
+    if (out_hilo) { out_hilo[0] = hi_d; out_hilo[1] = lo_d; }
+    if (out_str) quadmath_snprintf(out_str, 64, "%.36Qe", total);
+    if (out_npoints) *out_npoints = npts;
+    if (out_seconds) *out_seconds = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
+    for (int l = 1; l <= L + 1; ++l) { free(P.X[l]); free(P.W[l]); }
+    free(F.cinv2); free(item_sum); free(item_pts);
+    return 0;
+}
+
+/* Single-point evaluation (test hook): f at a full point x, plain and active forms. */
+int sgo_eval_point(int d, int kind, const double *c, const double *w, double u, const double *x,
+                   double *out_plain, double *out_active) {
+    integrand F;
+    memset(&F, 0, sizeof F);
+    F.d = d; F.kind = kind; F.c = c; F.w = w; F.u = u;
+    F.two_pi_u = 2 * M_PIq * (quad)u;
+    F.cinv2 = (quad *)malloc(sizeof(quad) * d);
+    F.peak_mid = 1;
+    int *ak = (int *)malloc(sizeof(int) * d);
+    double *ax = (double *)malloc(sizeof(double) * d);
+    int t = 0;
+    for (int k = 0; k < d; ++k) {
+        F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
+        if (kind == SGO_EXP || kind == SGO_OSC) F.s_mid += (quad)c[k] / 2;
+        if (kind == SGO_GAUSS) { quad b = 0.5Q - (quad)w[k]; F.s_mid += (quad)c[k] * (quad)c[k] * b * b; }
+        if (kind == SGO_PEAK) { quad b = 0.5Q - (quad)w[k]; F.peak_mid *= 1 / (F.cinv2[k] + b * b); }
+        if (x[k] != 0.5) { ak[t] = k; ax[t] = x[k]; ++t; }
+    }
+    quad a = f_plain(&F, x);
+    quad b = kind == SGO_MONOMIAL ? a : f_active(&F, t, ak, ax);
+    out_plain[0] = (double)a; out_plain[1] = (double)(a - (quad)out_plain[0]);
+    out_active[0] = (double)b; out_active[1] = (double)(b - (quad)out_active[0]);
+    free(F.cinv2); free(ak); free(ax);
+    return 0;
+}

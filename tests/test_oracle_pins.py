@@ -1,0 +1,323 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Every test here runs without a GPU.  The oracle (oracle/sg_oracle.c) is checked against:
+paper-printed values (Tables 5.6-5.8), 50-digit generating-function values of Eq 2.6 (tests/pins.py),
+closed-form integrals, weight-sum and polynomial-exactness identities, special cases (d = 1, L = 0,
+odd symmetry) and a brute-force tensor enumeration written independently below.
+"""
+import itertools
+import json
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import pins
+import sg_configs as S
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def qval(res):
+    return mp.mpf(res.text)
+
+
+# ----------------------------------------------------------------------------------------------
+# P4: 1-D rules
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 10)), (S.RULE_GL, range(1, 16))])
+def test_rule_tables_bit_identical_to_mpmath(rule, levels):
+    for l in levels:
+        x, w = oracle.rule(rule, l)
+        px, pw = pins.mp_rule(rule, l)
+        assert tuple(x) == px, (rule, l)
+        assert tuple(w) == pw, (rule, l)
+
+
+def test_rule_examples():
+    # CC n=3 -> weights (1,4,1)/6 on [0,1] (SPEC.md:70 scaled by 1/2; reading R4)
+    x, w = oracle.rule(S.RULE_CC, 2)
+    assert list(x) == [0.0, 0.5, 1.0]
+    np.testing.assert_allclose(w, [1 / 6, 4 / 6, 1 / 6], rtol=0, atol=1e-16)
+    # CC n=5 -> (1,8,12,8,1)/30
+    x, w = oracle.rule(S.RULE_CC, 3)
+    np.testing.assert_allclose(w, np.array([1, 8, 12, 8, 1]) / 30, rtol=0, atol=1e-16)
+    # GL n=2 -> 1/2 -+ 1/(2 sqrt 3), weights 1/2 (SPEC.md:69 mapped)
+    x, w = oracle.rule(S.RULE_GL, 2)
+    np.testing.assert_allclose(x, [0.5 - 0.5 / math.sqrt(3), 0.5 + 0.5 / math.sqrt(3)], atol=1e-16)
+    np.testing.assert_allclose(w, [0.5, 0.5], atol=1e-16)
+    # level 1 = midpoint, weight 1 (reading R3)
+    for r in (S.RULE_CC, S.RULE_GL):
+        assert oracle.rule(r, 1) == (np.array([0.5]), np.array([1.0])) or (
+            list(oracle.rule(r, 1)[0]) == [0.5] and list(oracle.rule(r, 1)[1]) == [1.0])
+
+
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+def test_rule_exactness_and_weight_sum(rule):
+    for l in range(1, 8):
+        x, w = oracle.rule(rule, l)
+        n = len(x)
+        with mp.workdps(40):
+            assert abs(mp.fsum(mp.mpf(a) for a in w) - 1) < 1e-15
+            # GL exact to degree 2n-1; CC (odd n) exact to degree n (pin P4)
+            deg = 2 * n - 1 if rule == S.RULE_GL else (n if n % 2 else n - 1)
+            for k in range(deg + 1):
+                q = mp.fsum(mp.mpf(wj) * mp.mpf(xj) ** k for xj, wj in zip(x, w))
+                assert abs(q - mp.mpf(1) / (k + 1)) < 5e-15, (rule, l, k)
+
+
+def test_cc_nesting_exact():
+    for l in range(2, 9):
+        xa, _ = oracle.rule(S.RULE_CC, l)
+        xb, _ = oracle.rule(S.RULE_CC, l + 1)
+        assert set(xa.tolist()) <= set(xb.tolist())
+        assert list(xb[::2]) == list(xa)
+
+
+# ----------------------------------------------------------------------------------------------
+# P6: the paper's printed Tables 5.6-5.8 (Gauss-Legendre, [-1,1]^d -> [0,1]^d)
+# ----------------------------------------------------------------------------------------------
+_ROWS = json.load(open(os.path.join(GOLDEN, "paper_tables_5_6_to_5_8.json")))["rows"]
+
+
+@pytest.mark.parametrize("row", _ROWS, ids=lambda r: f"T{r['table']}-d{r['d']}-N{r['N']}")
+def test_paper_tables_relative_error(row):
+    p = S.paper_table_problem(row["table"], row["d"], row["N"])
+    res = oracle.integrate_problem(p, eval_mode=1)
+    cf = pins.closed_form(p)
+    err = float(abs((qval(res) - cf) / cf))
+    # printed to 5 significant digits; allow 2.5 units in the 5th digit (truncation vs rounding,
+    # double-rounded parameters).  A dropped term or wrong sign moves these by orders of magnitude.
+    assert err == pytest.approx(row["rel_err"], rel=2.5e-4), (err, row)
+
+
+# ----------------------------------------------------------------------------------------------
+# P1: generating-function value of Eq 2.6 (50 digits) vs the oracle's plain enumeration
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("i", [1, 2])
+def test_dp_pin_baseline_configs(i):
+    p = S.baseline_config(i)
+    res = oracle.integrate_problem(p)
+    v = pins.dp_value(p)
+    assert abs((qval(res) - v) / v) < 1e-30
+    assert res.npoints == pins.n_points(p.rule, p.d, p.L)
+
+
+CASES = [
+    (7, 3, 2, S.RULE_CC, S.KIND_EXP), (8, 5, 3, S.RULE_CC, S.KIND_OSC),
+    (9, 12, 3, S.RULE_GL, S.KIND_PEAK), (10, 20, 2, S.RULE_CC, S.KIND_GAUSS),
+    (11, 3, 6, S.RULE_GL, S.KIND_OSC), (12, 2, 7, S.RULE_CC, S.KIND_PEAK),
+    (13, 40, 2, S.RULE_GL, S.KIND_GAUSS), (14, 6, 4, S.RULE_GL, S.KIND_EXP),
+]
+
+
+@pytest.mark.parametrize("seed,d,L,rule,kind", CASES)
+def test_dp_pin_random(seed, d, L, rule, kind):
+    p = S.random_problem(seed, d, L, rule, kind)
+    v = pins.dp_value(p)
+    for mode in (0, 1):
+        res = oracle.integrate_problem(p, eval_mode=mode)
+        assert abs((qval(res) - v) / v) < 1e-28, (mode, res.text, v)
+    assert res.npoints == pins.n_points(rule, d, L)
+    # Delta form (reading R6 of Eq 2.9) is the same number
+    assert abs((pins.dp_value(p, "delta") - v) / v) < 1e-40
+
+
+def test_golden_full_values_match_dp():
+    """Full-size oracle values (written by oracle/make_golden.py) against the 50-digit DP."""
+    path = os.path.join(GOLDEN, "oracle_full.json")
+    if not os.path.exists(path):
+        pytest.skip("golden full-size oracle values not generated yet")
+    data = json.load(open(path))
+    assert data["values"], "empty golden file"
+    for name, rec in data["values"].items():
+        p = S.baseline_config(int(name[1:]))
+        v = pins.dp_value(p)
+        assert abs((mp.mpf(rec["text"]) - v) / v) < 1e-25, name
+        assert rec["npoints"] == pins.n_points(p.rule, p.d, p.L)
+
+
+# ----------------------------------------------------------------------------------------------
+# P7: closed forms (BASELINE.json); P2 weight sum; P3 exactness; P8 special cases
+# ----------------------------------------------------------------------------------------------
+def test_closed_forms_configs_1_2():
+    p = S.baseline_config(1)
+    r = qval(oracle.integrate_problem(p))
+    cf = pins.closed_form(p)
+    assert abs((r - cf) / cf) < 5e-14          # smooth exp, d=4, L=4: Smolyak error ~1.7e-14
+    p = S.baseline_config(2)
+    r = qval(oracle.integrate_problem(p))
+    cf = pins.closed_form(p)
+    assert abs((r - cf) / cf) < 1e-8           # ~3.2e-9
+
+
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+@pytest.mark.parametrize("d,L", [(1, 5), (2, 4), (5, 3), (30, 2), (4, 7)])
+def test_weight_sum_is_one(rule, d, L):
+    """f = 1 (exp kind with c = 0): sum of all combination weights is 1 on [0,1]^d.
+
+    Exactly 1 for the exact rules: the integer identity sum_e c(e) #multi-indices(e) = 1.  With the
+    double-rounded weights the sum moves by at most sum_e |c(e)| #mi(e) * d * 2^-52; the oracle must
+    reproduce the exact sum of the double weights (generating function, 50 digits)."""
+    assert sum(pins.coef(d, L, e) * math.comb(e + d - 1, d - 1) for e in range(L + 1)) == 1
+    res = oracle.integrate(d, L, rule, S.KIND_EXP, np.zeros(d))
+    exact_double_tables = pins.dp_value(S.Problem("one", d, L, rule, S.KIND_EXP, np.zeros(d)))
+    assert abs(qval(res) - exact_double_tables) < 1e-28
+    bound = sum(abs(pins.coef(d, L, e)) * math.comb(e + d - 1, d - 1) for e in range(L + 1))
+    assert abs(qval(res) - 1) <= bound * d * 2.0 ** -52
+
+
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+def test_polynomial_exactness(rule):
+    """A exact for prod x_k^{a_k} when sum_k floor(a_k/2) <= L."""
+    rng = np.random.default_rng(5)
+    d, L = 4, 3
+    for _ in range(12):
+        a = np.zeros(d, dtype=int)
+        budget = L
+        for k in rng.permutation(d):
+            h = int(rng.integers(0, budget + 1))
+            a[k] = 2 * h + int(rng.integers(0, 2))
+            budget -= h
+        res = oracle.integrate(d, L, rule, 4, np.ones(d), a.astype(float))
+        exact = mp.mpf(1)
+        for ak in a:
+            exact /= (int(ak) + 1)
+        # exact for the exact rules; the double-rounded tables move it by O(1e-16)
+        assert abs(qval(res) - exact) < 1e-14, a
+    # and NOT exact one step beyond (guards against a rule that is secretly too good/bad)
+    # x1^2 x2^2 x3^2 x4^2 needs 4 active coordinates, more than L = 3 allows
+    a = np.array([2, 2, 2, 2])
+    res = oracle.integrate(d, L, rule, 4, np.ones(d), a.astype(float))
+    assert abs(qval(res) - mp.mpf(1) / 81) > 1e-6
+
+
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+def test_d1_is_the_1d_rule(rule):
+    """d = 1: A(q,1) f = J^{q} f (coefficient C(0,0) = 1)."""
+    for L in range(0, 6):
+        c = np.array([0.7])
+        res = oracle.integrate(1, L, rule, S.KIND_EXP, c)
+        x, w = pins.mp_rule(rule, L + 1)
+        with mp.workdps(40):
+            ref = mp.fsum(mp.mpf(wj) * mp.exp(mp.mpf(0.7) * mp.mpf(xj)) for xj, wj in zip(x, w))
+        assert abs(qval(res) - ref) < 1e-30
+
+
+def test_L0_is_midpoint():
+    p = S.random_problem(3, 9, 0, S.RULE_CC, S.KIND_GAUSS)
+    res = oracle.integrate_problem(p)
+    with mp.workdps(40):
+        ref = mp.exp(-mp.fsum(mp.mpf(c) ** 2 * (mp.mpf(0.5) - mp.mpf(w)) ** 2
+                              for c, w in zip(p.c, p.w)))
+    assert abs(qval(res) - ref) < 1e-30
+    assert res.npoints == 1
+
+
+def test_odd_symmetry_gives_zero():
+    """cos(pi/2 + sum c_k (x_k - 1/2)) is odd about the centre; CC nodes are symmetric."""
+    d = 5
+    c = np.array([0.3, 0.9, 0.5, 0.25, 0.75])      # sum c / 2 = 1.35 exactly representable
+    u = (math.pi / 2 - 1.35) / (2 * math.pi)
+    res = oracle.integrate(d, 4, S.RULE_CC, S.KIND_OSC, c, None, u)
+    assert abs(res.hi) < 1e-14
+
+
+# ----------------------------------------------------------------------------------------------
+# P9: brute-force tensor enumeration at tiny d (independent of the oracle's sparse walk)
+# ----------------------------------------------------------------------------------------------
+def _f_mp(kind, c, w, u, x):
+    if kind == S.KIND_EXP:
+        return mp.exp(mp.fsum(mp.mpf(a) * mp.mpf(b) for a, b in zip(c, x)))
+    if kind == S.KIND_OSC:
+        return mp.cos(2 * mp.pi * mp.mpf(u) + mp.fsum(mp.mpf(a) * mp.mpf(b) for a, b in zip(c, x)))
+    if kind == S.KIND_PEAK:
+        r = mp.mpf(1)
+        for a, b, xx in zip(c, w, x):
+            r /= (1 / mp.mpf(a) ** 2 + (mp.mpf(xx) - mp.mpf(b)) ** 2)
+        return r
+    if kind == S.KIND_GAUSS:
+        return mp.exp(-mp.fsum(mp.mpf(a) ** 2 * (mp.mpf(xx) - mp.mpf(b)) ** 2
+                               for a, b, xx in zip(c, w, x)))
+
+
+@pytest.mark.parametrize("seed,d,L,rule,kind", [
+    (21, 2, 3, S.RULE_CC, S.KIND_OSC), (22, 3, 2, S.RULE_GL, S.KIND_PEAK),
+    (23, 2, 4, S.RULE_GL, S.KIND_EXP), (24, 3, 3, S.RULE_CC, S.KIND_GAUSS)])
+def test_brute_force_tensor_enumeration(seed, d, L, rule, kind):
+    p = S.random_problem(seed, d, L, rule, kind)
+    w = p.w if p.w is not None else np.zeros(d)
+    with mp.workdps(40):
+        total = mp.mpf(0)
+        merged = {}
+        for lv in itertools.product(range(1, L + 2), repeat=d):
+            e = sum(lv) - d
+            cf = pins.coef(d, L, e)
+            if cf == 0:
+                continue
+            rules = [pins.mp_rule(rule, l) for l in lv]
+            for js in itertools.product(*[range(len(r[0])) for r in rules]):
+                x = tuple(rules[m][0][js[m]] for m in range(d))
+                wt = mp.mpf(cf)
+                for m in range(d):
+                    wt *= mp.mpf(rules[m][1][js[m]])
+                total += wt * _f_mp(kind, p.c, w, p.u, x)
+                merged[x] = merged.get(x, mp.mpf(0)) + wt
+        # Eq 2.8: the merged single-sum form gives the same value
+        total_merged = mp.fsum(wt * _f_mp(kind, p.c, w, p.u, x) for x, wt in merged.items())
+        assert any(wt < 0 for wt in merged.values()) or L == 0   # negative weights
+    res = oracle.integrate_problem(p)
+    assert abs(qval(res) - total) < 1e-28 * max(1, abs(total))
+    assert abs(total_merged - total) < 1e-28 * max(1, abs(total))
+
+
+def test_multi_index_enumeration_example():
+    """N_{2,4} = {[1,3],[2,2],[3,1]}, and #multi-indices = C(e+d-1, d-1)."""
+    n24 = [lv for lv in itertools.product(range(1, 5), repeat=2) if sum(lv) == 4]
+    assert sorted(n24) == [(1, 3), (2, 2), (3, 1)]
+    for d, e in [(3, 2), (5, 3)]:
+        cnt = sum(1 for lv in itertools.product(range(1, e + 2), repeat=d) if sum(lv) == d + e)
+        assert cnt == math.comb(e + d - 1, d - 1)
+
+
+def test_coefficients_examples():
+    """(d=2,q=4): +1 at |l|=4, -1 at |l|=3; (d=3,q=5): +1,-2,+1."""
+    assert pins.coef(2, 2, 2) == 1 and pins.coef(2, 2, 1) == -1 and pins.coef(2, 2, 0) == 0
+    assert [pins.coef(3, 2, e) for e in (2, 1, 0)] == [1, -2, 1]
+
+
+# ----------------------------------------------------------------------------------------------
+# oracle internals: plain vs active integrand, shard decomposition, thread-count invariance
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", [S.KIND_EXP, S.KIND_OSC, S.KIND_PEAK, S.KIND_GAUSS])
+def test_active_form_matches_plain_form_pointwise(kind):
+    rng = np.random.default_rng(77 + kind)
+    d = 60
+    p = S.random_problem(100 + kind, d, 3, S.RULE_CC, kind)
+    for _ in range(400):
+        x = np.full(d, 0.5)
+        for k in rng.choice(d, size=int(rng.integers(0, 5)), replace=False):
+            x[k] = rng.choice([0.0, 0.14644660940672624, 0.8535533905932737, 1.0, 0.25])
+        a, b = oracle.eval_point(kind, p.c, p.w, p.u, x)
+        assert abs((a[0] - b[0]) + (a[1] - b[1])) <= 1e-28 * abs(a[0]) + 1e-300
+
+
+def test_shards_sum_to_whole_and_threads_invariant():
+    p = S.random_problem(31, 12, 3, S.RULE_CC, S.KIND_OSC)
+    whole = oracle.integrate_problem(p, nthreads=1)
+    whole4 = oracle.integrate_problem(p, nthreads=4)
+    assert whole.text == whole4.text
+    M0 = sum(pins.node_count(p.rule, l) for l in range(2, p.L + 2))
+    total = p.d * M0
+    cuts = [0, 1, 17, 40, total // 2, total - 3, total]
+    acc = mp.mpf(0)
+    npts = 0
+    for i in range(len(cuts) - 1):
+        r = oracle.integrate_problem(p, lo=cuts[i], hi=cuts[i + 1], include_root=(i == 0))
+        acc += qval(r)
+        npts += r.npoints
+    assert npts == whole.npoints
+    assert abs(acc - qval(whole)) < 1e-30
