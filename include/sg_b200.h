@@ -1,0 +1,174 @@
+/*
+ * sg_b200.h — C ABI of the B200 Smolyak sparse-grid quadrature hot path (arXiv 2210.14313, MDI-SG).
+ *
+ * The library evaluates the Smolyak combination sum (Eq 2.6; tensor rule
+ * PAPER.md:69-71, Eq 2.7) on the unit cube [0,1]^d (reading R2 of DESIGN.md):
+ *
+ *   A(q,d) f = sum_{q-d+1 <= |i| <= q} (-1)^{q-|i|} C(d-1, q-|i|) (U^{i_1} x ... x U^{i_d}) f
+ *
+ * with q = d + L, by the paper's multilevel dimension iteration (Eqs 3.8-3.11):
+ * points sharing a prefix of active coordinates share one partial result, carried one active
+ * coordinate at a time through a level-synchronous prefix tree on the GPU.  Every Smolyak point
+ * (the n_d^q of PAPER.md:73-75) is evaluated individually; no point list is ever stored.
+ *
+ * Conventions for every entry point:
+ *  - Return value: SG_OK (0) or a negative sg_status code; no C++ exception crosses the ABI.
+ *  - "host" pointers are ordinary CPU memory; "device" pointers are CUDA global memory of the
+ *    current device.  The library never frees caller memory.
+ *  - Asynchronous entry points only ENQUEUE work on the given stream; the caller synchronises.
+ *  - A plan is immutable after sg_plan (except sg_update_integrand / sg_set_workspace) and may be
+ *    used by one stream at a time.
+ */
+#ifndef SG_B200_H
+#define SG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *sg_stream_t;  /* == cudaStream_t; NULL = legacy default stream */
+
+/* Status codes (error vocabulary after SPEC.md:66, 170, 194, 347). */
+typedef enum {
+    SG_OK = 0,
+    SG_EINVAL = -1,        /* d < 1, q < d (BudgetTooSmall), NULL pointer, bad enum, non-finite
+                              parameter, w missing for peak/gauss, rank/world/range inconsistent */
+    SG_EUNSUPPORTED = -2,  /* UnsupportedLevel: CC max level L+1 > 20, GL n > 64, d > 2^20-1,
+                              L > 19 */
+    SG_EOVERFLOW = -3,     /* a point or frontier count would reach 2^63 */
+    SG_ENOMEM = -4,        /* device allocation failed, or workspace smaller than required */
+    SG_ECUDA = -5,         /* a CUDA runtime call failed (launch error, bad stream, ...) */
+    SG_ENONFINITE = -6,    /* NonFiniteIntegrand: a per-coordinate factor or the result is not
+                              finite; the result is NaN */
+    SG_ENOWORKSPACE = -7   /* sg_integrate called before sg_set_workspace */
+} sg_status;
+
+/* 1-D rule families, numbered by the paper's parameter r. */
+typedef enum {
+    SG_RULE_CLENSHAW_CURTIS = 2,  /* nested, n_1 = 1, n_l = 2^{l-1}+1 (Eq 2.11) */
+    SG_RULE_GAUSS_LEGENDRE = 4    /* n_l = l (Eq 2.13)                         */
+} sg_rule;
+
+/* Integrand kinds (BASELINE.json configs; Genz families).  All are products of per-coordinate
+ * factors (or the real part of one), which the MDI prefix tree carries as partial products. */
+typedef enum {
+    SG_F_EXP_LINEAR = 0,    /* f(x) = exp(sum_k c_k x_k)                                      */
+    SG_F_OSCILLATORY = 1,   /* f(x) = cos(2 pi u + sum_k c_k x_k)                              */
+    SG_F_PRODUCT_PEAK = 2,  /* f(x) = prod_k (c_k^-2 + (x_k - w_k)^2)^-1                        */
+    SG_F_GAUSSIAN = 3       /* f(x) = exp(-sum_k c_k^2 (x_k - w_k)^2)                           */
+} sg_kind;
+
+/* Integrand description.  c: host array of d doubles (required); w: host array of d doubles
+ * (required for PRODUCT_PEAK and GAUSSIAN, ignored otherwise); u: phase (OSCILLATORY only).
+ * Copied by sg_plan / sg_update_integrand; the caller keeps ownership. */
+typedef struct {
+    sg_kind kind;
+    int d;
+    const double *c;
+    const double *w;
+    double u;
+} sg_integrand_desc;
+
+/* Form of the sum.  COMBINATION = literal Eq 2.6 (coefficients (-1)^{L-e} C(d-1, L-e) on the band
+ * e >= L-d+1); DELTA = the coordinate-wise difference form that Eq 2.9 stands for (reading R6):
+ * sum_{e=0}^{L} sum_{|i|=d+e} (Delta^{i_1} x ... x Delta^{i_d}) f, coefficient 1.  Same value. */
+typedef enum { SG_FORM_COMBINATION = 0, SG_FORM_DELTA = 1 } sg_form;
+
+/* Leaf arithmetic.  FACTOR_DD = double-double partial products of plan-time per-(coordinate,node)
+ * factors (parity-grade).  Only FACTOR_DD is implemented in this build; others -> SG_EUNSUPPORTED. */
+typedef enum { SG_ARITH_FACTOR_DD = 0, SG_ARITH_SFORM_FP64 = 1 } sg_arith;
+
+/* Work partition.  The Smolyak points are split into the root (all-midpoint point) and the
+ * subtrees of the depth-1 prefixes (k1, l1, j1) = (first active coordinate, its level >= 2, its node),
+ * ranked lexicographically: r1 = k1 * M0 + sum_{2<=l<l1} n_l + j1, M0 = sum_{l=2}^{L+1} n_l.
+ * If range_hi > range_lo >= 0 this plan evaluates exactly the subtrees r1 in [range_lo, range_hi)
+ * (plus the root iff range_lo == 0).  Otherwise it evaluates shard `rank` of `world` contiguous
+ * ranges balanced by subtree point counts (root on rank 0).  NULL options = whole problem. */
+typedef struct {
+    sg_form form;
+    sg_arith arith;
+    int rank, world;
+    long long range_lo, range_hi;
+} sg_options;
+
+typedef struct sg_plan_s *sg_plan_t;
+
+/* Build a plan: validates arguments, builds the 1-D rule tables (double, correctly rounded from
+ * quad evaluations of Eqs 2.11/2.13 on [0,1]), the counting tables of the prefix tree and the
+ * shard range; allocates plan-owned device tables and copies the integrand parameters (H2D,
+ * synchronous).  q = d + L.  On success *out owns device memory until sg_destroy. */
+int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, const sg_options *opt,
+            sg_plan_t *out);
+
+/* Bytes of caller-provided device workspace (frontier ping-pong buffers + reduction partials). */
+int sg_workspace_size(sg_plan_t p, size_t *bytes);
+
+/* Attach caller-owned device workspace of at least sg_workspace_size bytes (256-byte aligned). */
+int sg_set_workspace(sg_plan_t p, void *dev_ptr, size_t bytes);
+
+/* Replace the integrand parameters (same kind and d) by an async copy from `f` on stream s.
+ * f->c / f->w may be host memory (pinned for true asynchrony) or device memory. */
+int sg_update_integrand(sg_plan_t p, sg_stream_t s, const sg_integrand_desc *f);
+
+/* Enqueue the whole hot path on stream s: factor tables (K0), root pass, level-synchronous
+ * frontier/leaf passes (K2/K3), deterministic reduction (K4).  out_dev (device, 2 doubles) receives
+ * this plan's partial sum as a double-double (hi, lo).  Bitwise reproducible for a fixed plan. */
+int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev);
+
+/* Fixed-order double-double sum of `world` gathered partials (device, 2*world doubles, rank order)
+ * into result_dev (device, 2 doubles: value rounded to double, and the residual).  Writes NaN if
+ * the plan's non-finite flag is set. */
+int sg_finalize(sg_plan_t p, sg_stream_t s, const double *gathered_dev, int world,
+                double *result_dev);
+
+/* Synchronous convenience: H2D of nothing, runs sg_integrate + sg_finalize(world=1) on s,
+ * copies the 2-double result into result_host and synchronises s. Returns SG_ENONFINITE if
+ * the result is not finite. */
+int sg_integrate_host(sg_plan_t p, sg_stream_t s, double *result_host);
+
+/* Synchronously read the device status word (SG_OK or SG_ENONFINITE). */
+int sg_status_word(sg_plan_t p, int *status);
+
+/* Number of Smolyak points n_d^q this plan evaluates (its shard), and of the whole problem. */
+int sg_plan_points(sg_plan_t p, unsigned long long *shard_points,
+                   unsigned long long *total_points);
+
+/* Shard range actually used: [lo, hi) in depth-1 rank space, and M0 * d (= number of depth-1
+ * prefixes). */
+int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long long *n_depth1);
+
+/* Per-pass launch statistics of the last plan: number of passes, and for pass i the number of
+ * tree nodes (leaf terms) it evaluates and the frontier nodes it writes.  Arrays of length >=
+ * *npass (query with NULL arrays first). */
+int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
+                   unsigned long long *written);
+
+/* Debug/test hook: copy the device factor table (per level l = 2..L+1, coordinate k, node j;
+ * doubles per entry: 2 real dd or 4 complex dd) and the base value to host memory. */
+int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host);
+
+/* Host-only (no device touched): the plan's counts and shard range for (d, q, rule, kind, opt).
+ * Any output pointer may be NULL.  Same validation and error codes as sg_plan. */
+int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
+                  unsigned long long *shard_points, unsigned long long *total_points,
+                  long long *range_lo, long long *range_hi, int *n_passes);
+
+/* Host-only: the library's 1-D rule of `level` on [0,1] (n_l doubles each, ascending nodes),
+ * rounded once from __float128 evaluations of Eq 2.11 / Eq 2.13.  Returns n_l, or a negative
+ * status (SG_EINVAL bad rule/level, SG_EUNSUPPORTED above the table limits).  x, w: host arrays of
+ * at least n_l doubles. */
+int sg_rule_table(sg_rule rule, int level, double *x, double *w);
+
+/* Free plan-owned device memory.  The stream the plan was used on must be idle. */
+int sg_destroy(sg_plan_t p);
+
+/* Static string for a status code. */
+const char *sg_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SG_B200_H */

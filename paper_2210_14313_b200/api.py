@@ -1,0 +1,190 @@
+"""Thin Python API over the C ABI (include/sg_b200.h).  Same names as the ABI; PyTorch only provides
+device memory (workspace, outputs), the CUDA stream and torch.distributed process groups.
+
+    plan = sg_plan(d, q, rule, kind, c, w, u)          # -> Plan (owns the C plan + workspace)
+    out = plan.sg_integrate()                           # device tensor [hi, lo], async
+    res = plan.sg_finalize(out)                         # device tensor [value, residual]
+    value = plan.integrate_host()                       # synchronous float
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib, sg_integrand_desc, sg_options
+
+RULE_CC = 2
+RULE_GL = 4
+KIND_EXP, KIND_OSC, KIND_PEAK, KIND_GAUSS = 0, 1, 2, 3
+FORM_COMBINATION, FORM_DELTA = 0, 1
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class PassInfo:
+    terms: int       # tree nodes (Smolyak point terms) evaluated by the pass
+    written: int     # frontier nodes written for the next pass
+
+
+class Plan:
+    """One sg_plan_t plus its torch-allocated workspace."""
+
+    def __init__(self, d: int, q: int, rule: int, kind: int, c, w=None, u: float = 0.0,
+                 form: int = FORM_COMBINATION, rank: int = 0, world: int = 1,
+                 range_lo: int = 0, range_hi: int = -1, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2210_14313_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device if device is not None else "cuda")
+        self.d, self.q, self.rule, self.kind = int(d), int(q), int(rule), int(kind)
+        self._c = np.ascontiguousarray(c, dtype=np.float64)
+        self._w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        self.u = float(u)
+        desc = self._desc(self._c, self._w, self.u)
+        opts = sg_options(int(form), 0, int(rank), int(world), int(range_lo), int(range_hi))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().sg_plan(self.d, self.q, self.rule, ctypes.byref(desc), ctypes.byref(opts),
+                                ctypes.byref(h)), "sg_plan")
+            self._h = h
+            nbytes = ctypes.c_size_t()
+            check(lib().sg_workspace_size(h, ctypes.byref(nbytes)), "sg_workspace_size")
+            self.workspace_bytes = int(nbytes.value)
+            self._ws = torch.empty(max(self.workspace_bytes, 256), dtype=torch.uint8,
+                                   device=self.device)
+            check(lib().sg_set_workspace(h, _dptr(self._ws), self._ws.numel()), "sg_set_workspace")
+            self._out = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self._res = torch.zeros(2, dtype=torch.float64, device=self.device)
+
+    def _desc(self, c, w, u):
+        dp = ctypes.POINTER(ctypes.c_double)
+        return sg_integrand_desc(self.kind, self.d, c.ctypes.data_as(dp),
+                                 None if w is None else w.ctypes.data_as(dp), float(u))
+
+    # -- C ABI wrappers ------------------------------------------------------------------------
+    def sg_integrate(self, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = self._out if out is None else out
+        check(lib().sg_integrate(self._h, _stream_handle(stream), _dptr(out)), "sg_integrate")
+        return out
+
+    def sg_finalize(self, gathered: torch.Tensor, world: int = 1, stream=None,
+                    result: torch.Tensor | None = None) -> torch.Tensor:
+        result = self._res if result is None else result
+        check(lib().sg_finalize(self._h, _stream_handle(stream), _dptr(gathered), int(world),
+                                _dptr(result)), "sg_finalize")
+        return result
+
+    def sg_update_integrand(self, c, w=None, u: float | None = None, stream=None):
+        """Async parameter refresh.  c/w: numpy (host) or torch tensors (pinned host or device)."""
+        dp = ctypes.POINTER(ctypes.c_double)
+
+        def ptr(a):
+            if a is None:
+                return None
+            if isinstance(a, torch.Tensor):
+                return ctypes.cast(ctypes.c_void_p(a.data_ptr()), dp)
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            self._keep = getattr(self, "_keep", []) + [a]
+            return a.ctypes.data_as(dp)
+
+        desc = sg_integrand_desc(self.kind, self.d, ptr(c), ptr(w), float(self.u if u is None else u))
+        check(lib().sg_update_integrand(self._h, _stream_handle(stream), ctypes.byref(desc)),
+              "sg_update_integrand")
+        if u is not None:
+            self.u = float(u)
+
+    def integrate_host(self, stream=None) -> tuple[float, float]:
+        res = (ctypes.c_double * 2)()
+        rc = lib().sg_integrate_host(self._h, _stream_handle(stream), res)
+        check(rc, "sg_integrate_host")
+        return float(res[0]), float(res[1])
+
+    def status_word(self) -> int:
+        v = ctypes.c_int()
+        check(lib().sg_status_word(self._h, ctypes.byref(v)), "sg_status_word")
+        return v.value
+
+    def points(self) -> tuple[int, int]:
+        a, b = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        check(lib().sg_plan_points(self._h, ctypes.byref(a), ctypes.byref(b)), "sg_plan_points")
+        return int(a.value), int(b.value)
+
+    def range(self) -> tuple[int, int, int]:
+        a, b, n = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+        check(lib().sg_plan_range(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)),
+              "sg_plan_range")
+        return int(a.value), int(b.value), int(n.value)
+
+    def passes(self) -> list[PassInfo]:
+        n = ctypes.c_int(0)
+        check(lib().sg_plan_passes(self._h, ctypes.byref(n), None, None), "sg_plan_passes")
+        t = (ctypes.c_ulonglong * n.value)()
+        w = (ctypes.c_ulonglong * n.value)()
+        check(lib().sg_plan_passes(self._h, ctypes.byref(n), t, w), "sg_plan_passes")
+        return [PassInfo(int(t[i]), int(w[i])) for i in range(n.value)]
+
+    def debug_tables(self):
+        ncplx = 4 if self.kind == KIND_OSC else 2
+        lo, hi, nd1 = self.range()
+        buf = np.zeros(nd1 * ncplx)
+        base = np.zeros(4)
+        dp = ctypes.POINTER(ctypes.c_double)
+        check(lib().sg_debug_tables(self._h, buf.ctypes.data_as(dp), buf.size,
+                                    base.ctypes.data_as(dp)), "sg_debug_tables")
+        return buf.reshape(nd1, ncplx), base
+
+    def close(self):
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.device)
+            lib().sg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sg_plan(d, q, rule, kind, c, w=None, u=0.0, **kw) -> Plan:
+    return Plan(d, q, rule, kind, c, w, u, **kw)
+
+
+def integrate(d, L, rule, kind, c, w=None, u=0.0, form=FORM_COMBINATION, **kw) -> tuple[float, float]:
+    """One-shot A(d+L, d) f on the current CUDA device -> (value, residual) double-double."""
+    p = Plan(d, d + L, rule, kind, c, w, u, form=form, **kw)
+    try:
+        return p.integrate_host()
+    finally:
+        p.close()
+
+
+def integrate_distributed(d, L, rule, kind, c, w=None, u=0.0, form=FORM_COMBINATION,
+                          group=None) -> tuple[float, float]:
+    """Shard the depth-1 subtrees over the ranks of ``group`` (one GPU per rank), one
+    all_gather_into_tensor of the 2-double partials (NCCL over NVLink), fixed rank-order dd sum."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    p = Plan(d, d + L, rule, kind, c, w, u, form=form, rank=rank, world=world)
+    try:
+        part = p.sg_integrate()
+        gathered = torch.empty(2 * world, dtype=torch.float64, device=p.device)
+        dist.all_gather_into_tensor(gathered, part, group=group)
+        res = p.sg_finalize(gathered, world)
+        r = res.cpu()
+        return float(r[0]), float(r[1])
+    finally:
+        p.close()

@@ -1,0 +1,164 @@
+// dd.cuh — double-double (FP64-pair) arithmetic for the leaf, frontier and reduction kernels.
+//
+// A dd value is hi + lo with |lo| <= ulp(hi)/2.  Error-free transforms: TwoSum (Knuth) and the
+// FMA product error.  Products drop the lo*lo term (relative error <= ~2^-104).  Used because the
+// combination sum is ill-conditioned (Eq 2.8 negative weights):
+// per-point FP64 cannot meet 1e-12 on configs 4-5, dd partial products can.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+#define DD_HD __host__ __device__ __forceinline__
+
+struct dd {
+    double hi, lo;
+};
+struct cdd {   // complex dd (oscillatory kind): re + i im
+    dd re, im;
+};
+
+DD_HD dd dd_make(double h, double l = 0.0) { return dd{h, l}; }
+
+DD_HD void two_sum(double a, double b, double &s, double &e) {
+    s = a + b;
+    double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+DD_HD void quick_two_sum(double a, double b, double &s, double &e) {
+    s = a + b;
+    e = b - (s - a);
+}
+DD_HD dd dd_norm(double p, double e) {
+    dd r;
+    quick_two_sum(p, e, r.hi, r.lo);
+    return r;
+}
+// accurate dd + dd
+DD_HD dd dd_add(dd a, dd b) {
+    double s, e, t, f;
+    two_sum(a.hi, b.hi, s, e);
+    two_sum(a.lo, b.lo, t, f);
+    e += t;
+    quick_two_sum(s, e, s, e);
+    e += f;
+    dd r;
+    quick_two_sum(s, e, r.hi, r.lo);
+    return r;
+}
+DD_HD dd dd_neg(dd a) { return dd{-a.hi, -a.lo}; }
+DD_HD dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
+// unnormalised product: a*b = p + e (lo*lo dropped)
+DD_HD void dd_mul_pe(dd a, dd b, double &p, double &e) {
+    p = a.hi * b.hi;
+    e = fma(a.hi, b.hi, -p);
+    e = fma(a.hi, b.lo, e);
+    e = fma(a.lo, b.hi, e);
+}
+DD_HD dd dd_mul(dd a, dd b) {
+    double p, e;
+    dd_mul_pe(a, b, p, e);
+    return dd_norm(p, e);
+}
+DD_HD dd dd_mul_d(dd a, double b) {
+    double p = a.hi * b;
+    double e = fma(a.hi, b, -p);
+    e = fma(a.lo, b, e);
+    return dd_norm(p, e);
+}
+DD_HD dd dd_from_prod(double a, double b) {   // exact product of two doubles
+    double p = a * b;
+    return dd{p, fma(a, b, -p)};
+}
+DD_HD dd dd_from_sum(double a, double b) {    // exact sum of two doubles
+    dd r;
+    two_sum(a, b, r.hi, r.lo);
+    return r;
+}
+DD_HD dd dd_div(dd a, dd b) {
+    double q1 = a.hi / b.hi;
+    dd r = dd_sub(a, dd_mul_d(b, q1));
+    double q2 = r.hi / b.hi;
+    r = dd_sub(r, dd_mul_d(b, q2));
+    double q3 = r.hi / b.hi;
+    dd q = dd_norm(q1, q2);
+    return dd_add(q, dd{q3, 0.0});
+}
+DD_HD dd dd_div_d(dd a, double b) { return dd_div(a, dd{b, 0.0}); }
+DD_HD cdd cdd_mul(cdd a, cdd b) {
+    cdd r;
+    r.re = dd_sub(dd_mul(a.re, b.re), dd_mul(a.im, b.im));
+    r.im = dd_add(dd_mul(a.re, b.im), dd_mul(a.im, b.re));
+    return r;
+}
+DD_HD cdd cdd_mul_dd(cdd a, dd b) { return cdd{dd_mul(a.re, b), dd_mul(a.im, b)}; }
+
+// ---------------------------------------------------------------------------------------------
+// Transcendentals in dd (plan-time factor tables, K0).  Accuracy ~1e-31 relative on the ranges used
+// (|x| < 700 for exp; any |x| for sin/cos via reduction with a 3-part 2*pi).
+// ---------------------------------------------------------------------------------------------
+#define DD_LN2_HI 6.931471805599453e-01
+#define DD_LN2_LO 2.3190468138462996e-17
+// 2*pi as three doubles (hi + mid + lo)
+#define DD_2PI_0 6.283185307179586e+00
+#define DD_2PI_1 2.4492935982947064e-16
+#define DD_2PI_2 -5.989539619436679e-33
+#define DD_PI2_HI 1.5707963267948966e+00
+#define DD_PI2_LO 6.123233995736766e-17
+#define DD_PI2_LO2 -1.4973849048591698e-33
+
+DD_HD dd dd_ldexp(dd a, int e) { return dd{ldexp(a.hi, e), ldexp(a.lo, e)}; }
+
+// exp(a): a = m ln2 + r, r /= 2^6, Taylor to r^14 (|r| < 5.5e-3 -> truncation < 1e-45),
+// then 6 squarings in expm1 form t <- 2t + t^2 (error growth x64), result (1 + t) 2^m.
+DD_HD dd dd_exp(dd a) {
+    if (a.hi == 0.0 && a.lo == 0.0) return dd{1.0, 0.0};
+    double m = rint(a.hi / DD_LN2_HI);
+    dd r = dd_sub(a, dd_add(dd_from_prod(m, DD_LN2_HI), dd_from_prod(m, DD_LN2_LO)));
+    r = dd_ldexp(r, -6);
+    // expm1(r) = r + r^2/2! + ... + r^14/14!  (Horner: r(1 + r/2(1 + r/3(...))))
+    dd t = dd{1.0, 0.0};
+    for (int n = 14; n >= 2; --n) t = dd_add(dd{1.0, 0.0}, dd_div_d(dd_mul(r, t), (double)n));
+    t = dd_mul(r, t);
+    for (int i = 0; i < 6; ++i) t = dd_add(dd_ldexp(t, 1), dd_mul(t, t));
+    dd e = dd_add(dd{1.0, 0.0}, t);
+    return dd_ldexp(e, (int)m);
+}
+
+// sin and cos of r with |r| <= pi/4 by Taylor series (terms to r^27: truncation < 1e-34).
+DD_HD void dd_sincos_small(dd r, dd &s, dd &c) {
+    dd r2 = dd_mul(r, r);
+    // sin = r (1 - r2/(2*3) (1 - r2/(4*5) (1 - ...)))
+    dd ts = dd{1.0, 0.0}, tc = dd{1.0, 0.0};
+    for (int n = 13; n >= 1; --n) {
+        ts = dd_sub(dd{1.0, 0.0}, dd_div_d(dd_mul(r2, ts), (double)((2 * n) * (2 * n + 1))));
+        tc = dd_sub(dd{1.0, 0.0}, dd_div_d(dd_mul(r2, tc), (double)((2 * n - 1) * (2 * n))));
+    }
+    s = dd_mul(r, ts);
+    c = tc;
+}
+
+// sin/cos of a dd argument: reduce by 2*pi (3-part), then by pi/2 to |r| <= pi/4.
+DD_HD void dd_sincos(dd a, dd &s, dd &c) {
+    double n2 = rint(a.hi / DD_2PI_0);
+    dd x = a;
+    if (n2 != 0.0) {
+        x = dd_sub(x, dd_from_prod(n2, DD_2PI_0));
+        x = dd_sub(x, dd_from_prod(n2, DD_2PI_1));
+        x = dd_sub(x, dd{n2 * DD_2PI_2, 0.0});
+    }
+    double q = rint(x.hi / DD_PI2_HI);
+    int qi = (int)q;
+    if (q != 0.0) {
+        x = dd_sub(x, dd_from_prod(q, DD_PI2_HI));
+        x = dd_sub(x, dd_from_prod(q, DD_PI2_LO));
+        x = dd_sub(x, dd{q * DD_PI2_LO2, 0.0});
+    }
+    dd ss, cc;
+    dd_sincos_small(x, ss, cc);
+    switch (((qi % 4) + 4) % 4) {
+    case 0: s = ss; c = cc; break;
+    case 1: s = cc; c = dd_neg(ss); break;
+    case 2: s = dd_neg(ss); c = dd_neg(cc); break;
+    default: s = dd_neg(cc); c = ss; break;
+    }
+}

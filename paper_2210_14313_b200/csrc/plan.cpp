@@ -1,0 +1,391 @@
+// plan.cpp — host planning for the B200 Smolyak path (compiled by g++; uses __float128).
+//
+// K0 (rules):  Clenshaw-Curtis (Eq 2.11) and Gauss-Legendre (PAPER.md:133-147,
+//              Eq 2.13) on [0,1] (reading R2), evaluated in __float128 and rounded once to double.
+// K1 (counts): per-depth segment counts of the prefix tree, subtree point counts (PAPER.md:73-75
+//              n_d^q), balanced shard ranges of depth-1 subtrees, launch geometry.
+#include "plan.h"
+
+#include <quadmath.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "../../include/sg_b200.h"
+
+typedef __float128 q128;
+typedef unsigned __int128 u128;
+
+int host_node_count(int rule, int l) {
+    if (l < 1) return -1;
+    if (rule == SG_RULE_CLENSHAW_CURTIS) return l == 1 ? 1 : (1 << (l - 1)) + 1;
+    if (rule == SG_RULE_GAUSS_LEGENDRE) return l;
+    return -1;
+}
+
+// CC on [0,1]: x_j = (1 - cos(pi (j-1)/(n-1)))/2 = sin^2(pi (j-1) / (2(n-1)));
+// w_1 = w_n = 1/(2 n (n-2)); w_j = 1/(n-1) (1 + 2 sum'_{k=1}^{(n-1)/2} cos(2 pi (j-1) k/(n-1))/(1-4k^2)).
+static void cc_rule_q(int n, double *x, double *w) {
+    if (n == 1) {
+        x[0] = 0.5;
+        w[0] = 1.0;
+        return;
+    }
+    const int m = n - 1, half = m / 2;
+    for (int j = 0; j < n; ++j) {
+        q128 s = sinq(M_PIq * (q128)j / (q128)(2 * m));
+        x[j] = (double)(s * s);
+        if (j == 0 || j == m) {
+            w[j] = (double)((q128)1 / ((q128)2 * (q128)n * (q128)(n - 2)));
+            continue;
+        }
+        q128 acc = 0;
+        for (int k = half; k >= 1; --k) {   // summed from the last term (halved) down
+            q128 term = cosq((q128)2 * M_PIq * (q128)j * (q128)k / (q128)m) / (q128)(1 - 4 * k * k);
+            acc += (k == half) ? term / 2 : term;
+        }
+        w[j] = (double)(((q128)1 + 2 * acc) / (q128)m);
+    }
+}
+
+// GL on [0,1]: roots of P_n by Newton from Tricomi's initial guess, weights 2/((1-t^2) P_n'(t)^2),
+// mapped x = (1+t)/2, w/2.
+static void gl_rule_q(int n, double *x, double *w) {
+    if (n == 1) {
+        x[0] = 0.5;
+        w[0] = 1.0;
+        return;
+    }
+    for (int i = 0; i < n; ++i) {
+        // ascending root i: t ~ -cos(pi (4(i+1) - 1)/(4n + 2)) corrected
+        q128 th = M_PIq * (q128)(4 * (i + 1) - 1) / (q128)(4 * n + 2);
+        q128 t = -cosq(th) * (1 - (q128)(n - 1) / ((q128)8 * n * n * n));
+        q128 p1 = 0, p0 = 0, dp = 0;
+        for (int it = 0; it < 100; ++it) {
+            p0 = 1;
+            p1 = t;
+            for (int k = 2; k <= n; ++k) {
+                q128 p2 = ((q128)(2 * k - 1) * t * p1 - (q128)(k - 1) * p0) / (q128)k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = (q128)n * (p0 - t * p1) / (1 - t * t);
+            q128 step = p1 / dp;
+            t -= step;
+            if (fabsq(step) <= 1e-34Q * (1 + fabsq(t))) break;
+        }
+        p0 = 1;
+        p1 = t;
+        for (int k = 2; k <= n; ++k) {
+            q128 p2 = ((q128)(2 * k - 1) * t * p1 - (q128)(k - 1) * p0) / (q128)k;
+            p0 = p1;
+            p1 = p2;
+        }
+        dp = (q128)n * (p0 - t * p1) / (1 - t * t);
+        x[i] = (double)((1 + t) / 2);
+        w[i] = (double)((q128)1 / ((1 - t * t) * dp * dp));
+    }
+}
+
+int host_rule(int rule, int l, double *x, double *w) {
+    int n = host_node_count(rule, l);
+    if (n < 0) return -1;
+    if (rule == SG_RULE_CLENSHAW_CURTIS) {
+        if (l > SG_CC_MAX_LEVEL) return -1;
+        cc_rule_q(n, x, w);
+    } else {
+        if (n > SG_GL_MAX_N) return -1;
+        gl_rule_q(n, x, w);
+    }
+    return n;
+}
+
+static u128 sat_add(u128 a, u128 b) {
+    u128 r = a + b;
+    const u128 cap = (u128)1 << 100;
+    return r > cap ? cap : r;
+}
+static u128 sat_mul(u128 a, u128 b) {
+    const u128 cap = (u128)1 << 100;
+    if (a == 0 || b == 0) return 0;
+    if (a > cap / b) return cap;
+    return a * b;
+}
+
+int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
+                    long long range_lo, long long range_hi) {
+    if (d < 1 || L < 0) return SG_EINVAL;
+    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
+    if (kind < 0 || kind > 3 || form < 0 || form > 1) return SG_EINVAL;
+    if (world < 1 || rank < 0 || rank >= world) return SG_EINVAL;
+    if (d > SG_MAX_D || L > SG_MAX_L) return SG_EUNSUPPORTED;
+    if (rule == SG_RULE_CLENSHAW_CURTIS && L + 1 > SG_CC_MAX_LEVEL) return SG_EUNSUPPORTED;
+    if (rule == SG_RULE_GAUSS_LEGENDRE && L + 1 > SG_GL_MAX_N) return SG_EUNSUPPORTED;
+    hp.d = d;
+    hp.L = L;
+    hp.rule = rule;
+    hp.kind = kind;
+    hp.form = form;
+
+    // ---- rule entries per level (combination: the level-l rule; delta: Delta^l support) ----
+    std::vector<std::vector<double>> RX(L + 2), RW(L + 2);
+    for (int l = 1; l <= L + 1; ++l) {
+        int n = host_node_count(rule, l);
+        RX[l].resize(n);
+        RW[l].resize(n);
+        if (host_rule(rule, l, RX[l].data(), RW[l].data()) < 0) return SG_EUNSUPPORTED;
+    }
+    hp.X.clear();
+    hp.Whi.clear();
+    hp.Wlo.clear();
+    int off = 0;
+    for (int l = 2; l <= L + 1; ++l) {
+        hp.entry_off[l] = off;
+        if (form == SG_FORM_COMBINATION) {
+            for (size_t j = 0; j < RX[l].size(); ++j) {
+                hp.X.push_back(RX[l][j]);
+                hp.Whi.push_back(RW[l][j]);
+                hp.Wlo.push_back(0.0);
+            }
+            hp.nl[l] = (int)RX[l].size();
+        } else {
+            // Delta^l = J^l - J^{l-1} on the union of both node sets; weights as exact dd differences
+            std::vector<std::pair<double, std::pair<double, double>>> ent;
+            std::vector<bool> used(RX[l - 1].size(), false);
+            for (size_t j = 0; j < RX[l].size(); ++j) {
+                double wm = 0.0;
+                for (size_t i = 0; i < RX[l - 1].size(); ++i)
+                    if (RX[l - 1][i] == RX[l][j]) {
+                        wm = RW[l - 1][i];
+                        used[i] = true;
+                    }
+                double s = RW[l][j] - wm, bb = s - RW[l][j];
+                double e = (RW[l][j] - (s - bb)) + (-wm - bb);
+                ent.push_back({RX[l][j], {s, e}});
+            }
+            for (size_t i = 0; i < RX[l - 1].size(); ++i)
+                if (!used[i]) ent.push_back({RX[l - 1][i], {-RW[l - 1][i], 0.0}});
+            std::sort(ent.begin(), ent.end(),
+                      [](const auto &a, const auto &b) { return a.first < b.first; });
+            for (auto &e : ent) {
+                hp.X.push_back(e.first);
+                hp.Whi.push_back(e.second.first);
+                hp.Wlo.push_back(e.second.second);
+            }
+            hp.nl[l] = (int)ent.size();
+        }
+        off += hp.nl[l];
+    }
+    hp.entry_off[L + 2] = off;
+    hp.nl[1] = 1;
+    hp.M0 = 0;
+    for (int l = 2; l <= L + 1; ++l) {
+        hp.tab_off[l] = (int)(d * hp.M0);
+        hp.M0 += hp.nl[l];
+    }
+    if ((int64_t)d * hp.M0 > (int64_t)1 << 30) return SG_EUNSUPPORTED;
+    hp.tab_entries = (int)(d * hp.M0);
+    hp.tab_off[L + 2] = hp.tab_entries;
+
+    // ---- coefficients (Eq 2.6 with q = d + L; delta form: 1) ----
+    for (int e = 0; e <= L; ++e) {
+        if (form == SG_FORM_DELTA) {
+            hp.coef[e] = 1.0;
+            continue;
+        }
+        int m = L - e;
+        if (m > d - 1) {
+            hp.coef[e] = 0.0;
+            continue;
+        }
+        u128 b = 1;
+        for (int i = 1; i <= m; ++i) {
+            b = b * (u128)(d - 1 - m + i) / (u128)i;   // exact: C(n-m+i, i) stays integral
+            if (b > ((u128)1 << 53)) return SG_EUNSUPPORTED;
+        }
+        double v = (double)b;
+        hp.coef[e] = (m % 2) ? -v : v;
+    }
+
+    hp.maxdepth = std::min(L, d);
+    hp.nfront = std::max(0, std::min(L - 1, d - 1));
+    const int64_t nd1 = (int64_t)d * hp.M0;
+
+    // ---- subtree point counts Sub[b][k+1] (points with nonzero coefficient) ----
+    const int W = d + 1;   // k in [-1, d-1] -> index k+1
+    std::vector<u128> Sub((size_t)(L + 1) * W, 0), Suf((size_t)(L + 1) * (W + 1), 0);
+    for (int b = L; b >= 0; --b) {
+        for (int k = d - 1; k >= -1; --k) {
+            u128 s = hp.coef[b] != 0.0 ? 1 : 0;
+            for (int lp = 2; lp <= L + 1 - b; ++lp) {
+                int bp = b + lp - 1;
+                // children at k' > k: Suf[bp][k+1] = sum_{k' >= k+1} Sub[bp][k']
+                s = sat_add(s, sat_mul((u128)hp.nl[lp], Suf[(size_t)bp * (W + 1) + (k + 2)]));
+            }
+            Sub[(size_t)b * W + (k + 1)] = s;
+        }
+        for (int k = d - 1; k >= -1; --k)
+            Suf[(size_t)b * (W + 1) + (k + 1)] =
+                sat_add(Suf[(size_t)b * (W + 1) + (k + 2)], Sub[(size_t)b * W + (k + 1)]);
+    }
+    const u128 total = Sub[0];
+    if (total >= ((u128)1 << 63)) return SG_EOVERFLOW;
+    hp.total_points = (uint64_t)total;
+    const u128 root_w = hp.coef[0] != 0.0 ? 1 : 0;
+    auto item_weight = [&](int k1, int l1) -> u128 { return Sub[(size_t)(l1 - 1) * W + (k1 + 1)]; };
+
+    // ---- shard range in depth-1 rank space ----
+    int64_t lo = 0, hi = nd1;
+    if (range_hi > range_lo && range_lo >= 0) {
+        lo = std::min<int64_t>(range_lo, nd1);
+        hi = std::min<int64_t>(range_hi, nd1);
+    } else if (world > 1) {
+        auto cut = [&](int r) -> int64_t {
+            if (r <= 0) return 0;
+            if (r >= world) return nd1;
+            u128 target = total * (u128)r / (u128)world;   // total < 2^63, r < 2^31
+            u128 cum = root_w;
+            if (cum >= target) return 0;
+            int64_t pos = 0;
+            for (int k1 = 0; k1 < d; ++k1)
+                for (int l1 = 2; l1 <= L + 1; ++l1) {
+                    u128 wgt = item_weight(k1, l1), n = (u128)hp.nl[l1];
+                    if (cum + n * wgt >= target) {
+                        u128 need = target - cum;
+                        return pos + (int64_t)((need + wgt - 1) / wgt);
+                    }
+                    cum += n * wgt;
+                    pos += hp.nl[l1];
+                }
+            return nd1;
+        };
+        lo = cut(rank);
+        hi = cut(rank + 1);
+    }
+    hp.range_lo = lo;
+    hp.range_hi = hi;
+    hp.include_root = (lo == 0);
+    {
+        u128 sp = hp.include_root ? root_w : 0;
+        int64_t pos = 0;
+        for (int k1 = 0; k1 < d; ++k1)
+            for (int l1 = 2; l1 <= L + 1; ++l1) {
+                int64_t a = std::max<int64_t>(lo, pos), b = std::min<int64_t>(hi, pos + hp.nl[l1]);
+                if (b > a) sp += (u128)(b - a) * item_weight(k1, l1);
+                pos += hp.nl[l1];
+            }
+        hp.shard_points = (uint64_t)sp;
+    }
+
+    // ---- frontier counts ----
+    const size_t LD = (size_t)std::max(L, 1) * d;
+    hp.N.assign(hp.nfront + 2, std::vector<int64_t>());
+    hp.C.assign(hp.nfront + 2, std::vector<int64_t>());
+    hp.off.assign(hp.nfront + 2, std::vector<int64_t>());
+    hp.total.assign(hp.nfront + 2, 0);
+    hp.TB.assign(hp.nfront + 2, std::vector<int64_t>());
+    hp.JS.assign(LD, 0);
+    auto finish_depth = [&](int t) -> int {
+        std::vector<int64_t> &N = hp.N[t], &C = hp.C[t], &O = hp.off[t];
+        C.assign(LD, 0);
+        O.assign(LD, 0);
+        u128 run = 0;
+        for (int b = 0; b < L; ++b) {
+            int64_t c = 0;
+            for (int k = 0; k < d; ++k) {
+                C[(size_t)b * d + k] = c;
+                c += N[(size_t)b * d + k];
+                O[(size_t)b * d + k] = (int64_t)run;
+                run += (u128)N[(size_t)b * d + k];
+                if (run >= ((u128)1 << 62)) return SG_EOVERFLOW;
+            }
+        }
+        hp.total[t] = (int64_t)run;
+        return SG_OK;
+    };
+    if (hp.nfront >= 1) {
+        hp.N[1].assign(LD, 0);
+        int64_t pos = 0;
+        for (int k1 = 0; k1 < d; ++k1)
+            for (int l1 = 2; l1 <= L + 1; ++l1) {
+                int b = l1 - 1;
+                int64_t a = std::max<int64_t>(lo, pos), e = std::min<int64_t>(hi, pos + hp.nl[l1]);
+                if (e > a && b <= L - 1 && k1 <= d - 2) {
+                    hp.N[1][(size_t)b * d + k1] = e - a;
+                    hp.JS[(size_t)b * d + k1] = a - pos;
+                }
+                pos += hp.nl[l1];
+            }
+        int rc = finish_depth(1);
+        if (rc) return rc;
+        for (int t = 1; t < hp.nfront; ++t) {
+            std::vector<int64_t> &Nn = hp.N[t + 1];
+            Nn.assign(LD, 0);
+            for (int bp = t + 1; bp <= L - 1; ++bp)
+                for (int kp = 0; kp <= d - 2; ++kp) {
+                    u128 s = 0;
+                    for (int b = 0; b < bp; ++b)
+                        s += (u128)hp.nl[bp - b + 1] * (u128)hp.C[t][(size_t)b * d + kp];
+                    if (s >= ((u128)1 << 62)) return SG_EOVERFLOW;
+                    Nn[(size_t)bp * d + kp] = (int64_t)s;
+                }
+            rc = finish_depth(t + 1);
+            if (rc) return rc;
+            std::vector<int64_t> &T = hp.TB[t];
+            T.assign((size_t)L * L * d, 0);
+            for (int bp = t + 1; bp <= L - 1; ++bp)
+                for (int kp = 0; kp < d; ++kp) {
+                    int64_t acc = hp.off[t + 1][(size_t)bp * d + kp];
+                    for (int b = 0; b < bp; ++b) {
+                        T[((size_t)b * L + bp) * d + kp] = acc;
+                        acc += (int64_t)hp.nl[bp - b + 1] * hp.C[t][(size_t)b * d + kp];
+                    }
+                }
+        }
+    }
+
+    // ---- pass statistics and launch geometry ----
+    const int64_t WARPS_PER_BLOCK = 8, TARGET_WARPS = 148 * 64;
+    hp.pass_terms.assign(hp.nfront + 1, 0);
+    hp.pass_written.assign(hp.nfront + 1, 0);
+    hp.pass_nsplit.assign(hp.nfront + 1, 1);
+    hp.pass_ntasks.assign(hp.nfront + 1, 0);
+    hp.pass_blocks.assign(hp.nfront + 1, 0);
+    hp.pass_partial_off.assign(hp.nfront + 1, 0);
+    hp.pass_terms[0] = (uint64_t)(hi - lo);
+    hp.pass_written[0] = hp.nfront >= 1 ? (uint64_t)hp.total[1] : 0;
+    hp.root_blocks = std::max<int64_t>(1, (hi - lo + 255) / 256);
+    int64_t poff = hp.root_blocks;
+    for (int t = 1; t <= hp.nfront; ++t) {
+        u128 terms = 0;
+        for (int b = 0; b < L; ++b) {
+            int64_t ml = 0;
+            for (int lp = 2; lp <= L + 1 - b; ++lp) ml += hp.nl[lp];
+            for (int k = 0; k < d; ++k)
+                terms += (u128)hp.N[t][(size_t)b * d + k] * (u128)(d - 1 - k) * (u128)ml;
+        }
+        hp.pass_terms[t] = (uint64_t)terms;
+        hp.pass_written[t] = (t + 1 <= hp.nfront) ? (uint64_t)hp.total[t + 1] : 0;
+        int64_t chunks = (hp.total[t] + 31) / 32;
+        int64_t ns = chunks > 0 ? (TARGET_WARPS + chunks - 1) / chunks : 1;
+        ns = std::max<int64_t>(1, std::min<int64_t>(ns, d));
+        hp.pass_nsplit[t] = (int)ns;
+        hp.pass_ntasks[t] = chunks * ns;
+        hp.pass_blocks[t] = std::max<int64_t>(1, (hp.pass_ntasks[t] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+        hp.pass_partial_off[t] = poff;
+        poff += hp.pass_blocks[t];
+    }
+    hp.total_partials = poff;
+    const bool cplx = (kind == SG_F_OSCILLATORY);
+    const size_t per_node = (cplx ? 32 : 16) + 4;
+    for (int par = 0; par < 2; ++par) {
+        int64_t cap = 0;
+        for (int t = 1; t <= hp.nfront; ++t)
+            if (t % 2 == par) cap = std::max(cap, hp.total[t]);
+        cap = (cap + 63) / 64 * 64;
+        hp.ws_front_cap[par] = cap;
+        hp.ws_front_bytes[par] = (size_t)cap * per_node;
+    }
+    return SG_OK;
+}

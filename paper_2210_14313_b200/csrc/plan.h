@@ -1,0 +1,59 @@
+// plan.h — host-side plan of the prefix tree (internal; not part of the C ABI).
+//
+// Tree: a node at depth t is a list of t active coordinates
+// (k_1 < ... < k_t, levels l_m >= 2, node indices j_m); its excess is b = sum (l_m - 1) <= L and it
+// IS the Smolyak point whose other coordinates sit at level 1 (the midpoint).  Children append
+// (k' > k_t, l' in [2, L+1-b], j' in [0, nl[l'])).  Every node is one point of Eq 2.6 with
+// coefficient coef[b]; the root (t = 0) is the all-midpoint point.
+//
+// Frontier t (t >= 1) = the extendable depth-t nodes (b <= L-1, k_t <= d-2), stored in segments
+// (b, k) in b-major, k-minor order; inside segment (b', k') the children of source segment (b, k)
+// sit at  TB[b][b'][k'] + nl[l'] * C_t(b,k) + j' * N_t(b,k) + i   (i = index inside (b, k)).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#define SG_MAX_L 19        // L + 1 <= 20 levels in the tables
+#define SG_CC_MAX_LEVEL 12 // CC weights are O(n^2) quad evaluations; n_12 = 2049
+#define SG_GL_MAX_N 64
+#define SG_MAX_D ((1 << 20) - 1)
+#define SG_META_KBITS 20
+
+struct HostPlan {
+    int d = 0, L = 0, rule = 0, kind = 0, form = 0;
+    int nl[SG_MAX_L + 3] = {0};        // table entries per level (form-dependent)
+    // rule entries per level l >= 2, concatenated: node x and weight (dd: hi, lo)
+    std::vector<double> X, Whi, Wlo;
+    int entry_off[SG_MAX_L + 3] = {0}; // offset of level l in X/W (level 2 at 0)
+    int tab_off[SG_MAX_L + 3] = {0};   // offset (entries) of level l in the factor table: d*sum_{2<=m<l} nl[m]
+    int tab_entries = 0;               // d * M0
+    double coef[SG_MAX_L + 2] = {0};   // coefficient per excess e (combination / delta)
+    int64_t M0 = 0;                    // sum_{l=2}^{L+1} nl[l]
+    int64_t range_lo = 0, range_hi = 0;
+    bool include_root = true;
+    int maxdepth = 0;                  // min(L, d)
+    int nfront = 0;                    // deepest frontier depth = min(L-1, d-1) (>= 0)
+    // frontier tables, index t = 1..nfront, each [L * d] (b * d + k)
+    std::vector<std::vector<int64_t>> N, C, off;
+    std::vector<int64_t> total;        // frontier sizes, index t
+    std::vector<int64_t> JS;           // depth-1: first j1 of segment (b, k) in the range, [L * d]
+    // pass t = 1..nfront-1 (writes frontier t+1): TB [L * L * d]  ((b * L + b') * d + k')
+    std::vector<std::vector<int64_t>> TB;
+    // pass statistics: index 0 = root pass, t = pass from frontier t
+    std::vector<uint64_t> pass_terms, pass_written;
+    uint64_t shard_points = 0, total_points = 0;
+    // launch geometry
+    std::vector<int> pass_nsplit;      // index t
+    std::vector<int64_t> pass_ntasks, pass_blocks, pass_partial_off;
+    int64_t root_blocks = 0, total_partials = 0;
+    size_t ws_front_bytes[2] = {0, 0}; // ping-pong frontier buffers (odd / even depth)
+    int64_t ws_front_cap[2] = {0, 0};
+};
+
+// Build rules, counts, shard range and launch geometry. Returns an sg_status code.
+int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
+                    long long range_lo, long long range_hi);
+
+// 1-D rule (level l) on [0,1] as doubles rounded from quad; returns n or -1.
+int host_rule(int rule, int l, double *x, double *w);
+int host_node_count(int rule, int l);

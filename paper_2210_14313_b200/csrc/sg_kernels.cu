@@ -1,0 +1,780 @@
+// sg_kernels.cu — sm_100a kernels and the C ABI of the B200 Smolyak hot path.
+//
+//  K0  k_factor / k_base : per-(coordinate, level, node) factor table F = w * E_k(x) and the base B
+//                          in double-double, on the device.  The integrand
+//                          f(x) = Re(B * prod_{active k} E_k(x_k)) for all four kinds.
+//  K2+K3 k_root / k_pass : level-synchronous prefix-tree passes (Eqs 3.8-3.11:
+//                          the "multilevel dimension iteration").  Pass t reads frontier t (the
+//                          extendable depth-t prefixes, each carrying its dd partial product
+//                          P = B * prod w E), evaluates every depth-(t+1) Smolyak point
+//                          term = coef[e] * Re(P * F[k'][l'][j']) and writes the extendable
+//                          children into frontier t+1.
+//  K4  block/grid reduce : fixed-order dd warp-shuffle butterfly -> CTA -> per-CTA partials ->
+//                          single-CTA fixed-order pass (deterministic, bitwise reproducible).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <climits>
+#include <new>
+#include <vector>
+
+#include "../../include/sg_b200.h"
+#include "dd.cuh"
+#include "plan.h"
+
+#define WPB 8                 // warps per CTA in the pass kernels
+#define PASS_THREADS (WPB * 32)
+#define META_KMASK ((1u << SG_META_KBITS) - 1u)
+
+struct DevPlan {
+    int d, L, kind, nfront;
+    int nl[SG_MAX_L + 3];
+    int entry_off[SG_MAX_L + 3];
+    int tab_off[SG_MAX_L + 3];
+    double coef[SG_MAX_L + 2];
+    long long M0;
+    const double *X, *Whi, *Wlo;
+    const double *c, *w, *u;
+    double2 *Fre, *Fim;
+    double *base;   // re.hi, re.lo, im.hi, im.lo
+    int *status;
+};
+
+struct PassArgs {
+    long long nsrc, ntasks;
+    int nsplit;
+    const double2 *src_re, *src_im;
+    const uint32_t *src_meta;
+    double2 *dst_re, *dst_im;
+    uint32_t *dst_meta;
+    const long long *offT, *NT, *CT, *TB;
+    double2 *partials;
+};
+
+struct RootArgs {
+    long long lo, hi;
+    const long long *off1, *JS;
+    double2 *dst_re, *dst_im;
+    uint32_t *dst_meta;
+    double2 *partials;
+};
+
+// ---------------------------------------------------------------------------------------------
+// reductions (K4)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ dd warp_reduce_dd(dd v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dd w;
+        w.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+        w.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+        v = dd_add(v, w);
+    }
+    return v;
+}
+
+// CTA sum in fixed order; result valid in thread 0.
+template <int NWARPS>
+__device__ __forceinline__ dd block_reduce_dd(dd v) {
+    __shared__ double2 sm[NWARPS];
+    v = warp_reduce_dd(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sm[wid] = make_double2(v.hi, v.lo);
+    __syncthreads();
+    dd s = {0.0, 0.0};
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NWARPS; ++i) s = dd_add(s, dd{sm[i].x, sm[i].y});
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K0: factor table and base
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool dd_finite(dd a) { return isfinite(a.hi) && isfinite(a.lo); }
+
+__global__ void k_factor(const DevPlan P) {
+    const int n_ent = P.tab_off[P.L + 2];
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_ent) return;
+    int l = 2;
+    while (l < P.L + 1 && idx >= P.tab_off[l + 1]) ++l;
+    const int r = idx - P.tab_off[l], n = P.nl[l];
+    const int k = r / n, j = r - k * n;
+    const double x = P.X[P.entry_off[l] + j];
+    const dd wt = {P.Whi[P.entry_off[l] + j], P.Wlo[P.entry_off[l] + j]};
+    const double ck = P.c[k];
+    const dd xm = dd_from_sum(x, -0.5);   // x - 1/2 exactly
+    dd Er = {1.0, 0.0}, Ei = {0.0, 0.0};
+    switch (P.kind) {
+    case SG_F_EXP_LINEAR:
+        Er = dd_exp(dd_mul_d(xm, ck));
+        break;
+    case SG_F_OSCILLATORY: {
+        dd s, co;
+        dd_sincos(dd_mul_d(xm, ck), s, co);
+        Er = co;
+        Ei = s;
+        break;
+    }
+    case SG_F_GAUSSIAN: {
+        // -c^2 ((x-w)^2 - (1/2-w)^2) = -c^2 (x - 1/2)(x + 1/2 - 2w)
+        const double wk = P.w[k];
+        dd xp = dd_add(dd_from_sum(x, 0.5), dd{-2.0 * wk, 0.0});
+        dd arg = dd_mul(dd_mul(xm, xp), dd_from_prod(ck, ck));
+        Er = dd_exp(dd_neg(arg));
+        break;
+    }
+    case SG_F_PRODUCT_PEAK: {
+        // phi(x)/phi(1/2) = (c^-2 + (1/2-w)^2) / (c^-2 + (x-w)^2)
+        const double wk = P.w[k];
+        dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+        dd a = dd_from_sum(x, -wk), bm = dd_from_sum(0.5, -wk);
+        Er = dd_div(dd_add(ci2, dd_mul(bm, bm)), dd_add(ci2, dd_mul(a, a)));
+        break;
+    }
+    }
+    dd Fr = dd_mul(wt, Er);
+    P.Fre[idx] = make_double2(Fr.hi, Fr.lo);
+    bool ok = dd_finite(Fr);
+    if (P.kind == SG_F_OSCILLATORY) {
+        dd Fi = dd_mul(wt, Ei);
+        P.Fim[idx] = make_double2(Fi.hi, Fi.lo);
+        ok = ok && dd_finite(Fi);
+    }
+    if (!ok) atomicOr(P.status, 1);
+}
+
+__global__ void __launch_bounds__(256) k_base(const DevPlan P) {
+    // fixed-order strided partials, then a fixed CTA tree (sum; product for the peak kind)
+    const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
+    dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
+    for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
+        const double ck = P.c[k];
+        switch (P.kind) {
+        case SG_F_EXP_LINEAR:
+        case SG_F_OSCILLATORY:
+            acc = dd_add(acc, dd{0.5 * ck, 0.0});
+            break;
+        case SG_F_GAUSSIAN: {
+            dd bm = dd_from_sum(0.5, -P.w[k]);
+            acc = dd_add(acc, dd_mul(dd_mul(bm, bm), dd_from_prod(ck, ck)));
+            break;
+        }
+        case SG_F_PRODUCT_PEAK: {
+            dd bm = dd_from_sum(0.5, -P.w[k]);
+            dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+            acc = dd_mul(acc, dd_div(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
+            break;
+        }
+        }
+    }
+    __shared__ double2 sm[256];
+    sm[threadIdx.x] = make_double2(acc.hi, acc.lo);
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            dd a = {sm[threadIdx.x].x, sm[threadIdx.x].y}, b = {sm[threadIdx.x + s].x, sm[threadIdx.x + s].y};
+            dd r = prod ? dd_mul(a, b) : dd_add(a, b);
+            sm[threadIdx.x] = make_double2(r.hi, r.lo);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        dd s = {sm[0].x, sm[0].y};
+        dd Br = s, Bi = {0.0, 0.0};
+        switch (P.kind) {
+        case SG_F_EXP_LINEAR: Br = dd_exp(s); break;
+        case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(s)); break;
+        case SG_F_PRODUCT_PEAK: Br = s; break;
+        case SG_F_OSCILLATORY: {
+            const double u = P.u[0];
+            dd th = dd_add(dd_from_prod(DD_2PI_0, u), dd_from_prod(DD_2PI_1, u));
+            th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
+            th = dd_add(th, s);
+            dd sn, cs;
+            dd_sincos(th, sn, cs);
+            Br = cs;
+            Bi = sn;
+            break;
+        }
+        }
+        P.base[0] = Br.hi;
+        P.base[1] = Br.lo;
+        P.base[2] = Bi.hi;
+        P.base[3] = Bi.lo;
+        if (!dd_finite(Br) || !dd_finite(Bi)) atomicOr(P.status, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// leaf arithmetic helpers
+// ---------------------------------------------------------------------------------------------
+// acc (hi, lo) += p + e  : TwoSum on the high parts, plain sum of the low parts.
+__device__ __forceinline__ void acc_add(double &ah, double &al, double p, double e) {
+    double s = ah + p;
+    double bb = s - ah;
+    double err = (ah - (s - bb)) + (p - bb);
+    al += err + e;
+    ah = s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Root pass: every depth-1 point (k1, l1, j1) of this shard, one thread each.
+// ---------------------------------------------------------------------------------------------
+template <bool CPLX>
+__global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R) {
+    const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    dd tot = {0.0, 0.0};
+    if (r1 < R.hi) {
+        const int k1 = (int)(r1 / P.M0);
+        int rem = (int)(r1 - (long long)k1 * P.M0);
+        int l1 = 2;
+        while (rem >= P.nl[l1]) {
+            rem -= P.nl[l1];
+            ++l1;
+        }
+        const int j1 = rem;
+        const int ti = P.tab_off[l1] + k1 * P.nl[l1] + j1;
+        const dd Br = {P.base[0], P.base[1]};
+        const double2 fr = P.Fre[ti];
+        dd cr, ci = {0.0, 0.0};
+        if (CPLX) {
+            const dd Bi = {P.base[2], P.base[3]};
+            const double2 fi = P.Fim[ti];
+            cdd ch = cdd_mul(cdd{Br, Bi}, cdd{dd{fr.x, fr.y}, dd{fi.x, fi.y}});
+            cr = ch.re;
+            ci = ch.im;
+        } else {
+            cr = dd_mul(Br, dd{fr.x, fr.y});
+        }
+        const int b1 = l1 - 1;
+        tot = dd_mul_d(cr, P.coef[b1]);
+        if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
+            const long long seg = (long long)b1 * P.d + k1;
+            const long long o = R.off1[seg] + j1 - R.JS[seg];
+            R.dst_re[o] = make_double2(cr.hi, cr.lo);
+            if (CPLX) R.dst_im[o] = make_double2(ci.hi, ci.lo);
+            R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+        }
+    }
+    dd s = block_reduce_dd<8>(tot);
+    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Pass t >= 1 (K3 leaf + K2 frontier): warp task = (32 consecutive frontier-t nodes, a k' range).
+// Lane = one parent prefix, held in registers; the loop over its children (k', l', j') reads the
+// factor table at warp-uniform addresses (one broadcast transaction per load).
+// ---------------------------------------------------------------------------------------------
+template <bool CPLX, bool WRITE>
+__global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const PassArgs A) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long task = (long long)blockIdx.x * WPB + wib;
+    dd tot = {0.0, 0.0};
+    if (task < A.ntasks) {
+        const int d = P.d, L = P.L;
+        const long long chunk = task / A.nsplit;
+        const int split = (int)(task - chunk * A.nsplit);
+        const long long g = chunk * 32 + lane;
+        const bool valid = g < A.nsrc;
+        int b = L, k = d;
+        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
+        if (valid) {
+            const uint32_t m = A.src_meta[g];
+            b = (int)(m >> SG_META_KBITS);
+            k = (int)(m & META_KMASK);
+            const double2 v = A.src_re[g];
+            pr = dd{v.x, v.y};
+            if (CPLX) {
+                const double2 vi = A.src_im[g];
+                pim = dd{vi.x, vi.y};
+            }
+        }
+        const int ks0 = (int)((long long)split * d / A.nsplit);
+        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
+        const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
+        const int bmin = __reduce_min_sync(0xffffffffu, b);
+        long long iseg = 0, Nseg = 0, Cseg = 0;
+        if (WRITE && valid) {
+            const long long s = (long long)b * d + k;
+            iseg = g - A.offT[s];
+            Nseg = A.NT[s];
+            Cseg = A.CT[s];
+        }
+        const int kb = max(ks0, kmin + 1);
+        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
+            const bool lv = valid && (lp <= L + 1 - b);
+            const int n = P.nl[lp];
+            const int bp = b + lp - 1;
+            const double2 *Fr = P.Fre + P.tab_off[lp];
+            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            const bool wr = WRITE && lv && (bp <= L - 1);
+            const long long wbase = (long long)n * Cseg + iseg;
+            double ah = 0.0, al = 0.0;
+            for (int kp = kb; kp < ks1; ++kp) {
+                const bool kv = lv && (kp > k);
+                const dd er = kv ? pr : dd{0.0, 0.0};
+                const dd ei = kv ? pim : dd{0.0, 0.0};
+                const bool wk = wr && kv && (kp <= d - 2);
+                long long tb = 0;
+                if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
+                const double2 *fr_row = Fr + kp * n;
+                const double2 *fi_row = CPLX ? Fi + kp * n : nullptr;
+                for (int j = 0; j < n; ++j) {
+                    const double2 f = __ldg(fr_row + j);
+                    if (!CPLX) {
+                        double p, e;
+                        dd_mul_pe(er, dd{f.x, f.y}, p, e);
+                        acc_add(ah, al, p, e);
+                        if (WRITE && wk) {
+                            const long long o = tb + (long long)j * Nseg;
+                            dd ch = dd_norm(p, e);
+                            A.dst_re[o] = make_double2(ch.hi, ch.lo);
+                            A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                        }
+                    } else {
+                        const double2 fi = __ldg(fi_row + j);
+                        double p1, e1, p2, e2;
+                        dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
+                        dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
+                        acc_add(ah, al, p1, e1);
+                        acc_add(ah, al, -p2, -e2);
+                        if (WRITE && wk) {
+                            const long long o = tb + (long long)j * Nseg;
+                            cdd ch = cdd_mul(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{fi.x, fi.y}});
+                            A.dst_re[o] = make_double2(ch.re.hi, ch.re.lo);
+                            A.dst_im[o] = make_double2(ch.im.hi, ch.im.lo);
+                            A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                        }
+                    }
+                }
+            }
+            if (lv) tot = dd_add(tot, dd_mul_d(dd_norm(ah, al), P.coef[bp]));
+        }
+    }
+    dd s = block_reduce_dd<WPB>(tot);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
+// Final fixed-order reduction of all CTA partials (+ the root point) -> out[0..1].
+__global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 *partials,
+                                                 long long n, int include_root, double *out) {
+    dd s = {0.0, 0.0};
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
+    s = block_reduce_dd<32>(s);
+    if (threadIdx.x == 0) {
+        if (include_root && P.coef[0] != 0.0) s = dd_add(s, dd_mul_d(dd{P.base[0], P.base[1]}, P.coef[0]));
+        if (*P.status) s = dd{nan(""), nan("")};
+        out[0] = s.hi;
+        out[1] = s.lo;
+    }
+}
+
+__global__ void k_finalize(const double *gathered, int world, const int *status, double *result) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    dd s = {0.0, 0.0};
+    for (int r = 0; r < world; ++r) s = dd_add(s, dd{gathered[2 * r], gathered[2 * r + 1]});
+    if (*status || !isfinite(s.hi)) s = dd{nan(""), nan("")};
+    result[0] = s.hi;
+    result[1] = s.lo;
+}
+
+// ---------------------------------------------------------------------------------------------
+// plan object and C ABI
+// ---------------------------------------------------------------------------------------------
+struct sg_plan_s {
+    HostPlan hp;
+    DevPlan dp;
+    bool cplx = false;
+    // plan-owned device memory
+    void *dev_block = nullptr;
+    size_t dev_bytes = 0;
+    long long *d_tabs = nullptr;
+    std::vector<size_t> tab_offT, tab_NT, tab_CT, tab_TB;   // element offsets into d_tabs per depth
+    size_t tab_JS = 0, tab_off1 = 0;
+    double *d_scratch = nullptr;   // 4 doubles
+    // workspace
+    char *ws = nullptr;
+    size_t ws_bytes = 0;
+    size_t ws_front_off[2] = {0, 0}, ws_part_off = 0, ws_need = 0;
+};
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static bool finite_array(const double *a, int n) {
+    for (int i = 0; i < n; ++i)
+        if (!isfinite(a[i])) return false;
+    return true;
+}
+
+static int validate_desc(const sg_integrand_desc *f, int d) {
+    if (!f || !f->c) return SG_EINVAL;
+    if (f->d != d) return SG_EINVAL;
+    if ((int)f->kind < 0 || (int)f->kind > 3) return SG_EINVAL;
+    if ((f->kind == SG_F_PRODUCT_PEAK || f->kind == SG_F_GAUSSIAN) && !f->w) return SG_EINVAL;
+    return SG_OK;
+}
+
+extern "C" const char *sg_strerror(int code) {
+    switch (code) {
+    case SG_OK: return "ok";
+    case SG_EINVAL: return "invalid argument (bad pointer/enum/size, q < d, non-finite parameter)";
+    case SG_EUNSUPPORTED: return "unsupported level or size";
+    case SG_EOVERFLOW: return "point or frontier count overflows 63 bits";
+    case SG_ENOMEM: return "out of device memory or workspace too small";
+    case SG_ECUDA: return "CUDA runtime error";
+    case SG_ENONFINITE: return "non-finite integrand value";
+    case SG_ENOWORKSPACE: return "no workspace attached";
+    }
+    return "unknown status";
+}
+
+extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, const sg_options *opt,
+                       sg_plan_t *out) {
+    if (!out) return SG_EINVAL;
+    *out = nullptr;
+    if (d < 1 || q < d) return SG_EINVAL;
+    int rc = validate_desc(f, d);
+    if (rc) return rc;
+    if (!finite_array(f->c, d)) return SG_EINVAL;
+    if (f->w && (f->kind == SG_F_PRODUCT_PEAK || f->kind == SG_F_GAUSSIAN) && !finite_array(f->w, d))
+        return SG_EINVAL;
+    if (!isfinite(f->u)) return SG_EINVAL;
+    if (f->kind == SG_F_PRODUCT_PEAK)
+        for (int k = 0; k < d; ++k)
+            if (f->c[k] == 0.0) return SG_EINVAL;
+    sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
+    if (opt) o = *opt;
+    if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
+    sg_plan_s *p = new (std::nothrow) sg_plan_s();
+    if (!p) return SG_ENOMEM;
+    rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
+                         o.range_lo, o.range_hi);
+    if (rc) {
+        delete p;
+        return rc;
+    }
+    HostPlan &hp = p->hp;
+    p->cplx = (f->kind == SG_F_OSCILLATORY);
+    // ---- device tables: one allocation ----
+    const int L = hp.L, nent = (int)hp.X.size();
+    std::vector<long long> tabs;
+    p->tab_offT.assign(hp.nfront + 2, 0);
+    p->tab_NT.assign(hp.nfront + 2, 0);
+    p->tab_CT.assign(hp.nfront + 2, 0);
+    p->tab_TB.assign(hp.nfront + 2, 0);
+    auto push = [&](const std::vector<int64_t> &v) {
+        size_t o = tabs.size();
+        tabs.insert(tabs.end(), v.begin(), v.end());
+        return o;
+    };
+    for (int t = 1; t <= hp.nfront; ++t) {
+        p->tab_offT[t] = push(hp.off[t]);
+        p->tab_NT[t] = push(hp.N[t]);
+        p->tab_CT[t] = push(hp.C[t]);
+        if (t < hp.nfront) p->tab_TB[t] = push(hp.TB[t]);
+    }
+    p->tab_JS = push(hp.JS);
+    p->tab_off1 = hp.nfront >= 1 ? p->tab_offT[1] : 0;
+    if (tabs.empty()) tabs.push_back(0);
+    size_t sz = 0;
+    auto carve = [&](size_t bytes) {
+        size_t o = sz;
+        sz = align_up(sz + bytes, 256);
+        return o;
+    };
+    const size_t oX = carve(sizeof(double) * std::max(nent, 1));
+    const size_t oWh = carve(sizeof(double) * std::max(nent, 1));
+    const size_t oWl = carve(sizeof(double) * std::max(nent, 1));
+    const size_t oc = carve(sizeof(double) * d);
+    const size_t ow = carve(sizeof(double) * d);
+    const size_t ou = carve(sizeof(double));
+    const size_t oFr = carve(sizeof(double2) * std::max(hp.tab_entries, 1));
+    const size_t oFi = carve(p->cplx ? sizeof(double2) * std::max(hp.tab_entries, 1) : 0);
+    const size_t oB = carve(sizeof(double) * 4);
+    const size_t oS = carve(sizeof(int) * 4);
+    const size_t oT = carve(sizeof(long long) * tabs.size());
+    const size_t oScr = carve(sizeof(double) * 8);
+    if (cudaMalloc(&p->dev_block, sz) != cudaSuccess) {
+        cudaGetLastError();
+        delete p;
+        return SG_ENOMEM;
+    }
+    p->dev_bytes = sz;
+    char *base = (char *)p->dev_block;
+    DevPlan &dp = p->dp;
+    memset(&dp, 0, sizeof dp);
+    dp.d = d;
+    dp.L = L;
+    dp.kind = (int)f->kind;
+    dp.nfront = hp.nfront;
+    for (int l = 0; l < SG_MAX_L + 3; ++l) {
+        dp.nl[l] = hp.nl[l];
+        dp.entry_off[l] = hp.entry_off[l];
+        dp.tab_off[l] = hp.tab_off[l];
+    }
+    for (int e = 0; e < SG_MAX_L + 2; ++e) dp.coef[e] = hp.coef[e];
+    dp.M0 = hp.M0;
+    dp.X = (const double *)(base + oX);
+    dp.Whi = (const double *)(base + oWh);
+    dp.Wlo = (const double *)(base + oWl);
+    dp.c = (const double *)(base + oc);
+    dp.w = (const double *)(base + ow);
+    dp.u = (const double *)(base + ou);
+    dp.Fre = (double2 *)(base + oFr);
+    dp.Fim = p->cplx ? (double2 *)(base + oFi) : nullptr;
+    dp.base = (double *)(base + oB);
+    dp.status = (int *)(base + oS);
+    p->d_tabs = (long long *)(base + oT);
+    p->d_scratch = (double *)(base + oScr);
+    std::vector<double> wz(d, 0.0);
+    bool ok = true;
+    ok &= cudaMemcpy((void *)dp.X, hp.X.data(), sizeof(double) * nent, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.Whi, hp.Whi.data(), sizeof(double) * nent, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.Wlo, hp.Wlo.data(), sizeof(double) * nent, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.c, f->c, sizeof(double) * d, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.w, f->w ? f->w : wz.data(), sizeof(double) * d, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.u, &f->u, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemcpy(p->d_tabs, tabs.data(), sizeof(long long) * tabs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= cudaMemset(dp.status, 0, sizeof(int) * 4) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        cudaFree(p->dev_block);
+        delete p;
+        return SG_ECUDA;
+    }
+    // ---- workspace layout ----
+    size_t ws = 0;
+    const size_t rec = p->cplx ? 2 * sizeof(double2) : sizeof(double2);
+    for (int par = 0; par < 2; ++par) {
+        p->ws_front_off[par] = ws;
+        ws = align_up(ws + (size_t)hp.ws_front_cap[par] * (rec + sizeof(uint32_t)) + 1024, 256);
+    }
+    p->ws_part_off = ws;
+    ws = align_up(ws + sizeof(double2) * (size_t)std::max<int64_t>(hp.total_partials, 1), 256);
+    p->ws_need = ws;
+    *out = p;
+    return SG_OK;
+}
+
+extern "C" int sg_workspace_size(sg_plan_t p, size_t *bytes) {
+    if (!p || !bytes) return SG_EINVAL;
+    *bytes = p->ws_need;
+    return SG_OK;
+}
+
+extern "C" int sg_set_workspace(sg_plan_t p, void *dev_ptr, size_t bytes) {
+    if (!p || !dev_ptr) return SG_EINVAL;
+    if (((uintptr_t)dev_ptr) % 256) return SG_EINVAL;
+    if (bytes < p->ws_need) return SG_ENOMEM;
+    p->ws = (char *)dev_ptr;
+    p->ws_bytes = bytes;
+    return SG_OK;
+}
+
+extern "C" int sg_update_integrand(sg_plan_t p, sg_stream_t s, const sg_integrand_desc *f) {
+    if (!p) return SG_EINVAL;
+    int rc = validate_desc(f, p->hp.d);
+    if (rc) return rc;
+    if ((int)f->kind != p->hp.kind) return SG_EINVAL;
+    cudaStream_t st = (cudaStream_t)s;
+    const size_t nb = sizeof(double) * p->hp.d;
+    if (cudaMemcpyAsync((void *)p->dp.c, f->c, nb, cudaMemcpyDefault, st) != cudaSuccess) return SG_ECUDA;
+    if (f->w && (f->kind == SG_F_PRODUCT_PEAK || f->kind == SG_F_GAUSSIAN))
+        if (cudaMemcpyAsync((void *)p->dp.w, f->w, nb, cudaMemcpyDefault, st) != cudaSuccess) return SG_ECUDA;
+    // u travels by value: staged through the plan's pinned-free path (a single 8-byte H2D copy)
+    if (cudaMemcpyAsync((void *)p->dp.u, &f->u, sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return SG_ECUDA;
+    return SG_OK;
+}
+
+static void front_ptrs(sg_plan_s *p, int t, double2 *&re, double2 *&im, uint32_t *&meta) {
+    const int par = t % 2;
+    const int64_t cap = p->hp.ws_front_cap[par];
+    char *b = p->ws + p->ws_front_off[par];
+    re = (double2 *)b;
+    im = p->cplx ? (double2 *)(b + sizeof(double2) * cap) : nullptr;
+    meta = (uint32_t *)(b + (p->cplx ? 2 : 1) * sizeof(double2) * cap);
+}
+
+extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
+    if (!p || !out_dev) return SG_EINVAL;
+    if (!p->ws) return SG_ENOWORKSPACE;
+    cudaStream_t st = (cudaStream_t)s;
+    const HostPlan &hp = p->hp;
+    const DevPlan &dp = p->dp;
+    double2 *partials = (double2 *)(p->ws + p->ws_part_off);
+    if (cudaMemsetAsync(dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
+    // K0
+    if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+    k_base<<<1, 256, 0, st>>>(dp);
+    // root pass
+    RootArgs R;
+    memset(&R, 0, sizeof R);
+    R.lo = hp.range_lo;
+    R.hi = hp.range_hi;
+    R.off1 = p->d_tabs + p->tab_off1;
+    R.JS = p->d_tabs + p->tab_JS;
+    if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
+    R.partials = partials;
+    if (p->cplx)
+        k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    else
+        k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    // level-synchronous passes
+    for (int t = 1; t <= hp.nfront; ++t) {
+        PassArgs A;
+        memset(&A, 0, sizeof A);
+        A.nsrc = hp.total[t];
+        A.ntasks = hp.pass_ntasks[t];
+        A.nsplit = hp.pass_nsplit[t];
+        double2 *re, *im;
+        uint32_t *meta;
+        front_ptrs(p, t, re, im, meta);
+        A.src_re = re;
+        A.src_im = im;
+        A.src_meta = meta;
+        const bool write = (t + 1 <= hp.nfront);
+        if (write) front_ptrs(p, t + 1, A.dst_re, A.dst_im, A.dst_meta);
+        A.offT = p->d_tabs + p->tab_offT[t];
+        A.NT = p->d_tabs + p->tab_NT[t];
+        A.CT = p->d_tabs + p->tab_CT[t];
+        A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
+        A.partials = partials + hp.pass_partial_off[t];
+        const unsigned grid = (unsigned)hp.pass_blocks[t];
+        if (p->cplx) {
+            if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            else k_pass<true, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+        } else {
+            if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            else k_pass<false, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+        }
+    }
+    k_reduce<<<1, 1024, 0, st>>>(dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev);
+    if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
+    return SG_OK;
+}
+
+extern "C" int sg_finalize(sg_plan_t p, sg_stream_t s, const double *gathered_dev, int world,
+                           double *result_dev) {
+    if (!p || !gathered_dev || !result_dev || world < 1) return SG_EINVAL;
+    k_finalize<<<1, 32, 0, (cudaStream_t)s>>>(gathered_dev, world, p->dp.status, result_dev);
+    if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
+    return SG_OK;
+}
+
+extern "C" int sg_integrate_host(sg_plan_t p, sg_stream_t s, double *result_host) {
+    if (!p || !result_host) return SG_EINVAL;
+    int rc = sg_integrate(p, s, p->d_scratch);
+    if (rc) return rc;
+    rc = sg_finalize(p, s, p->d_scratch, 1, p->d_scratch + 2);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(result_host, p->d_scratch + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                        (cudaStream_t)s) != cudaSuccess)
+        return SG_ECUDA;
+    if (cudaStreamSynchronize((cudaStream_t)s) != cudaSuccess) return SG_ECUDA;
+    if (!isfinite(result_host[0])) return SG_ENONFINITE;
+    return SG_OK;
+}
+
+extern "C" int sg_status_word(sg_plan_t p, int *status) {
+    if (!p || !status) return SG_EINVAL;
+    int v = 0;
+    if (cudaMemcpy(&v, p->dp.status, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return SG_ECUDA;
+    *status = v ? SG_ENONFINITE : SG_OK;
+    return SG_OK;
+}
+
+extern "C" int sg_plan_points(sg_plan_t p, unsigned long long *shard_points,
+                              unsigned long long *total_points) {
+    if (!p) return SG_EINVAL;
+    if (shard_points) *shard_points = p->hp.shard_points;
+    if (total_points) *total_points = p->hp.total_points;
+    return SG_OK;
+}
+
+extern "C" int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long long *n_depth1) {
+    if (!p) return SG_EINVAL;
+    if (lo) *lo = p->hp.range_lo;
+    if (hi) *hi = p->hp.range_hi;
+    if (n_depth1) *n_depth1 = (long long)p->hp.d * p->hp.M0;
+    return SG_OK;
+}
+
+extern "C" int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
+                              unsigned long long *written) {
+    if (!p || !npass) return SG_EINVAL;
+    const int n = p->hp.nfront + 1;
+    if ((terms || written) && *npass < n) {
+        *npass = n;
+        return SG_EINVAL;
+    }
+    *npass = n;
+    for (int i = 0; i < n; ++i) {
+        if (terms) terms[i] = p->hp.pass_terms[i];
+        if (written) written[i] = p->hp.pass_written[i];
+    }
+    return SG_OK;
+}
+
+extern "C" int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host) {
+    if (!p) return SG_EINVAL;
+    const size_t per = p->cplx ? 4 : 2, n = (size_t)p->hp.tab_entries;
+    if (table_host) {
+        if (table_doubles < n * per) return SG_EINVAL;
+        std::vector<double2> re(n), im(p->cplx ? n : 0);
+        if (cudaMemcpy(re.data(), p->dp.Fre, sizeof(double2) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SG_ECUDA;
+        if (p->cplx && cudaMemcpy(im.data(), p->dp.Fim, sizeof(double2) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SG_ECUDA;
+        for (size_t i = 0; i < n; ++i) {
+            table_host[i * per + 0] = re[i].x;
+            table_host[i * per + 1] = re[i].y;
+            if (p->cplx) {
+                table_host[i * per + 2] = im[i].x;
+                table_host[i * per + 3] = im[i].y;
+            }
+        }
+    }
+    if (base_host)
+        if (cudaMemcpy(base_host, p->dp.base, 4 * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return SG_ECUDA;
+    return SG_OK;
+}
+
+extern "C" int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
+                             unsigned long long *shard_points, unsigned long long *total_points,
+                             long long *range_lo, long long *range_hi, int *n_passes) {
+    if (d < 1 || q < d) return SG_EINVAL;
+    sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
+    if (opt) o = *opt;
+    if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
+    HostPlan hp;
+    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, o.rank, o.world,
+                             o.range_lo, o.range_hi);
+    if (rc) return rc;
+    if (shard_points) *shard_points = hp.shard_points;
+    if (total_points) *total_points = hp.total_points;
+    if (range_lo) *range_lo = hp.range_lo;
+    if (range_hi) *range_hi = hp.range_hi;
+    if (n_passes) *n_passes = hp.nfront + 1;
+    return SG_OK;
+}
+
+extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
+    if (!x || !w || level < 1) return SG_EINVAL;
+    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
+    int n = host_rule((int)rule, level, x, w);
+    return n < 0 ? SG_EUNSUPPORTED : n;
+}
+
+extern "C" int sg_destroy(sg_plan_t p) {
+    if (!p) return SG_EINVAL;
+    if (p->dev_block) cudaFree(p->dev_block);
+    delete p;
+    return SG_OK;
+}

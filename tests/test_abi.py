@@ -1,0 +1,119 @@
+"""CPU-side checks of the C ABI library (no compute calls need a GPU here):
+symbols exported vs include/sg_b200.h, host rule tables vs the oracle's (bit-identical, reading R5),
+host plan counts vs the generating-function point counts, shard partitions, errors."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import pins
+import sg_configs as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2210_14313_b200 import build as B
+    B.build()
+    from paper_2210_14313_b200._lib import lib
+    return lib()
+
+
+def test_header_symbols_exported(L):
+    hdr = open(os.path.join(ROOT, "include", "sg_b200.h")).read()
+    names = set(re.findall(r"\b(sg_[a-z_]+)\s*\(", hdr))
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(L, n), n
+    from paper_2210_14313_b200._lib import SYMBOLS
+    assert set(SYMBOLS) == names
+
+
+def _rule(L, rule, level):
+    n = pins.node_count(rule, level)
+    x = np.zeros(n)
+    w = np.zeros(n)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = L.sg_rule_table(rule, level, x.ctypes.data_as(dp), w.ctypes.data_as(dp))
+    return rc, x, w
+
+
+@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 11)), (S.RULE_GL, range(1, 30))])
+def test_library_rules_bit_identical_to_oracle(L, rule, levels):
+    for l in levels:
+        rc, x, w = _rule(L, rule, l)
+        assert rc == len(x)
+        ox, ow = oracle.rule(rule, l)
+        assert np.array_equal(x, ox), (rule, l, x - ox)
+        assert np.array_equal(w, ow), (rule, l, w - ow)
+
+
+def test_rule_table_limits(L):
+    assert _rule(L, S.RULE_CC, 13)[0] == -2    # SG_EUNSUPPORTED beyond CC level 12
+    assert _rule(L, 3, 2)[0] == -1             # Gauss-Patterson not built: SG_EINVAL
+
+
+def _query(L, d, q, rule, kind=0, form=0, rank=0, world=1, lo=0, hi=-1):
+    from paper_2210_14313_b200._lib import sg_options
+    o = sg_options(form, 0, rank, world, lo, hi)
+    sp, tp = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+    a, b = ctypes.c_longlong(), ctypes.c_longlong()
+    npass = ctypes.c_int()
+    rc = L.sg_plan_query(d, q, rule, kind, ctypes.byref(o), ctypes.byref(sp), ctypes.byref(tp),
+                         ctypes.byref(a), ctypes.byref(b), ctypes.byref(npass))
+    return rc, sp.value, tp.value, a.value, b.value, npass.value
+
+
+@pytest.mark.parametrize("i", [1, 2, 3, 4, 5])
+def test_plan_point_counts_match_generating_function(L, i):
+    p = S.baseline_config(i)
+    rc, sp, tp, lo, hi, npass = _query(L, p.d, p.q, p.rule, p.kind)
+    assert rc == 0
+    assert tp == sp == pins.n_points(p.rule, p.d, p.L)
+    assert npass == min(p.L, p.d)
+
+
+@pytest.mark.parametrize("i,world", [(2, 3), (3, 4), (4, 8), (5, 8), (5, 2), (1, 5)])
+def test_balanced_shards_partition(L, i, world):
+    p = S.baseline_config(i)
+    total = pins.n_points(p.rule, p.d, p.L)
+    prev_hi, acc = 0, 0
+    sizes = []
+    for r in range(world):
+        rc, sp, tp, lo, hi, _ = _query(L, p.d, p.q, p.rule, p.kind, rank=r, world=world)
+        assert rc == 0 and tp == total
+        assert lo == prev_hi
+        prev_hi = hi
+        acc += sp
+        sizes.append(sp)
+    assert acc == total
+    nd1 = p.d * sum(pins.node_count(p.rule, l) for l in range(2, p.L + 2))
+    assert prev_hi == nd1
+    if total > 10 ** 8:     # big configs balance to a few percent (largest subtree < 1%)
+        assert max(sizes) / (total / world) < 1.05
+
+
+def test_explicit_range_counts(L):
+    p = S.baseline_config(2)
+    # subtree points of a depth-1 range must equal the oracle's point count for the same range
+    for lo, hi in [(0, 1), (5, 17), (100, 101), (300, 360)]:
+        rc, sp, *_ = _query(L, p.d, p.q, p.rule, p.kind, lo=lo, hi=hi)
+        assert rc == 0
+        r = oracle.integrate_problem(p, lo=lo, hi=hi, include_root=(lo == 0), eval_mode=1)
+        assert sp == r.npoints
+
+
+def test_errors(L):
+    assert _query(L, 5, 4, S.RULE_CC)[0] == -1          # q < d: BudgetTooSmall
+    assert _query(L, 0, 4, S.RULE_CC)[0] == -1
+    assert _query(L, 5, 8, 7)[0] == -1                  # bad rule
+    assert _query(L, 5, 8, S.RULE_CC, kind=9)[0] == -1
+    assert _query(L, 5, 8, S.RULE_CC, rank=2, world=2)[0] == -1
+    assert _query(L, 5, 5 + 12, S.RULE_CC)[0] == -2     # CC level 13
+    assert _query(L, 1000, 1000 + 19, S.RULE_GL)[0] in (-2, -3)   # coefficient/size limits
+    assert _query(L, 10 ** 5, 10 ** 5 + 8, S.RULE_CC)[0] in (-2, -3)
+    assert L.sg_strerror(-3).decode().startswith("point")

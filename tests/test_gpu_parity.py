@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C ABI) against the __float128 oracle on the same seeded inputs.
+
+Gate (BASELINE.json north_star): |A_gpu - A_oracle| <= 1e-12 |A_oracle| in FP64.  The factor-form
+double-double path is expected far inside it (<= 1.6e-18 simulated), so a second,
+tighter "health" bound (1e-15) flags numerical regressions long before the gate.
+"""
+import json
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import pins
+import sg_configs as S
+
+pytestmark = pytest.mark.gpu
+GATE = 1e-12
+HEALTH = 1e-15
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "oracle_full.json")
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_14313_b200 import build as B
+    B.build()
+    from paper_2210_14313_b200 import api as A
+    return A
+
+
+def gpu_value(api, p, **kw):
+    hi, lo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u, **kw)
+    return mp.mpf(hi) + mp.mpf(lo), hi
+
+
+def rel(a, b):
+    return abs((a - b) / b) if b != 0 else abs(a - b)
+
+
+def check(api, p, tol=GATE, health=HEALTH, **kw):
+    ref = oracle.integrate_problem(p, eval_mode=1, lo=kw.get("range_lo", 0),
+                                   hi=kw.get("range_hi", -1),
+                                   include_root=kw.get("range_lo", 0) == 0)
+    v, hi = gpu_value(api, p, **kw)
+    r = rel(v, mp.mpf(ref.text))
+    assert r <= tol, (p.name, float(r), hi, ref.text)
+    if health is not None:
+        assert r <= health, (p.name, float(r))
+    return float(r)
+
+
+@pytest.mark.parametrize("i", [1, 2])
+def test_baseline_small_configs(api, i):
+    check(api, S.baseline_config(i))
+
+
+def test_config3_full_vs_oracle(api):
+    p = S.baseline_config(3)
+    golden = json.load(open(GOLDEN))["values"]["c3"]
+    v, _ = gpu_value(api, p)
+    assert rel(v, mp.mpf(golden["text"])) <= HEALTH
+
+
+@pytest.mark.parametrize("i", [4, 5])
+def test_big_configs_full_size(api, i):
+    """Full BASELINE sizes in the bench launch configuration: against the stored full-size oracle
+    value when present (oracle/make_golden.py), and always against the 50-digit DP pin."""
+    p = S.baseline_config(i)
+    v, _ = gpu_value(api, p)
+    dp = pins.dp_value(p)
+    assert rel(v, dp) <= HEALTH
+    if os.path.exists(GOLDEN):
+        vals = json.load(open(GOLDEN))["values"]
+        if p.name in vals:
+            assert rel(v, mp.mpf(vals[p.name]["text"])) <= HEALTH
+
+
+# sampled full-size outputs: contiguous ranges of depth-1 subtrees of configs 4-5, each small enough
+# for the oracle to enumerate point by point
+@pytest.mark.parametrize("i,lo,hi", [(4, 16900, 16917), (4, 9000, 9008), (4, 16983, 17000),
+                                     (5, 9520, 9554), (5, 10100, 10200), (5, 8000, 8003)])
+def test_big_configs_sampled_subtrees(api, i, lo, hi):
+    p = S.baseline_config(i)
+    check(api, p, range_lo=lo, range_hi=hi)
+
+
+CASES = [
+    # seed, d, L, rule, kind   (ragged tails: d not multiple of 32, several tiles per pass)
+    (41, 1, 5, S.RULE_CC, S.KIND_EXP), (42, 1, 9, S.RULE_GL, S.KIND_OSC),
+    (43, 2, 7, S.RULE_CC, S.KIND_PEAK), (44, 3, 0, S.RULE_GL, S.KIND_GAUSS),
+    (45, 5, 1, S.RULE_CC, S.KIND_OSC), (46, 37, 2, S.RULE_CC, S.KIND_GAUSS),
+    (47, 33, 3, S.RULE_GL, S.KIND_PEAK), (48, 65, 3, S.RULE_CC, S.KIND_EXP),
+    (49, 7, 6, S.RULE_GL, S.KIND_EXP), (50, 12, 5, S.RULE_CC, S.KIND_OSC),
+    (51, 130, 2, S.RULE_GL, S.KIND_OSC), (52, 4, 8, S.RULE_CC, S.KIND_GAUSS),
+    (53, 300, 2, S.RULE_CC, S.KIND_PEAK), (54, 20, 4, S.RULE_GL, S.KIND_GAUSS),
+]
+
+
+@pytest.mark.parametrize("seed,d,L,rule,kind", CASES)
+def test_random_problems(api, seed, d, L, rule, kind):
+    check(api, S.random_problem(seed, d, L, rule, kind))
+
+
+@pytest.mark.parametrize("seed,d,L,rule,kind", CASES[::3])
+def test_delta_form_equals_combination(api, seed, d, L, rule, kind):
+    p = S.random_problem(seed, d, L, rule, kind)
+    check(api, p, form=1)
+
+
+def test_paper_table_rows(api):
+    for t, d, N in [("5.6", 5, 8), ("5.7", 10, 6), ("5.8", 10, 8)]:
+        check(api, S.paper_table_problem(t, d, N))
+
+
+def test_shards_sum_to_whole_and_deterministic(api):
+    import torch
+    p = S.baseline_config(3)
+    whole = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+    a = whole.integrate_host()
+    b = whole.integrate_host()
+    assert a == b                               # bitwise reproducible reruns
+    world = 4
+    parts = []
+    for r in range(world):
+        sp = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=r, world=world)
+        parts.append(sp.sg_integrate().clone())
+        torch.cuda.synchronize()
+        sp.close()
+    gathered = torch.cat(parts)
+    res = whole.sg_finalize(gathered, world).cpu().numpy()
+    v1 = mp.mpf(a[0]) + mp.mpf(a[1])
+    v4 = mp.mpf(res[0]) + mp.mpf(res[1])
+    assert rel(v4, v1) <= 1e-20
+    whole.close()
+
+
+def test_factor_table_matches_mpmath(api):
+    """K0 element by element: F[l][k][j] = w_j^l E_k(x_j^l) in dd vs 50-digit values."""
+    for kind in (S.KIND_EXP, S.KIND_OSC, S.KIND_PEAK, S.KIND_GAUSS):
+        p = S.random_problem(60 + kind, 7, 3, S.RULE_CC, kind)
+        plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+        plan.integrate_host()
+        tab, base = plan.debug_tables()
+        idx = 0
+        for l in range(2, p.L + 2):
+            x, w = pins.mp_rule(p.rule, l)
+            for k in range(p.d):
+                for j in range(len(x)):
+                    xm = mp.mpf(x[j]) - mp.mpf(0.5)
+                    ck = mp.mpf(p.c[k])
+                    if kind == S.KIND_EXP:
+                        e = mp.exp(ck * xm)
+                    elif kind == S.KIND_OSC:
+                        e = mp.expj(ck * xm)
+                    elif kind == S.KIND_GAUSS:
+                        wk = mp.mpf(p.w[k])
+                        e = mp.exp(-ck ** 2 * ((mp.mpf(x[j]) - wk) ** 2 - (mp.mpf(0.5) - wk) ** 2))
+                    else:
+                        wk = mp.mpf(p.w[k])
+                        e = (1 / ck ** 2 + (mp.mpf(0.5) - wk) ** 2) / (1 / ck ** 2 + (mp.mpf(x[j]) - wk) ** 2)
+                    ref = mp.mpf(w[j]) * e
+                    got = mp.mpf(tab[idx, 0]) + mp.mpf(tab[idx, 1])
+                    assert abs(got - mp.re(ref)) <= 1e-30 * max(abs(ref), 1e-300), (kind, l, k, j)
+                    if kind == S.KIND_OSC:
+                        goti = mp.mpf(tab[idx, 2]) + mp.mpf(tab[idx, 3])
+                        assert abs(goti - mp.im(ref)) <= 1e-30 * max(abs(ref), 1e-300)
+                    idx += 1
+        plan.close()
+
+
+def test_errors_and_nonfinite(api):
+    from paper_2210_14313_b200._lib import SGError
+    with pytest.raises(SGError):
+        api.Plan(4, 3, S.RULE_CC, S.KIND_EXP, np.ones(4))               # q < d
+    with pytest.raises(SGError):
+        api.Plan(4, 6, S.RULE_CC, S.KIND_PEAK, np.ones(4))              # w missing
+    with pytest.raises(SGError):
+        api.Plan(4, 6, S.RULE_CC, S.KIND_EXP, np.array([1, 2, np.nan, 3.0]))
+    # exp overflow in the factor table -> NonFiniteIntegrand, result NaN
+    p = api.Plan(3, 6, S.RULE_CC, S.KIND_EXP, np.array([2000.0, 1.0, 1.0]))
+    with pytest.raises(SGError) as ei:
+        p.integrate_host()
+    assert ei.value.code == -6
+    p.close()

@@ -1,0 +1,48 @@
+"""Quick GPU sanity/timing run: per-config relative error vs oracle/DP and CUDA-event time."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+
+import mpmath as mp  # noqa: E402
+import torch  # noqa: E402
+
+import pins  # noqa: E402
+import sg_configs as S  # noqa: E402
+from paper_2210_14313_b200 import api  # noqa: E402
+
+mp.mp.dps = 50
+
+
+def main():
+    cfgs = [int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,3,4,5".split(","))]
+    for i in cfgs:
+        p = S.baseline_config(i)
+        t0 = time.time()
+        plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+        tplan = time.time() - t0
+        hi, lo = plan.integrate_host()
+        dp = pins.dp_value(p)
+        err = abs((mp.mpf(hi) + mp.mpf(lo) - dp) / dp)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = []
+        for _ in range(5):
+            ev0.record()
+            plan.sg_integrate()
+            ev1.record()
+            torch.cuda.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+        ms = min(times)
+        sp, tp = plan.points()
+        print(f"{p.name}: value={hi!r} rel_err_vs_DP={float(err):.3e} plan={tplan*1e3:.1f}ms "
+              f"integrate={ms:.3f}ms points={tp} -> {tp / (ms * 1e-3):.3e} pts/s "
+              f"ws={plan.workspace_bytes/1e9:.3f}GB passes={[(x.terms, x.written) for x in plan.passes()]}",
+              flush=True)
+        plan.close()
+
+
+if __name__ == "__main__":
+    main()
