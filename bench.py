@@ -1,0 +1,377 @@
+"""bench.py — Smolyak points/s and time-to-integral (FP64) of the B200 hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Workload (default): BASELINE.json configs[4] — d=300, q=d+4, Clenshaw-Curtis, oscillatory Genz
+integrand (seed 4), 27,521,113,876 Smolyak points: the configuration BASELINE.json ties to the
+1/2/4/8-GPU scaling run; it fits one GPU.  A step = the whole hot path:
+K0 factor tables, root pass, all prefix-tree passes, deterministic reduction, the cross-rank
+all-gather + fixed-order finalize.  Rank r evaluates its shard of depth-1 subtrees (strong scaling:
+the integral is fixed, the work is split).  Inputs (integrand parameters) are device-resident at
+the start of the timed region; L2 is flushed (256 MiB write) between timed steps, outside the
+events.  Times: CUDA events on the launching stream, barrier + synchronize on both sides, max over
+ranks.  The "e2e" leg times the same step through the C ABI with HOST buffers: pinned H2D of the
+parameters (sg_update_integrand), the step, and the D2H read of the 16-byte result.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import sg_configs as S  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+# Algorithmic FP64 flops per Smolyak point of the factor-form dd leaf:
+# real kinds: dd x dd product (DMUL + 3 DFMA = 7) + dd accumulate (8 DADD) = 15;
+# oscillatory: Re of a complex dd product (2 x 7) + 2 dd accumulates (2 x 8) = 30.
+FLOPS_PER_POINT = {S.KIND_EXP: 15, S.KIND_GAUSS: 15, S.KIND_PEAK: 15, S.KIND_OSC: 30}
+# FP64 peak derived from the unit count and clock: 148 SMs x 64 FP64 FMA/clk x 2 flops
+# x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz) = 37.2 TFLOP/s.
+SM_COUNT = 148
+FP64_FMA_PER_SM_CLK = 64
+
+
+def peak_fp64_tflops():
+    mhz = 1965.0
+    try:
+        mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        pass
+    return SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * mhz * 1e6 / 1e12, mhz
+
+
+# ----------------------------------------------------------------------------------------------
+# clocks sampled during the timed region (pynvml)
+# ----------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------------------------
+def oracle_sample_range(p: S.Problem, target_points: int):
+    """Depth-1 range [lo, nd1) of the workload whose subtrees hold about target_points points
+    (host-only library query; the range is the sample the oracle times)."""
+    from paper_2210_14313_b200._lib import lib, sg_options
+    L = lib()
+
+    def pts(lo, hi):
+        o = sg_options(0, 0, 0, 1, lo, hi)
+        sp = ctypes.c_ulonglong()
+        rc = L.sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), ctypes.byref(sp), None,
+                             None, None, None)
+        assert rc == 0
+        return sp.value
+
+    o = sg_options(0, 0, 0, 1, 0, -1)
+    nd1 = ctypes.c_longlong()
+    hi_ = ctypes.c_longlong()
+    L.sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), None, None, None,
+                    ctypes.byref(hi_), None)
+    nd1 = hi_.value
+    a, b = 1, nd1
+    while a < b:   # smallest lo such that points(lo, nd1) <= target
+        m = (a + b) // 2
+        if pts(m, nd1) > target_points:
+            a = m + 1
+        else:
+            b = m
+    return a, nd1, pts(a, nd1)
+
+
+def run_oracle_sample(p, lo, hi):
+    import oracle
+    r = oracle.integrate_problem(p, lo=lo, hi=hi, include_root=False, eval_mode=1)
+    return r
+
+
+def cpu_baseline(p, target_points=int(1.2e8)):
+    lo, hi, npts = oracle_sample_range(p, target_points)
+    r = run_oracle_sample(p, lo, hi)
+    cores = os.cpu_count()
+    return {"value": r.npoints / r.seconds, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "sample": f"{p.name} depth-1 subtrees [{lo},{hi}) = {r.npoints} of "
+                      f"{S_total_points(p)} Smolyak points, __float128 oracle (eval_mode=1), "
+                      f"OpenMP {cores} threads, {r.seconds:.2f} s",
+            "seconds": r.seconds, "points": r.npoints}
+
+
+def S_total_points(p):
+    from paper_2210_14313_b200._lib import lib, sg_options
+    o = sg_options(0, 0, 0, 1, 0, -1)
+    tp = ctypes.c_ulonglong()
+    lib().sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), None, ctypes.byref(tp), None,
+                        None, None)
+    return tp.value
+
+
+def config_block(p, extra=None):
+    c = {"workload": f"BASELINE.json configs[{int(p.name[1:]) - 1}] ({p.name}): d={p.d}, "
+                     f"q=d+{p.L}, {S.RULE_NAMES[p.rule]}, {S.KIND_NAMES[p.kind]} integrand",
+         "d": p.d, "q": p.q, "L": p.L, "rule": S.RULE_NAMES[p.rule],
+         "integrand": S.KIND_NAMES[p.kind], "points": S_total_points(p),
+         "form": "combination (Eq 2.6)", "arith": "factor-form double-double",
+         "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ----------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    p = S.baseline_config(args.config)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        return bench_reference(p, args, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2210_14313_b200 import api
+    from paper_2210_14313_b200 import build as B
+
+    if rank == 0 or world == 1:
+        B.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world, device=dev)
+    plan.profile_enable(True)
+    shard_pts, total_pts = plan.points()
+    passes = plan.passes()
+    dominant = max(range(1, len(passes)), key=lambda i: passes[i].terms) if len(passes) > 1 else 0
+    gathered = torch.zeros(2 * world, dtype=torch.float64, device=dev)
+    result = torch.zeros(2, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        part = plan.sg_integrate(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, part)
+            plan.sg_finalize(gathered, world, stream, result)
+        else:
+            plan.sg_finalize(part, 1, stream, result)
+
+    def timed(fn, k):
+        times, dom = [], []
+        for _ in range(k):
+            flush.fill_(1.0)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ms], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            times.append(ms)
+            prof = plan.profile_read()
+            dom.append(prof[3 + dominant - 1] if dominant > 0 else prof[2])
+        return times, dom
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        times, dom = timed(step, args.steps)
+    ms = statistics.mean(times)
+
+    # e2e: host buffers through the C ABI (pinned H2D of c/w, step, D2H of the result)
+    c_host = torch.from_numpy(p.c.copy()).pin_memory()
+    w_host = torch.from_numpy(p.w.copy()).pin_memory() if p.w is not None else None
+    res_host = torch.zeros(2, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        plan.sg_update_integrand(c_host, w_host, p.u, stream)
+        step()
+        res_host.copy_(result, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_times, _ = timed(e2e_step, args.steps)
+    e2e_ms = statistics.mean(e2e_times)
+    h2d = 8 * p.d * (2 if p.w is not None else 1) + 8
+    value_res = result.cpu().numpy()
+
+    # rank-0 report
+    if rank == 0:
+        peak, mhz = peak_fp64_tflops()
+        dom_ms = statistics.mean(dom)
+        dom_terms = passes[dominant].terms
+        achieved = dom_terms * FLOPS_PER_POINT[p.kind] / (dom_ms * 1e-3) / 1e12
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            traffic = json.load(open(tfile)).get(f"c{args.config}")
+        parity = {}
+        gfile = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
+        if os.path.exists(gfile):
+            vals = json.load(open(gfile))["values"]
+            if p.name in vals and world >= 1:
+                ref = float(vals[p.name]["hi"]) + float(vals[p.name]["lo"])
+                got = float(value_res[0]) + float(value_res[1])
+                parity = {"oracle": vals[p.name]["text"], "value": float(value_res[0]),
+                          "rel_err_vs_oracle": abs(got - ref) / abs(ref)}
+        fp64_meas = measure_fp64_peak()
+        line = {
+            "metric": METRIC, "value": total_pts / (ms * 1e-3), "unit": "points/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "time_to_integral_ms": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(p, {"parallelism": f"dp{world} (depth-1 subtree shards)",
+                                       "shard_points_rank0": shard_pts}),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"k_pass (pass {dominant}: {dom_terms} points)",
+                         "kernel_ms": dom_ms, "flops_per_point": FLOPS_PER_POINT[p.kind],
+                         "peak_note": f"FP64 peak derived: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} "
+                                      f"DFMA/clk x 2 x {mhz:.0f} MHz; measured DFMA burst "
+                                      f"{fp64_meas} TFLOP/s"},
+            "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
+            "gpu_launches": (len(passes) + 3 + 1) * args.steps,
+            "clocks": clk.summary(),
+            "parity": parity,
+            "step_ms_all": [round(t, 4) for t in times],
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(p)
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_fp64_peak():
+    lib_path = os.path.join(ROOT, "tools", "libfp64peak.so")
+    try:
+        if not os.path.exists(lib_path):
+            import subprocess
+            subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode",
+                                   "arch=compute_100a,code=sm_100a", "-O3", "-shared",
+                                   "-Xcompiler", "-fPIC", os.path.join(ROOT, "tools", "fp64_peak.cu"),
+                                   "-o", lib_path])
+        L = ctypes.CDLL(lib_path)
+        L.fp64_peak_tflops.restype = ctypes.c_double
+        L.fp64_peak_tflops.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_double)]
+        ms = ctypes.c_double()
+        return round(L.fp64_peak_tflops(SM_COUNT, 10, 2000, ctypes.byref(ms)), 2)
+    except Exception as e:  # report, do not fail the bench
+        return f"unavailable: {e}"
+
+
+def bench_reference(p, args, world):
+    """--impl reference: the CPU oracle (oracle/, __float128, OpenMP) as it stands, each step a
+    bounded sample of the workload (a fixed depth-1 subtree range)."""
+    target = int(4e7)
+    lo, hi, npts = oracle_sample_range(p, target)
+    for _ in range(args.warmup):
+        run_oracle_sample(p, lo, hi)
+    secs, pts = [], 0
+    for _ in range(args.steps):
+        r = run_oracle_sample(p, lo, hi)
+        secs.append(r.seconds)
+        pts = r.npoints
+    ms = statistics.mean(secs) * 1e3
+    value = pts / (ms * 1e-3)
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f128",
+        "data": "synthetic",
+        "config": config_block(p, {"sample_points_per_step": pts, "sample_range": [lo, hi]}),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{p.name} depth-1 subtrees [{lo},{hi}) = {pts} points per step"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

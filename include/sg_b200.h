@@ -150,6 +150,14 @@ int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
  * doubles per entry: 2 real dd or 4 complex dd) and the base value to host memory. */
 int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host);
 
+/* Profiling hook.  When enabled, sg_integrate records a CUDA event on its stream before its first
+ * kernel and after each kernel.  sg_profile_read waits for the events of the LAST sg_integrate and
+ * writes the device duration (ms) of each launch, in launch order:
+ *   [K0 factor table, K0 base, root pass, pass 1 .. pass nfront, final reduce]
+ * *n: in = capacity of ms[], out = number of launches (query with ms = NULL). */
+int sg_profile_enable(sg_plan_t p, int enable);
+int sg_profile_read(sg_plan_t p, float *ms, int *n);
+
 /* Host-only (no device touched): the plan's counts and shard range for (d, q, rule, kind, opt).
  * Any output pointer may be NULL.  Same validation and error codes as sg_plan. */
 int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,

@@ -145,6 +145,18 @@ class Plan:
                                     base.ctypes.data_as(dp)), "sg_debug_tables")
         return buf.reshape(nd1, ncplx), base
 
+    def profile_enable(self, on: bool = True):
+        check(lib().sg_profile_enable(self._h, int(bool(on))), "sg_profile_enable")
+
+    def profile_read(self) -> list[float]:
+        """Device ms of each launch of the last sg_integrate:
+        [K0 factor, K0 base, root pass, pass 1..nfront, final reduce]."""
+        n = ctypes.c_int(0)
+        check(lib().sg_profile_read(self._h, None, ctypes.byref(n)), "sg_profile_read")
+        buf = (ctypes.c_float * n.value)()
+        check(lib().sg_profile_read(self._h, buf, ctypes.byref(n)), "sg_profile_read")
+        return [float(x) for x in buf]
+
     def close(self):
         if getattr(self, "_h", None):
             torch.cuda.synchronize(self.device)

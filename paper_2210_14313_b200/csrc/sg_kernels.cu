@@ -397,6 +397,9 @@ struct sg_plan_s {
     std::vector<size_t> tab_offT, tab_NT, tab_CT, tab_TB;   // element offsets into d_tabs per depth
     size_t tab_JS = 0, tab_off1 = 0;
     double *d_scratch = nullptr;   // 4 doubles
+    // profiling hook (sg_profile_enable): events around every launch of sg_integrate
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
@@ -609,9 +612,16 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     const DevPlan &dp = p->dp;
     double2 *partials = (double2 *)(p->ws + p->ws_part_off);
     if (cudaMemsetAsync(dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
+    int evi = 0;
+    auto mark = [&]() {
+        if (p->prof && evi < (int)p->ev.size()) cudaEventRecord(p->ev[evi++], st);
+    };
+    mark();
     // K0
     if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+    mark();
     k_base<<<1, 256, 0, st>>>(dp);
+    mark();
     // root pass
     RootArgs R;
     memset(&R, 0, sizeof R);
@@ -625,6 +635,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
     else
         k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    mark();
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
         PassArgs A;
@@ -653,8 +664,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
             else k_pass<false, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
         }
+        mark();
     }
     k_reduce<<<1, 1024, 0, st>>>(dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev);
+    mark();
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
 }
@@ -772,8 +785,35 @@ extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
     return n < 0 ? SG_EUNSUPPORTED : n;
 }
 
+extern "C" int sg_profile_enable(sg_plan_t p, int enable) {
+    if (!p) return SG_EINVAL;
+    if (enable && p->ev.empty()) {
+        p->ev.resize(5 + p->hp.nfront);
+        for (auto &e : p->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) return SG_ECUDA;
+    }
+    p->prof = enable != 0;
+    return SG_OK;
+}
+
+extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
+    if (!p || !n) return SG_EINVAL;
+    const int nl = 4 + p->hp.nfront;
+    if (!ms) {
+        *n = nl;
+        return SG_OK;
+    }
+    if (*n < nl || p->ev.empty()) return SG_EINVAL;
+    if (cudaEventSynchronize(p->ev.back()) != cudaSuccess) return SG_ECUDA;
+    for (int i = 0; i < nl; ++i)
+        if (cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess) return SG_ECUDA;
+    *n = nl;
+    return SG_OK;
+}
+
 extern "C" int sg_destroy(sg_plan_t p) {
     if (!p) return SG_EINVAL;
+    for (auto &e : p->ev) cudaEventDestroy(e);
     if (p->dev_block) cudaFree(p->dev_block);
     delete p;
     return SG_OK;

@@ -1,0 +1,30 @@
+"""Minimal driver for ncu: plan one BASELINE config and run `steps` hot-path steps.
+
+    python tools/prof_step.py <config> [steps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import sg_configs as S  # noqa: E402
+from paper_2210_14313_b200 import api  # noqa: E402
+
+
+def main():
+    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    p = S.baseline_config(cfg)
+    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+    for _ in range(steps):
+        out = plan.sg_integrate()
+        plan.sg_finalize(out, 1)
+    torch.cuda.synchronize()
+    print(p.name, plan.sg_finalize(out, 1).cpu().numpy())
+    plan.close()
+
+
+if __name__ == "__main__":
+    main()
