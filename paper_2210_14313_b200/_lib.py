@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsg_b200.so")
+LIB_PATH = os.environ.get("SG_B200_LIB") or os.path.join(_HERE, "libsg_b200.so")
 
 SG_OK = 0
 SG_EINVAL = -1

@@ -1,11 +1,12 @@
 """Build the in-tree C-ABI shared library ``libsg_b200.so`` for sm_100a (nvcc + g++).
 
-    python -m paper_2210_14313_b200.build [--force]
+    python -m paper_2210_14313_b200.build [--force] [-DNAME=VAL ... --out path.so]
 
 The .so lands next to this file (git-ignored, but it travels to the GPU box with gpurun).
 Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo; --fmad=false so nvcc never contracts
 the error-free transforms of the double-double arithmetic (explicit fma() calls remain DFMA);
-no --use_fast_math (reading R10).
+no --use_fast_math (reading R10).  Extra -D defines + --out build tuning variants side by side
+(loaded with SG_B200_LIB=path).
 """
 from __future__ import annotations
 
@@ -32,25 +33,30 @@ def _newer(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: tuple = (),
+          out: str | None = None) -> str:
+    """Build LIB (or `out`, with extra -D`defines`, for tuning experiments)."""
+    lib_path = LIB if out is None else out
+    bdir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(bdir, exist_ok=True)
     header = os.path.join(ROOT, "include", "sg_b200.h")
     all_deps = [os.path.join(CSRC, f) for f in SOURCES_CU + SOURCES_CPP + DEPS] + [header,
                                                                                    __file__]
-    if not force and not _newer(LIB, all_deps):
-        return LIB
+    if not force and not _newer(lib_path, all_deps):
+        return lib_path
+    dflags = [f"-D{d}" for d in defines]
     objs = []
     for f in SOURCES_CPP:
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(bdir, f + ".o")
         cmd = ["g++", "-O2", "-std=gnu++17", "-fPIC", "-Wall", "-I", "/usr/local/cuda/include",
-               "-c", os.path.join(CSRC, f), "-o", obj]
+               *dflags, "-c", os.path.join(CSRC, f), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
         objs.append(obj)
     for f in SOURCES_CU:
-        obj = os.path.join(BUILD, f + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+        obj = os.path.join(bdir, f + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", *dflags,
                "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-c", os.path.join(CSRC, f), "-o", obj]
         if verbose:
             print(" ".join(cmd))
@@ -58,17 +64,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise subprocess.CalledProcessError(res.returncode, cmd)
-        with open(os.path.join(BUILD, f + ".ptxas.txt"), "w") as fh:
+        with open(os.path.join(bdir, f + ".ptxas.txt"), "w") as fh:
             fh.write(res.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lquadmath"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    out = None
+    if "--out" in sys.argv:
+        out = os.path.abspath(sys.argv[sys.argv.index("--out") + 1])
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs, out=out))
