@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -519,20 +520,196 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
     if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_leaf1: the last pass when every source prefix has excess L-1 (t = L-1), so every child has
+// level 2 and coefficient coef[L]: the dominant kernel of configs 4-5 (c4: 99.6%, c5: 97.4% of the
+// points).  Lean register budget (<= 64 -> 32 warps/SM), one accumulator pair per lane with short
+// dependency chains, two rows (k', k'+1) per iteration for ILP.  Oscillatory leaf = 14 FP64
+// instructions: h1, h2 (4), acc.h += h1 + h2 (2), remainder t1 + cross-term FMA chain (5),
+// remainder t2 (1), acc.l (2); real leaf = 7.
+// ---------------------------------------------------------------------------------------------
+template <bool CPLX>
+__device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const double2 f, const double2 fi,
+                                           double sigma, double &ah, double &al) {
+    // the remainder t = P.hi F.hi - h (one rounding) seeds the FMA chain of the cross terms
+    if (!CPLX) {
+        const double h = fma(er.hi, f.x, sigma) - sigma;
+        ah += h;
+        double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
+        c = fma(er.hi, f.y, c);
+        al += c;
+    } else {
+        const double h1 = fma(er.hi, f.x, sigma) - sigma;
+        const double h2 = fma(-ei.hi, fi.x, sigma) - sigma;
+        ah += h1 + h2;
+        double c = fma(er.lo, f.x, fma(er.hi, f.x, -h1));
+        c = fma(er.hi, f.y, c);
+        c = fma(-ei.lo, fi.x, c);
+        c = fma(-ei.hi, fi.y, c);
+        al += c + fma(-ei.hi, fi.x, -h2);
+    }
+}
+
+#ifndef LEAF1_MINB
+#define LEAF1_MINB 4
+#endif
+#ifndef LEAF1_PERJ
+#define LEAF1_PERJ 1   // one accumulator pair per node j of the row (ILP across j)
+#endif
+#ifndef LEAF1_ROWS
+#define LEAF1_ROWS 2   // rows k' per loop iteration
+#endif
+
+template <bool CPLX, int NJ, int NA, bool SMEM>
+__device__ __forceinline__ void leaf1_row(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi, int kp,
+                                          const dd &er, const dd &ei, double sigma, double (&ah)[NA],
+                                          double (&al)[NA]) {
+    double2 f[NJ], g[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        f[j] = SMEM ? Fr[kp * NJ + j] : __ldg(Fr + kp * NJ + j);
+        g[j] = CPLX ? (SMEM ? Fi[kp * NJ + j] : __ldg(Fi + kp * NJ + j)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) leaf1_term<CPLX>(er, ei, f[j], g[j], sigma, ah[j % NA], al[j % NA]);
+}
+
+// One warp task of the single-level leaf pass: returns this lane's coefficient-free sum.
+template <bool CPLX, int NJ, bool SMEM>
+__device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, long long task,
+                                         const double2 *Fr, const double2 *Fi) {
+    constexpr int NA = LEAF1_PERJ ? NJ : 1;
+    const int lane = threadIdx.x & 31;
+    const int d = P.d;
+    const long long chunk = task / A.nsplit;
+    const int split = (int)(task - chunk * A.nsplit);
+    const long long g = chunk * 32 + lane;
+    const bool valid = g < A.nsrc;
+    int k = d;
+    dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
+    if (valid) {
+        k = (int)(A.src_meta[g] & META_KMASK);
+        const double2 v = A.src_re[g];
+        pr = dd{v.x, v.y};
+        if (CPLX) {
+            const double2 vi = A.src_im[g];
+            pim = dd{vi.x, vi.y};
+        }
+    }
+    const int ks0 = (int)((long long)split * d / A.nsplit);
+    const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
+    const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
+    const int kmax = __reduce_max_sync(0xffffffffu, valid ? k : -1);
+    const int kb = max(ks0, kmin + 1);
+    const double bound = valid ? (fabs(pr.hi) + (CPLX ? fabs(pim.hi) : 0.0)) *
+                                     P.SA[2LL * (d + 1) + min(k + 1, d)] * (1.0 + 0x1p-20)
+                               : 0.0;
+    int ex = 0;
+    frexp(2.0 * bound, &ex);
+    const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+    double ah[NA], al[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) ah[a] = al[a] = 0.0;
+    // boundary rows: lanes whose prefix ends at k >= k' contribute zero
+    const int kmid = min(kmax + 1, ks1);
+    for (int kp = kb; kp < kmid; ++kp) {
+        const bool kv = kp > k;
+        const dd er = kv ? pr : dd{0.0, 0.0};
+        const dd ei = kv ? pim : dd{0.0, 0.0};
+        leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, er, ei, sigma, ah, al);
+    }
+    // main rows, LEAF1_ROWS per iteration, folded back onto the grid every FOLD rows
+    int kp = max(kb, kmid);
+    while (kp < ks1) {
+        const int ke = min(ks1, kp + FOLD);
+        for (; kp + LEAF1_ROWS - 1 < ke; kp += LEAF1_ROWS) {
+#pragma unroll
+            for (int r = 0; r < LEAF1_ROWS; ++r)
+                leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp + r, pr, pim, sigma, ah, al);
+        }
+        for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, pr, pim, sigma, ah, al);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+            const double t = (al[a] + sigma) - sigma;
+            ah[a] += t;
+            al[a] -= t;
+        }
+    }
+    dd s = {0.0, 0.0};
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < NA; ++a) s = dd_add(s, dd_from_sum(ah[a], al[a]));
+    }
+    return s;
+}
+
+// Persistent: gridDim.x = resident CTAs; CTA c's warp w runs tasks (c*WPB + w) + i*gridDim.x*WPB
+// (static round robin over tasks sorted heavy-first, so partials stay deterministic).  With SMEM the
+// level-2 factor slice (d x NJ entries) is staged once per CTA in shared memory, so the warp-uniform
+// row loads are broadcast LDS instead of LDG through the L1 data path.
+template <bool CPLX, int NJ, bool SMEM>
+__global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPlan P, const PassArgs A) {
+    extern __shared__ double2 fsm[];
+    const int wib = threadIdx.x >> 5;
+    const double2 *Fr = P.Fre + P.tab_off[2];
+    const double2 *Fi = CPLX ? P.Fim + P.tab_off[2] : nullptr;
+    if (SMEM) {
+        const int n = P.d * NJ;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            fsm[i] = Fr[i];
+            if (CPLX) fsm[n + i] = Fi[i];
+        }
+        __syncthreads();
+        Fr = fsm;
+        Fi = CPLX ? fsm + n : nullptr;
+    }
+    dd tot = {0.0, 0.0};
+    for (long long task = (long long)blockIdx.x * WPB + wib; task < A.ntasks;
+         task += (long long)gridDim.x * WPB)
+        tot = dd_add(tot, leaf1_task<CPLX, NJ, SMEM>(P, A, task, Fr, Fi));
+    tot = dd_mul_d(tot, P.coef[P.L]);
+    dd s = block_reduce_dd<WPB>(tot);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
-__global__ void k_suffix_abs(const DevPlan P) {
-    const int l = 2 + blockIdx.x * blockDim.x + threadIdx.x;
+// One CTA per level: chunked row sums, a serial suffix scan over the 256 chunk sums, then each
+// thread writes the suffix values of its chunk (all loads in parallel; deterministic order).
+__global__ void __launch_bounds__(256) k_suffix_abs(const DevPlan P) {
+    const int l = 2 + blockIdx.x;
     if (l > P.L + 1) return;
     const int d = P.d, n = P.nl[l];
     const double2 *Fr = P.Fre + P.tab_off[l];
     const double2 *Fi = P.kind == SG_F_OSCILLATORY ? P.Fim + P.tab_off[l] : nullptr;
-    double s = 0.0;
-    P.SA[(long long)l * (d + 1) + d] = 0.0;
-    for (int k = d - 1; k >= 0; --k) {
+    const int chunk = (d + blockDim.x - 1) / blockDim.x;
+    const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
+    auto row = [&](int k) {
+        double r = 0.0;
         for (int j = 0; j < n; ++j) {
-            s += fabs(Fr[(long long)k * n + j].x);
-            if (Fi) s += fabs(Fi[(long long)k * n + j].x);
+            r += fabs(Fr[(long long)k * n + j].x);
+            if (Fi) r += fabs(Fi[(long long)k * n + j].x);
         }
+        return r;
+    };
+    double cs = 0.0;
+    for (int k = k0; k < k1; ++k) cs += row(k);
+    __shared__ double suf[257];
+    suf[threadIdx.x] = cs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        suf[blockDim.x] = 0.0;
+        for (int i = blockDim.x - 1; i >= 0; --i) {
+            const double v = suf[i];
+            suf[i] = run;   // sum of the chunks after chunk i
+            run += v;
+        }
+    }
+    __syncthreads();
+    double s = suf[threadIdx.x];
+    if (threadIdx.x == 0) P.SA[(long long)l * (d + 1) + d] = 0.0;
+    for (int k = k1 - 1; k >= k0; --k) {
+        s += row(k);
         P.SA[(long long)l * (d + 1) + k] = s;
     }
 }
@@ -576,6 +753,10 @@ struct sg_plan_s {
     double *d_scratch = nullptr;   // 4 doubles
     // profiling hook (sg_profile_enable): events around every launch of sg_integrate
     bool prof = false;
+    // specialised single-level leaf kernel (k_leaf1); SG_B200_GENERIC_LEAF=1 forces k_leaf (tests)
+    bool leaf1 = true;
+    int leaf1_t = -1;          // pass index run by the persistent k_leaf1 (or -1)
+    size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
     // workspace
     char *ws = nullptr;
@@ -584,6 +765,7 @@ struct sg_plan_s {
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static int setup_leaf1(sg_plan_s *p);
 
 static bool finite_array(const double *a, int n) {
     for (int i = 0; i < n; ++i)
@@ -640,6 +822,10 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     HostPlan &hp = p->hp;
     p->cplx = (f->kind == SG_F_OSCILLATORY);
+    {
+        const char *g = getenv("SG_B200_GENERIC_LEAF");
+        p->leaf1 = !(g && g[0] == '1');
+    }
     // ---- device tables: one allocation ----
     const int L = hp.L, nent = (int)hp.X.size();
     std::vector<long long> tabs;
@@ -729,6 +915,13 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         delete p;
         return SG_ECUDA;
     }
+    rc = setup_leaf1(p);
+    if (rc) {
+        cudaGetLastError();
+        cudaFree(p->dev_block);
+        delete p;
+        return rc;
+    }
     // ---- workspace layout ----
     size_t ws = 0;
     const size_t rec = p->cplx ? 2 * sizeof(double2) : sizeof(double2);
@@ -774,6 +967,55 @@ extern "C" int sg_update_integrand(sg_plan_t p, sg_stream_t s, const sg_integran
     return SG_OK;
 }
 
+template <bool CPLX>
+static const void *leaf1_kernel(int nj, bool smem) {
+    if (nj == 3) return smem ? (const void *)k_leaf1<CPLX, 3, true> : (const void *)k_leaf1<CPLX, 3, false>;
+    return smem ? (const void *)k_leaf1<CPLX, 2, true> : (const void *)k_leaf1<CPLX, 2, false>;
+}
+
+// Persistent geometry of the single-level leaf pass (called once by sg_plan).
+static int setup_leaf1(sg_plan_s *p) {
+    HostPlan &hp = p->hp;
+    p->leaf1_t = -1;
+    if (!p->leaf1 || hp.nfront < 1) return SG_OK;
+    const int t = hp.nfront, nj = hp.nl[2];
+    if (t != hp.L - 1 || (nj != 2 && nj != 3)) return SG_OK;
+    const size_t smem = (size_t)hp.d * nj * sizeof(double2) * (p->cplx ? 2 : 1);
+    p->leaf1_smem = smem <= 56 * 1024 ? smem : 0;
+    const void *fn = p->cplx ? leaf1_kernel<true>(nj, p->leaf1_smem > 0) : leaf1_kernel<false>(nj, p->leaf1_smem > 0);
+    if (p->leaf1_smem > 48 * 1024 &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
+        return SG_ECUDA;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PASS_THREADS, p->leaf1_smem) != cudaSuccess ||
+        cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return SG_ECUDA;
+    const long long grid = std::max<long long>(1, std::min<long long>(hp.pass_blocks[t], (long long)sms * per_sm));
+    hp.pass_blocks[t] = grid;
+    int64_t poff = hp.root_blocks;
+    for (int u = 1; u <= hp.nfront; ++u) {
+        hp.pass_partial_off[u] = poff;
+        poff += hp.pass_blocks[u];
+    }
+    hp.total_partials = poff;
+    p->leaf1_t = t;
+    return SG_OK;
+}
+
+template <bool CPLX>
+static void launch_leaf1(sg_plan_s *p, const PassArgs &A, int nj, cudaStream_t st) {
+    const unsigned grid = (unsigned)p->hp.pass_blocks[p->leaf1_t];
+    const size_t sm = p->leaf1_smem;
+    if (nj == 3) {
+        if (sm) k_leaf1<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 3, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    } else {
+        if (sm) k_leaf1<CPLX, 2, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 2, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    }
+}
+
 static void front_ptrs(sg_plan_s *p, int t, double2 *&re, double2 *&im, uint32_t *&meta) {
     const int par = t % 2;
     const int64_t cap = p->hp.ws_front_cap[par];
@@ -799,7 +1041,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // K0
     if (hp.tab_entries > 0) {
         k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-        k_suffix_abs<<<1, 32, 0, st>>>(dp);
+        k_suffix_abs<<<hp.L, 256, 0, st>>>(dp);
     }
     mark();
     k_base<<<1, 256, 0, st>>>(dp);
@@ -839,11 +1081,16 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
         A.partials = partials + hp.pass_partial_off[t];
         const unsigned grid = (unsigned)hp.pass_blocks[t];
+        // single-level last pass (every source has excess L-1): specialised k_leaf1
+        const int n2 = hp.nl[2];
+        const bool single = !write && t == p->leaf1_t;
         if (p->cplx) {
             if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            else if (single) launch_leaf1<true>(p, A, n2, st);
             else k_leaf<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
         } else {
             if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            else if (single) launch_leaf1<false>(p, A, n2, st);
             else k_leaf<false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
         }
         mark();

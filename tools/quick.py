@@ -29,13 +29,16 @@ def main():
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         times = []
+        plan.profile_enable(True)
         for _ in range(5):
             ev0.record()
             plan.sg_integrate()
             ev1.record()
             torch.cuda.synchronize()
             times.append(ev0.elapsed_time(ev1))
+        prof = plan.profile_read()
         ms = min(times)
+        print(f"   launches(ms): {[round(x, 4) for x in prof]}  all={[round(x, 3) for x in times]}")
         sp, tp = plan.points()
         print(f"{p.name}: value={hi!r} rel_err_vs_DP={float(err):.3e} plan={tplan*1e3:.1f}ms "
               f"integrate={ms:.3f}ms points={tp} -> {tp / (ms * 1e-3):.3e} pts/s "
