@@ -554,10 +554,10 @@ __device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const dou
 #define LEAF1_MINB 4
 #endif
 #ifndef LEAF1_PERJ
-#define LEAF1_PERJ 1   // one accumulator pair per node j of the row (ILP across j)
+#define LEAF1_PERJ 0   // 1 = one accumulator pair per node j of the row (measured slower)
 #endif
 #ifndef LEAF1_ROWS
-#define LEAF1_ROWS 2   // rows k' per loop iteration
+#define LEAF1_ROWS 4   // rows k' per loop iteration (A/B: 4 > 2 > 1)
 #endif
 
 template <bool CPLX, int NJ, int NA, bool SMEM>
