@@ -33,10 +33,10 @@ import numpy as np  # noqa: E402
 import sg_configs as S  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-# Algorithmic FP64 flops per Smolyak point of the factor-form dd leaf:
-# real kinds: dd x dd product (DMUL + 3 DFMA = 7) + dd accumulate (8 DADD) = 15;
-# oscillatory: Re of a complex dd product (2 x 7) + 2 dd accumulates (2 x 8) = 30.
-FLOPS_PER_POINT = {S.KIND_EXP: 15, S.KIND_GAUSS: 15, S.KIND_PEAK: 15, S.KIND_OSC: 30}
+# Algorithmic FP64 work per Smolyak point of the grid-split double-double leaf:
+# real kinds 7 FP64 instructions = 4 DFMA + 3 DADD = 11 flops; oscillatory 14 = 8 DFMA + 6 DADD = 22.
+FLOPS_PER_POINT = {S.KIND_EXP: 11, S.KIND_GAUSS: 11, S.KIND_PEAK: 11, S.KIND_OSC: 22}
+FP64_INST_PER_POINT = {S.KIND_EXP: 7, S.KIND_GAUSS: 7, S.KIND_PEAK: 7, S.KIND_OSC: 14}
 # FP64 peak derived from the unit count and clock: 148 SMs x 64 FP64 FMA/clk x 2 flops
 # x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz) = 37.2 TFLOP/s.
 SM_COUNT = 148
@@ -304,14 +304,20 @@ def main():
                                        "shard_points_rank0": shard_pts}),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"k_pass (pass {dominant}: {dom_terms} points)",
+                         "kernel": f"pass {dominant} leaf kernel ({dom_terms} points)",
                          "kernel_ms": dom_ms, "flops_per_point": FLOPS_PER_POINT[p.kind],
+                         "fp64_inst_per_point": FP64_INST_PER_POINT[p.kind],
+                         "pipe_frac": dom_terms * FP64_INST_PER_POINT[p.kind] / (dom_ms * 1e-3)
+                                      / (SM_COUNT * FP64_FMA_PER_SM_CLK * mhz * 1e6),
+                         "max_flop_frac_of_mix": FLOPS_PER_POINT[p.kind] / (2 * FP64_INST_PER_POINT[p.kind]),
                          "peak_note": f"FP64 peak derived: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} "
                                       f"DFMA/clk x 2 x {mhz:.0f} MHz; measured DFMA burst "
                                       f"{fp64_meas} TFLOP/s"},
             "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
-            "gpu_launches": (len(passes) + 3 + 1) * args.steps,
+            # per step: k_factor, k_suffix_abs, k_base, k_root, one kernel per pass >= 1,
+            # k_reduce, k_finalize
+            "gpu_launches": (len(passes) - 1 + 6) * args.steps,
             "clocks": clk.summary(),
             "parity": parity,
             "step_ms_all": [round(t, 4) for t in times],

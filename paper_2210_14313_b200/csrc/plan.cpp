@@ -114,7 +114,7 @@ static u128 sat_mul(u128 a, u128 b) {
 }
 
 int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
-                    long long range_lo, long long range_hi) {
+                    long long range_lo, long long range_hi, bool allow_fuse) {
     if (d < 1 || L < 0) return SG_EINVAL;
     if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
     if (kind < 0 || kind > 3 || form < 0 || form > 1) return SG_EINVAL;
@@ -377,12 +377,33 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         poff += hp.pass_blocks[t];
     }
     hp.total_partials = poff;
+    // ---- fused last two levels ----
+    hp.fuse = allow_fuse && L >= 3 && hp.nfront == L - 1 && (hp.nl[2] == 2 || hp.nl[2] == 3);
+    if (hp.fuse) {
+        const int tm = L - 2;   // depth of the stored parents; their excess is L-2
+        hp.pass_written[tm] = 0;
+        hp.TK.assign((size_t)d + 1, 0);
+        for (int k = 0; k < d; ++k) {
+            const int64_t cnt = k <= d - 2 ? hp.C[tm][(size_t)(L - 2) * d + k] : 0;
+            hp.TK[k + 1] = hp.TK[k] + (cnt + 31) / 32;
+        }
+        const int t = hp.nfront;
+        hp.pass_nsplit[t] = 1;
+        hp.pass_ntasks[t] = hp.TK[d];
+        hp.pass_blocks[t] = std::max<int64_t>(1, (hp.pass_ntasks[t] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+        poff = hp.root_blocks;
+        for (int u = 1; u <= hp.nfront; ++u) {
+            hp.pass_partial_off[u] = poff;
+            poff += hp.pass_blocks[u];
+        }
+        hp.total_partials = poff;
+    }
     const bool cplx = (kind == SG_F_OSCILLATORY);
     const size_t per_node = (cplx ? 32 : 16) + 4;
     for (int par = 0; par < 2; ++par) {
         int64_t cap = 0;
         for (int t = 1; t <= hp.nfront; ++t)
-            if (t % 2 == par) cap = std::max(cap, hp.total[t]);
+            if (t % 2 == par && !(hp.fuse && t == hp.nfront)) cap = std::max(cap, hp.total[t]);
         cap = (cap + 63) / 64 * 64;
         hp.ws_front_cap[par] = cap;
         hp.ws_front_bytes[par] = (size_t)cap * per_node;

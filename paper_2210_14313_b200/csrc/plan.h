@@ -48,11 +48,16 @@ struct HostPlan {
     int64_t root_blocks = 0, total_partials = 0;
     size_t ws_front_bytes[2] = {0, 0}; // ping-pong frontier buffers (odd / even depth)
     int64_t ws_front_cap[2] = {0, 0};
+    // Fused last two levels (L >= 3, d >= L, level-2 rows of 2 or 3 nodes): frontier L-1 is never
+    // stored; the last pass builds each depth-(L-1) prefix from its depth-(L-2) parent (excess L-2,
+    // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
+    bool fuse = false;
+    std::vector<int64_t> TK;           // [d + 1] prefix of fused tasks over k_mid
 };
 
 // Build rules, counts, shard range and launch geometry. Returns an sg_status code.
 int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
-                    long long range_lo, long long range_hi);
+                    long long range_lo, long long range_hi, bool allow_fuse = true);
 
 // 1-D rule (level l) on [0,1] as doubles rounded from quad; returns n or -1.
 int host_rule(int rule, int l, double *x, double *w);

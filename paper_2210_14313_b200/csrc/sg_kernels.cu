@@ -672,6 +672,103 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPla
     if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_leaf2: fused last two levels.  The depth-(L-1) prefixes are never stored: a warp task is
+// (k_mid, 32 stored depth-(L-2) parents of excess L-2 whose last active coordinate is < k_mid);
+// each lane forms P' = P * F[2][k_mid][j_mid] in full double-double for every node j_mid, then
+// walks the rows k' > k_mid of its level-2 children exactly like k_leaf1.  All lanes share k_mid,
+// so every row is warp-uniform (no boundary predication).  Saves the write + read of frontier
+// L-1 (config 5: 119 M nodes, 4.3 GB each way).
+// ---------------------------------------------------------------------------------------------
+struct Leaf2Args {
+    const double2 *src_re, *src_im;   // frontier L-2
+    long long base;                   // offset of segment (b = L-2, k = 0) in frontier L-2
+    const long long *Cmid;            // C_{L-2}(L-2, k): parents of excess L-2 with k_last < k
+    const long long *TK;              // [d+1] task prefix over k_mid
+    long long ntasks;
+    double2 *partials;
+};
+
+template <bool CPLX, int NJ, bool SMEM>
+__global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
+    extern __shared__ double2 fsm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int d = P.d;
+    const double2 *Fr = P.Fre + P.tab_off[2];
+    const double2 *Fi = CPLX ? P.Fim + P.tab_off[2] : nullptr;
+    if (SMEM) {
+        const int n = d * NJ;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            fsm[i] = Fr[i];
+            if (CPLX) fsm[n + i] = Fi[i];
+        }
+        __syncthreads();
+        Fr = fsm;
+        Fi = CPLX ? fsm + n : nullptr;
+    }
+    dd tot = {0.0, 0.0};
+    for (long long task = (long long)blockIdx.x * WPB + wib; task < A.ntasks;
+         task += (long long)gridDim.x * WPB) {
+        // k_mid = max k with TK[k] <= task (warp-uniform binary search)
+        int lo = 0, hi = d;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (A.TK[mid] <= task) lo = mid;
+            else hi = mid;
+        }
+        const int km = lo;
+        const long long i = (task - A.TK[km]) * 32 + lane;
+        const bool valid = i < A.Cmid[km];
+        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
+        if (valid) {
+            const double2 v = A.src_re[A.base + i];
+            pr = dd{v.x, v.y};
+            if (CPLX) {
+                const double2 vi = A.src_im[A.base + i];
+                pim = dd{vi.x, vi.y};
+            }
+        }
+        const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+        dd lane_sum = {0.0, 0.0};
+#pragma unroll 1
+        for (int jm = 0; jm < NJ; ++jm) {
+            const double2 f = Fr[km * NJ + jm];
+            dd er, ei = {0.0, 0.0};
+            if (CPLX) {
+                const double2 g = Fi[km * NJ + jm];
+                cdd c = cdd_mul(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
+                er = c.re;
+                ei = c.im;
+            } else {
+                er = dd_mul(pr, dd{f.x, f.y});
+            }
+            const double bound = (fabs(er.hi) + (CPLX ? fabs(ei.hi) : 0.0)) * sa;
+            int ex = 0;
+            frexp(2.0 * bound, &ex);
+            const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+            double ah[1] = {0.0}, al[1] = {0.0};
+            int kp = km + 1;
+            while (kp < d) {
+                const int ke = min(d, kp + FOLD);
+                for (; kp + LEAF1_ROWS - 1 < ke; kp += LEAF1_ROWS) {
+#pragma unroll
+                    for (int r = 0; r < LEAF1_ROWS; ++r)
+                        leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp + r, er, ei, sigma, ah, al);
+                }
+                for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp, er, ei, sigma, ah, al);
+                const double t = (al[0] + sigma) - sigma;
+                ah[0] += t;
+                al[0] -= t;
+            }
+            lane_sum = dd_add(lane_sum, dd_from_sum(ah[0], al[0]));
+        }
+        if (valid) tot = dd_add(tot, lane_sum);
+    }
+    tot = dd_mul_d(tot, P.coef[P.L]);
+    dd s = block_reduce_dd<WPB>(tot);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
 // One CTA per level: chunked row sums, a serial suffix scan over the 256 chunk sums, then each
 // thread writes the suffix values of its chunk (all loads in parallel; deterministic order).
@@ -749,13 +846,14 @@ struct sg_plan_s {
     size_t dev_bytes = 0;
     long long *d_tabs = nullptr;
     std::vector<size_t> tab_offT, tab_NT, tab_CT, tab_TB;   // element offsets into d_tabs per depth
-    size_t tab_JS = 0, tab_off1 = 0;
+    size_t tab_JS = 0, tab_off1 = 0, tab_TK = 0;
     double *d_scratch = nullptr;   // 4 doubles
     // profiling hook (sg_profile_enable): events around every launch of sg_integrate
     bool prof = false;
     // specialised single-level leaf kernel (k_leaf1); SG_B200_GENERIC_LEAF=1 forces k_leaf (tests)
     bool leaf1 = true;
-    int leaf1_t = -1;          // pass index run by the persistent k_leaf1 (or -1)
+    int leaf1_t = -1;          // pass index run by the persistent k_leaf1 / k_leaf2 (or -1)
+    bool leaf2 = false;        // last two levels fused (hp.fuse): k_leaf2
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
     // workspace
@@ -814,8 +912,11 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
     sg_plan_s *p = new (std::nothrow) sg_plan_s();
     if (!p) return SG_ENOMEM;
-    rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
-                         o.range_lo, o.range_hi);
+    {
+        const char *nf = getenv("SG_B200_NOFUSE");
+        rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
+                             o.range_lo, o.range_hi, !(nf && nf[0] == '1'));
+    }
     if (rc) {
         delete p;
         return rc;
@@ -845,6 +946,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         if (t < hp.nfront) p->tab_TB[t] = push(hp.TB[t]);
     }
     p->tab_JS = push(hp.JS);
+    if (hp.fuse) p->tab_TK = push(hp.TK);
     p->tab_off1 = hp.nfront >= 1 ? p->tab_offT[1] : 0;
     if (tabs.empty()) tabs.push_back(0);
     size_t sz = 0;
@@ -973,16 +1075,30 @@ static const void *leaf1_kernel(int nj, bool smem) {
     return smem ? (const void *)k_leaf1<CPLX, 2, true> : (const void *)k_leaf1<CPLX, 2, false>;
 }
 
-// Persistent geometry of the single-level leaf pass (called once by sg_plan).
+template <bool CPLX>
+static const void *leaf2_kernel(int nj, bool smem) {
+    if (nj == 3) return smem ? (const void *)k_leaf2<CPLX, 3, true> : (const void *)k_leaf2<CPLX, 3, false>;
+    return smem ? (const void *)k_leaf2<CPLX, 2, true> : (const void *)k_leaf2<CPLX, 2, false>;
+}
+
+// Persistent geometry of the single-level last pass (k_leaf1, or the fused k_leaf2; once per plan).
 static int setup_leaf1(sg_plan_s *p) {
     HostPlan &hp = p->hp;
     p->leaf1_t = -1;
-    if (!p->leaf1 || hp.nfront < 1) return SG_OK;
+    p->leaf2 = false;
+    if (hp.nfront < 1) return SG_OK;
     const int t = hp.nfront, nj = hp.nl[2];
-    if (t != hp.L - 1 || (nj != 2 && nj != 3)) return SG_OK;
+    if (hp.fuse) {
+        p->leaf2 = true;
+    } else {
+        if (!p->leaf1) return SG_OK;
+        if (t != hp.L - 1 || (nj != 2 && nj != 3)) return SG_OK;
+    }
     const size_t smem = (size_t)hp.d * nj * sizeof(double2) * (p->cplx ? 2 : 1);
     p->leaf1_smem = smem <= 56 * 1024 ? smem : 0;
-    const void *fn = p->cplx ? leaf1_kernel<true>(nj, p->leaf1_smem > 0) : leaf1_kernel<false>(nj, p->leaf1_smem > 0);
+    const bool sm = p->leaf1_smem > 0;
+    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm) : leaf2_kernel<false>(nj, sm))
+                              : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
@@ -1001,6 +1117,19 @@ static int setup_leaf1(sg_plan_s *p) {
     hp.total_partials = poff;
     p->leaf1_t = t;
     return SG_OK;
+}
+
+template <bool CPLX>
+static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
+    const unsigned grid = (unsigned)p->hp.pass_blocks[p->leaf1_t];
+    const size_t sm = p->leaf1_smem;
+    if (nj == 3) {
+        if (sm) k_leaf2<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 3, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    } else {
+        if (sm) k_leaf2<CPLX, 2, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 2, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    }
 }
 
 template <bool CPLX>
@@ -1062,6 +1191,25 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     mark();
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
+        if (p->leaf2 && t == hp.nfront) {
+            // fused last two levels: read the stored depth-(L-2) parents of excess L-2
+            Leaf2Args B;
+            memset(&B, 0, sizeof B);
+            double2 *re, *im;
+            uint32_t *meta;
+            front_ptrs(p, t - 1, re, im, meta);
+            B.src_re = re;
+            B.src_im = im;
+            B.base = hp.off[t - 1][(size_t)(hp.L - 2) * hp.d];
+            B.Cmid = p->d_tabs + p->tab_CT[t - 1] + (size_t)(hp.L - 2) * hp.d;
+            B.TK = p->d_tabs + p->tab_TK;
+            B.ntasks = hp.pass_ntasks[t];
+            B.partials = partials + hp.pass_partial_off[t];
+            if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
+            else launch_leaf2<false>(p, B, hp.nl[2], st);
+            mark();
+            continue;
+        }
         PassArgs A;
         memset(&A, 0, sizeof A);
         A.nsrc = hp.total[t];
@@ -1073,7 +1221,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         A.src_re = re;
         A.src_im = im;
         A.src_meta = meta;
-        const bool write = (t + 1 <= hp.nfront);
+        const bool write = (t + 1 <= hp.nfront) && !(p->leaf2 && t + 1 == hp.nfront);
         if (write) front_ptrs(p, t + 1, A.dst_re, A.dst_im, A.dst_meta);
         A.offT = p->d_tabs + p->tab_offT[t];
         A.NT = p->d_tabs + p->tab_NT[t];

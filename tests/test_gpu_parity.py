@@ -186,3 +186,25 @@ def test_errors_and_nonfinite(api):
         p.integrate_host()
     assert ei.value.code == -6
     p.close()
+
+
+# every last-pass kernel variant must agree with the oracle: fused k_leaf2 (default), stored
+# frontier + k_leaf1 (SG_B200_NOFUSE=1), stored frontier + generic k_leaf (+ SG_B200_GENERIC_LEAF=1)
+@pytest.mark.parametrize("mode", ["fused", "nofuse", "generic"])
+@pytest.mark.parametrize("seed,d,L,rule,kind", [
+    (61, 40, 3, S.RULE_CC, S.KIND_OSC), (62, 75, 4, S.RULE_CC, S.KIND_GAUSS),
+    (63, 33, 4, S.RULE_GL, S.KIND_PEAK), (64, 9, 5, S.RULE_GL, S.KIND_OSC),
+    (65, 200, 3, S.RULE_GL, S.KIND_EXP)])
+def test_last_pass_variants(api, monkeypatch, mode, seed, d, L, rule, kind):
+    if mode in ("nofuse", "generic"):
+        monkeypatch.setenv("SG_B200_NOFUSE", "1")
+    if mode == "generic":
+        monkeypatch.setenv("SG_B200_GENERIC_LEAF", "1")
+    check(api, S.random_problem(seed, d, L, rule, kind))
+
+
+@pytest.mark.parametrize("mode", ["fused", "nofuse"])
+def test_config5_sampled_variants(api, monkeypatch, mode):
+    if mode == "nofuse":
+        monkeypatch.setenv("SG_B200_NOFUSE", "1")
+    check(api, S.baseline_config(5), range_lo=9400, range_hi=9520)
