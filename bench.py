@@ -316,8 +316,8 @@ def main():
             "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
             # per step: k_factor, k_suffix_abs, k_base, k_root, one kernel per pass >= 1,
-            # k_reduce, k_finalize
-            "gpu_launches": (len(passes) - 1 + 6) * args.steps,
+            # k_reduce_l1, k_reduce, k_finalize
+            "gpu_launches": (len(passes) - 1 + 7) * args.steps,
             "clocks": clk.summary(),
             "parity": parity,
             "step_ms_all": [round(t, 4) for t in times],

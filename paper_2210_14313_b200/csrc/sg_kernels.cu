@@ -54,6 +54,7 @@ struct PassArgs {
     uint32_t *dst_meta;
     const long long *offT, *NT, *CT, *TB;
     double2 *partials;
+    unsigned long long *counter;   // dynamic task counter (persistent kernels), zeroed per launch
 };
 
 struct RootArgs {
@@ -663,13 +664,21 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPla
         Fr = fsm;
         Fi = CPLX ? fsm + n : nullptr;
     }
-    dd tot = {0.0, 0.0};
-    for (long long task = (long long)blockIdx.x * WPB + wib; task < A.ntasks;
-         task += (long long)gridDim.x * WPB)
-        tot = dd_add(tot, leaf1_task<CPLX, NJ, SMEM>(P, A, task, Fr, Fi));
-    tot = dd_mul_d(tot, P.coef[P.L]);
-    dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    (void)wib;
+    const int lane = threadIdx.x & 31;
+    // dynamic scheduling: warps pull tasks (sorted heavy-first) from a global counter; every task
+    // writes its own partial, so the fixed-order reduction keeps results bitwise reproducible
+    for (;;) {
+        unsigned long long task = 0;
+        if (lane == 0) task = atomicAdd(A.counter, 1ull);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if ((long long)task >= A.ntasks) break;
+        dd v = warp_reduce_dd(leaf1_task<CPLX, NJ, SMEM>(P, A, (long long)task, Fr, Fi));
+        if (lane == 0) {
+            v = dd_mul_d(v, P.coef[P.L]);
+            A.partials[task] = make_double2(v.hi, v.lo);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -686,7 +695,8 @@ struct Leaf2Args {
     const long long *Cmid;            // C_{L-2}(L-2, k): parents of excess L-2 with k_last < k
     const long long *TK;              // [d+1] task prefix over k_mid
     long long ntasks;
-    double2 *partials;
+    double2 *partials;             // one per task
+    unsigned long long *counter;   // dynamic task counter, zeroed per launch
 };
 
 template <bool CPLX, int NJ, bool SMEM>
@@ -706,9 +716,13 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPla
         Fr = fsm;
         Fi = CPLX ? fsm + n : nullptr;
     }
-    dd tot = {0.0, 0.0};
-    for (long long task = (long long)blockIdx.x * WPB + wib; task < A.ntasks;
-         task += (long long)gridDim.x * WPB) {
+    (void)wib;
+    for (;;) {
+        unsigned long long utask = 0;
+        if (lane == 0) utask = atomicAdd(A.counter, 1ull);
+        utask = __shfl_sync(0xffffffffu, utask, 0);
+        const long long task = (long long)utask;
+        if (task >= A.ntasks) break;
         // k_mid = max k with TK[k] <= task (warp-uniform binary search)
         int lo = 0, hi = d;
         while (hi - lo > 1) {
@@ -762,11 +776,12 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPla
             }
             lane_sum = dd_add(lane_sum, dd_from_sum(ah[0], al[0]));
         }
-        if (valid) tot = dd_add(tot, lane_sum);
+        dd v = warp_reduce_dd(valid ? lane_sum : dd{0.0, 0.0});
+        if (lane == 0) {
+            v = dd_mul_d(v, P.coef[P.L]);
+            A.partials[task] = make_double2(v.hi, v.lo);
+        }
     }
-    tot = dd_mul_d(tot, P.coef[P.L]);
-    dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
 }
 
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
@@ -811,7 +826,17 @@ __global__ void __launch_bounds__(256) k_suffix_abs(const DevPlan P) {
     }
 }
 
-// Final fixed-order reduction of all CTA partials (+ the root point) -> out[0..1].
+// Level-1 reduction: block b sums partials [b*RED_CHUNK, (b+1)*RED_CHUNK) in a fixed order.
+#define RED_CHUNK 8192
+__global__ void __launch_bounds__(256) k_reduce_l1(const double2 *partials, long long n, double2 *out) {
+    const long long b0 = (long long)blockIdx.x * RED_CHUNK, b1 = min(n, b0 + RED_CHUNK);
+    dd s = {0.0, 0.0};
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
+    s = block_reduce_dd<8>(s);
+    if (threadIdx.x == 0) out[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
+// Final fixed-order reduction of the level-1 partials (+ the root point) -> out[0..1].
 __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 *partials,
                                                  long long n, int include_root, double *out) {
     dd s = {0.0, 0.0};
@@ -854,12 +879,14 @@ struct sg_plan_s {
     bool leaf1 = true;
     int leaf1_t = -1;          // pass index run by the persistent k_leaf1 / k_leaf2 (or -1)
     bool leaf2 = false;        // last two levels fused (hp.fuse): k_leaf2
+    long long leaf1_grid = 0;  // persistent grid (resident CTAs) of k_leaf1 / k_leaf2
+    unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
-    size_t ws_front_off[2] = {0, 0}, ws_part_off = 0, ws_need = 0;
+    size_t ws_front_off[2] = {0, 0}, ws_part_off = 0, ws_red_off = 0, ws_need = 0;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -967,6 +994,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     const size_t oS = carve(sizeof(int) * 4);
     const size_t oT = carve(sizeof(long long) * tabs.size());
     const size_t oScr = carve(sizeof(double) * 8);
+    const size_t oCnt = carve(sizeof(unsigned long long) * 8);
     const size_t oSA = carve(sizeof(double) * (size_t)(L + 2) * (d + 1));
     if (cudaMalloc(&p->dev_block, sz) != cudaSuccess) {
         cudaGetLastError();
@@ -1000,6 +1028,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     dp.status = (int *)(base + oS);
     p->d_tabs = (long long *)(base + oT);
     p->d_scratch = (double *)(base + oScr);
+    p->d_counter = (unsigned long long *)(base + oCnt);
     dp.SA = (double *)(base + oSA);
     std::vector<double> wz(d, 0.0);
     bool ok = true;
@@ -1033,6 +1062,8 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     p->ws_part_off = ws;
     ws = align_up(ws + sizeof(double2) * (size_t)std::max<int64_t>(hp.total_partials, 1), 256);
+    p->ws_red_off = ws;
+    ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK - 1) / RED_CHUNK + 1), 256);
     p->ws_need = ws;
     *out = p;
     return SG_OK;
@@ -1107,8 +1138,9 @@ static int setup_leaf1(sg_plan_s *p) {
         cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         return SG_ECUDA;
-    const long long grid = std::max<long long>(1, std::min<long long>(hp.pass_blocks[t], (long long)sms * per_sm));
-    hp.pass_blocks[t] = grid;
+    const long long ntasks = hp.pass_ntasks[t];
+    p->leaf1_grid = std::max<long long>(1, std::min<long long>((ntasks + WPB - 1) / WPB, (long long)sms * per_sm));
+    hp.pass_blocks[t] = ntasks;   // partial slots: one per task (0 tasks -> no slot, no launch)
     int64_t poff = hp.root_blocks;
     for (int u = 1; u <= hp.nfront; ++u) {
         hp.pass_partial_off[u] = poff;
@@ -1121,7 +1153,7 @@ static int setup_leaf1(sg_plan_s *p) {
 
 template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
-    const unsigned grid = (unsigned)p->hp.pass_blocks[p->leaf1_t];
+    const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
     if (nj == 3) {
         if (sm) k_leaf2<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
@@ -1134,7 +1166,7 @@ static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t 
 
 template <bool CPLX>
 static void launch_leaf1(sg_plan_s *p, const PassArgs &A, int nj, cudaStream_t st) {
-    const unsigned grid = (unsigned)p->hp.pass_blocks[p->leaf1_t];
+    const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
     if (nj == 3) {
         if (sm) k_leaf1<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
@@ -1205,8 +1237,12 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.TK = p->d_tabs + p->tab_TK;
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
-            if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
-            else launch_leaf2<false>(p, B, hp.nl[2], st);
+            B.counter = p->d_counter;
+            if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
+            if (B.ntasks > 0) {
+                if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
+                else launch_leaf2<false>(p, B, hp.nl[2], st);
+            }
             mark();
             continue;
         }
@@ -1228,22 +1264,30 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         A.CT = p->d_tabs + p->tab_CT[t];
         A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
         A.partials = partials + hp.pass_partial_off[t];
+        A.counter = p->d_counter;
+        if (t == p->leaf1_t && cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess)
+            return SG_ECUDA;
         const unsigned grid = (unsigned)hp.pass_blocks[t];
         // single-level last pass (every source has excess L-1): specialised k_leaf1
         const int n2 = hp.nl[2];
         const bool single = !write && t == p->leaf1_t;
         if (p->cplx) {
             if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            else if (single) launch_leaf1<true>(p, A, n2, st);
+            else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, st); }
             else k_leaf<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
         } else {
             if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            else if (single) launch_leaf1<false>(p, A, n2, st);
+            else if (single) { if (A.ntasks > 0) launch_leaf1<false>(p, A, n2, st); }
             else k_leaf<false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
         }
         mark();
     }
-    k_reduce<<<1, 1024, 0, st>>>(dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev);
+    {
+        const long long nl1 = (hp.total_partials + RED_CHUNK - 1) / RED_CHUNK;
+        double2 *l1 = (double2 *)(p->ws + p->ws_red_off);
+        k_reduce_l1<<<(unsigned)nl1, 256, 0, st>>>(partials, hp.total_partials, l1);
+        k_reduce<<<1, 1024, 0, st>>>(dp, l1, nl1, hp.include_root ? 1 : 0, out_dev);
+    }
     mark();
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
