@@ -57,7 +57,7 @@ struct HostPlan {
 
 // Build rules, counts, shard range and launch geometry. Returns an sg_status code.
 int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
-                    long long range_lo, long long range_hi, bool allow_fuse = true);
+                    long long range_lo, long long range_hi, int fuse_mode = 1);   // 0 never, 1 auto, 2 always
 
 // 1-D rule (level l) on [0,1] as doubles rounded from quad; returns n or -1.
 int host_rule(int rule, int l, double *x, double *w);

@@ -699,8 +699,37 @@ struct Leaf2Args {
     unsigned long long *counter;   // dynamic task counter, zeroed per launch
 };
 
+#ifndef LEAF2_JMP
+#define LEAF2_JMP 1
+#endif
+#ifndef LEAF2_ROWS
+#define LEAF2_ROWS 1        // rows per iteration, real kinds (A/B on config 4: 1 > 2)
+#endif
+#ifndef LEAF2_ROWS_CPLX
+#define LEAF2_ROWS_CPLX 2   // rows per iteration, oscillatory (A/B on config 5: 2 > 1)
+#endif
+#ifndef LEAF2_MINB
+#define LEAF2_MINB 3
+#endif
+
 template <bool CPLX, int NJ, bool SMEM>
-__global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
+__device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
+                                                int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
+                                                const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
+    double2 f[NJ], g[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        f[j] = SMEM ? Fr[kp * NJ + j] : __ldg(Fr + kp * NJ + j);
+        g[j] = CPLX ? (SMEM ? Fi[kp * NJ + j] : __ldg(Fi + kp * NJ + j)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int jm = 0; jm < NJ; ++jm) leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], sg[jm], ah[jm], al[jm]);
+}
+
+template <bool CPLX, int NJ, bool SMEM>
+__global__ void __launch_bounds__(PASS_THREADS, LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int d = P.d;
@@ -744,6 +773,48 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPla
         }
         const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
         dd lane_sum = {0.0, 0.0};
+#if LEAF2_JMP
+        // all NJ mid prefixes of the lane at once: NJ independent accumulator chains that share
+        // every row load (ILP x NJ, shared-memory loads / leaf / NJ)
+        dd er[NJ], ei[NJ];
+        double sg[NJ], ah[NJ], al[NJ];
+#pragma unroll
+        for (int jm = 0; jm < NJ; ++jm) {
+            const double2 f = Fr[km * NJ + jm];
+            if (CPLX) {
+                const double2 g = Fi[km * NJ + jm];
+                cdd c = cdd_mul(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
+                er[jm] = c.re;
+                ei[jm] = c.im;
+            } else {
+                er[jm] = dd_mul(pr, dd{f.x, f.y});
+                ei[jm] = dd{0.0, 0.0};
+            }
+            const double bound = (fabs(er[jm].hi) + (CPLX ? fabs(ei[jm].hi) : 0.0)) * sa;
+            int ex = 0;
+            frexp(2.0 * bound, &ex);
+            sg[jm] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+            ah[jm] = al[jm] = 0.0;
+        }
+        int kp = km + 1;
+        while (kp < d) {
+            const int ke = min(d, kp + FOLD);
+            constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
+            for (; kp + RW - 1 < ke; kp += RW) {
+#pragma unroll
+                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM>(Fr, Fi, kp + r, er, ei, sg, ah, al);
+            }
+            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM>(Fr, Fi, kp, er, ei, sg, ah, al);
+#pragma unroll
+            for (int jm = 0; jm < NJ; ++jm) {
+                const double t = (al[jm] + sg[jm]) - sg[jm];
+                ah[jm] += t;
+                al[jm] -= t;
+            }
+        }
+#pragma unroll
+        for (int jm = 0; jm < NJ; ++jm) lane_sum = dd_add(lane_sum, dd_from_sum(ah[jm], al[jm]));
+#else
 #pragma unroll 1
         for (int jm = 0; jm < NJ; ++jm) {
             const double2 f = Fr[km * NJ + jm];
@@ -776,6 +847,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf2(const DevPla
             }
             lane_sum = dd_add(lane_sum, dd_from_sum(ah[0], al[0]));
         }
+#endif
         dd v = warp_reduce_dd(valid ? lane_sum : dd{0.0, 0.0});
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);
@@ -940,9 +1012,11 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     sg_plan_s *p = new (std::nothrow) sg_plan_s();
     if (!p) return SG_ENOMEM;
     {
-        const char *nf = getenv("SG_B200_NOFUSE");
+        // SG_B200_NOFUSE=1 / SG_B200_FUSE=1 override the automatic choice (tests, A/B runs)
+        const char *nf = getenv("SG_B200_NOFUSE"), *fu = getenv("SG_B200_FUSE");
+        const int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
         rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
-                             o.range_lo, o.range_hi, !(nf && nf[0] == '1'));
+                             o.range_lo, o.range_hi, mode);
     }
     if (rc) {
         delete p;

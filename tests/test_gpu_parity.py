@@ -188,7 +188,7 @@ def test_errors_and_nonfinite(api):
     p.close()
 
 
-# every last-pass kernel variant must agree with the oracle: fused k_leaf2 (default), stored
+# every last-pass kernel variant must agree with the oracle: fused k_leaf2 (SG_B200_FUSE=1), stored
 # frontier + k_leaf1 (SG_B200_NOFUSE=1), stored frontier + generic k_leaf (+ SG_B200_GENERIC_LEAF=1)
 @pytest.mark.parametrize("mode", ["fused", "nofuse", "generic"])
 @pytest.mark.parametrize("seed,d,L,rule,kind", [
@@ -196,6 +196,8 @@ def test_errors_and_nonfinite(api):
     (63, 33, 4, S.RULE_GL, S.KIND_PEAK), (64, 9, 5, S.RULE_GL, S.KIND_OSC),
     (65, 200, 3, S.RULE_GL, S.KIND_EXP)])
 def test_last_pass_variants(api, monkeypatch, mode, seed, d, L, rule, kind):
+    if mode == "fused":
+        monkeypatch.setenv("SG_B200_FUSE", "1")
     if mode in ("nofuse", "generic"):
         monkeypatch.setenv("SG_B200_NOFUSE", "1")
     if mode == "generic":
@@ -205,6 +207,8 @@ def test_last_pass_variants(api, monkeypatch, mode, seed, d, L, rule, kind):
 
 @pytest.mark.parametrize("mode", ["fused", "nofuse"])
 def test_config5_sampled_variants(api, monkeypatch, mode):
+    if mode == "fused":
+        monkeypatch.setenv("SG_B200_FUSE", "1")
     if mode == "nofuse":
         monkeypatch.setenv("SG_B200_NOFUSE", "1")
     check(api, S.baseline_config(5), range_lo=9400, range_hi=9520)
