@@ -21,6 +21,8 @@ RULE_CC = 2
 RULE_GL = 4
 KIND_EXP, KIND_OSC, KIND_PEAK, KIND_GAUSS = 0, 1, 2, 3
 FORM_COMBINATION, FORM_DELTA = 0, 1
+ARITH_FACTOR_DD, ARITH_SFORM_FP64 = 0, 1   # s-form = ablation (FP64 partial sums + FP64 exp/cos)
+ARITH_FACTOR_DD, ARITH_SFORM_FP64 = 0, 1
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
@@ -44,7 +46,8 @@ class Plan:
 
     def __init__(self, d: int, q: int, rule: int, kind: int, c, w=None, u: float = 0.0,
                  form: int = FORM_COMBINATION, rank: int = 0, world: int = 1,
-                 range_lo: int = 0, range_hi: int = -1, device=None):
+                 range_lo: int = 0, range_hi: int = -1, device=None,
+                 arith: int = ARITH_FACTOR_DD):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2210_14313_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
@@ -53,7 +56,7 @@ class Plan:
         self._w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
         self.u = float(u)
         desc = self._desc(self._c, self._w, self.u)
-        opts = sg_options(int(form), 0, int(rank), int(world), int(range_lo), int(range_hi))
+        opts = sg_options(int(form), int(arith), int(rank), int(world), int(range_lo), int(range_hi))
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(lib().sg_plan(self.d, self.q, self.rule, ctypes.byref(desc), ctypes.byref(opts),

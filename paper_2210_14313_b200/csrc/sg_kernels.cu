@@ -43,6 +43,7 @@ struct DevPlan {
     double *base;   // re.hi, re.lo, im.hi, im.lo
     double *SA;     // [(L+2) x (d+1)] suffix sums of |F| per level (k_leaf's accumulation bound)
     int *status;
+    int sform;      // SG_ARITH_SFORM_FP64 ablation: base[0] holds the argument S, not the value
 };
 
 struct PassArgs {
@@ -856,6 +857,158 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_MINB) k_leaf2(const DevPla
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// s-form ablation (SG_ARITH_SFORM_FP64): the literal "partial sums carried one
+// coordinate at a time, outer function applied in FP64 at the leaf" design.  A node carries
+// delta = sum_active a_k(x_k) in FP64 and its weight product W in dd; a leaf evaluates
+// g = exp(S + delta') (exp, Gaussian) or cos(theta + delta') (oscillatory) with CUDA's FP64 exp/cos
+// and accumulates c(e) W' g in dd.  Tables reuse the factor-table slots: Fre[idx] = weight (dd),
+// Fim[idx] = (a, 0); base[0..1] = S or theta (dd).  Not parity-grade on ill-conditioned configs
+// — it exists to measure what per-point FP64 transcendentals cost and lose.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_factor_s(const DevPlan P) {
+    const int n_ent = P.tab_off[P.L + 2];
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_ent) return;
+    int l = 2;
+    while (l < P.L + 1 && idx >= P.tab_off[l + 1]) ++l;
+    const int r = idx - P.tab_off[l], n = P.nl[l];
+    const int k = r / n, j = r - k * n;
+    const double x = P.X[P.entry_off[l] + j];
+    const double ck = P.c[k];
+    double a;
+    if (P.kind == SG_F_GAUSSIAN) {
+        const double wk = P.w[k];
+        a = -(ck * ck) * ((x - wk) * (x - wk) - (0.5 - wk) * (0.5 - wk));
+    } else {
+        a = ck * (x - 0.5);
+    }
+    P.Fre[idx] = make_double2(P.Whi[P.entry_off[l] + j], P.Wlo[P.entry_off[l] + j]);
+    P.Fim[idx] = make_double2(a, 0.0);
+    if (!isfinite(a)) atomicOr(P.status, 1);
+}
+
+__global__ void k_base_s(const DevPlan P) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int k = 0; k < P.d; ++k) {
+        const double ck = P.c[k];
+        if (P.kind == SG_F_GAUSSIAN) s -= ck * ck * (0.5 - P.w[k]) * (0.5 - P.w[k]);
+        else s += 0.5 * ck;
+    }
+    if (P.kind == SG_F_OSCILLATORY) s += 2.0 * M_PI * P.u[0];
+    P.base[0] = s;
+    P.base[1] = 0.0;
+    P.base[2] = 0.0;
+    P.base[3] = 0.0;
+}
+
+__device__ __forceinline__ double sform_g(int kind, double arg) {
+    return kind == SG_F_OSCILLATORY ? cos(arg) : exp(arg);
+}
+
+__global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs R) {
+    const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    dd tot = {0.0, 0.0};
+    if (r1 < R.hi) {
+        const int k1 = (int)(r1 / P.M0);
+        int rem = (int)(r1 - (long long)k1 * P.M0);
+        int l1 = 2;
+        while (rem >= P.nl[l1]) {
+            rem -= P.nl[l1];
+            ++l1;
+        }
+        const int j1 = rem;
+        const int ti = P.tab_off[l1] + k1 * P.nl[l1] + j1;
+        const double2 wv = P.Fre[ti];
+        const double delta = P.Fim[ti].x;
+        const dd W = {wv.x, wv.y};
+        const int b1 = l1 - 1;
+        tot = dd_mul_d(dd_mul_d(W, sform_g(P.kind, P.base[0] + delta)), P.coef[b1]);
+        if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
+            const long long seg = (long long)b1 * P.d + k1;
+            const long long o = R.off1[seg] + j1 - R.JS[seg];
+            R.dst_re[o] = wv;
+            R.dst_im[o] = make_double2(delta, 0.0);
+            R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+        }
+    }
+    dd s = block_reduce_dd<8>(tot);
+    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const PassArgs A) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long task = (long long)blockIdx.x * WPB + wib;
+    dd tot = {0.0, 0.0};
+    if (task < A.ntasks) {
+        const int d = P.d, L = P.L;
+        const long long chunk = task / A.nsplit;
+        const int split = (int)(task - chunk * A.nsplit);
+        const long long g = chunk * 32 + lane;
+        const bool valid = g < A.nsrc;
+        int b = L, k = d;
+        dd W = {0.0, 0.0};
+        double delta = 0.0;
+        if (valid) {
+            const uint32_t m = A.src_meta[g];
+            b = (int)(m >> SG_META_KBITS);
+            k = (int)(m & META_KMASK);
+            const double2 v = A.src_re[g];
+            W = dd{v.x, v.y};
+            delta = A.src_im[g].x;
+        }
+        const int ks0 = (int)((long long)split * d / A.nsplit);
+        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
+        const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
+        const int bmin = __reduce_min_sync(0xffffffffu, b);
+        long long iseg = 0, Nseg = 0, Cseg = 0;
+        if (WRITE && valid) {
+            const long long s = (long long)b * d + k;
+            iseg = g - A.offT[s];
+            Nseg = A.NT[s];
+            Cseg = A.CT[s];
+        }
+        const double S = P.base[0];
+        const int kb = max(ks0, kmin + 1);
+        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
+            const bool lv = valid && (lp <= L + 1 - b);
+            const int n = P.nl[lp];
+            const int bp = b + lp - 1;
+            const double2 *Wt = P.Fre + P.tab_off[lp];
+            const double2 *At = P.Fim + P.tab_off[lp];
+            const bool wr = WRITE && lv && (bp <= L - 1);
+            const long long wbase = (long long)n * Cseg + iseg;
+            double ah = 0.0, al = 0.0;
+            for (int kp = kb; kp < ks1; ++kp) {
+                const bool kv = lv && (kp > k);
+                const bool wk = wr && kv && (kp <= d - 2);
+                long long tb = 0;
+                if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
+                for (int j = 0; j < n; ++j) {
+                    const double2 wv = __ldg(Wt + kp * n + j);
+                    const double dl = delta + __ldg(At + kp * n + j).x;           // FP64 partial sum
+                    const dd Wc = dd_mul(W, dd{wv.x, wv.y});
+                    const double gv = kv ? sform_g(P.kind, S + dl) : 0.0;       // FP64 outer function
+                    double p, e;
+                    dd_mul_pe(Wc, dd{gv, 0.0}, p, e);
+                    acc_add(ah, al, p, e);
+                    if (WRITE && wk) {
+                        const long long o = tb + (long long)j * Nseg;
+                        A.dst_re[o] = make_double2(Wc.hi, Wc.lo);
+                        A.dst_im[o] = make_double2(dl, 0.0);
+                        A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                    }
+                }
+            }
+            if (lv) tot = dd_add(tot, dd_mul_d(dd_norm(ah, al), P.coef[bp]));
+        }
+    }
+    dd s = block_reduce_dd<WPB>(tot);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
 // One CTA per level: chunked row sums, a serial suffix scan over the 256 chunk sums, then each
 // thread writes the suffix values of its chunk (all loads in parallel; deterministic order).
@@ -915,7 +1068,10 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
     for (long long i = threadIdx.x; i < n; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
     s = block_reduce_dd<32>(s);
     if (threadIdx.x == 0) {
-        if (include_root && P.coef[0] != 0.0) s = dd_add(s, dd_mul_d(dd{P.base[0], P.base[1]}, P.coef[0]));
+        if (include_root && P.coef[0] != 0.0) {
+            const dd root = P.sform ? dd{sform_g(P.kind, P.base[0]), 0.0} : dd{P.base[0], P.base[1]};
+            s = dd_add(s, dd_mul_d(root, P.coef[0]));
+        }
         if (*P.status) s = dd{nan(""), nan("")};
         out[0] = s.hi;
         out[1] = s.lo;
@@ -938,6 +1094,8 @@ struct sg_plan_s {
     HostPlan hp;
     DevPlan dp;
     bool cplx = false;
+    bool sform = false;        // SG_ARITH_SFORM_FP64 ablation kernels
+    bool two = false;          // frontier layout with a second double2 array (complex or s-form)
     // plan-owned device memory
     void *dev_block = nullptr;
     size_t dev_bytes = 0;
@@ -1008,13 +1166,15 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             if (f->c[k] == 0.0) return SG_EINVAL;
     sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
     if (opt) o = *opt;
-    if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
+    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
+    if (o.arith == SG_ARITH_SFORM_FP64 && f->kind == SG_F_PRODUCT_PEAK) return SG_EUNSUPPORTED;
     sg_plan_s *p = new (std::nothrow) sg_plan_s();
     if (!p) return SG_ENOMEM;
     {
         // SG_B200_NOFUSE=1 / SG_B200_FUSE=1 override the automatic choice (tests, A/B runs)
         const char *nf = getenv("SG_B200_NOFUSE"), *fu = getenv("SG_B200_FUSE");
-        const int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
+        int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
+        if (o.arith == SG_ARITH_SFORM_FP64) mode = 0;
         rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
                              o.range_lo, o.range_hi, mode);
     }
@@ -1024,6 +1184,9 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     HostPlan &hp = p->hp;
     p->cplx = (f->kind == SG_F_OSCILLATORY);
+    p->sform = (o.arith == SG_ARITH_SFORM_FP64);
+    p->two = p->cplx || p->sform;
+    if (p->sform) p->leaf1 = false;
     {
         const char *g = getenv("SG_B200_GENERIC_LEAF");
         p->leaf1 = !(g && g[0] == '1');
@@ -1063,7 +1226,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     const size_t ow = carve(sizeof(double) * d);
     const size_t ou = carve(sizeof(double));
     const size_t oFr = carve(sizeof(double2) * std::max(hp.tab_entries, 1));
-    const size_t oFi = carve(p->cplx ? sizeof(double2) * std::max(hp.tab_entries, 1) : 0);
+    const size_t oFi = carve(p->two ? sizeof(double2) * std::max(hp.tab_entries, 1) : 0);
     const size_t oB = carve(sizeof(double) * 4);
     const size_t oS = carve(sizeof(int) * 4);
     const size_t oT = carve(sizeof(long long) * tabs.size());
@@ -1097,7 +1260,8 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     dp.w = (const double *)(base + ow);
     dp.u = (const double *)(base + ou);
     dp.Fre = (double2 *)(base + oFr);
-    dp.Fim = p->cplx ? (double2 *)(base + oFi) : nullptr;
+    dp.Fim = p->two ? (double2 *)(base + oFi) : nullptr;
+    dp.sform = p->sform ? 1 : 0;
     dp.base = (double *)(base + oB);
     dp.status = (int *)(base + oS);
     p->d_tabs = (long long *)(base + oT);
@@ -1129,7 +1293,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     // ---- workspace layout ----
     size_t ws = 0;
-    const size_t rec = p->cplx ? 2 * sizeof(double2) : sizeof(double2);
+    const size_t rec = p->two ? 2 * sizeof(double2) : sizeof(double2);
     for (int par = 0; par < 2; ++par) {
         p->ws_front_off[par] = ws;
         ws = align_up(ws + (size_t)hp.ws_front_cap[par] * (rec + sizeof(uint32_t)) + 1024, 256);
@@ -1191,7 +1355,7 @@ static int setup_leaf1(sg_plan_s *p) {
     HostPlan &hp = p->hp;
     p->leaf1_t = -1;
     p->leaf2 = false;
-    if (hp.nfront < 1) return SG_OK;
+    if (hp.nfront < 1 || p->sform) return SG_OK;
     const int t = hp.nfront, nj = hp.nl[2];
     if (hp.fuse) {
         p->leaf2 = true;
@@ -1256,8 +1420,8 @@ static void front_ptrs(sg_plan_s *p, int t, double2 *&re, double2 *&im, uint32_t
     const int64_t cap = p->hp.ws_front_cap[par];
     char *b = p->ws + p->ws_front_off[par];
     re = (double2 *)b;
-    im = p->cplx ? (double2 *)(b + sizeof(double2) * cap) : nullptr;
-    meta = (uint32_t *)(b + (p->cplx ? 2 : 1) * sizeof(double2) * cap);
+    im = p->two ? (double2 *)(b + sizeof(double2) * cap) : nullptr;
+    meta = (uint32_t *)(b + (p->two ? 2 : 1) * sizeof(double2) * cap);
 }
 
 extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
@@ -1275,11 +1439,16 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     mark();
     // K0
     if (hp.tab_entries > 0) {
-        k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-        k_suffix_abs<<<hp.L, 256, 0, st>>>(dp);
+        if (p->sform) {
+            k_factor_s<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+        } else {
+            k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+            k_suffix_abs<<<hp.L, 256, 0, st>>>(dp);
+        }
     }
     mark();
-    k_base<<<1, 256, 0, st>>>(dp);
+    if (p->sform) k_base_s<<<1, 32, 0, st>>>(dp);
+    else k_base<<<1, 256, 0, st>>>(dp);
     mark();
     // root pass
     RootArgs R;
@@ -1290,7 +1459,9 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     R.JS = p->d_tabs + p->tab_JS;
     if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
     R.partials = partials;
-    if (p->cplx)
+    if (p->sform)
+        k_root_s<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    else if (p->cplx)
         k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
     else
         k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
@@ -1345,7 +1516,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         // single-level last pass (every source has excess L-1): specialised k_leaf1
         const int n2 = hp.nl[2];
         const bool single = !write && t == p->leaf1_t;
-        if (p->cplx) {
+        if (p->sform) {
+            if (write) k_pass_s<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            else k_pass_s<false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+        } else if (p->cplx) {
             if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
             else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, st); }
             else k_leaf<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
@@ -1431,18 +1605,18 @@ extern "C" int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms
 
 extern "C" int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host) {
     if (!p) return SG_EINVAL;
-    const size_t per = p->cplx ? 4 : 2, n = (size_t)p->hp.tab_entries;
+    const size_t per = p->two ? 4 : 2, n = (size_t)p->hp.tab_entries;
     if (table_host) {
         if (table_doubles < n * per) return SG_EINVAL;
-        std::vector<double2> re(n), im(p->cplx ? n : 0);
+        std::vector<double2> re(n), im(p->two ? n : 0);
         if (cudaMemcpy(re.data(), p->dp.Fre, sizeof(double2) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
             return SG_ECUDA;
-        if (p->cplx && cudaMemcpy(im.data(), p->dp.Fim, sizeof(double2) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (p->two && cudaMemcpy(im.data(), p->dp.Fim, sizeof(double2) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
             return SG_ECUDA;
         for (size_t i = 0; i < n; ++i) {
             table_host[i * per + 0] = re[i].x;
             table_host[i * per + 1] = re[i].y;
-            if (p->cplx) {
+            if (p->two) {
                 table_host[i * per + 2] = im[i].x;
                 table_host[i * per + 3] = im[i].y;
             }
@@ -1460,7 +1634,7 @@ extern "C" int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_
     if (d < 1 || q < d) return SG_EINVAL;
     sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
     if (opt) o = *opt;
-    if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
+    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
     HostPlan hp;
     int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, o.rank, o.world,
                              o.range_lo, o.range_hi);
