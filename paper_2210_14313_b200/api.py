@@ -148,6 +148,29 @@ class Plan:
                                     base.ctypes.data_as(dp)), "sg_debug_tables")
         return buf.reshape(nd1, ncplx), base
 
+    def capture_graph(self):
+        """Capture one whole step (sg_integrate + sg_finalize(world=1)) into a CUDA graph.
+
+        Returns the torch.cuda.CUDAGraph; ``graph.replay()`` re-runs the step with ~one launch of
+        CPU overhead (the small configs are launch-latency bound).  The result lands in the
+        tensor returned by ``result()``.  Profiling events must be off while capturing."""
+        self.profile_enable(False)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.sg_finalize(self.sg_integrate(side), 1, side)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.sg_integrate()
+            self.sg_finalize(out, 1)
+        return g
+
+    def result(self) -> torch.Tensor:
+        """Device tensor [value, residual] written by sg_finalize (default output buffer)."""
+        return self._res
+
     def profile_enable(self, on: bool = True):
         check(lib().sg_profile_enable(self._h, int(bool(on))), "sg_profile_enable")
 

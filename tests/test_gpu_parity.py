@@ -212,3 +212,20 @@ def test_config5_sampled_variants(api, monkeypatch, mode):
     if mode == "nofuse":
         monkeypatch.setenv("SG_B200_NOFUSE", "1")
     check(api, S.baseline_config(5), range_lo=9400, range_hi=9520)
+
+
+@pytest.mark.parametrize("i", [1, 2, 3])
+def test_cuda_graph_replay_bitwise(api, i):
+    """A captured step (CUDA graph) replays to the same bits as the eager step."""
+    import torch
+    p = S.baseline_config(i)
+    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+    eager = plan.integrate_host()
+    g = plan.capture_graph()
+    for _ in range(3):
+        plan.result().zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        r = plan.result().cpu().numpy()
+        assert (float(r[0]), float(r[1])) == eager
+    plan.close()

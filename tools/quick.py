@@ -16,6 +16,10 @@ from paper_2210_14313_b200 import api  # noqa: E402
 mp.mp.dps = 50
 
 
+def tp_small(plan):
+    return plan.points()[1] < 10 ** 9
+
+
 def main():
     cfgs = [int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,3,4,5".split(","))]
     for i in cfgs:
@@ -38,6 +42,16 @@ def main():
             times.append(ev0.elapsed_time(ev1))
         prof = plan.profile_read()
         ms = min(times)
+        if tp_small(plan):
+            g = plan.capture_graph()
+            gt = []
+            for _ in range(10):
+                ev0.record()
+                g.replay()
+                ev1.record()
+                torch.cuda.synchronize()
+                gt.append(ev0.elapsed_time(ev1))
+            print(f"   cuda-graph step (integrate+finalize): min {min(gt):.4f} ms")
         print(f"   launches(ms): {[round(x, 4) for x in prof]}  all={[round(x, 3) for x in times]}")
         sp, tp = plan.points()
         print(f"{p.name}: value={hi!r} rel_err_vs_DP={float(err):.3e} plan={tplan*1e3:.1f}ms "
