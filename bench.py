@@ -140,7 +140,9 @@ def oracle_sample_range(p: S.Problem, target_points: int):
 
 def run_oracle_sample(p, lo, hi):
     import oracle
-    r = oracle.integrate_problem(p, lo=lo, hi=hi, include_root=False, eval_mode=1)
+    # all host cores, explicitly: torchrun sets OMP_NUM_THREADS=1 for its ranks
+    r = oracle.integrate_problem(p, lo=lo, hi=hi, include_root=False, eval_mode=1,
+                                 nthreads=os.cpu_count())
     return r
 
 
@@ -185,6 +187,11 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
+    # through host memory and every rank may share one device (ranks never wait on each other
+    # inside a kernel, so sharing is safe); the product configuration is nccl + one GPU per rank
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--device-index", type=int, default=None)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,9 +211,13 @@ def main():
 
     if rank == 0 or world == 1:
         B.build()
+    local = local if args.device_index is None else args.device_index
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         dist.barrier()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
@@ -223,7 +234,12 @@ def main():
     def step():
         part = plan.sg_integrate(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, part)
+            if args.dist_backend == "nccl":
+                dist.all_gather_into_tensor(gathered, part)
+            else:
+                g = torch.zeros(2 * world, dtype=torch.float64)
+                dist.all_gather_into_tensor(g, part.cpu())
+                gathered.copy_(g)
             plan.sg_finalize(gathered, world, stream, result)
         else:
             plan.sg_finalize(part, 1, stream, result)
@@ -243,7 +259,8 @@ def main():
             torch.cuda.synchronize(dev)
             ms = e0.elapsed_time(e1)
             if world > 1:
-                t = torch.tensor([ms], dtype=torch.float64, device=dev)
+                t = torch.tensor([ms], dtype=torch.float64,
+                                 device=dev if args.dist_backend == "nccl" else "cpu")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             times.append(ms)

@@ -108,16 +108,75 @@ DD_HD cdd cdd_mul_dd(cdd a, dd b) { return cdd{dd_mul(a.re, b), dd_mul(a.im, b)}
 
 DD_HD dd dd_ldexp(dd a, int e) { return dd{ldexp(a.hi, e), ldexp(a.lo, e)}; }
 
+#ifdef __CUDACC__
+// Reciprocal constants for the Taylor series below (dd, from 60-digit values): multiplying by
+// them replaces the dd divisions of the Horner steps.
+// 1/n, n = 0..14 (index n), as dd (hi, lo)
+__device__ __constant__ double DD_INV_N[15][2] = {
+    {0.0, 0.0},
+    {1.0, 0.0},
+    {0.5, 0.0},
+    {0.3333333333333333, 1.850371707708594e-17},
+    {0.25, 0.0},
+    {0.2, -1.1102230246251566e-17},
+    {0.16666666666666666, 9.25185853854297e-18},
+    {0.14285714285714285, 7.93016446160826e-18},
+    {0.125, 0.0},
+    {0.1111111111111111, 6.1679056923619804e-18},
+    {0.1, -5.551115123125783e-18},
+    {0.09090909090909091, -2.523234146875356e-18},
+    {0.08333333333333333, 4.625929269271485e-18},
+    {0.07692307692307693, -4.270088556250602e-18},
+    {0.07142857142857142, 3.96508223080413e-18}
+};
+// 1/((2n)(2n+1)) and 1/((2n-1)(2n)), n = 0..13
+__device__ __constant__ double DD_INV_SIN[14][2] = {
+    {0.0, 0.0},
+    {0.16666666666666666, 9.25185853854297e-18},
+    {0.05, -2.7755575615628915e-18},
+    {0.023809523809523808, 1.32169407693471e-18},
+    {0.013888888888888888, 7.709882115452476e-19},
+    {0.00909090909090909, 4.415659757031872e-19},
+    {0.00641025641025641, 2.2240044563805217e-19},
+    {0.004761904761904762, -4.295505750037808e-19},
+    {0.003676470588235294, 5.102127870520021e-20},
+    {0.0029239766081871343, 1.6231330769373633e-19},
+    {0.002380952380952381, -2.147752875018904e-19},
+    {0.001976284584980237, 1.3370398332627564e-19},
+    {0.0016666666666666668, -1.0697461435190311e-19},
+    {0.0014245014245014246, -7.104458680104445e-20}
+};
+__device__ __constant__ double DD_INV_COS[14][2] = {
+    {0.0, 0.0},
+    {0.5, 0.0},
+    {0.08333333333333333, 4.625929269271485e-18},
+    {0.03333333333333333, 4.625929269271486e-19},
+    {0.017857142857142856, 9.912705577010326e-19},
+    {0.011111111111111112, -4.2404351634988616e-19},
+    {0.007575757575757576, -2.1026951223961299e-19},
+    {0.005494505494505495, -4.2891514515910067e-19},
+    {0.004166666666666667, 5.782411586589357e-20},
+    {0.0032679738562091504, -9.920804192677818e-20},
+    {0.002631578947368421, 5.934580312552235e-20},
+    {0.0021645021645021645, 1.8774063592822588e-21},
+    {0.0018115942028985507, -2.199830494898125e-20},
+    {0.0015384615384615385, 1.3344026738283131e-21}
+};
+
+#define DD_DEV __device__ __forceinline__
+
+
 // exp(a): a = m ln2 + r, r /= 2^6, Taylor to r^14 (|r| < 5.5e-3 -> truncation < 1e-45),
 // then 6 squarings in expm1 form t <- 2t + t^2 (error growth x64), result (1 + t) 2^m.
-DD_HD dd dd_exp(dd a) {
+DD_DEV dd dd_exp(dd a) {
     if (a.hi == 0.0 && a.lo == 0.0) return dd{1.0, 0.0};
     double m = rint(a.hi / DD_LN2_HI);
     dd r = dd_sub(a, dd_add(dd_from_prod(m, DD_LN2_HI), dd_from_prod(m, DD_LN2_LO)));
     r = dd_ldexp(r, -6);
     // expm1(r) = r + r^2/2! + ... + r^14/14!  (Horner: r(1 + r/2(1 + r/3(...))))
     dd t = dd{1.0, 0.0};
-    for (int n = 14; n >= 2; --n) t = dd_add(dd{1.0, 0.0}, dd_div_d(dd_mul(r, t), (double)n));
+    for (int n = 14; n >= 2; --n)
+        t = dd_add(dd{1.0, 0.0}, dd_mul(dd_mul(r, t), dd{DD_INV_N[n][0], DD_INV_N[n][1]}));
     t = dd_mul(r, t);
     for (int i = 0; i < 6; ++i) t = dd_add(dd_ldexp(t, 1), dd_mul(t, t));
     dd e = dd_add(dd{1.0, 0.0}, t);
@@ -125,20 +184,20 @@ DD_HD dd dd_exp(dd a) {
 }
 
 // sin and cos of r with |r| <= pi/4 by Taylor series (terms to r^27: truncation < 1e-34).
-DD_HD void dd_sincos_small(dd r, dd &s, dd &c) {
+DD_DEV void dd_sincos_small(dd r, dd &s, dd &c) {
     dd r2 = dd_mul(r, r);
     // sin = r (1 - r2/(2*3) (1 - r2/(4*5) (1 - ...)))
     dd ts = dd{1.0, 0.0}, tc = dd{1.0, 0.0};
     for (int n = 13; n >= 1; --n) {
-        ts = dd_sub(dd{1.0, 0.0}, dd_div_d(dd_mul(r2, ts), (double)((2 * n) * (2 * n + 1))));
-        tc = dd_sub(dd{1.0, 0.0}, dd_div_d(dd_mul(r2, tc), (double)((2 * n - 1) * (2 * n))));
+        ts = dd_sub(dd{1.0, 0.0}, dd_mul(dd_mul(r2, ts), dd{DD_INV_SIN[n][0], DD_INV_SIN[n][1]}));
+        tc = dd_sub(dd{1.0, 0.0}, dd_mul(dd_mul(r2, tc), dd{DD_INV_COS[n][0], DD_INV_COS[n][1]}));
     }
     s = dd_mul(r, ts);
     c = tc;
 }
 
 // sin/cos of a dd argument: reduce by 2*pi (3-part), then by pi/2 to |r| <= pi/4.
-DD_HD void dd_sincos(dd a, dd &s, dd &c) {
+DD_DEV void dd_sincos(dd a, dd &s, dd &c) {
     double n2 = rint(a.hi / DD_2PI_0);
     dd x = a;
     if (n2 != 0.0) {
@@ -162,3 +221,4 @@ DD_HD void dd_sincos(dd a, dd &s, dd &c) {
     default: s = dd_neg(cc); c = ss; break;
     }
 }
+#endif  // __CUDACC__
