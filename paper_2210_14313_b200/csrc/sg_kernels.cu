@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const Pa
 // per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
 // ---------------------------------------------------------------------------------------------
 #ifndef FOLD
-#define FOLD 16
+#define FOLD 32   // rows between folds of acc_lo onto the grid
 #endif
 #ifndef LEAF_MINB
 #define LEAF_MINB 3
@@ -707,10 +707,13 @@ struct Leaf2Args {
 #define LEAF2_ROWS 1        // rows per iteration, real kinds (A/B on config 4: 1 > 2)
 #endif
 #ifndef LEAF2_ROWS_CPLX
-#define LEAF2_ROWS_CPLX 2   // rows per iteration, oscillatory (A/B on config 5: 2 > 1)
+#define LEAF2_ROWS_CPLX 4   // rows per iteration, oscillatory (A/B on config 5: 4 = 6 = 8 > 2 > 1)
 #endif
 #ifndef LEAF2_MINB
-#define LEAF2_MINB 3
+#define LEAF2_MINB 3        // CTAs/SM bound, real kinds (80 regs)
+#endif
+#ifndef LEAF2_MINB_CPLX
+#define LEAF2_MINB_CPLX 2   // CTAs/SM bound, oscillatory (108 regs, 16 warps/SM: 26.14 ms vs 27.52)
 #endif
 
 template <bool CPLX, int NJ, bool SMEM>
@@ -718,6 +721,9 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
                                                 const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
     double2 f[NJ], g[NJ];
+#ifdef LEAF2_FAKE_ROWS   // experiment only: same FP64 work on row 0 (upper bound without row loads)
+    kp = 0;
+#endif
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         f[j] = SMEM ? Fr[kp * NJ + j] : __ldg(Fr + kp * NJ + j);
@@ -730,7 +736,7 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
 }
 
 template <bool CPLX, int NJ, bool SMEM>
-__global__ void __launch_bounds__(PASS_THREADS, LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
+__global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int d = P.d;
