@@ -164,6 +164,16 @@ int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *op
                   unsigned long long *shard_points, unsigned long long *total_points,
                   long long *range_lo, long long *range_hi, int *n_passes);
 
+/* Host-only K1 unranker (north-star subsystem 1): the `index`-th Smolyak point of the shard
+ * described by (d, q, rule, kind, opt) in canonical order — the root (all-midpoint point) if the
+ * shard includes it and its coefficient is nonzero, then the depth-1 subtrees r1 = lo .. hi-1, each
+ * in preorder with children ordered by (k', l', j').  Outputs (host arrays of >= L entries): *t =
+ * number of active coordinates; k[m], l[m] >= 2, j[m] (0-based node index of level l[m]) for
+ * m < *t, ascending k; *coef = the point's Eq 2.6 coefficient (or 1 in the delta form).
+ * index >= shard points -> SG_EINVAL. */
+int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
+              unsigned long long index, int *t, int *k, int *l, int *j, double *coef);
+
 /* Host-only: the library's 1-D rule of `level` on [0,1] (n_l doubles each, ascending nodes),
  * rounded once from __float128 evaluations of Eq 2.11 / Eq 2.13.  Returns n_l, or a negative
  * status (SG_EINVAL bad rule/level, SG_EUNSUPPORTED above the table limits).  x, w: host arrays of

@@ -196,6 +196,21 @@ class Plan:
             pass
 
 
+def sg_unrank(d, q, rule, kind, index, form=FORM_COMBINATION, rank=0, world=1, range_lo=0,
+              range_hi=-1):
+    """Host-only K1 unranker: (coefficient, [(k, l, j), ...]) of the index-th Smolyak point of the
+    shard in canonical (root, then depth-1 subtrees in preorder) order.  No GPU needed."""
+    L = q - d
+    n = max(L, 1)
+    t = ctypes.c_int()
+    k, l, j = (ctypes.c_int * n)(), (ctypes.c_int * n)(), (ctypes.c_int * n)()
+    cf = ctypes.c_double()
+    o = sg_options(int(form), 0, int(rank), int(world), int(range_lo), int(range_hi))
+    check(lib().sg_unrank(d, q, rule, kind, ctypes.byref(o), int(index), ctypes.byref(t), k, l, j,
+                          ctypes.byref(cf)), "sg_unrank")
+    return cf.value, [(k[m], l[m], j[m]) for m in range(t.value)]
+
+
 def sg_plan(d, q, rule, kind, c, w=None, u=0.0, **kw) -> Plan:
     return Plan(d, q, rule, kind, c, w, u, **kw)
 

@@ -230,6 +230,9 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 sat_add(Suf[(size_t)b * (W + 1) + (k + 2)], Sub[(size_t)b * W + (k + 1)]);
     }
     const u128 total = Sub[0];
+    hp.Sub.assign(Sub.size(), 0);
+    for (size_t i = 0; i < Sub.size(); ++i)
+        hp.Sub[i] = Sub[i] >= ((u128)1 << 63) ? ~(uint64_t)0 : (uint64_t)Sub[i];
     if (total >= ((u128)1 << 63)) return SG_EOVERFLOW;
     hp.total_points = (uint64_t)total;
     const u128 root_w = hp.coef[0] != 0.0 ? 1 : 0;
@@ -411,5 +414,77 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         hp.ws_front_cap[par] = cap;
         hp.ws_front_bytes[par] = (size_t)cap * per_node;
     }
+    return SG_OK;
+}
+
+int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int *j, double *coef) {
+    if (index >= hp.shard_points) return SG_EINVAL;
+    const int d = hp.d, L = hp.L, W = d + 1;
+    auto sub = [&](int b, int kk) -> uint64_t { return hp.Sub[(size_t)b * W + (kk + 1)]; };
+    uint64_t r = index;
+    int depth = 0, b = 0, kl = -1;
+    // root
+    if (hp.include_root && hp.coef[0] != 0.0) {
+        if (r == 0) {
+            *t = 0;
+            *coef = hp.coef[0];
+            return SG_OK;
+        }
+        r -= 1;
+    }
+    // depth-1 subtrees of the shard's r1 range
+    bool found = false;
+    int64_t pos = 0;
+    for (int k1 = 0; k1 < d && !found; ++k1)
+        for (int l1 = 2; l1 <= L + 1 && !found; ++l1) {
+            const int64_t a = std::max<int64_t>(hp.range_lo, pos), e = std::min<int64_t>(hp.range_hi, pos + hp.nl[l1]);
+            if (e > a) {
+                const uint64_t s = sub(l1 - 1, k1);
+                const uint64_t blk = (uint64_t)(e - a) * s;
+                if (r < blk) {
+                    const int j1 = (int)(a - pos + (int64_t)(r / s));
+                    r %= s;
+                    k[0] = k1;
+                    l[0] = l1;
+                    j[0] = j1;
+                    depth = 1;
+                    b = l1 - 1;
+                    kl = k1;
+                    found = true;
+                } else {
+                    r -= blk;
+                }
+            }
+            pos += hp.nl[l1];
+        }
+    if (!found) return SG_EINVAL;
+    // descend in preorder
+    for (;;) {
+        if (hp.coef[b] != 0.0) {
+            if (r == 0) break;
+            r -= 1;
+        }
+        bool moved = false;
+        for (int kp = kl + 1; kp < d && !moved; ++kp)
+            for (int lp = 2; lp <= L + 1 - b && !moved; ++lp) {
+                const uint64_t s = sub(b + lp - 1, kp);
+                const uint64_t blk = (uint64_t)hp.nl[lp] * s;
+                if (r < blk) {
+                    k[depth] = kp;
+                    l[depth] = lp;
+                    j[depth] = (int)(r / s);
+                    r %= s;
+                    ++depth;
+                    b += lp - 1;
+                    kl = kp;
+                    moved = true;
+                } else {
+                    r -= blk;
+                }
+            }
+        if (!moved) return SG_EINVAL;   // inconsistent counts (cannot happen for a valid plan)
+    }
+    *t = depth;
+    *coef = hp.coef[b];
     return SG_OK;
 }

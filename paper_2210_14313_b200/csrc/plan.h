@@ -53,7 +53,15 @@ struct HostPlan {
     // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
     bool fuse = false;
     std::vector<int64_t> TK;           // [d + 1] prefix of fused tasks over k_mid
+    // Sub[b * (d + 1) + (k + 1)] = Smolyak points (nonzero coefficient) in the subtree of a node
+    // with excess b and last active coordinate k (k = -1: the root), the node itself included
+    std::vector<uint64_t> Sub;
 };
+
+// K1 unranker: the index-th Smolyak point of the plan's shard in canonical order (the root if the
+// shard includes it, then the depth-1 subtrees r1 = lo .. hi-1, each in preorder with children
+// ordered by (k', l', j')).  Writes the t active (k, l, j) triples and the Eq 2.6 coefficient.
+int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int *j, double *coef);
 
 // Build rules, counts, shard range and launch geometry. Returns an sg_status code.
 int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,

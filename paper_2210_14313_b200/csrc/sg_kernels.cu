@@ -1653,6 +1653,18 @@ extern "C" int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_
     return SG_OK;
 }
 
+extern "C" int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
+                         unsigned long long index, int *t, int *k, int *l, int *j, double *coef) {
+    if (d < 1 || q < d || !t || !k || !l || !j || !coef) return SG_EINVAL;
+    sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
+    if (opt) o = *opt;
+    HostPlan hp;
+    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, o.rank, o.world,
+                             o.range_lo, o.range_hi, 0);
+    if (rc) return rc;
+    return host_unrank(hp, index, t, k, l, j, coef);
+}
+
 extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
     if (!x || !w || level < 1) return SG_EINVAL;
     if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;

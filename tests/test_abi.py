@@ -117,3 +117,73 @@ def test_errors(L):
     assert _query(L, 1000, 1000 + 19, S.RULE_GL)[0] in (-2, -3)   # coefficient/size limits
     assert _query(L, 10 ** 5, 10 ** 5 + 8, S.RULE_CC)[0] in (-2, -3)
     assert L.sg_strerror(-3).decode().startswith("point")
+
+
+# ----------------------------------------------------------------------------------------------
+# K1 unranker (north-star subsystem 1): flat index -> multi-index, tensor point, coefficient
+# ----------------------------------------------------------------------------------------------
+def _brute_points(d, Lx, rule):
+    """Independent enumeration of Eq 2.6/2.7 points: every level vector in the band, every tensor
+    node index; returned as sparse tuples ((k, l, j), ...) of the active (level >= 2) coordinates."""
+    import itertools
+    pts = {}
+    for lv in itertools.product(range(1, Lx + 2), repeat=d):
+        e = sum(lv) - d
+        cf = pins.coef(d, Lx, e)
+        if cf == 0:
+            continue
+        act = [(kk, ll) for kk, ll in enumerate(lv) if ll >= 2]
+        for js in itertools.product(*[range(pins.node_count(rule, ll)) for _, ll in act]):
+            pts[tuple((kk, ll, jj) for (kk, ll), jj in zip(act, js))] = cf
+    return pts
+
+
+@pytest.mark.parametrize("d,Lx,rule", [(4, 4, S.RULE_CC), (5, 3, S.RULE_GL), (3, 5, S.RULE_CC),
+                                       (2, 6, S.RULE_GL), (6, 2, S.RULE_CC)])
+def test_unrank_is_a_bijection_in_lexicographic_order(L, d, Lx, rule):
+    from paper_2210_14313_b200 import api
+    brute = _brute_points(d, Lx, rule)
+    n = pins.n_points(rule, d, Lx)
+    assert len(brute) == n
+    seq = []
+    for i in range(n):
+        cf, trip = api.sg_unrank(d, d + Lx, rule, 0, i)
+        key = tuple(trip)
+        assert key in brute, (i, key)
+        assert cf == brute[key], (i, key)
+        seq.append(key)
+    assert len(set(seq)) == n                 # bijection
+    assert seq == sorted(seq)                 # canonical order = lexicographic (prefix first)
+    from paper_2210_14313_b200._lib import SGError
+    with pytest.raises(SGError):
+        api.sg_unrank(d, d + Lx, rule, 0, n)
+
+
+def test_unrank_full_size_config5_samples_and_shards(L):
+    from paper_2210_14313_b200 import api
+    p = S.baseline_config(5)
+    n = pins.n_points(p.rule, p.d, p.L)
+    rng = np.random.default_rng(9)
+    idx = np.sort(rng.integers(0, n, 300))
+    keys = []
+    for i in idx:
+        cf, trip = api.sg_unrank(p.d, p.q, p.rule, p.kind, int(i))
+        e = sum(l - 1 for _, l, _ in trip)
+        assert cf == pins.coef(p.d, p.L, e)
+        assert all(a[0] < b[0] for a, b in zip(trip, trip[1:]))
+        assert all(0 <= j < pins.node_count(p.rule, l) and 2 <= l for _, l, j in trip)
+        keys.append(tuple(trip))
+    assert keys == sorted(keys)
+    # shard r's points come from its own depth-1 range
+    world = 3
+    M0 = sum(pins.node_count(p.rule, l) for l in range(2, p.L + 2))
+    for r in range(world):
+        rc, sp, tp, lo, hi, _ = _query(L, p.d, p.q, p.rule, p.kind, rank=r, world=world)
+        for i in (0, sp // 2, sp - 1):
+            cf, trip = api.sg_unrank(p.d, p.q, p.rule, p.kind, int(i), rank=r, world=world)
+            if not trip:
+                assert r == 0 and i == 0      # the root belongs to rank 0
+                continue
+            k1, l1, j1 = trip[0]
+            r1 = k1 * M0 + sum(pins.node_count(p.rule, l) for l in range(2, l1)) + j1
+            assert lo <= r1 < hi
