@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const Pa
 // per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
 // ---------------------------------------------------------------------------------------------
 #ifndef FOLD
-#define FOLD 32   // rows between folds of acc_lo onto the grid
+#define FOLD 16   // rows between folds of acc_lo onto the grid (32: 0.3% faster, 150x larger error)
 #endif
 #ifndef LEAF_MINB
 #define LEAF_MINB 3
@@ -513,6 +513,9 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
             switch (n) {
             case 2: s = leaf_level<CPLX, 2>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             case 3: s = leaf_level<CPLX, 3>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
+#ifdef LEAF_NJ5
+            case 5: s = leaf_level<CPLX, 5>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
+#endif
             default: s = leaf_level<CPLX, 0>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             }
             if (lv) tot = dd_add(tot, dd_mul_d(s, P.coef[b + lp - 1]));
@@ -716,26 +719,40 @@ struct Leaf2Args {
 #define LEAF2_MINB_CPLX 2   // CTAs/SM bound, oscillatory (108 regs, 16 warps/SM: 26.14 ms vs 27.52)
 #endif
 
-template <bool CPLX, int NJ, bool SMEM>
+// Leaf term for a node whose factor is REAL (imaginary part exactly 0): the midpoint node x = 1/2 of
+// a level (E_k(1/2) = 1 for every kind, so F = w exactly real).  Re(P F) = P.re F: 7 FP64
+// instructions instead of 14 for the oscillatory kind; bitwise the same value the general formula
+// gives with F.im = 0 (every dropped term is an exact zero).
+__device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double sigma, double &ah,
+                                                      double &al) {
+    const double h = fma(er.hi, f.x, sigma) - sigma;
+    ah += h;
+    double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
+    c = fma(er.hi, f.y, c);
+    al += c;
+}
+
+// CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host.
+template <bool CPLX, int NJ, bool SMEM, int CJ>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
                                                 const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
     double2 f[NJ], g[NJ];
-#ifdef LEAF2_FAKE_ROWS   // experiment only: same FP64 work on row 0 (upper bound without row loads)
-    kp = 0;
-#endif
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         f[j] = SMEM ? Fr[kp * NJ + j] : __ldg(Fr + kp * NJ + j);
-        g[j] = CPLX ? (SMEM ? Fi[kp * NJ + j] : __ldg(Fi + kp * NJ + j)) : make_double2(0.0, 0.0);
+        g[j] = (CPLX && j != CJ) ? (SMEM ? Fi[kp * NJ + j] : __ldg(Fi + kp * NJ + j)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int jm = 0; jm < NJ; ++jm) leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], sg[jm], ah[jm], al[jm]);
+        for (int jm = 0; jm < NJ; ++jm) {
+            if (CPLX && j == CJ) leaf_real_factor_term(er[jm], f[j], sg[jm], ah[jm], al[jm]);
+            else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], sg[jm], ah[jm], al[jm]);
+        }
 }
 
-template <bool CPLX, int NJ, bool SMEM>
+template <bool CPLX, int NJ, bool SMEM, int CJ>
 __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -809,9 +826,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
             for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll
-                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM>(Fr, Fi, kp + r, er, ei, sg, ah, al);
+                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ>(Fr, Fi, kp + r, er, ei, sg, ah, al);
             }
-            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM>(Fr, Fi, kp, er, ei, sg, ah, al);
+            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ>(Fr, Fi, kp, er, ei, sg, ah, al);
 #pragma unroll
             for (int jm = 0; jm < NJ; ++jm) {
                 const double t = (al[jm] + sg[jm]) - sg[jm];
@@ -1116,6 +1133,7 @@ struct sg_plan_s {
     int leaf1_t = -1;          // pass index run by the persistent k_leaf1 / k_leaf2 (or -1)
     bool leaf2 = false;        // last two levels fused (hp.fuse): k_leaf2
     long long leaf1_grid = 0;  // persistent grid (resident CTAs) of k_leaf1 / k_leaf2
+    bool leaf2_center = false; // level-2 row has its midpoint at index 1 (real oscillatory factor)
     unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
@@ -1351,9 +1369,11 @@ static const void *leaf1_kernel(int nj, bool smem) {
 }
 
 template <bool CPLX>
-static const void *leaf2_kernel(int nj, bool smem) {
-    if (nj == 3) return smem ? (const void *)k_leaf2<CPLX, 3, true> : (const void *)k_leaf2<CPLX, 3, false>;
-    return smem ? (const void *)k_leaf2<CPLX, 2, true> : (const void *)k_leaf2<CPLX, 2, false>;
+static const void *leaf2_kernel(int nj, bool smem, bool center) {
+    if (nj == 3 && CPLX && center)
+        return smem ? (const void *)k_leaf2<CPLX, 3, true, 1> : (const void *)k_leaf2<CPLX, 3, false, 1>;
+    if (nj == 3) return smem ? (const void *)k_leaf2<CPLX, 3, true, -1> : (const void *)k_leaf2<CPLX, 3, false, -1>;
+    return smem ? (const void *)k_leaf2<CPLX, 2, true, -1> : (const void *)k_leaf2<CPLX, 2, false, -1>;
 }
 
 // Persistent geometry of the single-level last pass (k_leaf1, or the fused k_leaf2; once per plan).
@@ -1372,7 +1392,13 @@ static int setup_leaf1(sg_plan_s *p) {
     const size_t smem = (size_t)hp.d * nj * sizeof(double2) * (p->cplx ? 2 : 1);
     p->leaf1_smem = smem <= 56 * 1024 ? smem : 0;
     const bool sm = p->leaf1_smem > 0;
-    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm) : leaf2_kernel<false>(nj, sm))
+    // midpoint node of the level-2 row (x = 1/2 exactly -> its oscillatory factor is exactly real)
+    p->leaf2_center = (nj == 3 && hp.X[hp.entry_off[2] + 1] == 0.5);
+#ifdef LEAF2_NO_CENTER
+    p->leaf2_center = false;
+#endif
+    const bool ct = p->leaf2_center;
+    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct) : leaf2_kernel<false>(nj, sm, ct))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
@@ -1399,12 +1425,15 @@ template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
-    if (nj == 3) {
-        if (sm) k_leaf2<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 3, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    if (nj == 3 && CPLX && p->leaf2_center) {
+        if (sm) k_leaf2<CPLX, 3, true, 1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 3, false, 1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    } else if (nj == 3) {
+        if (sm) k_leaf2<CPLX, 3, true, -1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 3, false, -1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
     } else {
-        if (sm) k_leaf2<CPLX, 2, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 2, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+        if (sm) k_leaf2<CPLX, 2, true, -1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 2, false, -1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
     }
 }
 
