@@ -118,10 +118,13 @@ __global__ void k_factor(const DevPlan P) {
         Er = dd_exp(dd_mul_d(xm, ck));
         break;
     case SG_F_OSCILLATORY: {
-        dd s, co;
-        dd_sincos(dd_mul_d(xm, ck), s, co);
+        // sincos of |a| with the sign applied afterwards: nodes placed symmetrically about 1/2 get
+        // exactly conjugate factors (used by k_leaf2's symmetric-pair path)
+        dd a = dd_mul_d(xm, ck), s, co;
+        const bool neg = a.hi < 0.0;
+        dd_sincos(neg ? dd_neg(a) : a, s, co);
         Er = co;
-        Ei = s;
+        Ei = neg ? dd_neg(s) : s;
         break;
     }
     case SG_F_GAUSSIAN: {
@@ -732,11 +735,39 @@ __device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double
     al += c;
 }
 
-// CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host.
-template <bool CPLX, int NJ, bool SMEM, int CJ>
+// Symmetric pair (x_0 = 1 - x_2, w_0 = w_2; oscillatory): F_0 = conj(F_2) exactly, so the two
+// points' terms Re(P F_2) = A - B and Re(P F_0) = A + B share the products A = P.re F_2.re and
+// B = P.im F_2.im (their grid parts, remainders and cross terms); each point's term is still formed
+// and accumulated on its own.  18 FP64 instructions for the two points instead of 28.
+__device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, const double2 f, const double2 g,
+                                                    double sigma, double &ah, double &al) {
+    const double h1 = fma(er.hi, f.x, sigma) - sigma;
+    const double h2 = fma(ei.hi, g.x, sigma) - sigma;
+    const double cA = fma(er.lo, f.x, fma(er.hi, f.y, fma(er.hi, f.x, -h1)));
+    const double cB = fma(ei.lo, g.x, fma(ei.hi, g.y, fma(ei.hi, g.x, -h2)));
+    ah += h1 + h2;   // node 0: A + B
+    al += cA + cB;
+    ah += h1 - h2;   // node 2: A - B
+    al += cA - cB;
+}
+
+// CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
+// SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory).
+template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
                                                 const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
+    if constexpr (SYM && CPLX && NJ == 3 && CJ == 1) {
+        const double2 f2 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
+        const double2 g2 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
+        const double2 f1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
+#pragma unroll
+        for (int jm = 0; jm < 3; ++jm) {
+            leaf_sym_pair_terms(er[jm], ei[jm], f2, g2, sg[jm], ah[jm], al[jm]);
+            leaf_real_factor_term(er[jm], f1, sg[jm], ah[jm], al[jm]);
+        }
+        return;
+    }
     double2 f[NJ], g[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
@@ -752,7 +783,7 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
         }
 }
 
-template <bool CPLX, int NJ, bool SMEM, int CJ>
+template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false>
 __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -826,9 +857,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
             for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll
-                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ>(Fr, Fi, kp + r, er, ei, sg, ah, al);
+                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM>(Fr, Fi, kp + r, er, ei, sg, ah, al);
             }
-            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ>(Fr, Fi, kp, er, ei, sg, ah, al);
+            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM>(Fr, Fi, kp, er, ei, sg, ah, al);
 #pragma unroll
             for (int jm = 0; jm < NJ; ++jm) {
                 const double t = (al[jm] + sg[jm]) - sg[jm];
@@ -1134,6 +1165,7 @@ struct sg_plan_s {
     bool leaf2 = false;        // last two levels fused (hp.fuse): k_leaf2
     long long leaf1_grid = 0;  // persistent grid (resident CTAs) of k_leaf1 / k_leaf2
     bool leaf2_center = false; // level-2 row has its midpoint at index 1 (real oscillatory factor)
+    bool leaf2_sym = false;    // level-2 nodes 0 and 2 symmetric about 1/2 (conjugate factors)
     unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
@@ -1369,7 +1401,9 @@ static const void *leaf1_kernel(int nj, bool smem) {
 }
 
 template <bool CPLX>
-static const void *leaf2_kernel(int nj, bool smem, bool center) {
+static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym) {
+    if (nj == 3 && CPLX && center && sym)
+        return smem ? (const void *)k_leaf2<CPLX, 3, true, 1, true> : (const void *)k_leaf2<CPLX, 3, false, 1, true>;
     if (nj == 3 && CPLX && center)
         return smem ? (const void *)k_leaf2<CPLX, 3, true, 1> : (const void *)k_leaf2<CPLX, 3, false, 1>;
     if (nj == 3) return smem ? (const void *)k_leaf2<CPLX, 3, true, -1> : (const void *)k_leaf2<CPLX, 3, false, -1>;
@@ -1398,7 +1432,17 @@ static int setup_leaf1(sg_plan_s *p) {
     p->leaf2_center = false;
 #endif
     const bool ct = p->leaf2_center;
-    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct) : leaf2_kernel<false>(nj, sm, ct))
+    {
+        // symmetric pair: x_0 + x_2 == 1 and equal weights, exactly
+        const int e0 = hp.entry_off[2];
+        p->leaf2_sym = ct && p->cplx && hp.X[e0] + hp.X[e0 + 2] == 1.0 && hp.Whi[e0] == hp.Whi[e0 + 2] &&
+                       hp.Wlo[e0] == hp.Wlo[e0 + 2];
+#ifdef LEAF2_NO_SYM
+        p->leaf2_sym = false;
+#endif
+    }
+    const bool sy = p->leaf2_sym;
+    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy) : leaf2_kernel<false>(nj, sm, ct, sy))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
@@ -1425,7 +1469,10 @@ template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
-    if (nj == 3 && CPLX && p->leaf2_center) {
+    if (nj == 3 && CPLX && p->leaf2_center && p->leaf2_sym) {
+        if (sm) k_leaf2<CPLX, 3, true, 1, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf2<CPLX, 3, false, 1, true><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+    } else if (nj == 3 && CPLX && p->leaf2_center) {
         if (sm) k_leaf2<CPLX, 3, true, 1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
         else k_leaf2<CPLX, 3, false, 1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
     } else if (nj == 3) {
