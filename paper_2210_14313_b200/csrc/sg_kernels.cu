@@ -726,12 +726,14 @@ struct Leaf2Args {
 // a level (E_k(1/2) = 1 for every kind, so F = w exactly real).  Re(P F) = P.re F: 7 FP64
 // instructions instead of 14 for the oscillatory kind; bitwise the same value the general formula
 // gives with F.im = 0 (every dropped term is an exact zero).
+// CZ: the factor's low part is exactly 0 (combination form: F = w * 1), its cross term drops.
+template <bool CZ = false>
 __device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double sigma, double &ah,
                                                       double &al) {
     const double h = fma(er.hi, f.x, sigma) - sigma;
     ah += h;
     double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
-    c = fma(er.hi, f.y, c);
+    if (!CZ) c = fma(er.hi, f.y, c);
     al += c;
 }
 
@@ -753,7 +755,7 @@ __device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, 
 
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
 // SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory).
-template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false>
+template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
                                                 const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
@@ -764,7 +766,7 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
 #pragma unroll
         for (int jm = 0; jm < 3; ++jm) {
             leaf_sym_pair_terms(er[jm], ei[jm], f2, g2, sg[jm], ah[jm], al[jm]);
-            leaf_real_factor_term(er[jm], f1, sg[jm], ah[jm], al[jm]);
+            leaf_real_factor_term<CZ>(er[jm], f1, sg[jm], ah[jm], al[jm]);
         }
         return;
     }
@@ -778,12 +780,12 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int jm = 0; jm < NJ; ++jm) {
-            if (CPLX && j == CJ) leaf_real_factor_term(er[jm], f[j], sg[jm], ah[jm], al[jm]);
+            if (j == CJ) leaf_real_factor_term<CZ>(er[jm], f[j], sg[jm], ah[jm], al[jm]);
             else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], sg[jm], ah[jm], al[jm]);
         }
 }
 
-template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false>
+template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
 __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -857,9 +859,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
             for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll
-                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM>(Fr, Fi, kp + r, er, ei, sg, ah, al);
+                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, sg, ah, al);
             }
-            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM>(Fr, Fi, kp, er, ei, sg, ah, al);
+            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, sg, ah, al);
 #pragma unroll
             for (int jm = 0; jm < NJ; ++jm) {
                 const double t = (al[jm] + sg[jm]) - sg[jm];
@@ -1166,6 +1168,7 @@ struct sg_plan_s {
     long long leaf1_grid = 0;  // persistent grid (resident CTAs) of k_leaf1 / k_leaf2
     bool leaf2_center = false; // level-2 row has its midpoint at index 1 (real oscillatory factor)
     bool leaf2_sym = false;    // level-2 nodes 0 and 2 symmetric about 1/2 (conjugate factors)
+    bool leaf2_cz = false;     // midpoint factor has an exactly zero low part (combination form)
     unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     std::vector<cudaEvent_t> ev;
@@ -1400,14 +1403,21 @@ static const void *leaf1_kernel(int nj, bool smem) {
     return smem ? (const void *)k_leaf1<CPLX, 2, true> : (const void *)k_leaf1<CPLX, 2, false>;
 }
 
+// Variant of k_leaf2 for this plan: NJ level-2 nodes, factor rows in smem or L1, midpoint index
+// (center), symmetric pair (sym, oscillatory only), midpoint factor with zero low part (cz).
+template <bool CPLX, bool SMEM>
+static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
+    if (nj == 3 && center) {
+        if (CPLX && sym) return cz ? (const void *)k_leaf2<CPLX, 3, SMEM, 1, true, true>
+                                   : (const void *)k_leaf2<CPLX, 3, SMEM, 1, true, false>;
+        return cz ? (const void *)k_leaf2<CPLX, 3, SMEM, 1, false, true> : (const void *)k_leaf2<CPLX, 3, SMEM, 1, false, false>;
+    }
+    if (nj == 3) return (const void *)k_leaf2<CPLX, 3, SMEM, -1>;
+    return (const void *)k_leaf2<CPLX, 2, SMEM, -1>;
+}
 template <bool CPLX>
-static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym) {
-    if (nj == 3 && CPLX && center && sym)
-        return smem ? (const void *)k_leaf2<CPLX, 3, true, 1, true> : (const void *)k_leaf2<CPLX, 3, false, 1, true>;
-    if (nj == 3 && CPLX && center)
-        return smem ? (const void *)k_leaf2<CPLX, 3, true, 1> : (const void *)k_leaf2<CPLX, 3, false, 1>;
-    if (nj == 3) return smem ? (const void *)k_leaf2<CPLX, 3, true, -1> : (const void *)k_leaf2<CPLX, 3, false, -1>;
-    return smem ? (const void *)k_leaf2<CPLX, 2, true, -1> : (const void *)k_leaf2<CPLX, 2, false, -1>;
+static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz) {
+    return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz) : leaf2_fn<CPLX, false>(nj, center, sym, cz);
 }
 
 // Persistent geometry of the single-level last pass (k_leaf1, or the fused k_leaf2; once per plan).
@@ -1427,7 +1437,7 @@ static int setup_leaf1(sg_plan_s *p) {
     p->leaf1_smem = smem <= 56 * 1024 ? smem : 0;
     const bool sm = p->leaf1_smem > 0;
     // midpoint node of the level-2 row (x = 1/2 exactly -> its oscillatory factor is exactly real)
-    p->leaf2_center = (nj == 3 && hp.X[hp.entry_off[2] + 1] == 0.5);
+    p->leaf2_center = (nj == 3 && hp.X[hp.entry_off[2] + 1] == 0.5);   // any kind
 #ifdef LEAF2_NO_CENTER
     p->leaf2_center = false;
 #endif
@@ -1442,7 +1452,9 @@ static int setup_leaf1(sg_plan_s *p) {
 #endif
     }
     const bool sy = p->leaf2_sym;
-    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy) : leaf2_kernel<false>(nj, sm, ct, sy))
+    p->leaf2_cz = ct && hp.Wlo[hp.entry_off[2] + 1] == 0.0;
+    const bool cz = p->leaf2_cz;
+    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy, cz) : leaf2_kernel<false>(nj, sm, ct, sy, cz))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
@@ -1469,19 +1481,11 @@ template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
-    if (nj == 3 && CPLX && p->leaf2_center && p->leaf2_sym) {
-        if (sm) k_leaf2<CPLX, 3, true, 1, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 3, false, 1, true><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
-    } else if (nj == 3 && CPLX && p->leaf2_center) {
-        if (sm) k_leaf2<CPLX, 3, true, 1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 3, false, 1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
-    } else if (nj == 3) {
-        if (sm) k_leaf2<CPLX, 3, true, -1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 3, false, -1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
-    } else {
-        if (sm) k_leaf2<CPLX, 2, true, -1><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf2<CPLX, 2, false, -1><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
-    }
+    const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz);
+    DevPlan dp = p->dp;
+    Leaf2Args a = A;
+    void *args[] = {&dp, &a};
+    cudaLaunchKernel(fn, dim3(grid), dim3(PASS_THREADS), args, sm, st);
 }
 
 template <bool CPLX>
