@@ -33,20 +33,9 @@ import numpy as np  # noqa: E402
 import sg_configs as S  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-# Algorithmic FP64 work per Smolyak point of the grid-split double-double leaf:
-# real kinds 7 FP64 instructions = 4 DFMA + 3 DADD = 11 flops; oscillatory 14 = 8 DFMA + 6 DADD = 22.
-# The midpoint node x = 1/2 of a level has an exactly real factor (E_k(1/2) = 1), so its
-# oscillatory leaf is the real one (7 instructions / 11 flops): for the Clenshaw-Curtis level-2
-# children of the dominant pass (nodes 0, 1/2, 1) the average is (22 + 11 + 22)/3 flops.
-FLOPS_PER_POINT = {S.KIND_EXP: 11, S.KIND_GAUSS: 11, S.KIND_PEAK: 11, S.KIND_OSC: 22}
-FP64_INST_PER_POINT = {S.KIND_EXP: 7, S.KIND_GAUSS: 7, S.KIND_PEAK: 7, S.KIND_OSC: 14}
-
-
-def leaf_work(p):
-    """(flops, FP64 instructions) per point of the dominant (level-2 leaf) kernel."""
-    if p.kind == S.KIND_OSC and p.rule == S.RULE_CC:
-        return (2 * 22 + 11) / 3, (2 * 14 + 7) / 3
-    return FLOPS_PER_POINT[p.kind], FP64_INST_PER_POINT[p.kind]
+# Algorithmic FP64 work per Smolyak point of the dominant leaf kernel comes from the library
+# (sg_plan_leaf_work: DFMA and DADD thread-instructions per point of the variant the plan runs;
+# DESIGN.md §6): flops = 2 DFMA + DADD, pipe slots = DFMA + DADD.
 # FP64 peak derived from the unit count and clock (DESIGN.md): 148 SMs x 64 FP64 FMA/clk x 2 flops
 # x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz) = 37.2 TFLOP/s.
 SM_COUNT = 148
@@ -307,7 +296,8 @@ def main():
         peak, mhz = peak_fp64_tflops()
         dom_ms = statistics.mean(dom)
         dom_terms = passes[dominant].terms
-        fpp, ipp = leaf_work(p)
+        fma_pp, add_pp = plan.leaf_work()
+        fpp, ipp = 2 * fma_pp + add_pp, fma_pp + add_pp
         achieved = dom_terms * fpp / (dom_ms * 1e-3) / 1e12
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")

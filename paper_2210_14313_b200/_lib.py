@@ -22,7 +22,7 @@ SG_ENOWORKSPACE = -7
 # exported symbols (checked by tests/test_abi.py against include/sg_b200.h)
 SYMBOLS = ["sg_plan", "sg_workspace_size", "sg_set_workspace", "sg_update_integrand",
            "sg_integrate", "sg_finalize", "sg_integrate_host", "sg_status_word", "sg_plan_points",
-           "sg_plan_range", "sg_plan_passes", "sg_debug_tables", "sg_plan_query",
+           "sg_plan_range", "sg_plan_passes", "sg_plan_leaf_work", "sg_debug_tables", "sg_plan_query",
            "sg_rule_table", "sg_profile_enable", "sg_profile_read", "sg_unrank", "sg_destroy",
            "sg_strerror"]
 
@@ -74,6 +74,7 @@ def lib():
         L.sg_plan_points.argtypes = [vp, ull, ull]
         L.sg_plan_range.argtypes = [vp, ll, ll, ll]
         L.sg_plan_passes.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ull, ull]
+        L.sg_plan_leaf_work.argtypes = [vp, dp, dp]
         L.sg_debug_tables.argtypes = [vp, dp, ctypes.c_size_t, dp]
         L.sg_plan_query.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(sg_options), ull, ull, ll, ll,

@@ -138,6 +138,12 @@ class Plan:
         check(lib().sg_plan_passes(self._h, ctypes.byref(n), t, w), "sg_plan_passes")
         return [PassInfo(int(t[i]), int(w[i])) for i in range(n.value)]
 
+    def leaf_work(self) -> tuple[float, float]:
+        """(DFMA, DADD) FP64 thread-instructions per point of the dominant leaf kernel variant."""
+        f, a = ctypes.c_double(), ctypes.c_double()
+        check(lib().sg_plan_leaf_work(self._h, ctypes.byref(f), ctypes.byref(a)), "sg_plan_leaf_work")
+        return float(f.value), float(a.value)
+
     def debug_tables(self):
         ncplx = 4 if self.kind == KIND_OSC else 2
         lo, hi, nd1 = self.range()

@@ -19,10 +19,10 @@ for w in $what; do
              --log-file gpurun_out/${tag}_launches_c4.csv python tools/prof_step.py 4 2 > gpurun_out/${tag}_ncu2.log 2>&1 ;;
     ncufull) timeout 300 python tools/prof_step.py 5 1 > gpurun_out/${tag}_plain5.log 2>&1 && \
            timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-             -k regex:k_passILb1ELb0 -c 1 -o gpurun_out/${tag}_c5_pass python tools/prof_step.py 5 1 > gpurun_out/${tag}_ncu3.log 2>&1 ;
+             -k regex:k_leaf2 -c 1 -o gpurun_out/${tag}_c5_leaf2 python tools/prof_step.py 5 1 > gpurun_out/${tag}_ncu3.log 2>&1 ;
            timeout 300 python tools/prof_step.py 4 1 > gpurun_out/${tag}_plain4b.log 2>&1 && \
            timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-             -k regex:k_passILb0ELb0 -c 1 -o gpurun_out/${tag}_c4_pass python tools/prof_step.py 4 1 > gpurun_out/${tag}_ncu4.log 2>&1 ;;
+             -k regex:k_leaf2 -c 1 -o gpurun_out/${tag}_c4_leaf2 python tools/prof_step.py 4 1 > gpurun_out/${tag}_ncu4.log 2>&1 ;;
   esac
 done
 ls -la gpurun_out
