@@ -78,8 +78,24 @@ typedef struct {
 typedef enum { SG_FORM_COMBINATION = 0, SG_FORM_DELTA = 1 } sg_form;
 
 /* Leaf arithmetic.  FACTOR_DD = double-double partial products of plan-time per-(coordinate,node)
- * factors (parity-grade).  Only FACTOR_DD is implemented in this build; others -> SG_EUNSUPPORTED. */
+ * factors (parity-grade, default).  SFORM_FP64 = ablation: FP64 partial sums of the argument and
+ * per-point FP64 exp/cos (not parity-grade on ill-conditioned problems). */
 typedef enum { SG_ARITH_FACTOR_DD = 0, SG_ARITH_SFORM_FP64 = 1 } sg_arith;
+
+/* Repeated-point merging (Eq 2.8 writes Q as one weighted sum over the points, and
+ * the Fig 2.1 remark: "we would avoid the repeated points").  Every level of a rule that contains
+ * the midpoint 1/2 repeats it, and a point with a coordinate at 1/2 is the same point whether that
+ * coordinate is at level 1 or at a higher level.
+ *  MERGE_NONE     = every Eq 2.6/2.7 point is evaluated (n_d^q points).
+ *  MERGE_MIDPOINT = the tree only carries non-midpoint nodes; all the copies of a point that differ
+ *                   in the levels of its midpoint coordinates are summed into one merged
+ *                   coefficient C'(t, b) = sum_{e=b}^{L} c(e) [z^{e-b}] M(z)^{d-t}
+ *                   (t = non-midpoint actives, b = their excess, M(z) = 1 + sum_{l>=2} w^l(1/2) z^{l-1}
+ *                   the midpoint's weights per level; c(e) the form's coefficient), so each such
+ *                   point is evaluated once.  Same value (an exact regrouping of Eq 2.6); the point
+ *                   count is the number of tree nodes (sg_plan_points), 5x fewer on config 5.
+ *                   Requires arith FACTOR_DD (else SG_EUNSUPPORTED). */
+typedef enum { SG_MERGE_NONE = 0, SG_MERGE_MIDPOINT = 1 } sg_merge;
 
 /* Work partition.  The Smolyak points are split into the root (all-midpoint point) and the
  * subtrees of the depth-1 prefixes (k1, l1, j1) = (first active coordinate, its level >= 2, its node),
@@ -92,6 +108,7 @@ typedef struct {
     sg_arith arith;
     int rank, world;
     long long range_lo, range_hi;
+    sg_merge merge;   /* SG_MERGE_NONE (default) or SG_MERGE_MIDPOINT */
 } sg_options;
 
 typedef struct sg_plan_s *sg_plan_t;
@@ -145,6 +162,13 @@ int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long long *n_depth1
  * *npass (query with NULL arrays first). */
 int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
                    unsigned long long *written);
+
+/* Host-only measurement helper: the FP64 instructions per Smolyak point of the leaf kernel variant
+ * this plan runs for its dominant (last) pass — DFMA and DADD thread-instructions per point,
+ * averaged over one level-2 row (midpoint, symmetric-pair and zero-tail specialisations included).
+ * Used by bench.py to turn the measured kernel time into achieved FLOP/s (DFMA = 2 flops).
+ * Both pointers must be non-NULL (else SG_EINVAL). */
+int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_point);
 
 /* Debug/test hook: copy the device factor table (per level l = 2..L+1, coordinate k, node j;
  * doubles per entry: 2 real dd or 4 complex dd) and the base value to host memory. */

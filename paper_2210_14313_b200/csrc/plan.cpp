@@ -113,11 +113,12 @@ static u128 sat_mul(u128 a, u128 b) {
     return a * b;
 }
 
-int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
+int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int merge, int rank, int world,
                     long long range_lo, long long range_hi, int fuse_mode) {
     if (d < 1 || L < 0) return SG_EINVAL;
     if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
-    if (kind < 0 || kind > 3 || form < 0 || form > 1) return SG_EINVAL;
+    if (kind < 0 || kind > 3 || form < 0 || form > 1 || merge < 0 || merge > 1) return SG_EINVAL;
+    hp.merge = merge;
     if (world < 1 || rank < 0 || rank >= world) return SG_EINVAL;
     if (d > SG_MAX_D || L > SG_MAX_L) return SG_EUNSUPPORTED;
     if (rule == SG_RULE_CLENSHAW_CURTIS && L + 1 > SG_CC_MAX_LEVEL) return SG_EUNSUPPORTED;
@@ -139,6 +140,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     hp.X.clear();
     hp.Whi.clear();
     hp.Wlo.clear();
+    // midpoint weight of each level's entries (dd; 0 if the level has no node at 1/2)
+    std::vector<double> mid_hi(L + 2, 0.0), mid_lo(L + 2, 0.0);
     int off = 0;
     for (int l = 2; l <= L + 1; ++l) {
         hp.entry_off[l] = off;
@@ -148,7 +151,6 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 hp.Whi.push_back(RW[l][j]);
                 hp.Wlo.push_back(0.0);
             }
-            hp.nl[l] = (int)RX[l].size();
         } else {
             // Delta^l = J^l - J^{l-1} on the union of both node sets; weights as exact dd differences
             std::vector<std::pair<double, std::pair<double, double>>> ent;
@@ -173,8 +175,20 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 hp.Whi.push_back(e.second.first);
                 hp.Wlo.push_back(e.second.second);
             }
-            hp.nl[l] = (int)ent.size();
         }
+        // merge: take the midpoint entry out of the level (its copies go into C'(t, b))
+        for (size_t i = (size_t)off; i < hp.X.size(); ++i)
+            if (hp.X[i] == 0.5) {
+                mid_hi[l] = hp.Whi[i];
+                mid_lo[l] = hp.Wlo[i];
+                if (merge) {
+                    hp.X.erase(hp.X.begin() + i);
+                    hp.Whi.erase(hp.Whi.begin() + i);
+                    hp.Wlo.erase(hp.Wlo.begin() + i);
+                }
+                break;
+            }
+        hp.nl[l] = (int)hp.X.size() - off;
         off += hp.nl[l];
     }
     hp.entry_off[L + 2] = off;
@@ -208,6 +222,43 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         hp.coef[e] = (m % 2) ? -v : v;
     }
 
+    // ---- node coefficients per (t, b) ----
+    hp.cm_hi.assign((size_t)(L + 1) * (L + 1), 0.0);
+    hp.cm_lo.assign((size_t)(L + 1) * (L + 1), 0.0);
+    for (int t = 0; t <= std::min(L, d); ++t) {
+        std::vector<q128> P(L + 1, 0);   // M(z)^(d-t) truncated at z^L, by binary powering
+        if (merge) {
+            std::vector<q128> Mz(L + 1, 0), B(L + 1, 0), T(L + 1, 0);
+            Mz[0] = 1;
+            for (int sdeg = 1; sdeg <= L; ++sdeg) Mz[sdeg] = (q128)mid_hi[sdeg + 1] + (q128)mid_lo[sdeg + 1];
+            P[0] = 1;
+            B = Mz;
+            auto mul = [&](const std::vector<q128> &a, const std::vector<q128> &b) {
+                std::fill(T.begin(), T.end(), (q128)0);
+                for (int i = 0; i <= L; ++i)
+                    for (int j = 0; i + j <= L; ++j) T[i + j] += a[i] * b[j];
+                return T;
+            };
+            for (long long n = (long long)d - t; n > 0; n >>= 1) {
+                if (n & 1) P = mul(P, B);
+                B = mul(B, B);
+            }
+        }
+        for (int b = 0; b <= L; ++b) {
+            q128 v = 0;
+            if (merge) {
+                for (int e = b; e <= L; ++e) v += (q128)hp.coef[e] * P[e - b];
+            } else {
+                v = hp.coef[b];
+            }
+            const double hi = (double)v;
+            hp.cm_hi[(size_t)t * (L + 1) + b] = hi;
+            hp.cm_lo[(size_t)t * (L + 1) + b] = (double)(v - (q128)hi);
+        }
+    }
+    // a node counts as a point iff its coefficient is nonzero (merged: every tree node is a point)
+    auto counted = [&](int b) -> bool { return merge || hp.coef[b] != 0.0; };
+
     hp.maxdepth = std::min(L, d);
     hp.nfront = std::max(0, std::min(L - 1, d - 1));
     const int64_t nd1 = (int64_t)d * hp.M0;
@@ -217,7 +268,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     std::vector<u128> Sub((size_t)(L + 1) * W, 0), Suf((size_t)(L + 1) * (W + 1), 0);
     for (int b = L; b >= 0; --b) {
         for (int k = d - 1; k >= -1; --k) {
-            u128 s = hp.coef[b] != 0.0 ? 1 : 0;
+            u128 s = counted(b) ? 1 : 0;
             for (int lp = 2; lp <= L + 1 - b; ++lp) {
                 int bp = b + lp - 1;
                 // children at k' > k: Suf[bp][k+1] = sum_{k' >= k+1} Sub[bp][k']
@@ -235,7 +286,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         hp.Sub[i] = Sub[i] >= ((u128)1 << 63) ? ~(uint64_t)0 : (uint64_t)Sub[i];
     if (total >= ((u128)1 << 63)) return SG_EOVERFLOW;
     hp.total_points = (uint64_t)total;
-    const u128 root_w = hp.coef[0] != 0.0 ? 1 : 0;
+    const u128 root_w = counted(0) ? 1 : 0;
     auto item_weight = [&](int k1, int l1) -> u128 { return Sub[(size_t)(l1 - 1) * W + (k1 + 1)]; };
 
     // ---- shard range in depth-1 rank space ----
@@ -424,10 +475,11 @@ int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int 
     uint64_t r = index;
     int depth = 0, b = 0, kl = -1;
     // root
-    if (hp.include_root && hp.coef[0] != 0.0) {
+    auto counted = [&](int bb) -> bool { return hp.merge || hp.coef[bb] != 0.0; };
+    if (hp.include_root && counted(0)) {
         if (r == 0) {
             *t = 0;
-            *coef = hp.coef[0];
+            *coef = hp.cm_hi[0];
             return SG_OK;
         }
         r -= 1;
@@ -460,7 +512,7 @@ int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int 
     if (!found) return SG_EINVAL;
     // descend in preorder
     for (;;) {
-        if (hp.coef[b] != 0.0) {
+        if (counted(b)) {
             if (r == 0) break;
             r -= 1;
         }
@@ -485,6 +537,6 @@ int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int 
         if (!moved) return SG_EINVAL;   // inconsistent counts (cannot happen for a valid plan)
     }
     *t = depth;
-    *coef = hp.coef[b];
+    *coef = hp.cm_hi[(size_t)depth * (L + 1) + b];
     return SG_OK;
 }

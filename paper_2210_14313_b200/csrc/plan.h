@@ -4,7 +4,9 @@
 // (k_1 < ... < k_t, levels l_m >= 2, node indices j_m); its excess is b = sum (l_m - 1) <= L and it
 // IS the Smolyak point whose other coordinates sit at level 1 (the midpoint).  Children append
 // (k' > k_t, l' in [2, L+1-b], j' in [0, nl[l'])).  Every node is one point of Eq 2.6 with
-// coefficient coef[b]; the root (t = 0) is the all-midpoint point.
+// coefficient coef[b]; the root (t = 0) is the all-midpoint point.  With merge (SG_MERGE_MIDPOINT)
+// the per-level entries exclude the midpoint x = 1/2 and a node's coefficient is C'(t, b) (below):
+// the node then stands for all its copies with extra midpoint coordinates at levels >= 2.
 //
 // Frontier t (t >= 1) = the extendable depth-t nodes (b <= L-1, k_t <= d-2), stored in segments
 // (b, k) in b-major, k-minor order; inside segment (b', k') the children of source segment (b, k)
@@ -28,6 +30,11 @@ struct HostPlan {
     int tab_off[SG_MAX_L + 3] = {0};   // offset (entries) of level l in the factor table: d*sum_{2<=m<l} nl[m]
     int tab_entries = 0;               // d * M0
     double coef[SG_MAX_L + 2] = {0};   // coefficient per excess e (combination / delta)
+    // Node coefficient per (depth t, excess b), index t * (L + 1) + b, as double-double (hi, lo).
+    // merge == 0: coef[b].  merge == 1 (SG_MERGE_MIDPOINT): the merged coefficient
+    // C'(t, b) = sum_{e=b}^{L} coef[e] [z^{e-b}] M(z)^{d-t}, M(z) = 1 + sum_{l>=2} w^l(1/2) z^{l-1}.
+    int merge = 0;
+    std::vector<double> cm_hi, cm_lo;
     int64_t M0 = 0;                    // sum_{l=2}^{L+1} nl[l]
     int64_t range_lo = 0, range_hi = 0;
     bool include_root = true;
@@ -64,7 +71,7 @@ struct HostPlan {
 int host_unrank(const HostPlan &hp, uint64_t index, int *t, int *k, int *l, int *j, double *coef);
 
 // Build rules, counts, shard range and launch geometry. Returns an sg_status code.
-int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int rank, int world,
+int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int merge, int rank, int world,
                     long long range_lo, long long range_hi, int fuse_mode = 1);   // 0 never, 1 auto, 2 always
 
 // 1-D rule (level l) on [0,1] as doubles rounded from quad; returns n or -1.

@@ -44,11 +44,13 @@ struct DevPlan {
     double *SA;     // [(L+2) x (d+1)] suffix sums of |F| per level (k_leaf's accumulation bound)
     int *status;
     int sform;      // SG_ARITH_SFORM_FP64 ablation: base[0] holds the argument S, not the value
+    const double2 *coefm;   // node coefficient (dd) per (depth t, excess b): [t * (L + 1) + b]
 };
 
 struct PassArgs {
     long long nsrc, ntasks;
     int nsplit;
+    int t;                         // depth of the source frontier (children have depth t + 1)
     const double2 *src_re, *src_im;
     const uint32_t *src_meta;
     double2 *dst_re, *dst_im;
@@ -229,6 +231,12 @@ __device__ __forceinline__ void acc_add(double &ah, double &al, double p, double
     ah = s;
 }
 
+// v * C(t, b): the node coefficient of depth t and excess b (an exact integer double unless merged)
+__device__ __forceinline__ dd coef_mul(const DevPlan &P, dd v, int t, int b) {
+    const double2 c = P.coefm[t * (P.L + 1) + b];
+    return c.y == 0.0 ? dd_mul_d(v, c.x) : dd_mul(v, dd{c.x, c.y});
+}
+
 // ---------------------------------------------------------------------------------------------
 // Root pass: every depth-1 point (k1, l1, j1) of this shard, one thread each.
 // ---------------------------------------------------------------------------------------------
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
             cr = dd_mul(Br, dd{fr.x, fr.y});
         }
         const int b1 = l1 - 1;
-        tot = dd_mul_d(cr, P.coef[b1]);
+        tot = coef_mul(P, cr, 1, b1);
         if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
             const long long seg = (long long)b1 * P.d + k1;
             const long long o = R.off1[seg] + j1 - R.JS[seg];
@@ -360,7 +368,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const Pa
                     }
                 }
             }
-            if (lv) tot = dd_add(tot, dd_mul_d(dd_norm(ah, al), P.coef[bp]));
+            if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, bp));
         }
     }
     dd s = block_reduce_dd<WPB>(tot);
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
 #endif
             default: s = leaf_level<CPLX, 0>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             }
-            if (lv) tot = dd_add(tot, dd_mul_d(s, P.coef[b + lp - 1]));
+            if (lv) tot = dd_add(tot, coef_mul(P, s, A.t + 1, b + lp - 1));
         }
     }
     dd s = block_reduce_dd<WPB>(tot);
@@ -754,7 +762,8 @@ __device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, 
 }
 
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
-// SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory).
+// SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory), or nodes 0 and 1 do
+// (CJ == -1, NJ == 2: the midpoint-merged Clenshaw-Curtis level-2 row {0, 1}).
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
@@ -768,6 +777,13 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
             leaf_sym_pair_terms(er[jm], ei[jm], f2, g2, sg[jm], ah[jm], al[jm]);
             leaf_real_factor_term<CZ>(er[jm], f1, sg[jm], ah[jm], al[jm]);
         }
+        return;
+    }
+    if constexpr (SYM && CPLX && NJ == 2 && CJ == -1) {
+        const double2 f1 = SMEM ? Fr[kp * 2 + 1] : __ldg(Fr + kp * 2 + 1);
+        const double2 g1 = SMEM ? Fi[kp * 2 + 1] : __ldg(Fi + kp * 2 + 1);
+#pragma unroll
+        for (int jm = 0; jm < 2; ++jm) leaf_sym_pair_terms(er[jm], ei[jm], f1, g1, sg[jm], ah[jm], al[jm]);
         return;
     }
     double2 f[NJ], g[NJ];
@@ -1124,9 +1140,9 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
     for (long long i = threadIdx.x; i < n; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
     s = block_reduce_dd<32>(s);
     if (threadIdx.x == 0) {
-        if (include_root && P.coef[0] != 0.0) {
+        if (include_root && P.coefm[0].x != 0.0) {
             const dd root = P.sform ? dd{sform_g(P.kind, P.base[0]), 0.0} : dd{P.base[0], P.base[1]};
-            s = dd_add(s, dd_mul_d(root, P.coef[0]));
+            s = dd_add(s, coef_mul(P, root, 0, 0));
         }
         if (*P.status) s = dd{nan(""), nan("")};
         out[0] = s.hi;
@@ -1227,6 +1243,8 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     if (opt) o = *opt;
     if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
     if (o.arith == SG_ARITH_SFORM_FP64 && f->kind == SG_F_PRODUCT_PEAK) return SG_EUNSUPPORTED;
+    if (o.merge != SG_MERGE_NONE && o.merge != SG_MERGE_MIDPOINT) return SG_EINVAL;
+    if (o.merge != SG_MERGE_NONE && o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
     sg_plan_s *p = new (std::nothrow) sg_plan_s();
     if (!p) return SG_ENOMEM;
     {
@@ -1234,7 +1252,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         const char *nf = getenv("SG_B200_NOFUSE"), *fu = getenv("SG_B200_FUSE");
         int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
         if (o.arith == SG_ARITH_SFORM_FP64) mode = 0;
-        rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, o.rank, o.world,
+        rc = host_plan_build(p->hp, d, q - d, (int)rule, (int)f->kind, (int)o.form, (int)o.merge, o.rank, o.world,
                              o.range_lo, o.range_hi, mode);
     }
     if (rc) {
@@ -1292,6 +1310,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     const size_t oScr = carve(sizeof(double) * 8);
     const size_t oCnt = carve(sizeof(unsigned long long) * 8);
     const size_t oSA = carve(sizeof(double) * (size_t)(L + 2) * (d + 1));
+    const size_t oCm = carve(sizeof(double2) * hp.cm_hi.size());
     if (cudaMalloc(&p->dev_block, sz) != cudaSuccess) {
         cudaGetLastError();
         delete p;
@@ -1327,7 +1346,10 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->d_scratch = (double *)(base + oScr);
     p->d_counter = (unsigned long long *)(base + oCnt);
     dp.SA = (double *)(base + oSA);
+    dp.coefm = (const double2 *)(base + oCm);
     std::vector<double> wz(d, 0.0);
+    std::vector<double2> cm(hp.cm_hi.size());
+    for (size_t i = 0; i < cm.size(); ++i) cm[i] = make_double2(hp.cm_hi[i], hp.cm_lo[i]);
     bool ok = true;
     ok &= cudaMemcpy((void *)dp.X, hp.X.data(), sizeof(double) * nent, cudaMemcpyHostToDevice) == cudaSuccess;
     ok &= cudaMemcpy((void *)dp.Whi, hp.Whi.data(), sizeof(double) * nent, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -1337,6 +1359,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     ok &= cudaMemcpy((void *)dp.u, &f->u, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
     ok &= cudaMemcpy(p->d_tabs, tabs.data(), sizeof(long long) * tabs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     ok &= cudaMemset(dp.status, 0, sizeof(int) * 4) == cudaSuccess;
+    ok &= cudaMemcpy((void *)dp.coefm, cm.data(), sizeof(double2) * cm.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         cudaFree(p->dev_block);
@@ -1413,6 +1436,7 @@ static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
         return cz ? (const void *)k_leaf2<CPLX, 3, SMEM, 1, false, true> : (const void *)k_leaf2<CPLX, 3, SMEM, 1, false, false>;
     }
     if (nj == 3) return (const void *)k_leaf2<CPLX, 3, SMEM, -1>;
+    if (CPLX && sym) return (const void *)k_leaf2<CPLX, 2, SMEM, -1, true>;
     return (const void *)k_leaf2<CPLX, 2, SMEM, -1>;
 }
 template <bool CPLX>
@@ -1443,10 +1467,11 @@ static int setup_leaf1(sg_plan_s *p) {
 #endif
     const bool ct = p->leaf2_center;
     {
-        // symmetric pair: x_0 + x_2 == 1 and equal weights, exactly
-        const int e0 = hp.entry_off[2];
-        p->leaf2_sym = ct && p->cplx && hp.X[e0] + hp.X[e0 + 2] == 1.0 && hp.Whi[e0] == hp.Whi[e0 + 2] &&
-                       hp.Wlo[e0] == hp.Wlo[e0 + 2];
+        // symmetric pair: x_0 + x_last == 1 and equal weights, exactly (NJ = 3 around the midpoint,
+        // or NJ = 2 without one)
+        const int e0 = hp.entry_off[2], e1 = e0 + nj - 1;
+        p->leaf2_sym = (ct || nj == 2) && p->cplx && 1.0 - hp.X[e1] == hp.X[e0] && hp.Whi[e0] == hp.Whi[e1] &&
+                       hp.Wlo[e0] == hp.Wlo[e1];
 #ifdef LEAF2_NO_SYM
         p->leaf2_sym = false;
 #endif
@@ -1582,6 +1607,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         A.nsrc = hp.total[t];
         A.ntasks = hp.pass_ntasks[t];
         A.nsplit = hp.pass_nsplit[t];
+        A.t = t;
         double2 *re, *im;
         uint32_t *meta;
         front_ptrs(p, t, re, im, meta);
@@ -1689,6 +1715,30 @@ extern "C" int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms
     return SG_OK;
 }
 
+// FP64 instruction mix per leaf of the last pass's kernel variant (counted from the leaf helpers
+// above: leaf1_term real 4 DFMA + 3 DADD, complex 8 + 6; leaf_real_factor_term 4 + 3, or 3 + 3
+// with CZ; leaf_sym_pair_terms 8 + 10 for its two leaves).
+extern "C" int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_point) {
+    if (!p || !dfma_per_point || !dadd_per_point) return SG_EINVAL;
+    double f = p->cplx ? 8.0 : 4.0, a = p->cplx ? 6.0 : 3.0;
+    if (p->leaf2 && p->leaf2_sym && !p->leaf2_center) {   // NJ = 2 symmetric pair
+        f = 8.0 / 2.0;
+        a = 10.0 / 2.0;
+    } else if (p->leaf2 && p->leaf2_center) {
+        const double cf = p->leaf2_cz ? 3.0 : 4.0, ca = 3.0;
+        if (p->leaf2_sym) {
+            f = (8.0 + cf) / 3.0;
+            a = (10.0 + ca) / 3.0;
+        } else {
+            f = (2.0 * f + cf) / 3.0;
+            a = (2.0 * a + ca) / 3.0;
+        }
+    }
+    *dfma_per_point = f;
+    *dadd_per_point = a;
+    return SG_OK;
+}
+
 extern "C" int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host) {
     if (!p) return SG_EINVAL;
     const size_t per = p->two ? 4 : 2, n = (size_t)p->hp.tab_entries;
@@ -1722,7 +1772,7 @@ extern "C" int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_
     if (opt) o = *opt;
     if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
     HostPlan hp;
-    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, o.rank, o.world,
+    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, (int)o.merge, o.rank, o.world,
                              o.range_lo, o.range_hi);
     if (rc) return rc;
     if (shard_points) *shard_points = hp.shard_points;
@@ -1739,7 +1789,7 @@ extern "C" int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_opti
     sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
     if (opt) o = *opt;
     HostPlan hp;
-    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, o.rank, o.world,
+    int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, (int)o.merge, o.rank, o.world,
                              o.range_lo, o.range_hi, 0);
     if (rc) return rc;
     return host_unrank(hp, index, t, k, l, j, coef);

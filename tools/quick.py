@@ -25,7 +25,8 @@ def main():
     for i in cfgs:
         p = S.baseline_config(i)
         t0 = time.time()
-        plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+        plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
+                        merge=int(os.environ.get("QUICK_MERGE", "0")))
         tplan = time.time() - t0
         hi, lo = plan.integrate_host()
         dp = pins.dp_value(p)
