@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
     # through host memory and every rank may share one device (ranks never wait on each other
     # inside a kernel, so sharing is safe); the product configuration is nccl + one GPU per rank
@@ -230,7 +231,7 @@ def main():
     result = torch.zeros(2, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
+    def step(plan=plan):
         part = plan.sg_integrate(stream)
         if world > 1:
             if args.dist_backend == "nccl":
@@ -243,7 +244,7 @@ def main():
         else:
             plan.sg_finalize(part, 1, stream, result)
 
-    def timed(fn, k):
+    def timed(fn, k, plan=plan, dominant=dominant):
         times, dom = [], []
         for _ in range(k):
             flush.fill_(1.0)
@@ -290,6 +291,44 @@ def main():
     e2e_ms = statistics.mean(e2e_times)
     h2d = 8 * p.d * (2 if p.w is not None else 1) + 8
     value_res = result.cpu().numpy()
+
+    # merged leg (SG_MERGE_MIDPOINT): the same integral with the midpoint copies of
+    # every point summed into merged coefficients, each remaining point evaluated once
+    merged = None
+    if not args.no_merged:
+        mplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
+                         device=dev, merge=api.MERGE_MIDPOINT)
+        mplan.profile_enable(True)
+        m_shard, m_total = mplan.points()
+        mpasses = mplan.passes()
+        mdom = max(range(1, len(mpasses)), key=lambda i: mpasses[i].terms) if len(mpasses) > 1 else 0
+        for _ in range(args.warmup):
+            step(mplan)
+        torch.cuda.synchronize(dev)
+        m_times, m_dom = timed(lambda: step(mplan), args.steps, mplan, mdom)
+        m_res = result.cpu().numpy()
+        m_ms = statistics.mean(m_times)
+        mf, ma = mplan.leaf_work()
+        m_dom_ms = statistics.mean(m_dom)
+        peak_, mhz_ = peak_fp64_tflops()
+        m_ach = mpasses[mdom].terms * (2 * mf + ma) / (m_dom_ms * 1e-3) / 1e12
+        merged = {
+            "time_to_integral_ms": m_ms, "points": m_total,
+            "value": m_total / (m_ms * 1e-3), "unit": "points/s",
+            "eq26_points_per_s": total_pts / (m_ms * 1e-3),
+            "speedup_vs_combination": ms / m_ms,
+            "result": float(m_res[0]),
+            "rel_diff_vs_combination": abs((float(m_res[0]) + float(m_res[1]))
+                                           - (float(value_res[0]) + float(value_res[1])))
+                                       / abs(float(value_res[0])),
+            "roofline": {"bound": "alu", "achieved": m_ach, "peak": peak_, "unit": "TFLOP/s",
+                         "frac": m_ach / peak_, "kernel": f"pass {mdom} ({mpasses[mdom].terms} points)",
+                         "kernel_ms": m_dom_ms, "fp64_inst_per_point": mf + ma,
+                         "pipe_frac": mpasses[mdom].terms * (mf + ma) / (m_dom_ms * 1e-3)
+                                      / (SM_COUNT * FP64_FMA_PER_SM_CLK * mhz_ * 1e6)},
+            "step_ms_all": [round(t, 4) for t in m_times],
+        }
+        mplan.close()
 
     # rank-0 report
     if rank == 0:
@@ -340,6 +379,8 @@ def main():
             "parity": parity,
             "step_ms_all": [round(t, 4) for t in times],
         }
+        if merged is not None:
+            line["merged"] = merged
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
         print(json.dumps(line), flush=True)

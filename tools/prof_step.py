@@ -17,7 +17,8 @@ def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     p = S.baseline_config(cfg)
-    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
+                    merge=int(os.environ.get("QUICK_MERGE", "0")))
     for _ in range(steps):
         out = plan.sg_integrate()
         plan.sg_finalize(out, 1)
