@@ -187,6 +187,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
+    ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
     # through host memory and every rank may share one device (ranks never wait on each other
     # inside a kernel, so sharing is safe); the product configuration is nccl + one GPU per rank
@@ -330,6 +331,49 @@ def main():
         }
         mplan.close()
 
+    # collapse leg (SG_METHOD_COLLAPSE): the same integral as a per-coordinate
+    # polynomial product in the level budget, O(d L^2) dd work and no points (not sharded: rank 0
+    # emits the value, the other ranks a zero partial; the all-gather + finalize are unchanged)
+    collapse = None
+    if not args.no_collapse:
+        cplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
+                         device=dev, method=api.METHOD_COLLAPSE)
+        for _ in range(args.warmup):
+            step(cplan)
+        torch.cuda.synchronize(dev)
+        c_times = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(cplan)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            c_ms_i = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([c_ms_i], dtype=torch.float64,
+                                 device=dev if args.dist_backend == "nccl" else "cpu")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                c_ms_i = float(t.item())
+            c_times.append(c_ms_i)
+        c_res = result.cpu().numpy()
+        c_ms = statistics.mean(c_times)
+        collapse = {
+            "time_to_integral_ms": c_ms, "eq26_points_per_s": total_pts / (c_ms * 1e-3),
+            "speedup_vs_combination": ms / c_ms, "result": float(c_res[0]),
+            "rel_diff_vs_combination": abs((float(c_res[0]) + float(c_res[1]))
+                                           - (float(value_res[0]) + float(value_res[1])))
+                                       / abs(float(value_res[0])),
+            "work": f"d*(L+1) = {p.d * (p.L + 1)} level sums + d truncated polynomial products "
+                    f"of degree {p.L} (dd); launch-latency bound",
+            "step_ms_all": [round(t, 4) for t in c_times],
+        }
+        cplan.close()
+
     # rank-0 report
     if rank == 0:
         peak, mhz = peak_fp64_tflops()
@@ -381,6 +425,8 @@ def main():
         }
         if merged is not None:
             line["merged"] = merged
+        if collapse is not None:
+            line["collapse"] = collapse
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
         print(json.dumps(line), flush=True)

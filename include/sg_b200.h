@@ -97,6 +97,21 @@ typedef enum { SG_ARITH_FACTOR_DD = 0, SG_ARITH_SFORM_FP64 = 1 } sg_arith;
  *                   Requires arith FACTOR_DD (else SG_EUNSUPPORTED). */
 typedef enum { SG_MERGE_NONE = 0, SG_MERGE_MIDPOINT = 1 } sg_merge;
 
+/* Evaluation method.
+ *  METHOD_TREE     = the multilevel dimension iteration over the Smolyak points (default; every
+ *                    point of the prefix tree is evaluated).
+ *  METHOD_COLLAPSE = separable collapse: the paper's symbolic partial function f_{t-m}
+ *                     carried as a truncated polynomial in the level budget.
+ *                    All four kinds are Re(B prod_k E_k(x_k)), so the Eq 2.6 sum over every tensor
+ *                    point of every multi-index of excess e is [z^e] prod_k p_k(z) with
+ *                    p_k(z) = sum_{l=1}^{L+1} (sum_j w_j^l E_k(x_j^l)) z^{l-1}; A = Re(B sum_e
+ *                    coef[e] [z^e] prod_k p_k).  O(d L^2) double-double work, no points; same value
+ *                    as the tree up to dd rounding.  Not sharded: rank 0 of `world` emits the value,
+ *                    every other rank a zero partial (so sg_finalize's sum is the value).  Requires
+ *                    SG_MERGE_NONE (else SG_EINVAL) and SG_ARITH_FACTOR_DD (else SG_EUNSUPPORTED);
+ *                    sg_plan_passes reports 0 passes. */
+typedef enum { SG_METHOD_TREE = 0, SG_METHOD_COLLAPSE = 1 } sg_method;
+
 /* Work partition.  The Smolyak points are split into the root (all-midpoint point) and the
  * subtrees of the depth-1 prefixes (k1, l1, j1) = (first active coordinate, its level >= 2, its node),
  * ranked lexicographically: r1 = k1 * M0 + sum_{2<=l<l1} n_l + j1, M0 = sum_{l=2}^{L+1} n_l.
@@ -109,6 +124,7 @@ typedef struct {
     int rank, world;
     long long range_lo, range_hi;
     sg_merge merge;   /* SG_MERGE_NONE (default) or SG_MERGE_MIDPOINT */
+    sg_method method; /* SG_METHOD_TREE (default) or SG_METHOD_COLLAPSE */
 } sg_options;
 
 typedef struct sg_plan_s *sg_plan_t;

@@ -43,7 +43,7 @@ class sg_integrand_desc(ctypes.Structure):
 class sg_options(ctypes.Structure):
     _fields_ = [("form", ctypes.c_int), ("arith", ctypes.c_int), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("range_lo", ctypes.c_longlong),
-                ("range_hi", ctypes.c_longlong), ("merge", ctypes.c_int)]
+                ("range_hi", ctypes.c_longlong), ("merge", ctypes.c_int), ("method", ctypes.c_int)]
 
 
 _lib = None

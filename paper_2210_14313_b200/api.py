@@ -23,6 +23,7 @@ KIND_EXP, KIND_OSC, KIND_PEAK, KIND_GAUSS = 0, 1, 2, 3
 FORM_COMBINATION, FORM_DELTA = 0, 1
 ARITH_FACTOR_DD, ARITH_SFORM_FP64 = 0, 1   # s-form = ablation (FP64 partial sums + FP64 exp/cos)
 MERGE_NONE, MERGE_MIDPOINT = 0, 1          # midpoint-merged evaluation (sg_merge)
+METHOD_TREE, METHOD_COLLAPSE = 0, 1        # sg_method: prefix tree over the points / separable collapse
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
@@ -47,7 +48,7 @@ class Plan:
     def __init__(self, d: int, q: int, rule: int, kind: int, c, w=None, u: float = 0.0,
                  form: int = FORM_COMBINATION, rank: int = 0, world: int = 1,
                  range_lo: int = 0, range_hi: int = -1, device=None,
-                 arith: int = ARITH_FACTOR_DD, merge: int = MERGE_NONE):
+                 arith: int = ARITH_FACTOR_DD, merge: int = MERGE_NONE, method: int = METHOD_TREE):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2210_14313_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
@@ -57,7 +58,7 @@ class Plan:
         self.u = float(u)
         desc = self._desc(self._c, self._w, self.u)
         opts = sg_options(int(form), int(arith), int(rank), int(world), int(range_lo), int(range_hi),
-                          int(merge))
+                          int(merge), int(method))
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(lib().sg_plan(self.d, self.q, self.rule, ctypes.byref(desc), ctypes.byref(opts),
@@ -212,7 +213,7 @@ def sg_unrank(d, q, rule, kind, index, form=FORM_COMBINATION, rank=0, world=1, r
     t = ctypes.c_int()
     k, l, j = (ctypes.c_int * n)(), (ctypes.c_int * n)(), (ctypes.c_int * n)()
     cf = ctypes.c_double()
-    o = sg_options(int(form), 0, int(rank), int(world), int(range_lo), int(range_hi), int(merge))
+    o = sg_options(int(form), 0, int(rank), int(world), int(range_lo), int(range_hi), int(merge), 0)
     check(lib().sg_unrank(d, q, rule, kind, ctypes.byref(o), int(index), ctypes.byref(t), k, l, j,
                           ctypes.byref(cf)), "sg_unrank")
     return cf.value, [(k[m], l[m], j[m]) for m in range(t.value)]

@@ -187,3 +187,27 @@ def test_unrank_full_size_config5_samples_and_shards(L):
             k1, l1, j1 = trip[0]
             r1 = k1 * M0 + sum(pins.node_count(p.rule, l) for l in range(2, l1)) + j1
             assert lo <= r1 < hi
+
+
+def test_ctypes_structs_match_header(tmp_path):
+    """The Python marshalling structs have the C layout of include/sg_b200.h (size and every field
+    offset), compiled here with gcc from the header itself."""
+    import subprocess
+    from paper_2210_14313_b200._lib import sg_integrand_desc, sg_options
+    src = tmp_path / "layout.c"
+    fields = {"sg_options": [f for f, _ in sg_options._fields_],
+              "sg_integrand_desc": [f for f, _ in sg_integrand_desc._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sg_b200.h"', 'int main(void) {']
+    for st, fs in fields.items():
+        lines.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            lines.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines += ["return 0;", "}"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)], text=True).splitlines())
+    for st, cls in (("sg_options", sg_options), ("sg_integrand_desc", sg_integrand_desc)):
+        assert int(got[st]) == ctypes.sizeof(cls), st
+        for f in fields[st]:
+            assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
