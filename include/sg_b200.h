@@ -36,8 +36,8 @@ typedef enum {
     SG_OK = 0,
     SG_EINVAL = -1,        /* d < 1, q < d (BudgetTooSmall), NULL pointer, bad enum, non-finite
                               parameter, w missing for peak/gauss, rank/world/range inconsistent */
-    SG_EUNSUPPORTED = -2,  /* UnsupportedLevel: CC max level L+1 > 20, GL n > 64, d > 2^20-1,
-                              L > 19 */
+    SG_EUNSUPPORTED = -2,  /* UnsupportedLevel: CC / trapezoidal max level L+1 > 12, GL n > 64,
+                              Gauss-Patterson rule > 63 points, d > 2^20-1, L > 19 */
     SG_EOVERFLOW = -3,     /* a point or frontier count would reach 2^63 */
     SG_ENOMEM = -4,        /* device allocation failed, or workspace smaller than required */
     SG_ECUDA = -5,         /* a CUDA runtime call failed (launch error, bad stream, ...) */
@@ -48,7 +48,12 @@ typedef enum {
 
 /* 1-D rule families, numbered by the paper's parameter r. */
 typedef enum {
+    SG_RULE_TRAPEZOIDAL = 1,      /* nested, n_1 = 1, n_l = 2^{l-1}+1, equal spacing, end weights
+                                     halved (Eq 2.10)                          */
     SG_RULE_CLENSHAW_CURTIS = 2,  /* nested, n_1 = 1, n_l = 2^{l-1}+1 (Eq 2.11) */
+    SG_RULE_GAUSS_PATTERSON = 3,  /* nested, delayed: n_l = 1, 3, 3, 7, 7, 7, 15, ... = the smallest
+                                     Patterson rule exact to degree 2l-1 (Eq 2.12,
+                                     sequence of PAPER.md:615; reading R16)            */
     SG_RULE_GAUSS_LEGENDRE = 4    /* n_l = l (Eq 2.13)                         */
 } sg_rule;
 

@@ -26,7 +26,7 @@
 
 typedef __float128 quad;
 
-enum { SGO_RULE_CC = 2, SGO_RULE_GL = 4 };
+enum { SGO_RULE_TRAP = 1, SGO_RULE_CC = 2, SGO_RULE_GP = 3, SGO_RULE_GL = 4 };
 enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_MONOMIAL = 4 };
 #define SGO_MAX_LEVEL 20
 #define SGO_MAX_GL 64
@@ -35,10 +35,25 @@ enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_MONOMIAL = 4 }
  * 1-D rules on [0,1]
  * ------------------------------------------------------------------------------------------- */
 
-/* n_l: CC n_1 = 1, n_l = 2^{l-1} + 1 (Eq 2.11); GL n_l = l. */
+/* Gauss-Patterson, delayed (q = 1..10 -> N = 1, 3, 3, 7, 7, 7, 15, 15, 15, 15): level l
+ * uses the Patterson rule with i extensions (2^{i+1} - 1 points) whose polynomial degree of
+ * exactness, 1 for i = 0 and 3 * 2^i - 1 for i >= 1, is the first to reach that of the l-point
+ * Gauss-Legendre rule, 2l - 1 (reading R16). */
+static int gp_extensions(int l) {
+    int i = 0;
+    for (;;) {
+        int exact = i == 0 ? 1 : 3 * (1 << i) - 1;
+        if (exact >= 2 * l - 1) return i;
+        ++i;
+    }
+}
+
+/* n_l: trapezoidal and CC n_1 = 1, n_l = 2^{l-1} + 1 (Eqs 2.10, 2.11);
+ * Gauss-Patterson 2^{i+1} - 1 (above); GL n_l = l. */
 int sgo_node_count(int rule, int l) {
     if (l < 1) return -1;
-    if (rule == SGO_RULE_CC) return l == 1 ? 1 : (1 << (l - 1)) + 1;
+    if (rule == SGO_RULE_CC || rule == SGO_RULE_TRAP) return l == 1 ? 1 : (1 << (l - 1)) + 1;
+    if (rule == SGO_RULE_GP) return (2 << gp_extensions(l)) - 1;
     if (rule == SGO_RULE_GL) return l;
     return -1;
 }
@@ -104,6 +119,154 @@ static void gl_rule(int n, double *x, double *w) {
     }
 }
 
+/* Trapezoidal rule (Eq 2.10): x_j = (j-1) 2^{2-l} - 1, w_j = 2^{2-l} with the first
+ * and last halved, on [-1,1]; mapped to [0,1] (reading R2).  Level 1: midpoint, weight 1 (R3). */
+static void trap_rule(int l, double *x, double *w) {
+    if (l == 1) { x[0] = 0.5; w[0] = 1.0; return; }
+    const int n = (1 << (l - 1)) + 1;
+    const double h = ldexp(1.0, 2 - l);
+    for (int j = 1; j <= n; ++j) {
+        double xj = (j - 1) * h - 1.0, wj = h;
+        if (j == 1 || j == n) wj /= 2;
+        x[j - 1] = (xj + 1.0) / 2;
+        w[j - 1] = wj / 2;
+    }
+}
+
+/* Gauss-Legendre nodes/weights in quad on [-1,1] (descending), for the integrals below. */
+static void gl_quad_rule(int n, quad *t, quad *wt) {
+    for (int i = 1; i <= n; ++i) {
+        quad r = cosq(M_PIq * ((quad)i - 0.25Q) / ((quad)n + 0.5Q)), p, dp;
+        for (int it = 0; it < 200; ++it) {
+            legendre(n, r, &p, &dp);
+            quad dr = p / dp;
+            r -= dr;
+            if (fabsq(dr) < 1e-33Q) break;
+        }
+        legendre(n, r, &p, &dp);
+        t[i - 1] = r;
+        wt[i - 1] = 2 / ((1 - r * r) * dp * dp);
+    }
+}
+
+/* sum_k a[k] P_k(x), k = 0..deg, by Clenshaw's recurrence (P_{k+1} = ((2k+1) x P_k - k P_{k-1})/(k+1)). */
+static quad legendre_series(const quad *a, int deg, quad x) {
+    quad b1 = 0, b2 = 0;
+    for (int k = deg; k >= 1; --k) {
+        /* alpha_k(x) = (2k+1) x / (k+1), beta_{k+1} = -(k+1)/(k+2) */
+        quad b0 = a[k] + (2 * k + 1) * x / (k + 1) * b1 - (quad)(k + 1) / (k + 2) * b2;
+        b2 = b1; b1 = b0;
+    }
+    return a[0] + x * b1 - 0.5Q * b2;
+}
+
+/* Solve A z = b (n x n, row-major, destroyed) by Gaussian elimination with partial pivoting. */
+static int solve_quad(int n, quad *A, quad *b, quad *z) {
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r) if (fabsq(A[r * n + c]) > fabsq(A[piv * n + c])) piv = r;
+        if (A[piv * n + c] == 0) return -1;
+        if (piv != c) {
+            for (int j = 0; j < n; ++j) { quad t = A[c * n + j]; A[c * n + j] = A[piv * n + j]; A[piv * n + j] = t; }
+            quad t = b[c]; b[c] = b[piv]; b[piv] = t;
+        }
+        for (int r = c + 1; r < n; ++r) {
+            quad f = A[r * n + c] / A[c * n + c];
+            for (int j = c; j < n; ++j) A[r * n + j] -= f * A[c * n + j];
+            b[r] -= f * b[c];
+        }
+    }
+    for (int c = n - 1; c >= 0; --c) {
+        quad v = b[c];
+        for (int j = c + 1; j < n; ++j) v -= A[c * n + j] * z[j];
+        z[c] = v / A[c * n + c];
+    }
+    return 0;
+}
+
+/* Gauss-Patterson rule with `ext` extensions (Eq 2.12), on [0,1], written from the
+ * definition with n = 1: the nodes are the zero of P_1 and the zeros of G_1, ..., G_ext, where G_i has
+ * degree 2^{i-1}(n+1) = 2^i and is orthogonal to every polynomial of degree < 2^i with respect to the
+ * weight P_1(x) G_1(x) ... G_{i-1}(x) on [-1,1].  Each G_i is monic-in-P (G_i = P_{2^i} + sum a_k P_k),
+ * stored by its Legendre coefficients.  G_i is even and the weight odd, so the orthogonality
+ * conditions against even P_k hold identically; the conditions against odd P_k (k < 2^i) determine
+ * the even coefficients a_k (k < 2^i).  Zeros: sign changes of G_i on a fine grid in arccos space,
+ * refined by bisection.  Weights: the rule is interpolatory, so w solves the moment equations
+ * sum_j w_j P_k(x_j) = 2 delta_{k0}, k = 0 .. N-1.  All in quad, rounded once to double. */
+#define GP_MAXN 63
+static int gp_rule(int ext, double *x, double *w) {
+    static quad G[7][GP_MAXN + 2];          /* Legendre coefficients of G_1 .. G_ext */
+    quad nodes[GP_MAXN];
+    int N = 1;
+    nodes[0] = 0;                             /* zero of P_1 */
+    for (int i = 1; i <= ext; ++i) {
+        const int deg = 1 << i, nu = deg / 2;
+        const int nq = (3 * deg) / 2 + 2;     /* Gauss points: exact for the integrand degree < 2 nq */
+        quad *gt = malloc(sizeof(quad) * nq), *gw = malloc(sizeof(quad) * nq);
+        quad *A = calloc((size_t)nu * nu, sizeof(quad)), *b = calloc(nu, sizeof(quad));
+        quad *z = calloc(nu, sizeof(quad));
+        gl_quad_rule(nq, gt, gw);
+        for (int q = 0; q < nq; ++q) {
+            quad wgt = gt[q];                 /* P_1 */
+            for (int j = 1; j < i; ++j) wgt *= legendre_series(G[j], 1 << j, gt[q]);
+            for (int r = 0; r < nu; ++r) {
+                quad pk, dpk, pc, dpc, ptop, dtop;
+                legendre(2 * r + 1, gt[q], &pk, &dpk);
+                legendre(deg, gt[q], &ptop, &dtop);
+                for (int c = 0; c < nu; ++c) {
+                    legendre(2 * c, gt[q], &pc, &dpc);
+                    A[r * nu + c] += gw[q] * wgt * pk * pc;
+                }
+                b[r] -= gw[q] * wgt * pk * ptop;
+            }
+        }
+        if (solve_quad(nu, A, b, z)) return -1;
+        for (int k = 0; k <= deg; ++k) G[i][k] = 0;
+        G[i][deg] = 1;
+        for (int c = 0; c < nu; ++c) G[i][2 * c] = z[c];
+        free(gt); free(gw); free(A); free(b); free(z);
+        /* zeros of G_i */
+        const int grid = 1 << 14;
+        int found = 0;
+        quad xa = -1, fa = legendre_series(G[i], deg, xa);
+        for (int g = 1; g <= grid; ++g) {
+            quad xb = -cosq(M_PIq * g / grid), fb = legendre_series(G[i], deg, xb);
+            if (g == grid) xb = 1;
+            if ((fa < 0) != (fb < 0)) {
+                quad lo = xa, hi = xb, flo = fa;
+                for (int it = 0; it < 300 && hi - lo > 1e-36Q; ++it) {
+                    quad mid = (lo + hi) / 2, fm = legendre_series(G[i], deg, mid);
+                    if ((fm < 0) == (flo < 0)) { lo = mid; flo = fm; } else hi = mid;
+                }
+                if (N + found >= GP_MAXN) return -1;
+                nodes[N + found++] = (lo + hi) / 2;
+            }
+            xa = xb; fa = fb;
+        }
+        if (found != deg) return -1;
+        N += found;
+    }
+    /* ascending order */
+    for (int a = 1; a < N; ++a)
+        for (int c = a; c > 0 && nodes[c] < nodes[c - 1]; --c) { quad t = nodes[c]; nodes[c] = nodes[c - 1]; nodes[c - 1] = t; }
+    quad *A = calloc((size_t)N * N, sizeof(quad)), *b = calloc(N, sizeof(quad)), *z = calloc(N, sizeof(quad));
+    for (int k = 0; k < N; ++k) {
+        for (int j = 0; j < N; ++j) {
+            quad p, dp;
+            legendre(k, nodes[j], &p, &dp);
+            A[k * N + j] = p;
+        }
+        b[k] = k == 0 ? 2 : 0;
+    }
+    int rc = solve_quad(N, A, b, z);
+    for (int j = 0; j < N && !rc; ++j) {
+        x[j] = (double)((1 + nodes[j]) / 2);
+        w[j] = (double)(z[j] / 2);
+    }
+    free(A); free(b); free(z);
+    return rc ? -1 : N;
+}
+
 /* Public: fill nodes/weights of level l, return n_l (or -1). */
 int sgo_rule(int rule, int l, double *x, double *w) {
     int n = sgo_node_count(rule, l);
@@ -111,6 +274,12 @@ int sgo_rule(int rule, int l, double *x, double *w) {
     if (rule == SGO_RULE_CC) {
         if (l > SGO_MAX_LEVEL) return -1;
         cc_rule(n, x, w);
+    } else if (rule == SGO_RULE_TRAP) {
+        if (l > SGO_MAX_LEVEL) return -1;
+        trap_rule(l, x, w);
+    } else if (rule == SGO_RULE_GP) {
+        if (n > GP_MAXN) return -1;
+        if (gp_rule(gp_extensions(l), x, w) != n) return -1;
     } else {
         if (n > SGO_MAX_GL) return -1;
         gl_rule(n, x, w);

@@ -1,7 +1,9 @@
 // plan.cpp — host planning for the B200 Smolyak path (compiled by g++; uses __float128).
 //
-// K0 (rules):  Clenshaw-Curtis (Eq 2.11) and Gauss-Legendre (PAPER.md:133-147,
-//              Eq 2.13) on [0,1] (reading R2), evaluated in __float128 and rounded once to double.
+// K0 (rules):  trapezoidal (Eq 2.10), Clenshaw-Curtis (Eq 2.11),
+//              Gauss-Patterson (Eq 2.12; delayed sequence of PAPER.md:615) and
+//              Gauss-Legendre (Eq 2.13) on [0,1] (reading R2), evaluated in
+//              __float128 and rounded once to double.
 // K1 (counts): per-depth segment counts of the prefix tree, subtree point counts (PAPER.md:73-75
 //              n_d^q), balanced shard ranges of depth-1 subtrees, launch geometry.
 #include "plan.h"
@@ -17,10 +19,22 @@
 typedef __float128 q128;
 typedef unsigned __int128 u128;
 
+// Gauss-Patterson level l -> Patterson rule index k (2^k - 1 points): the smallest rule whose degree
+// of exactness (1 for k = 1, 3 * 2^(k-1) - 1 for k >= 2) reaches 2l - 1, the exactness of the
+// l-point Gauss-Legendre rule.  Gives the "delayed" sequence n_l = 1, 3, 3, 7, 7, 7, 15, ... that
+// PAPER.md:615 lists for r = 3 (reading R16), and reproduces the paper's node counts (Tables 4.1,
+// 4.3, 4.5, 4.6).
+static int gp_index(int l) {
+    int k = 1;
+    while ((k == 1 ? 1 : 3 * (1 << (k - 1)) - 1) < 2 * l - 1) ++k;
+    return k;
+}
+
 int host_node_count(int rule, int l) {
     if (l < 1) return -1;
-    if (rule == SG_RULE_CLENSHAW_CURTIS) return l == 1 ? 1 : (1 << (l - 1)) + 1;
+    if (rule == SG_RULE_CLENSHAW_CURTIS || rule == SG_RULE_TRAPEZOIDAL) return l == 1 ? 1 : (1 << (l - 1)) + 1;
     if (rule == SG_RULE_GAUSS_LEGENDRE) return l;
+    if (rule == SG_RULE_GAUSS_PATTERSON) return (1 << gp_index(l)) - 1;
     return -1;
 }
 
@@ -88,12 +102,176 @@ static void gl_rule_q(int n, double *x, double *w) {
     }
 }
 
+// Trapezoidal rule (Eq 2.10) on [0,1]: x_j = (j-1)/(n-1), weights 1/(n-1) with the
+// first and last halved (the paper's h = 2^{2-l} on [-1,1], halved by the map); level 1 = midpoint,
+// weight 1 (reading R3).  All values are exact dyadic rationals.
+static void trap_rule_q(int n, double *x, double *w) {
+    if (n == 1) {
+        x[0] = 0.5;
+        w[0] = 1.0;
+        return;
+    }
+    const int m = n - 1;
+    for (int j = 0; j < n; ++j) {
+        x[j] = (double)j / (double)m;
+        w[j] = (j == 0 || j == m) ? 0.5 / (double)m : 1.0 / (double)m;
+    }
+}
+
+// Gauss-Legendre n-point rule on [-1,1] in quad (ascending), for the Patterson construction.
+static void gl_quad(int n, std::vector<q128> &t, std::vector<q128> &wt) {
+    t.assign(n, 0);
+    wt.assign(n, 0);
+    for (int i = 0; i < n; ++i) {
+        q128 th = M_PIq * (q128)(4 * (i + 1) - 1) / (q128)(4 * n + 2);
+        q128 r = -cosq(th), p0 = 1, p1 = r, dp = 0;
+        for (int it = 0; it < 100; ++it) {
+            p0 = 1;
+            p1 = r;
+            for (int k = 2; k <= n; ++k) {
+                q128 p2 = ((q128)(2 * k - 1) * r * p1 - (q128)(k - 1) * p0) / (q128)k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = (q128)n * (p0 - r * p1) / (1 - r * r);
+            q128 step = p1 / dp;
+            r -= step;
+            if (fabsq(step) <= 1e-34Q) break;
+        }
+        p0 = 1;
+        p1 = r;
+        for (int k = 2; k <= n; ++k) {
+            q128 p2 = ((q128)(2 * k - 1) * r * p1 - (q128)(k - 1) * p0) / (q128)k;
+            p0 = p1;
+            p1 = p2;
+        }
+        dp = (q128)n * (p0 - r * p1) / (1 - r * r);
+        t[i] = r;
+        wt[i] = (q128)2 / ((1 - r * r) * dp * dp);
+    }
+}
+
+// P_0(x) .. P_N(x) by the three-term recurrence
+static void legendre_all(int N, q128 x, q128 *P) {
+    P[0] = 1;
+    if (N >= 1) P[1] = x;
+    for (int k = 2; k <= N; ++k) P[k] = ((q128)(2 * k - 1) * x * P[k - 1] - (q128)(k - 1) * P[k - 2]) / (q128)k;
+}
+
+// Gauss-Patterson rule k (2^k - 1 points) on [-1,1] in quad (Eq 2.12): start from the
+// 1-point Gauss rule (the zero of P_1) and extend m -> 2m + 1 points, m = 2^s - 1: the m + 1 new nodes
+// are the zeros of G = P_{m+1} + sum_j a_j P_j, orthogonal to every polynomial of degree <= m with
+// respect to the weight p_m(t) = prod (t - old nodes).  G has the parity of m + 1 (even), so only the
+// equations against odd P_i and the even coefficients a_j remain: a square (m+1)/2 system, solved
+// in quad with partial pivoting (integrals by Gauss-Legendre, exact for degree 3m + 1).  The new zeros
+// interlace the old nodes: one by bisection in each gap.  Weights: interpolatory, w_j = integral of
+// the Lagrange basis polynomial (Gauss-Legendre, exact).  Returns false if a bracket fails.
+static bool gp_quad(int k, std::vector<q128> &t, std::vector<q128> &wt) {
+    t.assign(1, (q128)0);
+    for (int s = 1; s < k; ++s) {
+        const int m = (int)t.size(), nu = (m + 1) / 2, nq = (3 * m + 3) / 2 + 1;
+        std::vector<q128> g, gw;
+        gl_quad(nq, g, gw);
+        std::vector<q128> A((size_t)nu * nu, 0), b(nu, 0), P(m + 2);
+        for (int q = 0; q < nq; ++q) {
+            q128 pm = 1;
+            for (int i = 0; i < m; ++i) pm *= g[q] - t[i];
+            legendre_all(m + 1, g[q], P.data());
+            for (int r = 0; r < nu; ++r) {
+                const q128 f = gw[q] * pm * P[2 * r + 1];
+                for (int c = 0; c < nu; ++c) A[(size_t)r * nu + c] += f * P[2 * c];
+                b[r] -= f * P[m + 1];
+            }
+        }
+        for (int c = 0; c < nu; ++c) {   // Gaussian elimination, partial pivoting
+            int piv = c;
+            for (int r = c + 1; r < nu; ++r)
+                if (fabsq(A[(size_t)r * nu + c]) > fabsq(A[(size_t)piv * nu + c])) piv = r;
+            if (piv != c) {
+                for (int j = 0; j < nu; ++j) std::swap(A[(size_t)c * nu + j], A[(size_t)piv * nu + j]);
+                std::swap(b[c], b[piv]);
+            }
+            for (int r = c + 1; r < nu; ++r) {
+                const q128 f = A[(size_t)r * nu + c] / A[(size_t)c * nu + c];
+                for (int j = c; j < nu; ++j) A[(size_t)r * nu + j] -= f * A[(size_t)c * nu + j];
+                b[r] -= f * b[c];
+            }
+        }
+        std::vector<q128> a(nu, 0);
+        for (int c = nu - 1; c >= 0; --c) {
+            q128 v = b[c];
+            for (int j = c + 1; j < nu; ++j) v -= A[(size_t)c * nu + j] * a[j];
+            a[c] = v / A[(size_t)c * nu + c];
+        }
+        auto G = [&](q128 x) {
+            legendre_all(m + 1, x, P.data());
+            q128 v = P[m + 1];
+            for (int c = 0; c < nu; ++c) v += a[c] * P[2 * c];
+            return v;
+        };
+        std::vector<q128> nt = t;
+        for (int i = 0; i <= m; ++i) {
+            q128 lo = i == 0 ? (q128)-1 : t[i - 1], hi = i == m ? (q128)1 : t[i];
+            q128 flo = G(lo), fhi = G(hi);
+            if (!(flo * fhi < 0)) return false;
+            for (int it = 0; it < 200 && hi - lo > 1e-36Q; ++it) {
+                const q128 mid = (lo + hi) / 2, fm = G(mid);
+                if (fm == 0) {
+                    lo = hi = mid;
+                    break;
+                }
+                if ((fm < 0) == (flo < 0)) {
+                    lo = mid;
+                    flo = fm;
+                } else {
+                    hi = mid;
+                }
+            }
+            nt.push_back((lo + hi) / 2);
+        }
+        std::sort(nt.begin(), nt.end());
+        t = nt;
+    }
+    const int n = (int)t.size();
+    std::vector<q128> g, gw;
+    gl_quad(n / 2 + 2, g, gw);
+    wt.assign(n, 0);
+    for (int j = 0; j < n; ++j) {
+        q128 acc = 0;
+        for (size_t q = 0; q < g.size(); ++q) {
+            q128 lj = 1;
+            for (int i = 0; i < n; ++i)
+                if (i != j) lj *= (g[q] - t[i]) / (t[j] - t[i]);
+            acc += gw[q] * lj;
+        }
+        wt[j] = acc;
+    }
+    return true;
+}
+
+// Gauss-Patterson on [0,1] (reading R2): x = (1 + t)/2, w/2; the midpoint is exactly 1/2.
+static bool gp_rule_q(int l, double *x, double *w) {
+    std::vector<q128> t, wt;
+    if (!gp_quad(gp_index(l), t, wt)) return false;
+    for (size_t j = 0; j < t.size(); ++j) {
+        x[j] = (double)((1 + t[j]) / 2);
+        w[j] = (double)(wt[j] / 2);
+    }
+    return true;
+}
+
 int host_rule(int rule, int l, double *x, double *w) {
     int n = host_node_count(rule, l);
     if (n < 0) return -1;
     if (rule == SG_RULE_CLENSHAW_CURTIS) {
         if (l > SG_CC_MAX_LEVEL) return -1;
         cc_rule_q(n, x, w);
+    } else if (rule == SG_RULE_TRAPEZOIDAL) {
+        if (l > SG_CC_MAX_LEVEL) return -1;
+        trap_rule_q(n, x, w);
+    } else if (rule == SG_RULE_GAUSS_PATTERSON) {
+        if (gp_index(l) > SG_GP_MAX_K) return -1;
+        if (!gp_rule_q(l, x, w)) return -1;
     } else {
         if (n > SG_GL_MAX_N) return -1;
         gl_rule_q(n, x, w);
@@ -116,12 +294,16 @@ static u128 sat_mul(u128 a, u128 b) {
 int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, int merge, int rank, int world,
                     long long range_lo, long long range_hi, int fuse_mode) {
     if (d < 1 || L < 0) return SG_EINVAL;
-    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
+    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE && rule != SG_RULE_TRAPEZOIDAL &&
+        rule != SG_RULE_GAUSS_PATTERSON)
+        return SG_EINVAL;
     if (kind < 0 || kind > 3 || form < 0 || form > 1 || merge < 0 || merge > 1) return SG_EINVAL;
     hp.merge = merge;
     if (world < 1 || rank < 0 || rank >= world) return SG_EINVAL;
     if (d > SG_MAX_D || L > SG_MAX_L) return SG_EUNSUPPORTED;
-    if (rule == SG_RULE_CLENSHAW_CURTIS && L + 1 > SG_CC_MAX_LEVEL) return SG_EUNSUPPORTED;
+    if ((rule == SG_RULE_CLENSHAW_CURTIS || rule == SG_RULE_TRAPEZOIDAL) && L + 1 > SG_CC_MAX_LEVEL)
+        return SG_EUNSUPPORTED;
+    if (rule == SG_RULE_GAUSS_PATTERSON && gp_index(L + 1) > SG_GP_MAX_K) return SG_EUNSUPPORTED;
     if (rule == SG_RULE_GAUSS_LEGENDRE && L + 1 > SG_GL_MAX_N) return SG_EUNSUPPORTED;
     hp.d = d;
     hp.L = L;

@@ -18,6 +18,7 @@
 #define SG_MAX_L 19        // L + 1 <= 20 levels in the tables
 #define SG_CC_MAX_LEVEL 12 // CC weights are O(n^2) quad evaluations; n_12 = 2049
 #define SG_GL_MAX_N 64
+#define SG_GP_MAX_K 6      // Gauss-Patterson rules up to 2^6 - 1 = 63 points (levels <= 48)
 #define SG_MAX_D ((1 << 20) - 1)
 #define SG_META_KBITS 20
 

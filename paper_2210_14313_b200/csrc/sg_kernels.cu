@@ -2003,7 +2003,9 @@ extern "C" int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_opti
 
 extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
     if (!x || !w || level < 1) return SG_EINVAL;
-    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE) return SG_EINVAL;
+    if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE && rule != SG_RULE_TRAPEZOIDAL &&
+        rule != SG_RULE_GAUSS_PATTERSON)
+        return SG_EINVAL;
     int n = host_rule((int)rule, level, x, w);
     return n < 0 ? SG_EUNSUPPORTED : n;
 }

@@ -20,7 +20,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 # Rule ids follow the paper's r parameter: 2 = Clenshaw-Curtis, 4 = Gauss-Legendre.
+RULE_TRAP = 1   # trapezoidal (Eq 2.10)
 RULE_CC = 2
+RULE_GP = 3     # Gauss-Patterson, delayed sequence
 RULE_GL = 4
 # Integrand kinds (BASELINE.json configs; Genz families).
 KIND_EXP = 0      # exp(sum c_k x_k)
@@ -29,7 +31,8 @@ KIND_PEAK = 2     # prod (c_k^-2 + (x_k - w_k)^2)^-1
 KIND_GAUSS = 3    # exp(-sum c_k^2 (x_k - w_k)^2)
 
 KIND_NAMES = {KIND_EXP: "exp", KIND_OSC: "osc", KIND_PEAK: "peak", KIND_GAUSS: "gauss"}
-RULE_NAMES = {RULE_CC: "clenshaw_curtis", RULE_GL: "gauss_legendre"}
+RULE_NAMES = {RULE_TRAP: "trapezoidal", RULE_CC: "clenshaw_curtis", RULE_GP: "gauss_patterson",
+              RULE_GL: "gauss_legendre"}
 
 
 @dataclass

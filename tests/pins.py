@@ -58,12 +58,102 @@ def mp_rule(rule: int, level: int):
                 xs.append(float((1 + t) / 2))
                 ws.append(float(wt / 2))
             return tuple(xs), tuple(ws)
+        if rule == S.RULE_TRAP:
+            # Eq 2.10 on [-1,1]: x_j = (j-1) 2^{2-l} - 1, w = 2^{2-l}, ends halved; mapped to [0,1]
+            if level == 1:
+                return (0.5,), (1.0,)
+            n = 2 ** (level - 1) + 1
+            h = mp.mpf(2) ** (2 - level)
+            xs = [float(((j - 1) * h - 1 + 1) / 2) for j in range(1, n + 1)]
+            ws = [float((h / 2 if j in (1, n) else h) / 2) for j in range(1, n + 1)]
+            return tuple(xs), tuple(ws)
+        if rule == S.RULE_GP:
+            t, w = _mp_patterson(gp_extensions(level))
+            return tuple(float((1 + a) / 2) for a in t), tuple(float(b / 2) for b in w)
     raise ValueError(rule)
 
 
+def gp_extensions(level: int) -> int:
+    """Patterson extensions for Gauss-Patterson level l: the first rule (2^{i+1}-1 points, degree of
+    exactness 1 or 3*2^i - 1) exact to the degree 2l-1 of the l-point Gauss rule (PAPER.md:615
+    sequence 1, 3, 3, 7, 7, 7, 15, ...)."""
+    i = 0
+    while (1 if i == 0 else 3 * 2 ** i - 1) < 2 * level - 1:
+        i += 1
+    return i
+
+
+def _mp_legendre_all(n, x):
+    P = [mp.mpf(1), x]
+    for k in range(2, n + 1):
+        P.append(((2 * k - 1) * x * P[-1] - (k - 1) * P[-2]) / k)
+    return P[:n + 1]
+
+
+@functools.lru_cache(maxsize=None)
+def _mp_gauss(n):
+    """n-point Gauss-Legendre on [-1,1] at the working precision (Newton on P_n)."""
+    xs, ws = [], []
+    for i in range(1, n + 1):
+        x = mp.cos(mp.pi * (i - mp.mpf(0.25)) / (n + mp.mpf(0.5)))
+        for _ in range(200):
+            P = _mp_legendre_all(n, x)
+            dp = n * (x * P[n] - P[n - 1]) / (x * x - 1)
+            dx = P[n] / dp
+            x -= dx
+            if abs(dx) < mp.mpf(10) ** (-mp.mp.dps + 3):
+                break
+        P = _mp_legendre_all(n, x)
+        dp = n * (x * P[n] - P[n - 1]) / (x * x - 1)
+        xs.append(x)
+        ws.append(2 / ((1 - x * x) * dp * dp))
+    return xs, ws
+
+
+@functools.lru_cache(maxsize=None)
+def _mp_patterson(ext):
+    """Gauss-Patterson nodes/weights on [-1,1] at 60 digits: Kronrod-Patterson extensions of the
+    1-point Gauss rule; each extension's m+1 new nodes are the zeros of the polynomial of degree
+    m+1 orthogonal to all polynomials of degree <= m against prod(x - old nodes) (mpmath findroot
+    between consecutive old nodes); weights from the exact integrals of the Lagrange basis."""
+    with mp.workdps(60):
+        t = [mp.mpf(0)]
+        for _ in range(ext):
+            m = len(t)
+            xs, ws = _mp_gauss(2 * m + 2)
+            pm = [mp.fprod([x - a for a in t]) for x in xs]
+            Ps = [_mp_legendre_all(m + 1, x) for x in xs]
+            # G has the parity of m+1 (even), prod(x - old) that of m (odd): only odd test
+            # polynomials P_i give nontrivial conditions, on the even coefficients of G
+            idx = [j for j in range(m + 1) if j % 2 == 0]
+            rows = [i for i in range(m + 1) if i % 2 == 1]
+            A = mp.matrix(len(rows), len(idx))
+            b = mp.matrix(len(rows), 1)
+            for r, i in enumerate(rows):
+                for c, j in enumerate(idx):
+                    A[r, c] = mp.fsum(w * P[i] * P[j] * p for w, P, p in zip(ws, Ps, pm))
+                b[r] = -mp.fsum(w * P[i] * P[m + 1] * p for w, P, p in zip(ws, Ps, pm))
+            a = mp.lu_solve(A, b)
+
+            def G(x, a=a, m=m, idx=idx):
+                P = _mp_legendre_all(m + 1, x)
+                return P[m + 1] + mp.fsum(a[c] * P[j] for c, j in enumerate(idx))
+
+            ends = [mp.mpf(-1)] + t + [mp.mpf(1)]
+            t = sorted(t + [mp.findroot(G, (lo, hi), solver="anderson")
+                            for lo, hi in zip(ends[:-1], ends[1:])])
+        n = len(t)
+        xs, ws = _mp_gauss(n // 2 + 2)
+        w = [mp.fsum(W * mp.fprod([(X - t[i]) / (t[j] - t[i]) for i in range(n) if i != j])
+                     for X, W in zip(xs, ws)) for j in range(n)]
+        return t, w
+
+
 def node_count(rule: int, level: int) -> int:
-    if rule == S.RULE_CC:
+    if rule in (S.RULE_CC, S.RULE_TRAP):
         return 1 if level == 1 else 2 ** (level - 1) + 1
+    if rule == S.RULE_GP:
+        return 2 ** (gp_extensions(level) + 1) - 1
     return level
 
 

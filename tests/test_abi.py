@@ -42,7 +42,8 @@ def _rule(L, rule, level):
     return rc, x, w
 
 
-@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 11)), (S.RULE_GL, range(1, 30))])
+@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 11)), (S.RULE_GL, range(1, 30)),
+                                         (S.RULE_TRAP, range(1, 13)), (S.RULE_GP, range(1, 30))])
 def test_library_rules_bit_identical_to_oracle(L, rule, levels):
     for l in levels:
         rc, x, w = _rule(L, rule, l)
@@ -54,7 +55,10 @@ def test_library_rules_bit_identical_to_oracle(L, rule, levels):
 
 def test_rule_table_limits(L):
     assert _rule(L, S.RULE_CC, 13)[0] == -2    # SG_EUNSUPPORTED beyond CC level 12
-    assert _rule(L, 3, 2)[0] == -1             # Gauss-Patterson not built: SG_EINVAL
+    assert _rule(L, 5, 2)[0] == -1             # no rule 5: SG_EINVAL
+    assert _rule(L, S.RULE_TRAP, 13)[0] == -2  # trapezoid shares the CC level limit
+    assert _rule(L, S.RULE_GP, 48)[0] == 63    # 63-point Patterson rule up to level 48
+    assert _rule(L, S.RULE_GP, 49)[0] == -2
 
 
 def _query(L, d, q, rule, kind=0, form=0, rank=0, world=1, lo=0, hi=-1):

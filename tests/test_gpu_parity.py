@@ -97,6 +97,10 @@ CASES = [
     (49, 7, 6, S.RULE_GL, S.KIND_EXP), (50, 12, 5, S.RULE_CC, S.KIND_OSC),
     (51, 130, 2, S.RULE_GL, S.KIND_OSC), (52, 4, 8, S.RULE_CC, S.KIND_GAUSS),
     (53, 300, 2, S.RULE_CC, S.KIND_PEAK), (54, 20, 4, S.RULE_GL, S.KIND_GAUSS),
+    # trapezoidal (r = 1) and Gauss-Patterson (r = 3, delayed: repeated levels) rules
+    (55, 8, 5, S.RULE_GP, S.KIND_OSC), (56, 50, 3, S.RULE_GP, S.KIND_GAUSS),
+    (57, 6, 6, S.RULE_TRAP, S.KIND_EXP), (58, 100, 3, S.RULE_TRAP, S.KIND_PEAK),
+    (59, 3, 9, S.RULE_GP, S.KIND_PEAK),
 ]
 
 
@@ -194,7 +198,8 @@ def test_errors_and_nonfinite(api):
 @pytest.mark.parametrize("seed,d,L,rule,kind", [
     (61, 40, 3, S.RULE_CC, S.KIND_OSC), (62, 75, 4, S.RULE_CC, S.KIND_GAUSS),
     (63, 33, 4, S.RULE_GL, S.KIND_PEAK), (64, 9, 5, S.RULE_GL, S.KIND_OSC),
-    (65, 200, 3, S.RULE_GL, S.KIND_EXP)])
+    (65, 200, 3, S.RULE_GL, S.KIND_EXP), (66, 45, 4, S.RULE_GP, S.KIND_OSC),
+    (67, 60, 3, S.RULE_TRAP, S.KIND_OSC)])
 def test_last_pass_variants(api, monkeypatch, mode, seed, d, L, rule, kind):
     if mode == "fused":
         monkeypatch.setenv("SG_B200_FUSE", "1")

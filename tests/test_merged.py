@@ -212,6 +212,7 @@ MCASES = [
     (77, 65, 3, S.RULE_CC, S.KIND_OSC), (78, 7, 6, S.RULE_GL, S.KIND_EXP),
     (79, 12, 5, S.RULE_CC, S.KIND_OSC), (80, 130, 4, S.RULE_CC, S.KIND_OSC),
     (81, 20, 4, S.RULE_GL, S.KIND_GAUSS), (82, 4, 0, S.RULE_CC, S.KIND_EXP),
+    (86, 9, 5, S.RULE_GP, S.KIND_OSC), (87, 40, 3, S.RULE_TRAP, S.KIND_GAUSS),
 ]
 
 

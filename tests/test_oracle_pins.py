@@ -5,6 +5,7 @@ paper-printed values (Tables 5.6-5.8), 50-digit generating-function values of Eq
 closed-form integrals, weight-sum and polynomial-exactness identities, special cases (d = 1, L = 0,
 odd symmetry) and a brute-force tensor enumeration written independently below.
 """
+import functools
 import itertools
 import json
 import math
@@ -28,7 +29,8 @@ def qval(res):
 # ----------------------------------------------------------------------------------------------
 # P4: 1-D rules
 # ----------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 10)), (S.RULE_GL, range(1, 16))])
+@pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 10)), (S.RULE_GL, range(1, 16)),
+                                         (S.RULE_TRAP, range(1, 12)), (S.RULE_GP, range(1, 21))])
 def test_rule_tables_bit_identical_to_mpmath(rule, levels):
     for l in levels:
         x, w = oracle.rule(rule, l)
@@ -67,6 +69,119 @@ def test_rule_exactness_and_weight_sum(rule):
             for k in range(deg + 1):
                 q = mp.fsum(mp.mpf(wj) * mp.mpf(xj) ** k for xj, wj in zip(x, w))
                 assert abs(q - mp.mpf(1) / (k + 1)) < 5e-15, (rule, l, k)
+
+
+def test_trapezoid_and_patterson_examples():
+    # trapezoid (Eq 2.10) level 3 on [0,1]: h = 1/4, weights (1,2,2,2,1)/8, exact dyadics
+    x, w = oracle.rule(S.RULE_TRAP, 3)
+    assert list(x) == [0.0, 0.25, 0.5, 0.75, 1.0]
+    assert list(w) == [0.125, 0.25, 0.25, 0.25, 0.125]
+    # the 3-point Patterson rule is the 3-point Gauss rule: 1/2 -+ sqrt(15)/10, weights 5/18, 4/9
+    x, w = oracle.rule(S.RULE_GP, 2)
+    gx, gw = oracle.rule(S.RULE_GL, 3)
+    np.testing.assert_allclose(x, gx, rtol=0, atol=2e-16)
+    np.testing.assert_allclose(w, [5 / 18, 4 / 9, 5 / 18], rtol=0, atol=2e-16)
+    assert x[1] == 0.5
+    # delayed sequence of PAPER.md:615 (q = 1..10 -> N = 1, 3, 3, 7, 7, 7, 15, 15, 15, 15)
+    assert [oracle.node_count(S.RULE_GP, l) for l in range(1, 11)] == [1, 3, 3, 7, 7, 7, 15, 15, 15, 15]
+    assert [oracle.node_count(S.RULE_GP, l) for l in (13, 24, 25)] == [31, 31, 63]
+
+
+@pytest.mark.parametrize("ext", [1, 2, 3, 4, 5])
+def test_patterson_exactness_degree(ext):
+    """2^{i+1}-1 Patterson points integrate every polynomial of degree <= 3*2^i - 1 exactly, and
+    x^{3*2^i} not (the defining property of the Kronrod-Patterson extension; unique given the
+    nested node set).  Checked on [-1,1]-symmetric moments of x - 1/2 on [0,1]."""
+    l = [2, 4, 7, 13, 25][ext - 1]
+    x, w = oracle.rule(S.RULE_GP, l)
+    assert len(x) == 2 ** (ext + 1) - 1
+    deg = 3 * 2 ** ext - 1
+    with mp.workdps(40):
+        xs = [mp.mpf(a) - mp.mpf(0.5) for a in x]
+        for k in range(0, deg + 2):
+            q = mp.fsum(mp.mpf(b) * a ** k for a, b in zip(xs, w))
+            scale = mp.mpf(2) ** (-k) / (k + 1)          # |even moment| of (x - 1/2)^k on [0,1]
+            exact = mp.mpf(0) if k % 2 else scale
+            if k <= deg:
+                assert abs(q - exact) < 1e-14 * scale, (ext, k, q - exact)
+            elif ext <= 3:
+                # beyond the degree the error is 0.16 / 1.8e-3 / 6.7e-8 relative; for the 31- and
+                # 63-point rules it falls below the double rounding of the nodes (not testable)
+                assert abs(q - exact) > 1e-9 * scale, (ext, k)
+
+
+def test_trapezoid_error_order():
+    """Eq 2.10 error estimate C 2^{-2q}: the error for e^x on [0,1] falls 4x per level."""
+    errs = []
+    for l in range(3, 9):
+        x, w = oracle.rule(S.RULE_TRAP, l)
+        with mp.workdps(40):
+            q = mp.fsum(mp.mpf(b) * mp.exp(mp.mpf(a)) for a, b in zip(x, w))
+            errs.append(q - (mp.e - 1))
+    for a, b in zip(errs, errs[1:]):
+        assert 3.9 < a / b < 4.1
+
+
+@pytest.mark.parametrize("rule", [S.RULE_GP, S.RULE_TRAP])
+def test_new_rules_nested_exactly(rule):
+    for l in range(1, 12 if rule == S.RULE_TRAP else 20):
+        xa, _ = oracle.rule(rule, l)
+        xb, _ = oracle.rule(rule, l + 1)
+        assert set(xa.tolist()) <= set(xb.tolist()), (rule, l)
+
+
+@functools.lru_cache(maxsize=None)
+def _nodes(rule, l):
+    return tuple(oracle.rule(rule, l)[0].tolist())
+
+
+def _distinct_points_formula(rule, d, L):
+    """Distinct points of the Smolyak grid with max level L+1 for a nested rule: each point is new
+    at exactly one level per coordinate, so the count is [z^{<=L}] (sum_l new_l z^{l-1})^d with
+    new_l = #(nodes of level l not in level l-1), taken from the oracle's double tables."""
+    prev = set()
+    new = []
+    for l in range(1, L + 2):
+        xs = set(_nodes(rule, l))
+        new.append(len(xs - prev))
+        prev |= xs
+    poly = [1] + [0] * L
+    for _ in range(d):
+        nw = [0] * (L + 1)
+        for a in range(L + 1):
+            for b in range(L + 1 - a):
+                nw[a + b] += poly[a] * new[b]
+        poly = nw
+    return sum(poly)
+
+
+def _distinct_points_brute(rule, d, L):
+    pts = set()
+    for lv in itertools.product(range(1, L + 2), repeat=d):
+        if sum(lv) - d > L:
+            continue
+        pts.update(itertools.product(*[_nodes(rule, l) for l in lv]))
+    return len(pts)
+
+
+# PAPER.md:322-401 "Total nodes" columns (Gauss-Patterson, r = 3), reading R1: the paper's accuracy
+# level q is the maximum 1-D level, L = q - 1.  Rows beyond d = 12 of Tables 4.5/4.6 do not follow
+# any nested count (printed 5036449 < 4286913 * 4 growth breaks), so they are not pins.
+_NODE_ROWS = (
+    [("4.1", 2, q, n) for q, n in [(6, 33), (7, 65), (9, 97), (10, 161), (13, 257), (14, 321)]]
+    + [("4.3", 3, q, n) for q, n in [(9, 495), (10, 751), (11, 1135), (13, 1759), (14, 2335),
+                                     (15, 2527), (16, 3679)]]
+    + [("4.5", d, 10, n) for d, n in [(2, 161), (4, 2881), (8, 206465), (10, 1041185),
+                                      (12, 4286913)]]
+    + [("4.6", d, 12, n) for d, n in [(2, 161), (4, 6465), (6, 93665), (8, 791169), (10, 5020449),
+                                      (12, 25549761)]])
+
+
+@pytest.mark.parametrize("table,d,q,n", _NODE_ROWS, ids=lambda v: str(v))
+def test_paper_total_nodes_gauss_patterson(table, d, q, n):
+    assert _distinct_points_formula(S.RULE_GP, d, q - 1) == n
+    if d <= 3:
+        assert _distinct_points_brute(S.RULE_GP, d, q - 1) == n
 
 
 def test_cc_nesting_exact():
@@ -111,6 +226,8 @@ CASES = [
     (9, 12, 3, S.RULE_GL, S.KIND_PEAK), (10, 20, 2, S.RULE_CC, S.KIND_GAUSS),
     (11, 3, 6, S.RULE_GL, S.KIND_OSC), (12, 2, 7, S.RULE_CC, S.KIND_PEAK),
     (13, 40, 2, S.RULE_GL, S.KIND_GAUSS), (14, 6, 4, S.RULE_GL, S.KIND_EXP),
+    (15, 5, 5, S.RULE_GP, S.KIND_OSC), (16, 30, 3, S.RULE_GP, S.KIND_GAUSS),
+    (17, 4, 5, S.RULE_TRAP, S.KIND_EXP), (18, 9, 3, S.RULE_TRAP, S.KIND_PEAK),
 ]
 
 
@@ -154,7 +271,7 @@ def test_closed_forms_configs_1_2():
     assert abs((r - cf) / cf) < 1e-8           # ~3.2e-9
 
 
-@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL, S.RULE_GP, S.RULE_TRAP])
 @pytest.mark.parametrize("d,L", [(1, 5), (2, 4), (5, 3), (30, 2), (4, 7)])
 def test_weight_sum_is_one(rule, d, L):
     """f = 1 (exp kind with c = 0): sum of all combination weights is 1 on [0,1]^d.
@@ -170,7 +287,7 @@ def test_weight_sum_is_one(rule, d, L):
     assert abs(qval(res) - 1) <= bound * d * 2.0 ** -52
 
 
-@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL, S.RULE_GP])
 def test_polynomial_exactness(rule):
     """A exact for prod x_k^{a_k} when sum_k floor(a_k/2) <= L."""
     rng = np.random.default_rng(5)
@@ -195,7 +312,7 @@ def test_polynomial_exactness(rule):
     assert abs(qval(res) - mp.mpf(1) / 81) > 1e-6
 
 
-@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL])
+@pytest.mark.parametrize("rule", [S.RULE_CC, S.RULE_GL, S.RULE_GP, S.RULE_TRAP])
 def test_d1_is_the_1d_rule(rule):
     """d = 1: A(q,1) f = J^{q} f (coefficient C(0,0) = 1)."""
     for L in range(0, 6):
@@ -246,7 +363,8 @@ def _f_mp(kind, c, w, u, x):
 
 @pytest.mark.parametrize("seed,d,L,rule,kind", [
     (21, 2, 3, S.RULE_CC, S.KIND_OSC), (22, 3, 2, S.RULE_GL, S.KIND_PEAK),
-    (23, 2, 4, S.RULE_GL, S.KIND_EXP), (24, 3, 3, S.RULE_CC, S.KIND_GAUSS)])
+    (23, 2, 4, S.RULE_GL, S.KIND_EXP), (24, 3, 3, S.RULE_CC, S.KIND_GAUSS),
+    (25, 2, 4, S.RULE_GP, S.KIND_OSC), (26, 3, 2, S.RULE_TRAP, S.KIND_PEAK)])
 def test_brute_force_tensor_enumeration(seed, d, L, rule, kind):
     p = S.random_problem(seed, d, L, rule, kind)
     w = p.w if p.w is not None else np.zeros(d)

@@ -18,7 +18,8 @@ def main():
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     p = S.baseline_config(cfg)
     plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
-                    merge=int(os.environ.get("QUICK_MERGE", "0")))
+                    merge=int(os.environ.get("QUICK_MERGE", "0")),
+                    method=int(os.environ.get("QUICK_METHOD", "0")))
     for _ in range(steps):
         out = plan.sg_integrate()
         plan.sg_finalize(out, 1)

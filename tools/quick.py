@@ -26,7 +26,8 @@ def main():
         p = S.baseline_config(i)
         t0 = time.time()
         plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
-                        merge=int(os.environ.get("QUICK_MERGE", "0")))
+                        merge=int(os.environ.get("QUICK_MERGE", "0")),
+                        method=int(os.environ.get("QUICK_METHOD", "0")))
         tplan = time.time() - t0
         hi, lo = plan.integrate_host()
         dp = pins.dp_value(p)
