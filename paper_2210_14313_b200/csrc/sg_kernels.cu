@@ -398,23 +398,30 @@ struct LeafAcc {
     double h, l;
 };
 
+// Biased grid accumulator (all leaf kernels).  The lane's high accumulator a.h starts at sigma =
+// 1.5 * 2^m (2^m > 2 * bound on the sum of |P F| over the lane's children) and stays inside the
+// binade [2^m, 2^(m+1)), where the double grid is u = ulp(sigma).  fma(P.hi, F.hi, a.h) therefore adds
+// P.hi * F.hi rounded ONCE to the grid, exactly; the grid part h = new - old is exact (Sterbenz), and
+// the remainder P.hi*F.hi - h (|.| <= u/2) and the cross terms P.hi*F.lo + P.lo*F.hi go to a.l by
+// FMAs.  The lane result is (a.h - sigma) + a.l.  One FP64 instruction per product fewer than
+// forming h = fma(P.hi, F.hi, sigma) - sigma and adding it.
 template <bool CPLX>
 __device__ __forceinline__ void leaf_term(const dd &er, const dd &ei, const double2 f, const double2 fi,
-                                          double sigma, LeafAcc &a) {
-    // h = round_u(P.hi * F.hi) in ONE rounding: fma(P.hi, F.hi, sigma) lands in [2^m, 2^(m+1)) where
-    // the double grid is u = ulp(sigma); subtracting sigma is exact (Sterbenz).  The remainder
-    // P.hi*F.hi - h (|.| <= u/2) and the cross terms P.hi*F.lo + P.lo*F.hi go to a.l by FMAs.
+                                          LeafAcc &a) {
     if (!CPLX) {
-        const double h = fma(er.hi, f.x, sigma) - sigma;
-        a.h += h;
+        const double a1 = fma(er.hi, f.x, a.h);
+        const double h = a1 - a.h;
+        a.h = a1;
         a.l += fma(er.hi, f.x, -h);
         a.l = fma(er.hi, f.y, a.l);
         a.l = fma(er.lo, f.x, a.l);
     } else {
-        // Re((er + i ei)(f + i fi)) = er f - ei fi
-        const double h1 = fma(er.hi, f.x, sigma) - sigma;
-        const double h2 = fma(-ei.hi, fi.x, sigma) - sigma;
-        a.h += h1 + h2;   // exact: multiples of u, |h1 + h2| < 2^(m+1)
+        // Re((er + i ei)(f + i fi)) = er f - ei fi, both grid parts added to a.h in turn
+        const double a1 = fma(er.hi, f.x, a.h);
+        const double h1 = a1 - a.h;
+        const double a2 = fma(-ei.hi, fi.x, a1);
+        const double h2 = a2 - a1;
+        a.h = a2;
         a.l += fma(er.hi, f.x, -h1) + fma(-ei.hi, fi.x, -h2);
         a.l = fma(er.hi, f.y, a.l);
         a.l = fma(er.lo, f.x, a.l);
@@ -447,13 +454,13 @@ __device__ __forceinline__ void leaf_rows(const double2 *__restrict__ Fr, const 
                 for (int j = 0; j < (NJ > 0 ? NJ : 1); ++j) {
                     const double2 f = __ldg(fr + j);
                     const double2 g = CPLX ? __ldg(fi + j) : make_double2(0.0, 0.0);
-                    leaf_term<CPLX>(er, ei, f, g, sigma, acc[j]);
+                    leaf_term<CPLX>(er, ei, f, g, acc[j]);
                 }
             } else {
                 for (int j = 0; j < nj; ++j) {
                     const double2 f = __ldg(fr + j);
                     const double2 g = CPLX ? __ldg(fi + j) : make_double2(0.0, 0.0);
-                    leaf_term<CPLX>(er, ei, f, g, sigma, acc[0]);
+                    leaf_term<CPLX>(er, ei, f, g, acc[0]);
                 }
             }
         }
@@ -467,13 +474,13 @@ __device__ __forceinline__ dd leaf_level(const double2 *Fr, const double2 *Fi, i
                                          int ks1, int k, const dd &pr, const dd &pim, double sigma) {
     LeafAcc acc[NJ > 0 ? NJ : 1];
 #pragma unroll
-    for (int j = 0; j < (NJ > 0 ? NJ : 1); ++j) acc[j] = LeafAcc{0.0, 0.0};
+    for (int j = 0; j < (NJ > 0 ? NJ : 1); ++j) acc[j] = LeafAcc{sigma, 0.0};   // biased accumulator
     // boundary rows (some lanes of the warp have k >= k'), then the unpredicated main rows
     leaf_rows<CPLX, NJ>(Fr, Fi, n, kb, min(kmain, ks1), k, true, pr, pim, sigma, acc);
     leaf_rows<CPLX, NJ>(Fr, Fi, n, max(kb, kmain), ks1, k, false, pr, pim, sigma, acc);
     dd s = {0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < (NJ > 0 ? NJ : 1); ++j) s = dd_add(s, dd_norm(acc[j].h, acc[j].l));
+    for (int j = 0; j < (NJ > 0 ? NJ : 1); ++j) s = dd_add(s, dd_norm(acc[j].h - sigma, acc[j].l));
     return s;
 }
 
@@ -546,18 +553,22 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
 // ---------------------------------------------------------------------------------------------
 template <bool CPLX>
 __device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const double2 f, const double2 fi,
-                                           double sigma, double &ah, double &al) {
-    // the remainder t = P.hi F.hi - h (one rounding) seeds the FMA chain of the cross terms
+                                           double &ah, double &al) {
+    // biased accumulator ah (see leaf_term); the remainder t = P.hi F.hi - h (one rounding) seeds the
+    // FMA chain of the cross terms.  Real: 6 FP64 instructions (4 DFMA + 2 DADD); oscillatory: 12.
     if (!CPLX) {
-        const double h = fma(er.hi, f.x, sigma) - sigma;
-        ah += h;
+        const double a1 = fma(er.hi, f.x, ah);
+        const double h = a1 - ah;
+        ah = a1;
         double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
         c = fma(er.hi, f.y, c);
         al += c;
     } else {
-        const double h1 = fma(er.hi, f.x, sigma) - sigma;
-        const double h2 = fma(-ei.hi, fi.x, sigma) - sigma;
-        ah += h1 + h2;
+        const double a1 = fma(er.hi, f.x, ah);
+        const double h1 = a1 - ah;
+        const double a2 = fma(-ei.hi, fi.x, a1);
+        const double h2 = a2 - a1;
+        ah = a2;
         double c = fma(er.lo, f.x, fma(er.hi, f.x, -h1));
         c = fma(er.hi, f.y, c);
         c = fma(-ei.lo, fi.x, c);
@@ -578,8 +589,7 @@ __device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const dou
 
 template <bool CPLX, int NJ, int NA, bool SMEM>
 __device__ __forceinline__ void leaf1_row(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi, int kp,
-                                          const dd &er, const dd &ei, double sigma, double (&ah)[NA],
-                                          double (&al)[NA]) {
+                                          const dd &er, const dd &ei, double (&ah)[NA], double (&al)[NA]) {
     double2 f[NJ], g[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
@@ -587,7 +597,7 @@ __device__ __forceinline__ void leaf1_row(const double2 *__restrict__ Fr, const 
         g[j] = CPLX ? (SMEM ? Fi[kp * NJ + j] : __ldg(Fi + kp * NJ + j)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) leaf1_term<CPLX>(er, ei, f[j], g[j], sigma, ah[j % NA], al[j % NA]);
+    for (int j = 0; j < NJ; ++j) leaf1_term<CPLX>(er, ei, f[j], g[j], ah[j % NA], al[j % NA]);
 }
 
 // One warp task of the single-level leaf pass: returns this lane's coefficient-free sum.
@@ -625,14 +635,17 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
     const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
     double ah[NA], al[NA];
 #pragma unroll
-    for (int a = 0; a < NA; ++a) ah[a] = al[a] = 0.0;
+    for (int a = 0; a < NA; ++a) {
+        ah[a] = sigma;   // biased accumulator
+        al[a] = 0.0;
+    }
     // boundary rows: lanes whose prefix ends at k >= k' contribute zero
     const int kmid = min(kmax + 1, ks1);
     for (int kp = kb; kp < kmid; ++kp) {
         const bool kv = kp > k;
         const dd er = kv ? pr : dd{0.0, 0.0};
         const dd ei = kv ? pim : dd{0.0, 0.0};
-        leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, er, ei, sigma, ah, al);
+        leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, er, ei, ah, al);
     }
     // main rows, LEAF1_ROWS per iteration, folded back onto the grid every FOLD rows
     int kp = max(kb, kmid);
@@ -641,9 +654,9 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
         for (; kp + LEAF1_ROWS - 1 < ke; kp += LEAF1_ROWS) {
 #pragma unroll
             for (int r = 0; r < LEAF1_ROWS; ++r)
-                leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp + r, pr, pim, sigma, ah, al);
+                leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp + r, pr, pim, ah, al);
         }
-        for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, pr, pim, sigma, ah, al);
+        for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, NA, SMEM>(Fr, Fi, kp, pr, pim, ah, al);
 #pragma unroll
         for (int a = 0; a < NA; ++a) {
             const double t = (al[a] + sigma) - sigma;
@@ -654,7 +667,7 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
     dd s = {0.0, 0.0};
     if (valid) {
 #pragma unroll
-        for (int a = 0; a < NA; ++a) s = dd_add(s, dd_from_sum(ah[a], al[a]));
+        for (int a = 0; a < NA; ++a) s = dd_add(s, dd_from_sum(ah[a] - sigma, al[a]));
     }
     return s;
 }
@@ -736,28 +749,30 @@ struct Leaf2Args {
 // gives with F.im = 0 (every dropped term is an exact zero).
 // CZ: the factor's low part is exactly 0 (combination form: F = w * 1), its cross term drops.
 template <bool CZ = false>
-__device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double sigma, double &ah,
-                                                      double &al) {
-    const double h = fma(er.hi, f.x, sigma) - sigma;
-    ah += h;
+__device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double &ah, double &al) {
+    const double a1 = fma(er.hi, f.x, ah);   // biased accumulator (leaf_term)
+    const double h = a1 - ah;
+    ah = a1;
     double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
     if (!CZ) c = fma(er.hi, f.y, c);
     al += c;
 }
 
 // Symmetric pair (x_0 = 1 - x_2, w_0 = w_2; oscillatory): F_0 = conj(F_2) exactly, so the two
-// points' terms Re(P F_2) = A - B and Re(P F_0) = A + B share the products A = P.re F_2.re and
+// points' terms Re(P F_0) = A + B and Re(P F_2) = A - B share the products A = P.re F_2.re and
 // B = P.im F_2.im (their grid parts, remainders and cross terms); each point's term is still formed
-// and accumulated on its own.  18 FP64 instructions for the two points instead of 28.
+// and accumulated on its own: node 0 adds the grid parts of A and B in turn (biased accumulator,
+// leaf_term), node 2 forms h_A - h_B and adds it.  16 FP64 instructions for the two points.
 __device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, const double2 f, const double2 g,
-                                                    double sigma, double &ah, double &al) {
-    const double h1 = fma(er.hi, f.x, sigma) - sigma;
-    const double h2 = fma(ei.hi, g.x, sigma) - sigma;
+                                                    double &ah, double &al) {
+    const double a1 = fma(er.hi, f.x, ah);
+    const double h1 = a1 - ah;
+    const double a2 = fma(ei.hi, g.x, a1);   // node 0: A + B
+    const double h2 = a2 - a1;
     const double cA = fma(er.lo, f.x, fma(er.hi, f.y, fma(er.hi, f.x, -h1)));
     const double cB = fma(ei.lo, g.x, fma(ei.hi, g.y, fma(ei.hi, g.x, -h2)));
-    ah += h1 + h2;   // node 0: A + B
     al += cA + cB;
-    ah += h1 - h2;   // node 2: A - B
+    ah = a2 + (h1 - h2);                     // node 2: A - B
     al += cA - cB;
 }
 
@@ -767,15 +782,15 @@ __device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, 
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
-                                                const double (&sg)[NJ], double (&ah)[NJ], double (&al)[NJ]) {
+                                                double (&ah)[NJ], double (&al)[NJ]) {
     if constexpr (SYM && CPLX && NJ == 3 && CJ == 1) {
         const double2 f2 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
         const double2 g2 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
         const double2 f1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
 #pragma unroll
         for (int jm = 0; jm < 3; ++jm) {
-            leaf_sym_pair_terms(er[jm], ei[jm], f2, g2, sg[jm], ah[jm], al[jm]);
-            leaf_real_factor_term<CZ>(er[jm], f1, sg[jm], ah[jm], al[jm]);
+            leaf_sym_pair_terms(er[jm], ei[jm], f2, g2, ah[jm], al[jm]);
+            leaf_real_factor_term<CZ>(er[jm], f1, ah[jm], al[jm]);
         }
         return;
     }
@@ -783,7 +798,7 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
         const double2 f1 = SMEM ? Fr[kp * 2 + 1] : __ldg(Fr + kp * 2 + 1);
         const double2 g1 = SMEM ? Fi[kp * 2 + 1] : __ldg(Fi + kp * 2 + 1);
 #pragma unroll
-        for (int jm = 0; jm < 2; ++jm) leaf_sym_pair_terms(er[jm], ei[jm], f1, g1, sg[jm], ah[jm], al[jm]);
+        for (int jm = 0; jm < 2; ++jm) leaf_sym_pair_terms(er[jm], ei[jm], f1, g1, ah[jm], al[jm]);
         return;
     }
     double2 f[NJ], g[NJ];
@@ -796,8 +811,8 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int jm = 0; jm < NJ; ++jm) {
-            if (j == CJ) leaf_real_factor_term<CZ>(er[jm], f[j], sg[jm], ah[jm], al[jm]);
-            else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], sg[jm], ah[jm], al[jm]);
+            if (j == CJ) leaf_real_factor_term<CZ>(er[jm], f[j], ah[jm], al[jm]);
+            else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], ah[jm], al[jm]);
         }
 }
 
@@ -867,7 +882,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             int ex = 0;
             frexp(2.0 * bound, &ex);
             sg[jm] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
-            ah[jm] = al[jm] = 0.0;
+            ah[jm] = sg[jm];   // biased accumulator
+            al[jm] = 0.0;
         }
         int kp = km + 1;
         while (kp < d) {
@@ -875,9 +891,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
             for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll
-                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, sg, ah, al);
+                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, ah, al);
             }
-            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, sg, ah, al);
+            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al);
 #pragma unroll
             for (int jm = 0; jm < NJ; ++jm) {
                 const double t = (al[jm] + sg[jm]) - sg[jm];
@@ -886,7 +902,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             }
         }
 #pragma unroll
-        for (int jm = 0; jm < NJ; ++jm) lane_sum = dd_add(lane_sum, dd_from_sum(ah[jm], al[jm]));
+        for (int jm = 0; jm < NJ; ++jm) lane_sum = dd_add(lane_sum, dd_from_sum(ah[jm] - sg[jm], al[jm]));
 #else
 #pragma unroll 1
         for (int jm = 0; jm < NJ; ++jm) {
@@ -904,21 +920,21 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             int ex = 0;
             frexp(2.0 * bound, &ex);
             const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
-            double ah[1] = {0.0}, al[1] = {0.0};
+            double ah[1] = {sigma}, al[1] = {0.0};   // biased accumulator
             int kp = km + 1;
             while (kp < d) {
                 const int ke = min(d, kp + FOLD);
                 for (; kp + LEAF1_ROWS - 1 < ke; kp += LEAF1_ROWS) {
 #pragma unroll
                     for (int r = 0; r < LEAF1_ROWS; ++r)
-                        leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp + r, er, ei, sigma, ah, al);
+                        leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp + r, er, ei, ah, al);
                 }
-                for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp, er, ei, sigma, ah, al);
+                for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp, er, ei, ah, al);
                 const double t = (al[0] + sigma) - sigma;
                 ah[0] += t;
                 al[0] -= t;
             }
-            lane_sum = dd_add(lane_sum, dd_from_sum(ah[0], al[0]));
+            lane_sum = dd_add(lane_sum, dd_from_sum(ah[0] - sigma, al[0]));
         }
 #endif
         dd v = warp_reduce_dd(valid ? lane_sum : dd{0.0, 0.0});
@@ -1926,15 +1942,17 @@ extern "C" int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms
 // with CZ; leaf_sym_pair_terms 8 + 10 for its two leaves).
 extern "C" int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_point) {
     if (!p || !dfma_per_point || !dadd_per_point) return SG_EINVAL;
-    double f = p->cplx ? 8.0 : 4.0, a = p->cplx ? 6.0 : 3.0;
+    // biased grid accumulator (leaf_term): generic real 4 DFMA + 2 DADD, oscillatory 8 + 4;
+    // symmetric pair 8 + 8 for two points; real midpoint factor 3 (CZ) / 4 DFMA + 2 DADD
+    double f = p->cplx ? 8.0 : 4.0, a = p->cplx ? 4.0 : 2.0;
     if (p->leaf2 && p->leaf2_sym && !p->leaf2_center) {   // NJ = 2 symmetric pair
         f = 8.0 / 2.0;
-        a = 10.0 / 2.0;
+        a = 8.0 / 2.0;
     } else if (p->leaf2 && p->leaf2_center) {
-        const double cf = p->leaf2_cz ? 3.0 : 4.0, ca = 3.0;
+        const double cf = p->leaf2_cz ? 3.0 : 4.0, ca = 2.0;
         if (p->leaf2_sym) {
             f = (8.0 + cf) / 3.0;
-            a = (10.0 + ca) / 3.0;
+            a = (8.0 + ca) / 3.0;
         } else {
             f = (2.0 * f + cf) / 3.0;
             a = (2.0 * a + ca) / 3.0;
@@ -2023,13 +2041,15 @@ extern "C" int sg_profile_enable(sg_plan_t p, int enable) {
 
 extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
     if (!p || !n) return SG_EINVAL;
-    const int nl = 4 + p->hp.nfront;
+    // launches: tree [K0 factor, K0 base, root, pass 1..nfront, reduce];
+    //           collapse [K0 factor, K0 base, k_collapse_part, k_collapse_final]
+    const int nl = p->collapse ? 4 : 4 + p->hp.nfront;
     if (!ms) {
         *n = nl;
         return SG_OK;
     }
     if (*n < nl || p->ev.empty()) return SG_EINVAL;
-    if (cudaEventSynchronize(p->ev.back()) != cudaSuccess) return SG_ECUDA;
+    if (cudaEventSynchronize(p->ev[nl]) != cudaSuccess) return SG_ECUDA;
     for (int i = 0; i < nl; ++i)
         if (cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess) return SG_ECUDA;
     *n = nl;
