@@ -92,6 +92,42 @@ DD_HD cdd cdd_mul(cdd a, cdd b) {
 }
 DD_HD cdd cdd_mul_dd(cdd a, dd b) { return cdd{dd_mul(a.re, b), dd_mul(a.im, b)}; }
 
+// "sloppy" dd addition (one TwoSum on the high parts, low parts added in FP64): 11 FP64 ops instead
+// of 20; error <= ~2^-104 (|a| + |b|), which is all the leaf partial sums need (their own grid error
+// is relative to the same bound).
+DD_HD dd dd_add_fast(dd a, dd b) {
+    double s, e;
+    two_sum(a.hi, b.hi, s, e);
+    e += a.lo + b.lo;
+    return dd_norm(s, e);
+}
+// x +/- y for two unnormalised products (p, e) = dd_mul_pe outputs, renormalised: 11 FP64 ops
+DD_HD dd dd_combine_pe(double px, double ex, double py, double ey) {
+    double s, e;
+    two_sum(px, py, s, e);
+    e += ex + ey;
+    return dd_norm(s, e);
+}
+// complex dd product from four shared unnormalised products: 4 x (1 DMUL + 3 DFMA) + 2 x 11
+DD_HD cdd cdd_mul_fast(cdd a, cdd b) {
+    double p1, e1, p2, e2, p3, e3, p4, e4;
+    dd_mul_pe(a.re, b.re, p1, e1);
+    dd_mul_pe(a.im, b.im, p2, e2);
+    dd_mul_pe(a.re, b.im, p3, e3);
+    dd_mul_pe(a.im, b.re, p4, e4);
+    return cdd{dd_combine_pe(p1, e1, -p2, -e2), dd_combine_pe(p3, e3, p4, e4)};
+}
+// a * b and a * conj(b) sharing the four products (symmetric node pairs: F_0 = conj(F_2))
+DD_HD void cdd_mul_conj_pair(cdd a, cdd b, cdd &ab, cdd &abc) {
+    double p1, e1, p2, e2, p3, e3, p4, e4;
+    dd_mul_pe(a.re, b.re, p1, e1);
+    dd_mul_pe(a.im, b.im, p2, e2);
+    dd_mul_pe(a.re, b.im, p3, e3);
+    dd_mul_pe(a.im, b.re, p4, e4);
+    ab = cdd{dd_combine_pe(p1, e1, -p2, -e2), dd_combine_pe(p3, e3, p4, e4)};
+    abc = cdd{dd_combine_pe(p1, e1, p2, e2), dd_combine_pe(p4, e4, -p3, -e3)};
+}
+
 // ---------------------------------------------------------------------------------------------
 // Transcendentals in dd (plan-time factor tables, K0).  Accuracy ~1e-31 relative on the ranges used
 // (|x| < 700 for exp; any |x| for sin/cos via reduction with a 3-part 2*pi).

@@ -82,6 +82,18 @@ __device__ __forceinline__ dd warp_reduce_dd(dd v) {
     return v;
 }
 
+// same butterfly with the sloppy dd add (leaf task partials; fixed order, deterministic)
+__device__ __forceinline__ dd warp_reduce_dd_fast(dd v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dd w;
+        w.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+        w.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+        v = dd_add_fast(v, w);
+    }
+    return v;
+}
+
 // CTA sum in fixed order; result valid in thread 0.
 template <int NWARPS>
 __device__ __forceinline__ dd block_reduce_dd(dd v) {
@@ -866,18 +878,43 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         // every row load (ILP x NJ, shared-memory loads / leaf / NJ)
         dd er[NJ], ei[NJ];
         double sg[NJ], ah[NJ], al[NJ];
+        if constexpr (CPLX && SYM && NJ == 3 && CJ == 1) {
+            // mids 0 and 2 are conjugate (F_0 = conj(F_2)): P F_2 and P conj(F_2) share their four
+            // products; mid 1 (the midpoint) is real
+            const double2 f = Fr[km * 3 + 2], g = Fi[km * 3 + 2], w1 = Fr[km * 3 + 1];
+            cdd c2, c0;
+            cdd_mul_conj_pair(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c2, c0);
+            er[0] = c0.re;
+            ei[0] = c0.im;
+            er[2] = c2.re;
+            ei[2] = c2.im;
+            er[1] = CZ ? dd_mul_d(pr, w1.x) : dd_mul(pr, dd{w1.x, w1.y});
+            ei[1] = CZ ? dd_mul_d(pim, w1.x) : dd_mul(pim, dd{w1.x, w1.y});
+        } else if constexpr (CPLX && SYM && NJ == 2 && CJ == -1) {
+            const double2 f = Fr[km * 2 + 1], g = Fi[km * 2 + 1];
+            cdd c1, c0;
+            cdd_mul_conj_pair(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c1, c0);
+            er[0] = c0.re;
+            ei[0] = c0.im;
+            er[1] = c1.re;
+            ei[1] = c1.im;
+        } else {
+#pragma unroll
+            for (int jm = 0; jm < NJ; ++jm) {
+                const double2 f = Fr[km * NJ + jm];
+                if (CPLX) {
+                    const double2 g = Fi[km * NJ + jm];
+                    cdd c = cdd_mul_fast(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
+                    er[jm] = c.re;
+                    ei[jm] = c.im;
+                } else {
+                    er[jm] = dd_mul(pr, dd{f.x, f.y});
+                    ei[jm] = dd{0.0, 0.0};
+                }
+            }
+        }
 #pragma unroll
         for (int jm = 0; jm < NJ; ++jm) {
-            const double2 f = Fr[km * NJ + jm];
-            if (CPLX) {
-                const double2 g = Fi[km * NJ + jm];
-                cdd c = cdd_mul(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
-                er[jm] = c.re;
-                ei[jm] = c.im;
-            } else {
-                er[jm] = dd_mul(pr, dd{f.x, f.y});
-                ei[jm] = dd{0.0, 0.0};
-            }
             const double bound = (fabs(er[jm].hi) + (CPLX ? fabs(ei[jm].hi) : 0.0)) * sa;
             int ex = 0;
             frexp(2.0 * bound, &ex);
@@ -901,8 +938,17 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 al[jm] -= t;
             }
         }
+        {
+            // lane value = sum_jm (ah - sigma) + al: exact grid parts via TwoSum, low parts in FP64
+            double hs = ah[0] - sg[0], ls = al[0];
 #pragma unroll
-        for (int jm = 0; jm < NJ; ++jm) lane_sum = dd_add(lane_sum, dd_from_sum(ah[jm] - sg[jm], al[jm]));
+            for (int jm = 1; jm < NJ; ++jm) {
+                double e;
+                two_sum(hs, ah[jm] - sg[jm], hs, e);
+                ls += al[jm] + e;
+            }
+            lane_sum = dd_norm(hs, ls);
+        }
 #else
 #pragma unroll 1
         for (int jm = 0; jm < NJ; ++jm) {
@@ -937,7 +983,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             lane_sum = dd_add(lane_sum, dd_from_sum(ah[0] - sigma, al[0]));
         }
 #endif
-        dd v = warp_reduce_dd(valid ? lane_sum : dd{0.0, 0.0});
+        dd v = warp_reduce_dd_fast(valid ? lane_sum : dd{0.0, 0.0});
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);
             A.partials[task] = make_double2(v.hi, v.lo);
