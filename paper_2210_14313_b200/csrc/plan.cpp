@@ -621,14 +621,43 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     if (hp.fuse) {
         const int tm = L - 2;   // depth of the stored parents; their excess is L-2
         hp.pass_written[tm] = 0;
-        hp.TK.assign((size_t)d + 1, 0);
-        for (int k = 0; k < d; ++k) {
-            const int64_t cnt = k <= d - 2 ? hp.C[tm][(size_t)(L - 2) * d + k] : 0;
-            hp.TK[k + 1] = hp.TK[k] + (cnt + 31) / 32;
+        // Cmid[k] = parents (excess L-2) whose last active coordinate is < k; chunk c of 32 parents
+        // has a valid lane for every k_mid >= kstart(c) (Cmid is nondecreasing); k_mid <= d-2
+        auto cmid = [&](int k) -> int64_t { return k <= d - 2 ? hp.C[tm][(size_t)(L - 2) * d + k] : 0; };
+        const int64_t nchunks = (cmid(d - 2) + 31) / 32;
+        struct Task {
+            int64_t rows, first;
+            int ka, kb;
+        };
+        std::vector<Task> tasks;
+        int k0 = 0;
+        for (int64_t c = 0; c < nchunks; ++c) {
+            while (k0 <= d - 2 && cmid(k0) <= 32 * c) ++k0;   // kstart(c), nondecreasing in c
+            int64_t acc = 0;
+            int ka = k0;
+            for (int k = k0; k <= d - 2; ++k) {
+                acc += d - 1 - k;
+                if (acc >= LEAF2_TASK_ROWS || k == d - 2) {
+                    tasks.push_back(Task{acc, 32 * c, ka, k + 1});
+                    acc = 0;
+                    ka = k + 1;
+                }
+            }
+        }
+        // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, chunk)
+        std::stable_sort(tasks.begin(), tasks.end(), [](const Task &a, const Task &b) {
+            if (a.rows != b.rows) return a.rows > b.rows;
+            if (a.ka != b.ka) return a.ka < b.ka;
+            return a.first < b.first;
+        });
+        hp.T2.resize(2 * tasks.size());
+        for (size_t i = 0; i < tasks.size(); ++i) {
+            hp.T2[2 * i] = tasks[i].first;
+            hp.T2[2 * i + 1] = ((int64_t)tasks[i].ka << 32) | (int64_t)tasks[i].kb;
         }
         const int t = hp.nfront;
         hp.pass_nsplit[t] = 1;
-        hp.pass_ntasks[t] = hp.TK[d];
+        hp.pass_ntasks[t] = (int64_t)tasks.size();
         hp.pass_blocks[t] = std::max<int64_t>(1, (hp.pass_ntasks[t] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
         poff = hp.root_blocks;
         for (int u = 1; u <= hp.nfront; ++u) {

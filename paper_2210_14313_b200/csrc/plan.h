@@ -21,6 +21,7 @@
 #define SG_GP_MAX_K 6      // Gauss-Patterson rules up to 2^6 - 1 = 63 points (levels <= 48)
 #define SG_MAX_D ((1 << 20) - 1)
 #define SG_META_KBITS 20
+#define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 
 struct HostPlan {
     int d = 0, L = 0, rule = 0, kind = 0, form = 0;
@@ -60,7 +61,11 @@ struct HostPlan {
     // stored; the last pass builds each depth-(L-1) prefix from its depth-(L-2) parent (excess L-2,
     // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
     bool fuse = false;
-    std::vector<int64_t> TK;           // [d + 1] prefix of fused tasks over k_mid
+    // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
+    // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
+    // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.
+    // Two int64 per task: first parent index (chunk * 32), (ka << 32) | kb; sorted heavy-first.
+    std::vector<int64_t> T2;
     // Sub[b * (d + 1) + (k + 1)] = Smolyak points (nonzero coefficient) in the subtree of a node
     // with excess b and last active coordinate k (k = -1: the root), the node itself included
     std::vector<uint64_t> Sub;

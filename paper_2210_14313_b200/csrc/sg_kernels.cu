@@ -733,15 +733,12 @@ struct Leaf2Args {
     const double2 *src_re, *src_im;   // frontier L-2
     long long base;                   // offset of segment (b = L-2, k = 0) in frontier L-2
     const long long *Cmid;            // C_{L-2}(L-2, k): parents of excess L-2 with k_last < k
-    const long long *TK;              // [d+1] task prefix over k_mid
+    const long long *T2;              // task descriptors: first parent, (ka << 32) | kb (plan.h)
     long long ntasks;
     double2 *partials;             // one per task
     unsigned long long *counter;   // dynamic task counter, zeroed per launch
 };
 
-#ifndef LEAF2_JMP
-#define LEAF2_JMP 1
-#endif
 #ifndef LEAF2_ROWS
 #define LEAF2_ROWS 1        // rows per iteration, real kinds (A/B on config 4: 1 > 2)
 #endif
@@ -852,18 +849,12 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         utask = __shfl_sync(0xffffffffu, utask, 0);
         const long long task = (long long)utask;
         if (task >= A.ntasks) break;
-        // k_mid = max k with TK[k] <= task (warp-uniform binary search)
-        int lo = 0, hi = d;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (A.TK[mid] <= task) lo = mid;
-            else hi = mid;
-        }
-        const int km = lo;
-        const long long i = (task - A.TK[km]) * 32 + lane;
-        const bool valid = i < A.Cmid[km];
+        // task = (chunk of 32 parents starting at `first`, k_mid range [ka, kb)), plan.h T2
+        const long long first = A.T2[2 * task], kk = A.T2[2 * task + 1];
+        const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
+        const long long i = first + lane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
-        if (valid) {
+        if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
             const double2 v = A.src_re[A.base + i];
             pr = dd{v.x, v.y};
             if (CPLX) {
@@ -871,74 +862,77 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 pim = dd{vi.x, vi.y};
             }
         }
-        const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
         dd lane_sum = {0.0, 0.0};
-#if LEAF2_JMP
-        // all NJ mid prefixes of the lane at once: NJ independent accumulator chains that share
-        // every row load (ILP x NJ, shared-memory loads / leaf / NJ)
-        dd er[NJ], ei[NJ];
-        double sg[NJ], ah[NJ], al[NJ];
-        if constexpr (CPLX && SYM && NJ == 3 && CJ == 1) {
-            // mids 0 and 2 are conjugate (F_0 = conj(F_2)): P F_2 and P conj(F_2) share their four
-            // products; mid 1 (the midpoint) is real
-            const double2 f = Fr[km * 3 + 2], g = Fi[km * 3 + 2], w1 = Fr[km * 3 + 1];
-            cdd c2, c0;
-            cdd_mul_conj_pair(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c2, c0);
-            er[0] = c0.re;
-            ei[0] = c0.im;
-            er[2] = c2.re;
-            ei[2] = c2.im;
-            er[1] = CZ ? dd_mul_d(pr, w1.x) : dd_mul(pr, dd{w1.x, w1.y});
-            ei[1] = CZ ? dd_mul_d(pim, w1.x) : dd_mul(pim, dd{w1.x, w1.y});
-        } else if constexpr (CPLX && SYM && NJ == 2 && CJ == -1) {
-            const double2 f = Fr[km * 2 + 1], g = Fi[km * 2 + 1];
-            cdd c1, c0;
-            cdd_mul_conj_pair(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c1, c0);
-            er[0] = c0.re;
-            ei[0] = c0.im;
-            er[1] = c1.re;
-            ei[1] = c1.im;
-        } else {
+        for (int km = ka; km < kb; ++km) {
+            const bool valid = i < A.Cmid[km];
+            const dd prv = valid ? pr : dd{0.0, 0.0};
+            const dd pimv = valid ? pim : dd{0.0, 0.0};
+            const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+            // all NJ mid prefixes of the lane at once: NJ independent accumulator chains that share
+            // every row load (ILP x NJ, shared-memory loads / leaf / NJ)
+            dd er[NJ], ei[NJ];
+            double sg[NJ], ah[NJ], al[NJ];
+            if constexpr (CPLX && SYM && NJ == 3 && CJ == 1) {
+                // mids 0 and 2 are conjugate (F_0 = conj(F_2)): P F_2 and P conj(F_2) share their
+                // four products; mid 1 (the midpoint) is real
+                const double2 f = Fr[km * 3 + 2], g = Fi[km * 3 + 2], w1 = Fr[km * 3 + 1];
+                cdd c2, c0;
+                cdd_mul_conj_pair(cdd{prv, pimv}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c2, c0);
+                er[0] = c0.re;
+                ei[0] = c0.im;
+                er[2] = c2.re;
+                ei[2] = c2.im;
+                er[1] = CZ ? dd_mul_d(prv, w1.x) : dd_mul(prv, dd{w1.x, w1.y});
+                ei[1] = CZ ? dd_mul_d(pimv, w1.x) : dd_mul(pimv, dd{w1.x, w1.y});
+            } else if constexpr (CPLX && SYM && NJ == 2 && CJ == -1) {
+                const double2 f = Fr[km * 2 + 1], g = Fi[km * 2 + 1];
+                cdd c1, c0;
+                cdd_mul_conj_pair(cdd{prv, pimv}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, c1, c0);
+                er[0] = c0.re;
+                ei[0] = c0.im;
+                er[1] = c1.re;
+                ei[1] = c1.im;
+            } else {
 #pragma unroll
-            for (int jm = 0; jm < NJ; ++jm) {
-                const double2 f = Fr[km * NJ + jm];
-                if (CPLX) {
-                    const double2 g = Fi[km * NJ + jm];
-                    cdd c = cdd_mul_fast(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
-                    er[jm] = c.re;
-                    ei[jm] = c.im;
-                } else {
-                    er[jm] = dd_mul(pr, dd{f.x, f.y});
-                    ei[jm] = dd{0.0, 0.0};
+                for (int jm = 0; jm < NJ; ++jm) {
+                    const double2 f = Fr[km * NJ + jm];
+                    if (CPLX) {
+                        const double2 g = Fi[km * NJ + jm];
+                        cdd c = cdd_mul_fast(cdd{prv, pimv}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
+                        er[jm] = c.re;
+                        ei[jm] = c.im;
+                    } else {
+                        er[jm] = dd_mul(prv, dd{f.x, f.y});
+                        ei[jm] = dd{0.0, 0.0};
+                    }
                 }
             }
-        }
-#pragma unroll
-        for (int jm = 0; jm < NJ; ++jm) {
-            const double bound = (fabs(er[jm].hi) + (CPLX ? fabs(ei[jm].hi) : 0.0)) * sa;
-            int ex = 0;
-            frexp(2.0 * bound, &ex);
-            sg[jm] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
-            ah[jm] = sg[jm];   // biased accumulator
-            al[jm] = 0.0;
-        }
-        int kp = km + 1;
-        while (kp < d) {
-            const int ke = min(d, kp + FOLD);
-            constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
-            for (; kp + RW - 1 < ke; kp += RW) {
-#pragma unroll
-                for (int r = 0; r < RW; ++r) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, ah, al);
-            }
-            for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al);
 #pragma unroll
             for (int jm = 0; jm < NJ; ++jm) {
-                const double t = (al[jm] + sg[jm]) - sg[jm];
-                ah[jm] += t;
-                al[jm] -= t;
+                const double bound = (fabs(er[jm].hi) + (CPLX ? fabs(ei[jm].hi) : 0.0)) * sa;
+                int ex = 0;
+                frexp(2.0 * bound, &ex);
+                sg[jm] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+                ah[jm] = sg[jm];   // biased accumulator
+                al[jm] = 0.0;
             }
-        }
-        {
+            int kp = km + 1;
+            while (kp < d) {
+                const int ke = min(d, kp + FOLD);
+                constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
+                for (; kp + RW - 1 < ke; kp += RW) {
+#pragma unroll
+                    for (int r = 0; r < RW; ++r)
+                        leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, ah, al);
+                }
+                for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al);
+#pragma unroll
+                for (int jm = 0; jm < NJ; ++jm) {
+                    const double t = (al[jm] + sg[jm]) - sg[jm];
+                    ah[jm] += t;
+                    al[jm] -= t;
+                }
+            }
             // lane value = sum_jm (ah - sigma) + al: exact grid parts via TwoSum, low parts in FP64
             double hs = ah[0] - sg[0], ls = al[0];
 #pragma unroll
@@ -947,43 +941,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 two_sum(hs, ah[jm] - sg[jm], hs, e);
                 ls += al[jm] + e;
             }
-            lane_sum = dd_norm(hs, ls);
+            lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
         }
-#else
-#pragma unroll 1
-        for (int jm = 0; jm < NJ; ++jm) {
-            const double2 f = Fr[km * NJ + jm];
-            dd er, ei = {0.0, 0.0};
-            if (CPLX) {
-                const double2 g = Fi[km * NJ + jm];
-                cdd c = cdd_mul(cdd{pr, pim}, cdd{dd{f.x, f.y}, dd{g.x, g.y}});
-                er = c.re;
-                ei = c.im;
-            } else {
-                er = dd_mul(pr, dd{f.x, f.y});
-            }
-            const double bound = (fabs(er.hi) + (CPLX ? fabs(ei.hi) : 0.0)) * sa;
-            int ex = 0;
-            frexp(2.0 * bound, &ex);
-            const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
-            double ah[1] = {sigma}, al[1] = {0.0};   // biased accumulator
-            int kp = km + 1;
-            while (kp < d) {
-                const int ke = min(d, kp + FOLD);
-                for (; kp + LEAF1_ROWS - 1 < ke; kp += LEAF1_ROWS) {
-#pragma unroll
-                    for (int r = 0; r < LEAF1_ROWS; ++r)
-                        leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp + r, er, ei, ah, al);
-                }
-                for (; kp < ke; ++kp) leaf1_row<CPLX, NJ, 1, SMEM>(Fr, Fi, kp, er, ei, ah, al);
-                const double t = (al[0] + sigma) - sigma;
-                ah[0] += t;
-                al[0] -= t;
-            }
-            lane_sum = dd_add(lane_sum, dd_from_sum(ah[0] - sigma, al[0]));
-        }
-#endif
-        dd v = warp_reduce_dd_fast(valid ? lane_sum : dd{0.0, 0.0});
+        dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);
             A.partials[task] = make_double2(v.hi, v.lo);
@@ -1501,7 +1461,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         if (t < hp.nfront) p->tab_TB[t] = push(hp.TB[t]);
     }
     p->tab_JS = push(hp.JS);
-    if (hp.fuse) p->tab_TK = push(hp.TK);
+    if (hp.fuse) p->tab_TK = push(hp.T2);
     p->tab_off1 = hp.nfront >= 1 ? p->tab_offT[1] : 0;
     if (tabs.empty()) tabs.push_back(0);
     size_t sz = 0;
@@ -1853,7 +1813,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.src_im = im;
             B.base = hp.off[t - 1][(size_t)(hp.L - 2) * hp.d];
             B.Cmid = p->d_tabs + p->tab_CT[t - 1] + (size_t)(hp.L - 2) * hp.d;
-            B.TK = p->d_tabs + p->tab_TK;
+            B.T2 = p->d_tabs + p->tab_TK;
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
             B.counter = p->d_counter;
