@@ -21,7 +21,9 @@
 #define SG_GP_MAX_K 6      // Gauss-Patterson rules up to 2^6 - 1 = 63 points (levels <= 48)
 #define SG_MAX_D ((1 << 20) - 1)
 #define SG_META_KBITS 20
+#ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
+#endif
 
 struct HostPlan {
     int d = 0, L = 0, rule = 0, kind = 0, form = 0;

@@ -788,10 +788,34 @@ __device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, 
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
 // SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory), or nodes 0 and 1 do
 // (CJ == -1, NJ == 2: the midpoint-merged Clenshaw-Curtis level-2 row {0, 1}).
+#ifndef LEAF2_SPLIT
+#define LEAF2_SPLIT 1   // second accumulator pair per mid (node 2 + midpoint): shorter chains, c5 -1%
+#endif
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
 __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                                 int kp, const dd (&er)[NJ], const dd (&ei)[NJ],
-                                                double (&ah)[NJ], double (&al)[NJ]) {
+                                                double (&ah)[NJ], double (&al)[NJ], double (&bh)[NJ],
+                                                double (&bl)[NJ]) {
+    if constexpr (LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) {
+        const double2 f2 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
+        const double2 g2 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
+        const double2 f1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
+#pragma unroll
+        for (int jm = 0; jm < 3; ++jm) {
+            // node 0 (A + B) into accumulator a, node 2 (A - B) and the midpoint into b
+            const double u1 = fma(er[jm].hi, f2.x, ah[jm]);
+            const double h1 = u1 - ah[jm];
+            ah[jm] = fma(ei[jm].hi, g2.x, u1);
+            const double h2 = ah[jm] - u1;
+            const double cA = fma(er[jm].lo, f2.x, fma(er[jm].hi, f2.y, fma(er[jm].hi, f2.x, -h1)));
+            const double cB = fma(ei[jm].lo, g2.x, fma(ei[jm].hi, g2.y, fma(ei[jm].hi, g2.x, -h2)));
+            al[jm] += cA + cB;
+            bh[jm] += h1 - h2;
+            bl[jm] += cA - cB;
+            leaf_real_factor_term<CZ>(er[jm], f1, bh[jm], bl[jm]);
+        }
+        return;
+    }
     if constexpr (SYM && CPLX && NJ == 3 && CJ == 1) {
         const double2 f2 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
         const double2 g2 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
@@ -871,7 +895,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             // all NJ mid prefixes of the lane at once: NJ independent accumulator chains that share
             // every row load (ILP x NJ, shared-memory loads / leaf / NJ)
             dd er[NJ], ei[NJ];
-            double sg[NJ], ah[NJ], al[NJ];
+            double sg[NJ], ah[NJ], al[NJ], bh[NJ], bl[NJ];
             if constexpr (CPLX && SYM && NJ == 3 && CJ == 1) {
                 // mids 0 and 2 are conjugate (F_0 = conj(F_2)): P F_2 and P conj(F_2) share their
                 // four products; mid 1 (the midpoint) is real
@@ -915,6 +939,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 sg[jm] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
                 ah[jm] = sg[jm];   // biased accumulator
                 al[jm] = 0.0;
+                bh[jm] = sg[jm];
+                bl[jm] = 0.0;
             }
             int kp = km + 1;
             while (kp < d) {
@@ -923,17 +949,25 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll
                     for (int r = 0; r < RW; ++r)
-                        leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, ah, al);
+                        leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp + r, er, ei, ah, al, bh, bl);
                 }
-                for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al);
+                for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al, bh, bl);
 #pragma unroll
                 for (int jm = 0; jm < NJ; ++jm) {
+                    if (LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) al[jm] += bl[jm], bl[jm] = 0.0;
                     const double t = (al[jm] + sg[jm]) - sg[jm];
                     ah[jm] += t;
                     al[jm] -= t;
                 }
             }
             // lane value = sum_jm (ah - sigma) + al: exact grid parts via TwoSum, low parts in FP64
+            if (LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) {
+#pragma unroll
+                for (int jm = 0; jm < NJ; ++jm) {   // same grid, |sum| < 2^m: exact
+                    ah[jm] += bh[jm] - sg[jm];
+                    al[jm] += bl[jm];
+                }
+            }
             double hs = ah[0] - sg[0], ls = al[0];
 #pragma unroll
             for (int jm = 1; jm < NJ; ++jm) {
