@@ -57,13 +57,18 @@ typedef enum {
     SG_RULE_GAUSS_LEGENDRE = 4    /* n_l = l (Eq 2.13)                         */
 } sg_rule;
 
-/* Integrand kinds (BASELINE.json configs; Genz families).  All are products of per-coordinate
- * factors (or the real part of one), which the MDI prefix tree carries as partial products. */
+/* Integrand kinds (BASELINE.json configs; Genz families).  Kinds 0-3 are products of
+ * per-coordinate factors (or the real part of one), which the MDI prefix tree carries as partial
+ * products.  Kind 4 is not: the tree carries the partial sum s = sum_k c_k x_k and the outer
+ * function is applied once per point (SG_ARITH_SFORM_DD). */
 typedef enum {
     SG_F_EXP_LINEAR = 0,    /* f(x) = exp(sum_k c_k x_k)                                      */
     SG_F_OSCILLATORY = 1,   /* f(x) = cos(2 pi u + sum_k c_k x_k)                              */
     SG_F_PRODUCT_PEAK = 2,  /* f(x) = prod_k (c_k^-2 + (x_k - w_k)^2)^-1                        */
-    SG_F_GAUSSIAN = 3       /* f(x) = exp(-sum_k c_k^2 (x_k - w_k)^2)                           */
+    SG_F_GAUSSIAN = 3,      /* f(x) = exp(-sum_k c_k^2 (x_k - w_k)^2)                           */
+    SG_F_CORNER_PEAK = 4    /* f(x) = (1 + sum_k c_k x_k)^-(d+1), requires 1 + sum min(c_k,0) > 0
+                               (SG_EINVAL at sg_plan; sg_update_integrand values outside the
+                               domain set the NonFiniteIntegrand flag) */
 } sg_kind;
 
 /* Integrand description.  c: host array of d doubles (required); w: host array of d doubles
@@ -82,10 +87,18 @@ typedef struct {
  * sum_{e=0}^{L} sum_{|i|=d+e} (Delta^{i_1} x ... x Delta^{i_d}) f, coefficient 1.  Same value. */
 typedef enum { SG_FORM_COMBINATION = 0, SG_FORM_DELTA = 1 } sg_form;
 
-/* Leaf arithmetic.  FACTOR_DD = double-double partial products of plan-time per-(coordinate,node)
- * factors (parity-grade, default).  SFORM_FP64 = ablation: FP64 partial sums of the argument and
- * per-point FP64 exp/cos (not parity-grade on ill-conditioned problems). */
-typedef enum { SG_ARITH_FACTOR_DD = 0, SG_ARITH_SFORM_FP64 = 1 } sg_arith;
+/* Leaf arithmetic.
+ *  FACTOR_DD  = double-double partial products of plan-time per-(coordinate,node) factors
+ *               (parity-grade, default; kinds 0-3).  For SG_F_CORNER_PEAK, which has no factor
+ *               form, FACTOR_DD selects SFORM_DD.
+ *  SFORM_FP64 = ablation: FP64 partial sums of the argument and per-point FP64 exp/cos/pow (not
+ *               parity-grade on ill-conditioned problems).
+ *  SFORM_DD   = double-double partial sums of the argument and a per-point dd outer function
+ *               (exp, cos, or the corner peak's power): parity-grade, ~20-40x the FP64 work of the
+ *               factor form per point; the general path for non-separable outer functions.
+ * The s-forms support kinds EXP_LINEAR, OSCILLATORY, GAUSSIAN and CORNER_PEAK (PRODUCT_PEAK ->
+ * SG_EUNSUPPORTED), the tree method only, no merge (SG_EUNSUPPORTED). */
+typedef enum { SG_ARITH_FACTOR_DD = 0, SG_ARITH_SFORM_FP64 = 1, SG_ARITH_SFORM_DD = 2 } sg_arith;
 
 /* Repeated-point merging (Eq 2.8 writes Q as one weighted sum over the points, and
  * the Fig 2.1 remark: "we would avoid the repeated points").  Every level of a rule that contains

@@ -1,7 +1,7 @@
 """Write tests/golden/oracle_full.json: the oracle's full-size values for BASELINE configs 1-5.
 
 Calls only ``oracle/`` (and the seeded input module).  Usage:
-    python -m oracle.make_golden [--configs 1,2,3,4,5] [--threads N]
+    python -m oracle.make_golden [--configs 1,2,3,4,5,cp] [--threads N]
 Configs 4-5 take core-hours (4.5e9 / 2.75e10 quad transcendentals); results are merged into the
 existing file config by config, so the script can be run in pieces.
 """
@@ -29,8 +29,9 @@ def main():
             "values": {}}
     if os.path.exists(OUT):
         data = json.load(open(OUT))
-    for i in [int(s) for s in args.configs.split(",") if s]:
-        p = S.baseline_config(i)
+    for name in [s for s in args.configs.split(",") if s]:
+        # BASELINE configs by number; "cp" = the corner-peak workload of the dd s-form path
+        p = S.corner_config() if name == "cp" else S.baseline_config(int(name))
         t0 = time.time()
         r = oracle.integrate_problem(p, eval_mode=1, nthreads=args.threads)
         data["values"][p.name] = {

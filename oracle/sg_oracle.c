@@ -27,7 +27,7 @@
 typedef __float128 quad;
 
 enum { SGO_RULE_TRAP = 1, SGO_RULE_CC = 2, SGO_RULE_GP = 3, SGO_RULE_GL = 4 };
-enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_MONOMIAL = 4 };
+enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_CORNER = 4, SGO_MONOMIAL = 9 };
 #define SGO_MAX_LEVEL 20
 #define SGO_MAX_GL 64
 
@@ -323,6 +323,9 @@ static quad f_plain(const integrand *F, const double *x) {
             s += (quad)F->c[k] * (quad)F->c[k] * t * t;
         }
         return expq(-s);
+    case SGO_CORNER: /* Genz corner peak: (1 + sum_k c_k x_k)^-(d+1) */
+        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
+        return powq(1 + s, -(quad)(d + 1));
     case SGO_MONOMIAL: /* test-only: prod x_k^{alpha_k}, alpha_k = (int) w[k] */
         for (int k = 0; k < d; ++k) {
             int a = (int)F->w[k];
@@ -346,6 +349,9 @@ static quad f_active(const integrand *F, int t, const int *ak, const double *ax)
     case SGO_OSC:
         for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
         return cosq(F->two_pi_u + F->s_mid + s);
+    case SGO_CORNER:
+        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
+        return powq(1 + F->s_mid + s, -(quad)(F->d + 1));
     case SGO_GAUSS:
         for (int m = 0; m < t; ++m) {
             int k = ak[m];
@@ -475,6 +481,11 @@ int sgo_integrate(int d, int L, int rule, int kind, const double *c, const doubl
     if (d < 1 || L < 0 || L + 1 > SGO_MAX_LEVEL || !c) return -1;
     if ((kind == SGO_PEAK || kind == SGO_GAUSS || kind == SGO_MONOMIAL) && !w) return -1;
     if (kind == SGO_MONOMIAL && eval_mode != 0) return -1;
+    if (kind == SGO_CORNER) {   /* 1 + sum c_k x_k > 0 on the cube */
+        double m = 1.0;
+        for (int k = 0; k < d; ++k) m += c[k] < 0 ? c[k] : 0.0;
+        if (!(m > 0)) return -1;
+    }
     problem P;
     memset(&P, 0, sizeof P);
     P.d = d; P.L = L; P.rule = rule; P.eval_mode = eval_mode;
@@ -503,7 +514,7 @@ int sgo_integrate(int d, int L, int rule, int kind, const double *c, const doubl
     F.s_mid = 0; F.peak_mid = 1;
     for (int k = 0; k < d; ++k) {
         F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
-        if (kind == SGO_EXP || kind == SGO_OSC) F.s_mid += (quad)c[k] / 2;
+        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (quad)c[k] / 2;
         if (kind == SGO_GAUSS) {
             quad b = 0.5Q - (quad)w[k];
             F.s_mid += (quad)c[k] * (quad)c[k] * b * b;
@@ -583,7 +594,7 @@ int sgo_eval_point(int d, int kind, const double *c, const double *w, double u, 
     int t = 0;
     for (int k = 0; k < d; ++k) {
         F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
-        if (kind == SGO_EXP || kind == SGO_OSC) F.s_mid += (quad)c[k] / 2;
+        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (quad)c[k] / 2;
         if (kind == SGO_GAUSS) { quad b = 0.5Q - (quad)w[k]; F.s_mid += (quad)c[k] * (quad)c[k] * b * b; }
         if (kind == SGO_PEAK) { quad b = 0.5Q - (quad)w[k]; F.peak_mid *= 1 / (F.cinv2[k] + b * b); }
         if (x[k] != 0.5) { ak[t] = k; ax[t] = x[k]; ++t; }

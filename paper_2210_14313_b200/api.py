@@ -19,9 +19,10 @@ from ._lib import check, lib, sg_integrand_desc, sg_options
 
 RULE_CC = 2
 RULE_GL = 4
-KIND_EXP, KIND_OSC, KIND_PEAK, KIND_GAUSS = 0, 1, 2, 3
+KIND_EXP, KIND_OSC, KIND_PEAK, KIND_GAUSS, KIND_CORNER = 0, 1, 2, 3, 4
 FORM_COMBINATION, FORM_DELTA = 0, 1
-ARITH_FACTOR_DD, ARITH_SFORM_FP64 = 0, 1   # s-form = ablation (FP64 partial sums + FP64 exp/cos)
+ARITH_FACTOR_DD, ARITH_SFORM_FP64, ARITH_SFORM_DD = 0, 1, 2   # s-forms: per-point outer function
+                                                            # (FP64 ablation / dd, parity-grade)
 MERGE_NONE, MERGE_MIDPOINT = 0, 1          # midpoint-merged evaluation (sg_merge)
 METHOD_TREE, METHOD_COLLAPSE = 0, 1        # sg_method: prefix tree over the points / separable collapse
 

@@ -297,7 +297,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     if (rule != SG_RULE_CLENSHAW_CURTIS && rule != SG_RULE_GAUSS_LEGENDRE && rule != SG_RULE_TRAPEZOIDAL &&
         rule != SG_RULE_GAUSS_PATTERSON)
         return SG_EINVAL;
-    if (kind < 0 || kind > 3 || form < 0 || form > 1 || merge < 0 || merge > 1) return SG_EINVAL;
+    if (kind < 0 || kind > 4 || form < 0 || form > 1 || merge < 0 || merge > 1) return SG_EINVAL;
     hp.merge = merge;
     if (world < 1 || rank < 0 || rank >= world) return SG_EINVAL;
     if (d > SG_MAX_D || L > SG_MAX_L) return SG_EUNSUPPORTED;

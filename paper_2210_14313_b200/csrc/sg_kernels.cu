@@ -43,7 +43,7 @@ struct DevPlan {
     double *base;   // re.hi, re.lo, im.hi, im.lo
     double *SA;     // [(L+2) x (d+1)] suffix sums of |F| per level (k_leaf's accumulation bound)
     int *status;
-    int sform;      // SG_ARITH_SFORM_FP64 ablation: base[0] holds the argument S, not the value
+    int sform;      // 0 factor form; 1 SG_ARITH_SFORM_FP64, 2 SG_ARITH_SFORM_DD: base[0..1] = argument S
     const double2 *coefm;   // node coefficient (dd) per (depth t, excess b): [t * (L + 1) + b]
 };
 
@@ -986,14 +986,20 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 }
 
 // ---------------------------------------------------------------------------------------------
-// s-form ablation (SG_ARITH_SFORM_FP64): the literal "partial sums carried one
-// coordinate at a time, outer function applied in FP64 at the leaf" design.  A node carries
-// delta = sum_active a_k(x_k) in FP64 and its weight product W in dd; a leaf evaluates
-// g = exp(S + delta') (exp, Gaussian) or cos(theta + delta') (oscillatory) with CUDA's FP64 exp/cos
-// and accumulates c(e) W' g in dd.  Tables reuse the factor-table slots: Fre[idx] = weight (dd),
-// Fim[idx] = (a, 0); base[0..1] = S or theta (dd).  Not parity-grade on ill-conditioned configs
-// — it exists to measure what per-point FP64 transcendentals cost and lose.
+// s-form: the literal "partial sums carried one coordinate at a time, outer function applied at the
+// leaf" design (§8f row 4).  A node carries delta = sum_active a_k(x_k) and its
+// weight product W; a leaf evaluates g(S + delta') once per point and accumulates c(e) W' g in dd.
+//   SG_ARITH_SFORM_FP64 (DDS = false): delta and g in FP64 (CUDA exp/cos/pow) — the ablation that
+//     measures what per-point FP64 outer functions cost and lose (not parity-grade).
+//   SG_ARITH_SFORM_DD (DDS = true): delta, S and g in double-double (dd exp / sincos / powers) —
+//     parity-grade, and the only path for integrands that are NOT products of per-coordinate
+//     factors: the Genz corner peak g(s) = (1 + s)^-(d+1) of s = sum c_k x_k.
+// Kinds: exp / Gaussian g = exp(S + delta) (Gaussian a_k = -c_k^2 ((x-w_k)^2 - (1/2-w_k)^2)),
+// oscillatory g = cos(S + delta) (S includes 2 pi u), corner peak g = (S + delta)^-(d+1) with
+// S = 1 + sum c_k / 2.  Tables reuse the factor-table slots: Fre[idx] = weight (dd),
+// Fim[idx] = a (dd; lo = 0 in FP64 mode); base[0..1] = S (dd); frontier re = W, im = delta.
 // ---------------------------------------------------------------------------------------------
+template <bool DDS>
 __global__ void k_factor_s(const DevPlan P) {
     const int n_ent = P.tab_off[P.L + 2];
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1004,37 +1010,103 @@ __global__ void k_factor_s(const DevPlan P) {
     const int k = r / n, j = r - k * n;
     const double x = P.X[P.entry_off[l] + j];
     const double ck = P.c[k];
-    double a;
+    dd a;
     if (P.kind == SG_F_GAUSSIAN) {
         const double wk = P.w[k];
-        a = -(ck * ck) * ((x - wk) * (x - wk) - (0.5 - wk) * (0.5 - wk));
+        if (DDS) {
+            // -c^2 ((x-w)^2 - (1/2-w)^2) = -c^2 (x - 1/2)(x + 1/2 - 2w)
+            const dd xm = dd_from_sum(x, -0.5);
+            const dd xp = dd_add(dd_from_sum(x, 0.5), dd{-2.0 * wk, 0.0});
+            a = dd_neg(dd_mul(dd_mul(xm, xp), dd_from_prod(ck, ck)));
+        } else {
+            a = dd{-(ck * ck) * ((x - wk) * (x - wk) - (0.5 - wk) * (0.5 - wk)), 0.0};
+        }
     } else {
-        a = ck * (x - 0.5);
+        a = DDS ? dd_mul_d(dd_from_sum(x, -0.5), ck) : dd{ck * (x - 0.5), 0.0};
     }
     P.Fre[idx] = make_double2(P.Whi[P.entry_off[l] + j], P.Wlo[P.entry_off[l] + j]);
-    P.Fim[idx] = make_double2(a, 0.0);
-    if (!isfinite(a)) atomicOr(P.status, 1);
+    P.Fim[idx] = make_double2(a.hi, a.lo);
+    if (!isfinite(a.hi)) atomicOr(P.status, 1);
 }
 
-__global__ void k_base_s(const DevPlan P) {
-    if (threadIdx.x != 0) return;
-    double s = 0.0;
-    for (int k = 0; k < P.d; ++k) {
+// S in dd: fixed-order strided partials, then a fixed CTA tree (deterministic)
+__global__ void __launch_bounds__(256) k_base_s(const DevPlan P) {
+    dd acc = {0.0, 0.0};
+    double cneg = 0.0;   // corner peak: sum of negative c_k (domain 1 + sum min(c_k, 0) > 0)
+    for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
         const double ck = P.c[k];
-        if (P.kind == SG_F_GAUSSIAN) s -= ck * ck * (0.5 - P.w[k]) * (0.5 - P.w[k]);
-        else s += 0.5 * ck;
+        cneg += ck < 0.0 ? ck : 0.0;
+        if (P.kind == SG_F_GAUSSIAN) {
+            const dd bm = dd_from_sum(0.5, -P.w[k]);
+            acc = dd_sub(acc, dd_mul(dd_mul(bm, bm), dd_from_prod(ck, ck)));
+        } else {
+            acc = dd_add(acc, dd{0.5 * ck, 0.0});
+        }
     }
-    if (P.kind == SG_F_OSCILLATORY) s += 2.0 * M_PI * P.u[0];
-    P.base[0] = s;
-    P.base[1] = 0.0;
-    P.base[2] = 0.0;
-    P.base[3] = 0.0;
+    __shared__ double2 sm[256];
+    __shared__ double sneg[256];
+    sm[threadIdx.x] = make_double2(acc.hi, acc.lo);
+    sneg[threadIdx.x] = cneg;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if (threadIdx.x < st) {
+            const dd r = dd_add(dd{sm[threadIdx.x].x, sm[threadIdx.x].y}, dd{sm[threadIdx.x + st].x, sm[threadIdx.x + st].y});
+            sm[threadIdx.x] = make_double2(r.hi, r.lo);
+            sneg[threadIdx.x] += sneg[threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && P.kind == SG_F_CORNER_PEAK && !(1.0 + sneg[0] > 0.0)) atomicOr(P.status, 1);
+    if (threadIdx.x == 0) {
+        dd S = {sm[0].x, sm[0].y};
+        if (P.kind == SG_F_OSCILLATORY) {
+            const double u = P.u[0];
+            dd th = dd_add(dd_from_prod(DD_2PI_0, u), dd_from_prod(DD_2PI_1, u));
+            th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
+            S = dd_add(S, th);
+        }
+        if (P.kind == SG_F_CORNER_PEAK) S = dd_add(S, dd{1.0, 0.0});
+        P.base[0] = S.hi;
+        P.base[1] = S.lo;
+        P.base[2] = 0.0;
+        P.base[3] = 0.0;
+        if (!dd_finite(S)) atomicOr(P.status, 1);
+    }
 }
 
-__device__ __forceinline__ double sform_g(int kind, double arg) {
-    return kind == SG_F_OSCILLATORY ? cos(arg) : exp(arg);
+__device__ __forceinline__ double sform_g(int kind, int d, double arg) {
+    if (kind == SG_F_OSCILLATORY) return cos(arg);
+    if (kind == SG_F_CORNER_PEAK) return pow(arg, -(double)(d + 1));
+    return exp(arg);
 }
 
+// y^n, n >= 1, by binary powering in dd (left-to-right; ~2 log2 n products)
+__device__ __forceinline__ dd dd_powi(dd y, int n) {
+    int top = 31 - __clz(n);
+    dd r = y;
+    for (int bit = top - 1; bit >= 0; --bit) {
+        r = dd_mul(r, r);
+        if ((n >> bit) & 1) r = dd_mul(r, y);
+    }
+    return r;
+}
+
+__device__ __forceinline__ dd sform_g_dd(int kind, int d, dd y) {
+    if (kind == SG_F_OSCILLATORY) {
+        dd sn, cs;
+        dd_sincos(y, sn, cs);
+        return cs;
+    }
+    if (kind == SG_F_CORNER_PEAK) return dd_powi(dd_div(dd{1.0, 0.0}, y), d + 1);
+    return dd_exp(y);
+}
+
+template <bool DDS>
+__device__ __forceinline__ dd sform_value(const DevPlan &P, dd arg) {
+    return DDS ? sform_g_dd(P.kind, P.d, arg) : dd{sform_g(P.kind, P.d, arg.hi), 0.0};
+}
+
+template <bool DDS>
 __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs R) {
     const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     dd tot = {0.0, 0.0};
@@ -1048,16 +1120,17 @@ __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs 
         }
         const int j1 = rem;
         const int ti = P.tab_off[l1] + k1 * P.nl[l1] + j1;
-        const double2 wv = P.Fre[ti];
-        const double delta = P.Fim[ti].x;
-        const dd W = {wv.x, wv.y};
+        const double2 wv = P.Fre[ti], av = P.Fim[ti];
+        const dd W = {wv.x, wv.y}, delta = {av.x, av.y};
+        const dd S = {P.base[0], P.base[1]};
+        const dd arg = DDS ? dd_add(S, delta) : dd{S.hi + delta.hi, 0.0};
         const int b1 = l1 - 1;
-        tot = dd_mul_d(dd_mul_d(W, sform_g(P.kind, P.base[0] + delta)), P.coef[b1]);
+        tot = dd_mul_d(dd_mul(W, sform_value<DDS>(P, arg)), P.coef[b1]);
         if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
             const long long seg = (long long)b1 * P.d + k1;
             const long long o = R.off1[seg] + j1 - R.JS[seg];
             R.dst_re[o] = wv;
-            R.dst_im[o] = make_double2(delta, 0.0);
+            R.dst_im[o] = av;
             R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
         }
     }
@@ -1065,7 +1138,7 @@ __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs 
     if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
 }
 
-template <bool WRITE>
+template <bool DDS, bool WRITE>
 __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const PassArgs A) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
@@ -1077,15 +1150,14 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
         const long long g = chunk * 32 + lane;
         const bool valid = g < A.nsrc;
         int b = L, k = d;
-        dd W = {0.0, 0.0};
-        double delta = 0.0;
+        dd W = {0.0, 0.0}, delta = {0.0, 0.0};
         if (valid) {
             const uint32_t m = A.src_meta[g];
             b = (int)(m >> SG_META_KBITS);
             k = (int)(m & META_KMASK);
-            const double2 v = A.src_re[g];
+            const double2 v = A.src_re[g], dv = A.src_im[g];
             W = dd{v.x, v.y};
-            delta = A.src_im[g].x;
+            delta = dd{dv.x, dv.y};
         }
         const int ks0 = (int)((long long)split * d / A.nsplit);
         const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
@@ -1098,7 +1170,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
             Nseg = A.NT[s];
             Cseg = A.CT[s];
         }
-        const double S = P.base[0];
+        const dd S = {P.base[0], P.base[1]};
         const int kb = max(ks0, kmin + 1);
         for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
             const bool lv = valid && (lp <= L + 1 - b);
@@ -1115,17 +1187,19 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
                 long long tb = 0;
                 if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
                 for (int j = 0; j < n; ++j) {
-                    const double2 wv = __ldg(Wt + kp * n + j);
-                    const double dl = delta + __ldg(At + kp * n + j).x;           // FP64 partial sum
+                    const double2 wv = __ldg(Wt + kp * n + j), av = __ldg(At + kp * n + j);
+                    // partial sum carried one coordinate further: dd (DDS) or FP64 (ablation)
+                    const dd dl = DDS ? dd_add(delta, dd{av.x, av.y}) : dd{delta.hi + av.x, 0.0};
                     const dd Wc = dd_mul(W, dd{wv.x, wv.y});
-                    const double gv = kv ? sform_g(P.kind, S + dl) : 0.0;       // FP64 outer function
+                    dd gv = {0.0, 0.0};
+                    if (kv) gv = sform_value<DDS>(P, DDS ? dd_add(S, dl) : dd{S.hi + dl.hi, 0.0});
                     double p, e;
-                    dd_mul_pe(Wc, dd{gv, 0.0}, p, e);
+                    dd_mul_pe(Wc, gv, p, e);
                     acc_add(ah, al, p, e);
                     if (WRITE && wk) {
                         const long long o = tb + (long long)j * Nseg;
                         A.dst_re[o] = make_double2(Wc.hi, Wc.lo);
-                        A.dst_im[o] = make_double2(dl, 0.0);
+                        A.dst_im[o] = make_double2(dl.hi, dl.lo);
                         A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
                     }
                 }
@@ -1197,7 +1271,9 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
     s = block_reduce_dd<32>(s);
     if (threadIdx.x == 0) {
         if (include_root && P.coefm[0].x != 0.0) {
-            const dd root = P.sform ? dd{sform_g(P.kind, P.base[0]), 0.0} : dd{P.base[0], P.base[1]};
+            const dd root = P.sform == 2   ? sform_g_dd(P.kind, P.d, dd{P.base[0], P.base[1]})
+                            : P.sform == 1 ? dd{sform_g(P.kind, P.d, P.base[0]), 0.0}
+                                           : dd{P.base[0], P.base[1]};
             s = dd_add(s, coef_mul(P, root, 0, 0));
         }
         if (*P.status) s = dd{nan(""), nan("")};
@@ -1358,7 +1434,8 @@ struct sg_plan_s {
     HostPlan hp;
     DevPlan dp;
     bool cplx = false;
-    bool sform = false;        // SG_ARITH_SFORM_FP64 ablation kernels
+    bool sform = false;        // s-form kernels (SG_ARITH_SFORM_FP64 or SG_ARITH_SFORM_DD)
+    bool sform_dd = false;     // SG_ARITH_SFORM_DD: dd partial sums and outer function
     bool two = false;          // frontier layout with a second double2 array (complex or s-form)
     bool collapse = false;     // SG_METHOD_COLLAPSE: O(d L^2) per-coordinate polynomial product
     int collapse_blocks = 0;   // CTAs of k_collapse_part (one partial polynomial each)
@@ -1401,9 +1478,16 @@ static bool finite_array(const double *a, int n) {
 static int validate_desc(const sg_integrand_desc *f, int d) {
     if (!f || !f->c) return SG_EINVAL;
     if (f->d != d) return SG_EINVAL;
-    if ((int)f->kind < 0 || (int)f->kind > 3) return SG_EINVAL;
+    if ((int)f->kind < 0 || (int)f->kind > 4) return SG_EINVAL;
     if ((f->kind == SG_F_PRODUCT_PEAK || f->kind == SG_F_GAUSSIAN) && !f->w) return SG_EINVAL;
     return SG_OK;
+}
+
+// corner peak: 1 + sum c_k x_k > 0 on the whole cube (its minimum is 1 + sum min(c_k, 0))
+static bool corner_domain_ok(const double *c, int d) {
+    double m = 1.0;
+    for (int k = 0; k < d; ++k) m += c[k] < 0.0 ? c[k] : 0.0;
+    return m > 0.0;
 }
 
 extern "C" const char *sg_strerror(int code) {
@@ -1434,10 +1518,16 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     if (f->kind == SG_F_PRODUCT_PEAK)
         for (int k = 0; k < d; ++k)
             if (f->c[k] == 0.0) return SG_EINVAL;
+    if (f->kind == SG_F_CORNER_PEAK && !corner_domain_ok(f->c, d)) return SG_EINVAL;
     sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
     if (opt) o = *opt;
-    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
-    if (o.arith == SG_ARITH_SFORM_FP64 && f->kind == SG_F_PRODUCT_PEAK) return SG_EUNSUPPORTED;
+    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64 && o.arith != SG_ARITH_SFORM_DD)
+        return SG_EINVAL;
+    // the corner peak is not a product of per-coordinate factors: no factor table exists, its
+    // parity-grade path is the dd s-form (collapse and merge need the factor form)
+    if (f->kind == SG_F_CORNER_PEAK && o.method == SG_METHOD_COLLAPSE) return SG_EUNSUPPORTED;
+    if (f->kind == SG_F_CORNER_PEAK && o.arith == SG_ARITH_FACTOR_DD) o.arith = SG_ARITH_SFORM_DD;
+    if (o.arith != SG_ARITH_FACTOR_DD && f->kind == SG_F_PRODUCT_PEAK) return SG_EUNSUPPORTED;
     if (o.merge != SG_MERGE_NONE && o.merge != SG_MERGE_MIDPOINT) return SG_EINVAL;
     if (o.merge != SG_MERGE_NONE && o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
     if (o.method != SG_METHOD_TREE && o.method != SG_METHOD_COLLAPSE) return SG_EINVAL;
@@ -1452,7 +1542,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         // SG_B200_NOFUSE=1 / SG_B200_FUSE=1 override the automatic choice (tests, A/B runs)
         const char *nf = getenv("SG_B200_NOFUSE"), *fu = getenv("SG_B200_FUSE");
         int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
-        if (o.arith == SG_ARITH_SFORM_FP64) mode = 0;
+        if (o.arith != SG_ARITH_FACTOR_DD) mode = 0;
         if (o.method == SG_METHOD_COLLAPSE) {
             // whole problem on every rank (the collapse is not sharded); no tree passes run
             p->collapse = true;
@@ -1469,7 +1559,8 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     HostPlan &hp = p->hp;
     p->cplx = (f->kind == SG_F_OSCILLATORY);
-    p->sform = (o.arith == SG_ARITH_SFORM_FP64);
+    p->sform = (o.arith == SG_ARITH_SFORM_FP64 || o.arith == SG_ARITH_SFORM_DD);
+    p->sform_dd = (o.arith == SG_ARITH_SFORM_DD);
     p->two = p->cplx || p->sform;
     if (p->sform) p->leaf1 = false;
     {
@@ -1547,7 +1638,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     dp.u = (const double *)(base + ou);
     dp.Fre = (double2 *)(base + oFr);
     dp.Fim = p->two ? (double2 *)(base + oFi) : nullptr;
-    dp.sform = p->sform ? 1 : 0;
+    dp.sform = p->sform_dd ? 2 : p->sform ? 1 : 0;
     dp.base = (double *)(base + oB);
     dp.status = (int *)(base + oS);
     p->d_tabs = (long long *)(base + oT);
@@ -1808,14 +1899,15 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // K0
     if (hp.tab_entries > 0) {
         if (p->sform) {
-            k_factor_s<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+            if (p->sform_dd) k_factor_s<true><<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+            else k_factor_s<false><<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
         } else {
             k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
             k_suffix_abs<<<hp.L, 256, 0, st>>>(dp);
         }
     }
     mark();
-    if (p->sform) k_base_s<<<1, 32, 0, st>>>(dp);
+    if (p->sform) k_base_s<<<1, 256, 0, st>>>(dp);
     else k_base<<<1, 256, 0, st>>>(dp);
     mark();
     // root pass
@@ -1828,7 +1920,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
     R.partials = partials;
     if (p->sform)
-        k_root_s<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+        (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
     else if (p->cplx)
         k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
     else
@@ -1886,8 +1978,13 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         const int n2 = hp.nl[2];
         const bool single = !write && t == p->leaf1_t;
         if (p->sform) {
-            if (write) k_pass_s<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            else k_pass_s<false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            if (p->sform_dd) {
+                if (write) k_pass_s<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+                else k_pass_s<true, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            } else {
+                if (write) k_pass_s<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+                else k_pass_s<false, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            }
         } else if (p->cplx) {
             if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
             else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, st); }
@@ -2034,7 +2131,8 @@ extern "C" int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_
     if (d < 1 || q < d) return SG_EINVAL;
     sg_options o = {SG_FORM_COMBINATION, SG_ARITH_FACTOR_DD, 0, 1, 0, -1};
     if (opt) o = *opt;
-    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64) return SG_EINVAL;
+    if (o.arith != SG_ARITH_FACTOR_DD && o.arith != SG_ARITH_SFORM_FP64 && o.arith != SG_ARITH_SFORM_DD)
+        return SG_EINVAL;
     HostPlan hp;
     int rc = host_plan_build(hp, d, q - d, (int)rule, (int)kind, (int)o.form, (int)o.merge, o.rank, o.world,
                              o.range_lo, o.range_hi);

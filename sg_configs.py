@@ -29,8 +29,10 @@ KIND_EXP = 0      # exp(sum c_k x_k)
 KIND_OSC = 1      # cos(2 pi u + sum c_k x_k)
 KIND_PEAK = 2     # prod (c_k^-2 + (x_k - w_k)^2)^-1
 KIND_GAUSS = 3    # exp(-sum c_k^2 (x_k - w_k)^2)
+KIND_CORNER = 4   # (1 + sum c_k x_k)^-(d+1)  (Genz corner peak; not separable: s-form dd path)
 
-KIND_NAMES = {KIND_EXP: "exp", KIND_OSC: "osc", KIND_PEAK: "peak", KIND_GAUSS: "gauss"}
+KIND_NAMES = {KIND_EXP: "exp", KIND_OSC: "osc", KIND_PEAK: "peak", KIND_GAUSS: "gauss",
+              KIND_CORNER: "corner_peak"}
 RULE_NAMES = {RULE_TRAP: "trapezoidal", RULE_CC: "clenshaw_curtis", RULE_GP: "gauss_patterson",
               RULE_GL: "gauss_legendre"}
 
@@ -113,11 +115,20 @@ def paper_table_problem(table: str, d: int, N: int) -> Problem:
     raise ValueError(table)
 
 
+def corner_config(d: int = 100, L: int = 4, rule: int = RULE_CC, seed: int = 5) -> Problem:
+    """Extra (non-BASELINE) workload for the non-separable s-form dd path: Genz corner peak
+    (1 + sum c_k x_k)^-(d+1), c_k ~ U(0,1) from `seed` rescaled to sum c_k = 1 (reading R9 draw
+    order); d = 100, L = 4, Clenshaw-Curtis by default."""
+    c, w, u = _draw(seed, d, 0.0, 1.0, False, False, 1.0)
+    return Problem(f"cp_d{d}_L{L}", d, L, rule, KIND_CORNER, c, w, u)
+
+
 def random_problem(seed: int, d: int, L: int, rule: int, kind: int) -> Problem:
     """Small seeded problems for parity sweeps (same draw convention, generic parameter ranges)."""
     c_lo, c_hi = {KIND_EXP: (-1.0, 1.0), KIND_OSC: (0.0, 1.0), KIND_PEAK: (0.5, 1.5),
-                  KIND_GAUSS: (0.0, 0.5)}[kind]
+                  KIND_GAUSS: (0.0, 0.5), KIND_CORNER: (0.0, 1.0)}[kind]
     has_w = kind in (KIND_PEAK, KIND_GAUSS)
     has_u = kind == KIND_OSC
-    c, w, u = _draw(seed, d, c_lo, c_hi, has_w, has_u, None)
+    # corner peak: Genz-style normalisation sum c_k = 1 (f ranges over (2^-(d+1), 1])
+    c, w, u = _draw(seed, d, c_lo, c_hi, has_w, has_u, 1.0 if kind == KIND_CORNER else None)
     return Problem(f"rand_s{seed}_d{d}_L{L}_r{rule}_k{kind}", d, L, rule, kind, c, w, u)

@@ -244,6 +244,16 @@ def closed_form(p: S.Problem):
                 ck, wk = mp.mpf(ck), mp.mpf(wk)
                 r *= mp.sqrt(mp.pi) / (2 * ck) * (mp.erf(ck * (1 - wk)) + mp.erf(ck * wk))
             return r
+        if p.kind == S.KIND_CORNER:
+            # d-fold integration of (1 + c.x)^-(d+1): each step int_0^1 (a + c x)^-(n+1) dx =
+            # (a^-n - (a + c)^-n) / (n c), so I = sum_{v in {0,1}^d} (-1)^|v| / (1 + c.v) / (d! prod c)
+            # (all c_k != 0; exponential in d, cancelling: only for small d at 50 digits)
+            import itertools
+            d = p.d
+            tot = mp.mpf(0)
+            for v in itertools.product((0, 1), repeat=d):
+                tot += (-1) ** sum(v) / (1 + mp.fsum(mp.mpf(ci) for ci, vi in zip(p.c, v) if vi))
+            return tot / (mp.factorial(d) * mp.fprod([mp.mpf(ci) for ci in p.c]))
     raise ValueError(p.kind)
 
 
