@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
     ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
+    ap.add_argument("--no-corner", action="store_true",
+                    help="skip the non-separable corner-peak leg (SG_ARITH_SFORM_DD)")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
     # through host memory and every rank may share one device (ranks never wait on each other
     # inside a kernel, so sharing is safe); the product configuration is nccl + one GPU per rank
@@ -374,6 +376,36 @@ def main():
         }
         cplan.close()
 
+    # corner-peak leg (SG_ARITH_SFORM_DD): the non-separable Genz corner peak on its own workload
+    # (sg_configs.corner_config: d=100, L=4, CC), partial sums carried in dd, dd outer function per
+    # point; sharded like the headline tree
+    corner = None
+    if not args.no_corner:
+        pc = S.corner_config()
+        kplan = api.Plan(pc.d, pc.q, pc.rule, pc.kind, pc.c, pc.w, pc.u, rank=rank, world=world,
+                         device=dev, arith=api.ARITH_SFORM_DD)
+        kplan.profile_enable(True)
+        k_shard, k_total = kplan.points()
+        for _ in range(args.warmup):
+            step(kplan)
+        torch.cuda.synchronize(dev)
+        k_times, _ = timed(lambda: step(kplan), args.steps, kplan, 0)
+        k_res = result.cpu().numpy()
+        k_ms = statistics.mean(k_times)
+        corner = {"workload": f"{pc.name}: Genz corner peak (1 + sum c_k x_k)^-(d+1), d={pc.d}, "
+                              f"q=d+{pc.L}, {S.RULE_NAMES[pc.rule]}, c~U(0,1) seed 5, sum c = 1",
+                  "arith": "s-form double-double (dd partial sums, dd power per point)",
+                  "points": k_total, "time_to_integral_ms": k_ms,
+                  "value": k_total / (k_ms * 1e-3), "unit": "points/s",
+                  "result": float(k_res[0]), "step_ms_all": [round(t, 4) for t in k_times]}
+        gfile = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
+        if os.path.exists(gfile):
+            vals = json.load(open(gfile))["values"]
+            if pc.name in vals:
+                ref = float(vals[pc.name]["hi"]) + float(vals[pc.name]["lo"])
+                corner["rel_err_vs_oracle"] = abs(float(k_res[0]) + float(k_res[1]) - ref) / abs(ref)
+        kplan.close()
+
     # rank-0 report
     if rank == 0:
         peak, mhz = peak_fp64_tflops()
@@ -427,6 +459,8 @@ def main():
             line["merged"] = merged
         if collapse is not None:
             line["collapse"] = collapse
+        if corner is not None:
+            line["corner_peak"] = corner
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
         print(json.dumps(line), flush=True)

@@ -84,6 +84,13 @@ DD_HD dd dd_div(dd a, dd b) {
     return dd_add(q, dd{q3, 0.0});
 }
 DD_HD dd dd_div_d(dd a, double b) { return dd_div(a, dd{b, 0.0}); }
+// 1 / y: FP64 quotient r0 and one Newton correction r0 (1 + e), e = 1 - y r0 (two FMAs): ~2^-104
+DD_HD dd dd_recip(dd y) {
+    const double r0 = 1.0 / y.hi;
+    double e = fma(-y.hi, r0, 1.0);
+    e = fma(-y.lo, r0, e);
+    return dd_norm(r0, r0 * e);
+}
 DD_HD cdd cdd_mul(cdd a, cdd b) {
     cdd r;
     r.re = dd_sub(dd_mul(a.re, b.re), dd_mul(a.im, b.im));

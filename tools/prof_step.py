@@ -14,12 +14,13 @@ from paper_2210_14313_b200 import api  # noqa: E402
 
 
 def main():
-    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "5"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-    p = S.baseline_config(cfg)
+    p = S.corner_config() if cfg == "cp" else S.baseline_config(int(cfg))
     plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
                     merge=int(os.environ.get("QUICK_MERGE", "0")),
-                    method=int(os.environ.get("QUICK_METHOD", "0")))
+                    method=int(os.environ.get("QUICK_METHOD", "0")),
+                    arith=int(os.environ.get("QUICK_ARITH", "0")))
     for _ in range(steps):
         out = plan.sg_integrate()
         plan.sg_finalize(out, 1)

@@ -21,17 +21,22 @@ def tp_small(plan):
 
 
 def main():
-    cfgs = [int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,3,4,5".split(","))]
+    cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,3,4,5".split(",")
     for i in cfgs:
-        p = S.baseline_config(i)
+        # "cp" = the corner-peak workload (non-separable: dd s-form, no DP pin)
+        p = S.corner_config() if i == "cp" else S.baseline_config(int(i))
         t0 = time.time()
         plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
                         merge=int(os.environ.get("QUICK_MERGE", "0")),
-                        method=int(os.environ.get("QUICK_METHOD", "0")))
+                        method=int(os.environ.get("QUICK_METHOD", "0")),
+                        arith=int(os.environ.get("QUICK_ARITH", "0")))
         tplan = time.time() - t0
         hi, lo = plan.integrate_host()
-        dp = pins.dp_value(p)
-        err = abs((mp.mpf(hi) + mp.mpf(lo) - dp) / dp)
+        if p.kind == S.KIND_CORNER:
+            err = mp.nan
+        else:
+            dp = pins.dp_value(p)
+            err = abs((mp.mpf(hi) + mp.mpf(lo) - dp) / dp)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         times = []
