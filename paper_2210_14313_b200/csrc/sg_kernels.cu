@@ -44,8 +44,8 @@ struct DevPlan {
     double *SA;     // [(L+2) x (d+1)] suffix sums of |F| per level (k_leaf's accumulation bound)
     int *status;
     int sform;      // 0 factor form; 1 SG_ARITH_SFORM_FP64, 2 SG_ARITH_SFORM_DD: base[0..1] = argument S
-    int symmask;    // bit l: level-l row symmetric about 1/2 with its midpoint at the centre (odd n,
-                    // x_j = 1 - x_{n-1-j}, equal dd weights): oscillatory factors of a pair are
+    int symmask;    // bit l: level-l row symmetric about 1/2 (x_j = 1 - x_{n-1-j}, equal dd weights,
+                    // the midpoint at the centre if n is odd): oscillatory factors of a pair are
                     // exact conjugates, the midpoint's is real (k_leaf's symmetric-row path)
     const double2 *coefm;   // node coefficient (dd) per (depth t, excess b): [t * (L + 1) + b]
 };
@@ -532,10 +532,10 @@ __device__ __forceinline__ dd leaf_level(const double2 *Fr, const double2 *Fi, i
     return s;
 }
 
-// Symmetric oscillatory row of NJ (odd) nodes: pairs (j, NJ-1-j) share their products
-// (leaf_sym_pair_terms, F_j = conj(F_{NJ-1-j})), the midpoint's factor is real; one biased
-// accumulator pair per pair plus one for the midpoint.  7 FP64 instructions per point for NJ = 3,
-// 7.4 for NJ = 5, instead of 12.
+// Symmetric oscillatory row of NJ nodes: pairs (j, NJ-1-j) share their products
+// (leaf_sym_pair_terms, F_j = conj(F_{NJ-1-j})), the midpoint's factor (odd NJ) is real; one biased
+// accumulator pair per pair plus one for the midpoint.  8 FP64 instructions per point for even NJ
+// (midpoint-merged rows), 7.0 for NJ = 3, 7.4 for NJ = 5, instead of 12.
 template <int NJ>
 __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                               int kp0, int kp1, int klane, bool pred, const dd &pr, const dd &pim,
@@ -552,10 +552,10 @@ __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, co
 #pragma unroll
             for (int q = 0; q < NP; ++q)
                 leaf_sym_pair_terms(er, ei, __ldg(fr + NJ - 1 - q), __ldg(fi + NJ - 1 - q), acc[q].h, acc[q].l);
-            leaf_real_factor_term<false>(er, __ldg(fr + NP), acc[NP].h, acc[NP].l);
+            if constexpr (NJ % 2 == 1) leaf_real_factor_term<false>(er, __ldg(fr + NP), acc[NP].h, acc[NP].l);
         }
 #pragma unroll
-        for (int q = 0; q <= NP; ++q) leaf_fold(acc[q], sigma);
+        for (int q = 0; q < (NJ + 1) / 2; ++q) leaf_fold(acc[q], sigma);
     }
 }
 
@@ -620,6 +620,8 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
             const bool sym = CPLX && ((P.symmask >> lp) & 1);
             if (sym && n == 3) s = leaf_level_sym<3>(Fr, Fi, kb, kmain, ks1, k, er, ei, sigma);
             else if (sym && n == 5) s = leaf_level_sym<5>(Fr, Fi, kb, kmain, ks1, k, er, ei, sigma);
+            else if (sym && n == 2) s = leaf_level_sym<2>(Fr, Fi, kb, kmain, ks1, k, er, ei, sigma);
+            else if (sym && n == 4) s = leaf_level_sym<4>(Fr, Fi, kb, kmain, ks1, k, er, ei, sigma);
             else switch (n) {
             case 2: s = leaf_level<CPLX, 2>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             case 3: s = leaf_level<CPLX, 3>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
@@ -1680,7 +1682,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     dp.symmask = 0;
     for (int l = 2; l <= L + 1; ++l) {
         const int n = hp.nl[l], e0 = hp.entry_off[l];
-        bool sym = (n % 2 == 1) && hp.X[e0 + n / 2] == 0.5;
+        bool sym = n >= 2 && (n % 2 == 0 || hp.X[e0 + n / 2] == 0.5);
         for (int j = 0; sym && j < n / 2; ++j) {
             const int m = e0 + n - 1 - j;
             sym = (1.0 - hp.X[m] == hp.X[e0 + j]) && hp.Whi[m] == hp.Whi[e0 + j] && hp.Wlo[m] == hp.Wlo[e0 + j];
