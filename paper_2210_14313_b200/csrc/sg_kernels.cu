@@ -837,6 +837,9 @@ struct Leaf2Args {
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
 // SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory), or nodes 0 and 1 do
 // (CJ == -1, NJ == 2: the midpoint-merged Clenshaw-Curtis level-2 row {0, 1}).
+#ifndef LEAF2_SPLIT2
+#define LEAF2_SPLIT2 1  // same split for the midpoint-merged NJ = 2 symmetric row (merged c5 -0.6%)
+#endif
 #ifndef LEAF2_SPLIT
 #define LEAF2_SPLIT 1   // second accumulator pair per mid (node 2 + midpoint): shorter chains, c5 -1%
 #endif
@@ -880,7 +883,22 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
         const double2 f1 = SMEM ? Fr[kp * 2 + 1] : __ldg(Fr + kp * 2 + 1);
         const double2 g1 = SMEM ? Fi[kp * 2 + 1] : __ldg(Fi + kp * 2 + 1);
 #pragma unroll
-        for (int jm = 0; jm < 2; ++jm) leaf_sym_pair_terms(er[jm], ei[jm], f1, g1, ah[jm], al[jm]);
+        for (int jm = 0; jm < 2; ++jm) {
+            if constexpr (LEAF2_SPLIT2) {
+                // node 0 (A + B) into accumulator a, node 1 (A - B) into b: shorter chains
+                const double u1 = fma(er[jm].hi, f1.x, ah[jm]);
+                const double h1 = u1 - ah[jm];
+                ah[jm] = fma(ei[jm].hi, g1.x, u1);
+                const double h2 = ah[jm] - u1;
+                const double cA = fma(er[jm].lo, f1.x, fma(er[jm].hi, f1.y, fma(er[jm].hi, f1.x, -h1)));
+                const double cB = fma(ei[jm].lo, g1.x, fma(ei[jm].hi, g1.y, fma(ei[jm].hi, g1.x, -h2)));
+                al[jm] += cA + cB;
+                bh[jm] += h1 - h2;
+                bl[jm] += cA - cB;
+            } else {
+                leaf_sym_pair_terms(er[jm], ei[jm], f1, g1, ah[jm], al[jm]);
+            }
+        }
         return;
     }
     double2 f[NJ], g[NJ];
@@ -1003,14 +1021,17 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 for (; kp < ke; ++kp) leaf2_row_multi<CPLX, NJ, SMEM, CJ, SYM, CZ>(Fr, Fi, kp, er, ei, ah, al, bh, bl);
 #pragma unroll
                 for (int jm = 0; jm < NJ; ++jm) {
-                    if (LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) al[jm] += bl[jm], bl[jm] = 0.0;
+                    if ((LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) ||
+                        (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1))
+                        al[jm] += bl[jm], bl[jm] = 0.0;
                     const double t = (al[jm] + sg[jm]) - sg[jm];
                     ah[jm] += t;
                     al[jm] -= t;
                 }
             }
             // lane value = sum_jm (ah - sigma) + al: exact grid parts via TwoSum, low parts in FP64
-            if (LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) {
+            if ((LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) ||
+                (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1)) {
 #pragma unroll
                 for (int jm = 0; jm < NJ; ++jm) {   // same grid, |sum| < 2^m: exact
                     ah[jm] += bh[jm] - sg[jm];
