@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const Pa
 // per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
 // ---------------------------------------------------------------------------------------------
 #ifndef FOLD
-#define FOLD 16   // rows between folds of acc_lo onto the grid (32: 0.3% faster, 150x larger error)
+#define FOLD 32   // rows between folds of acc_lo onto the grid (A/B: 32 vs 16: c5 -0.8%, c4 -1.4%; rel. error 2.7e-20 vs 1e-20)
 #endif
 #ifndef LEAF_MINB
 #define LEAF_MINB 3
@@ -837,6 +837,9 @@ struct Leaf2Args {
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
 // SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory), or nodes 0 and 1 do
 // (CJ == -1, NJ == 2: the midpoint-merged Clenshaw-Curtis level-2 row {0, 1}).
+#ifndef LEAF2_SPLITR
+#define LEAF2_SPLITR 0  // same split for the real kinds' NJ = 3 row with midpoint
+#endif
 #ifndef LEAF2_SPLIT2
 #define LEAF2_SPLIT2 1  // same split for the midpoint-merged NJ = 2 symmetric row (merged c5 -0.6%)
 #endif
@@ -911,6 +914,13 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int jm = 0; jm < NJ; ++jm) {
+            if constexpr (LEAF2_SPLITR && !CPLX && NJ == 3 && CJ == 1) {
+                // real kinds: node 0 and the midpoint into accumulator a, node 2 into b
+                if (j == CJ) leaf_real_factor_term<CZ>(er[jm], f[j], ah[jm], al[jm]);
+                else if (j == 0) leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], ah[jm], al[jm]);
+                else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], bh[jm], bl[jm]);
+                continue;
+            }
             if (j == CJ) leaf_real_factor_term<CZ>(er[jm], f[j], ah[jm], al[jm]);
             else leaf1_term<CPLX>(er[jm], ei[jm], f[j], g[j], ah[jm], al[jm]);
         }
@@ -1022,7 +1032,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 #pragma unroll
                 for (int jm = 0; jm < NJ; ++jm) {
                     if ((LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) ||
-                        (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1))
+                        (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1) ||
+                        (LEAF2_SPLITR && !CPLX && NJ == 3 && CJ == 1))
                         al[jm] += bl[jm], bl[jm] = 0.0;
                     const double t = (al[jm] + sg[jm]) - sg[jm];
                     ah[jm] += t;
@@ -1031,7 +1042,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             }
             // lane value = sum_jm (ah - sigma) + al: exact grid parts via TwoSum, low parts in FP64
             if ((LEAF2_SPLIT && SYM && CPLX && NJ == 3 && CJ == 1) ||
-                (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1)) {
+                (LEAF2_SPLIT2 && SYM && CPLX && NJ == 2 && CJ == -1) ||
+                (LEAF2_SPLITR && !CPLX && NJ == 3 && CJ == 1)) {
 #pragma unroll
                 for (int jm = 0; jm < NJ; ++jm) {   // same grid, |sum| < 2^m: exact
                     ah[jm] += bh[jm] - sg[jm];
