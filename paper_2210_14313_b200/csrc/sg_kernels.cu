@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
 template <bool CPLX, bool WRITE>
-__global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const PassArgs A) {
+__global__ void __launch_bounds__(PASS_THREADS, 3) k_pass(const DevPlan P, const PassArgs A) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
     dd tot = {0.0, 0.0};
@@ -374,10 +374,15 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(const DevPlan P, const Pa
                         acc_add(ah, al, p1, e1);
                         acc_add(ah, al, -p2, -e2);
                         if (WRITE && wk) {
+                            // the stored child product P F reuses the two products of its real part
                             const long long o = tb + (long long)j * Nseg;
-                            cdd ch = cdd_mul(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{fi.x, fi.y}});
-                            A.dst_re[o] = make_double2(ch.re.hi, ch.re.lo);
-                            A.dst_im[o] = make_double2(ch.im.hi, ch.im.lo);
+                            const dd cre = dd_combine_pe(p1, e1, -p2, -e2);
+                            double p3, e3, p4, e4;
+                            dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
+                            dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
+                            const dd cim = dd_combine_pe(p3, e3, p4, e4);
+                            A.dst_re[o] = make_double2(cre.hi, cre.lo);
+                            A.dst_im[o] = make_double2(cim.hi, cim.lo);
                             A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
                         }
                     }
