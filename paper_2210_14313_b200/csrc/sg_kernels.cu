@@ -300,113 +300,6 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // Lane = one parent prefix, held in registers; the loop over its children (k', l', j') reads the
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
-template <bool CPLX, bool WRITE>
-__global__ void __launch_bounds__(PASS_THREADS, 3) k_pass(const DevPlan P, const PassArgs A) {
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long task = (long long)blockIdx.x * WPB + wib;
-    dd tot = {0.0, 0.0};
-    if (task < A.ntasks) {
-        const int d = P.d, L = P.L;
-        const long long chunk = task / A.nsplit;
-        const int split = (int)(task - chunk * A.nsplit);
-        const long long g = chunk * 32 + lane;
-        const bool valid = g < A.nsrc;
-        int b = L, k = d;
-        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
-        if (valid) {
-            const uint32_t m = A.src_meta[g];
-            b = (int)(m >> SG_META_KBITS);
-            k = (int)(m & META_KMASK);
-            const double2 v = A.src_re[g];
-            pr = dd{v.x, v.y};
-            if (CPLX) {
-                const double2 vi = A.src_im[g];
-                pim = dd{vi.x, vi.y};
-            }
-        }
-        const int ks0 = (int)((long long)split * d / A.nsplit);
-        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
-        const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
-        const int bmin = __reduce_min_sync(0xffffffffu, b);
-        long long iseg = 0, Nseg = 0, Cseg = 0;
-        if (WRITE && valid) {
-            const long long s = (long long)b * d + k;
-            iseg = g - A.offT[s];
-            Nseg = A.NT[s];
-            Cseg = A.CT[s];
-        }
-        const int kb = max(ks0, kmin + 1);
-        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
-            const bool lv = valid && (lp <= L + 1 - b);
-            const int n = P.nl[lp];
-            const int bp = b + lp - 1;
-            const double2 *Fr = P.Fre + P.tab_off[lp];
-            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
-            const bool wr = WRITE && lv && (bp <= L - 1);
-            const long long wbase = (long long)n * Cseg + iseg;
-            double ah = 0.0, al = 0.0;
-            for (int kp = kb; kp < ks1; ++kp) {
-                const bool kv = lv && (kp > k);
-                const dd er = kv ? pr : dd{0.0, 0.0};
-                const dd ei = kv ? pim : dd{0.0, 0.0};
-                const bool wk = wr && kv && (kp <= d - 2);
-                long long tb = 0;
-                if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
-                const double2 *fr_row = Fr + kp * n;
-                const double2 *fi_row = CPLX ? Fi + kp * n : nullptr;
-                for (int j = 0; j < n; ++j) {
-                    const double2 f = __ldg(fr_row + j);
-                    if (!CPLX) {
-                        double p, e;
-                        dd_mul_pe(er, dd{f.x, f.y}, p, e);
-                        acc_add(ah, al, p, e);
-                        if (WRITE && wk) {
-                            const long long o = tb + (long long)j * Nseg;
-                            dd ch = dd_norm(p, e);
-                            A.dst_re[o] = make_double2(ch.hi, ch.lo);
-                            A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
-                        }
-                    } else {
-                        const double2 fi = __ldg(fi_row + j);
-                        double p1, e1, p2, e2;
-                        dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
-                        dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
-                        acc_add(ah, al, p1, e1);
-                        acc_add(ah, al, -p2, -e2);
-                        if (WRITE && wk) {
-                            // the stored child product P F reuses the two products of its real part
-                            const long long o = tb + (long long)j * Nseg;
-                            const dd cre = dd_combine_pe(p1, e1, -p2, -e2);
-                            double p3, e3, p4, e4;
-                            dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
-                            dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
-                            const dd cim = dd_combine_pe(p3, e3, p4, e4);
-                            A.dst_re[o] = make_double2(cre.hi, cre.lo);
-                            A.dst_im[o] = make_double2(cim.hi, cim.lo);
-                            A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
-                        }
-                    }
-                }
-            }
-            if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, bp));
-        }
-    }
-    dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
-}
-
-// ---------------------------------------------------------------------------------------------
-// Leaf-only pass (no extendable children): the hot loop of configs 4-5 (>= 97% of the points).
-//
-// Same task mapping as k_pass, but the accumulation is "grid-split": with sigma = 1.5 * 2^m and
-// 2^m >= 2 * (bound on sum |P F| over the lane's children, from the suffix table SA), the high part
-// h = fma(P.hi, F.hi, sigma) - sigma of every product is P.hi F.hi rounded once to the grid
-// u = ulp(sigma), so acc_hi += h is EXACT; the remainder and the cross terms are small and go to
-// acc_lo by FMAs (folded back onto the grid every FOLD rows).  7 FP64 instructions per real leaf
-// and 14 per oscillatory leaf, against 12 / 24 with TwoSum + dd products (DESIGN.md §K3).
-// Children (k', j') are walked row by row (k'), NJ nodes per row unrolled with one accumulator pair
-// per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
-// ---------------------------------------------------------------------------------------------
 #ifndef FOLD
 #define FOLD 32   // rows between folds of acc_lo onto the grid (A/B: 32 vs 16: c5 -0.8%, c4 -1.4%; rel. error 2.7e-20 vs 1e-20)
 #endif
@@ -455,6 +348,120 @@ __device__ __forceinline__ void leaf_fold(LeafAcc &a, double sigma) {
     a.h += t;
     a.l -= t;
 }
+
+#ifndef PASS_MINB
+#define PASS_MINB 3   // CTAs/SM bound of k_pass
+#endif
+template <bool CPLX, bool WRITE>
+__global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan P, const PassArgs A) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long task = (long long)blockIdx.x * WPB + wib;
+    dd tot = {0.0, 0.0};
+    if (task < A.ntasks) {
+        const int d = P.d, L = P.L;
+        const long long chunk = task / A.nsplit;
+        const int split = (int)(task - chunk * A.nsplit);
+        const long long g = chunk * 32 + lane;
+        const bool valid = g < A.nsrc;
+        int b = L, k = d;
+        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
+        if (valid) {
+            const uint32_t m = A.src_meta[g];
+            b = (int)(m >> SG_META_KBITS);
+            k = (int)(m & META_KMASK);
+            const double2 v = A.src_re[g];
+            pr = dd{v.x, v.y};
+            if (CPLX) {
+                const double2 vi = A.src_im[g];
+                pim = dd{vi.x, vi.y};
+            }
+        }
+        const int ks0 = (int)((long long)split * d / A.nsplit);
+        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
+        const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
+        const int bmin = __reduce_min_sync(0xffffffffu, b);
+        long long iseg = 0, Nseg = 0, Cseg = 0;
+        if (WRITE && valid) {
+            const long long s = (long long)b * d + k;
+            iseg = g - A.offT[s];
+            Nseg = A.NT[s];
+            Cseg = A.CT[s];
+        }
+        const double pabs = fabs(pr.hi) + (CPLX ? fabs(pim.hi) : 0.0);
+        const int kb = max(ks0, kmin + 1);
+        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
+            const bool lv = valid && (lp <= L + 1 - b);
+            const int n = P.nl[lp];
+            const int bp = b + lp - 1;
+            const double2 *Fr = P.Fre + P.tab_off[lp];
+            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            const bool wr = WRITE && lv && (bp <= L - 1);
+            const long long wbase = (long long)n * Cseg + iseg;
+            // biased grid accumulator (leaf_term): sigma = 1.5 * 2^m > 2 * bound on the lane's
+            // children of this level, from the suffix table SA
+            const double bound = lv ? pabs * P.SA[(long long)lp * (d + 1) + min(k + 1, d)] * (1.0 + 0x1p-20) : 0.0;
+            int ex = 0;
+            frexp(2.0 * bound, &ex);
+            const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+            LeafAcc acc = {sigma, 0.0};
+            int nfold = 0;
+            for (int kp = kb; kp < ks1; ++kp) {
+                const bool kv = lv && (kp > k);
+                const dd er = kv ? pr : dd{0.0, 0.0};
+                const dd ei = kv ? pim : dd{0.0, 0.0};
+                const bool wk = wr && kv && (kp <= d - 2);
+                long long tb = 0;
+                if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
+                const double2 *fr_row = Fr + kp * n;
+                const double2 *fi_row = CPLX ? Fi + kp * n : nullptr;
+                for (int j = 0; j < n; ++j) {
+                    const double2 f = __ldg(fr_row + j);
+                    const double2 fi = CPLX ? __ldg(fi_row + j) : make_double2(0.0, 0.0);
+                    leaf_term<CPLX>(er, ei, f, fi, acc);
+                    if (WRITE && wk) {
+                        // the stored child product P F in dd (complex for the oscillatory kind)
+                        const long long o = tb + (long long)j * Nseg;
+                        double p1, e1;
+                        dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
+                        if (!CPLX) {
+                            const dd ch = dd_norm(p1, e1);
+                            A.dst_re[o] = make_double2(ch.hi, ch.lo);
+                        } else {
+                            double p2, e2, p3, e3, p4, e4;
+                            dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
+                            dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
+                            dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
+                            const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
+                            A.dst_re[o] = make_double2(cre.hi, cre.lo);
+                            A.dst_im[o] = make_double2(cim.hi, cim.lo);
+                        }
+                        A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                    }
+                }
+                if (++nfold == FOLD) {
+                    nfold = 0;
+                    leaf_fold(acc, sigma);
+                }
+            }
+            if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(acc.h - sigma, acc.l), A.t + 1, bp));
+        }
+    }
+    dd s = block_reduce_dd<WPB>(tot);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Leaf-only pass (no extendable children): the hot loop of configs 4-5 (>= 97% of the points).
+//
+// Same task mapping as k_pass, but the accumulation is "grid-split": with sigma = 1.5 * 2^m and
+// 2^m >= 2 * (bound on sum |P F| over the lane's children, from the suffix table SA), the high part
+// h = fma(P.hi, F.hi, sigma) - sigma of every product is P.hi F.hi rounded once to the grid
+// u = ulp(sigma), so acc_hi += h is EXACT; the remainder and the cross terms are small and go to
+// acc_lo by FMAs (folded back onto the grid every FOLD rows).  7 FP64 instructions per real leaf
+// and 14 per oscillatory leaf, against 12 / 24 with TwoSum + dd products (DESIGN.md §K3).
+// Children (k', j') are walked row by row (k'), NJ nodes per row unrolled with one accumulator pair
+// per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
+// ---------------------------------------------------------------------------------------------
 
 // Leaf term for a node whose factor is REAL (imaginary part exactly 0): the midpoint node x = 1/2 of
 // a level (E_k(1/2) = 1 for every kind, so F = w exactly real).  Re(P F) = P.re F: 7 FP64
