@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
     ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
+    ap.add_argument("--no-frontier", action="store_true",
+                    help="skip the stored-frontier (unfused) leg that measures the HBM-bound frontier kernel")
     ap.add_argument("--no-corner", action="store_true",
                     help="skip the non-separable corner-peak leg (SG_ARITH_SFORM_DD)")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
@@ -376,6 +378,45 @@ def main():
         }
         cplan.close()
 
+    # frontier leg: the same workload with the last two levels NOT fused (SG_B200_NOFUSE=1), so the
+    # frontier kernel k_pass<., WRITE> materialises the deepest frontier (config 5: 119 M records,
+    # 4.3 GB) — the HBM-bound step of the level-synchronous design that the default fused path
+    # avoids.  Reports that launch's HBM bytes / time against MEASURED_PEAKS.json hbm_gbs.
+    frontier = None
+    if not args.no_frontier:
+        os.environ["SG_B200_NOFUSE"] = "1"
+        try:
+            fplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
+                             device=dev)
+        finally:
+            del os.environ["SG_B200_NOFUSE"]
+        fplan.profile_enable(True)
+        fpasses = fplan.passes()
+        # the pass writing the largest frontier
+        wpass = max(range(1, len(fpasses)), key=lambda i: fpasses[i].written) if len(fpasses) > 1 else 0
+        for _ in range(min(args.warmup, 2)):
+            step(fplan)
+        torch.cuda.synchronize(dev)
+        f_times, f_kern = timed(lambda: step(fplan), min(args.steps, 3), fplan, wpass)
+        rec = (32 if p.kind == S.KIND_OSC else 16) + 4
+        wbytes = fpasses[wpass].written * rec
+        rbytes = fpasses[wpass - 1].written * rec if wpass >= 1 else 0
+        k_ms = statistics.mean(f_kern)
+        hbm = None
+        try:
+            hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            pass
+        gbs = (wbytes + rbytes) / (k_ms * 1e-3) / 1e9
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        ftraffic = json.load(open(tfile)).get(f"c{args.config}_frontier") if os.path.exists(tfile) else None
+        frontier = {"what": f"unfused step; pass {wpass} (k_pass WRITE) writes {fpasses[wpass].written} "
+                            f"frontier records of {rec} B and evaluates {fpasses[wpass].terms} points",
+                    "step_ms": statistics.mean(f_times), "kernel_ms": k_ms,
+                    "algorithmic_bytes": wbytes + rbytes, "achieved_gbs": gbs,
+                    "peak_gbs": hbm, "frac": (gbs / hbm) if hbm else None, "traffic": ftraffic}
+        fplan.close()
+
     # corner-peak leg (SG_ARITH_SFORM_DD): the non-separable Genz corner peak on its own workload
     # (sg_configs.corner_config: d=100, L=4, CC), partial sums carried in dd, dd outer function per
     # point; sharded like the headline tree
@@ -461,6 +502,8 @@ def main():
             line["collapse"] = collapse
         if corner is not None:
             line["corner_peak"] = corner
+        if frontier is not None:
+            line["frontier_kernel"] = frontier
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
         print(json.dumps(line), flush=True)
