@@ -548,10 +548,28 @@ __device__ __forceinline__ dd leaf_level(const double2 *Fr, const double2 *Fi, i
 // (leaf_sym_pair_terms, F_j = conj(F_{NJ-1-j})), the midpoint's factor (odd NJ) is real; one biased
 // accumulator pair per pair plus one for the midpoint.  8 FP64 instructions per point for even NJ
 // (midpoint-merged rows), 7.0 for NJ = 3, 7.4 for NJ = 5, instead of 12.
+#ifndef LEAF_SYM_SPLIT
+#define LEAF_SYM_SPLIT 0   // 1: the two nodes of a pair in separate accumulators (shorter chains)
+#endif
+#define LEAF_SYM_NACC(NJ) (LEAF_SYM_SPLIT ? NJ : (NJ + 1) / 2)
+// node 0 (A + B) into accumulator a, node 2 (A - B) into b
+__device__ __forceinline__ void leaf_sym_pair_split(const dd &er, const dd &ei, const double2 f, const double2 g,
+                                                    LeafAcc &a, LeafAcc &b) {
+    const double u1 = fma(er.hi, f.x, a.h);
+    const double h1 = u1 - a.h;
+    a.h = fma(ei.hi, g.x, u1);
+    const double h2 = a.h - u1;
+    const double cA = fma(er.lo, f.x, fma(er.hi, f.y, fma(er.hi, f.x, -h1)));
+    const double cB = fma(ei.lo, g.x, fma(ei.hi, g.y, fma(ei.hi, g.x, -h2)));
+    a.l += cA + cB;
+    b.h += h1 - h2;
+    b.l += cA - cB;
+}
+
 template <int NJ>
 __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
                                               int kp0, int kp1, int klane, bool pred, const dd &pr, const dd &pim,
-                                              double sigma, LeafAcc (&acc)[(NJ + 1) / 2]) {
+                                              double sigma, LeafAcc (&acc)[LEAF_SYM_NACC(NJ)]) {
     constexpr int NP = NJ / 2;
     for (int kp = kp0; kp < kp1;) {
         const int ke = min(kp1, kp + FOLD);
@@ -562,26 +580,30 @@ __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, co
             const double2 *fr = Fr + (long long)kp * NJ;
             const double2 *fi = Fi + (long long)kp * NJ;
 #pragma unroll
-            for (int q = 0; q < NP; ++q)
-                leaf_sym_pair_terms(er, ei, __ldg(fr + NJ - 1 - q), __ldg(fi + NJ - 1 - q), acc[q].h, acc[q].l);
+            for (int q = 0; q < NP; ++q) {
+                if constexpr (LEAF_SYM_SPLIT)
+                    leaf_sym_pair_split(er, ei, __ldg(fr + NJ - 1 - q), __ldg(fi + NJ - 1 - q), acc[q], acc[NJ - 1 - q]);
+                else
+                    leaf_sym_pair_terms(er, ei, __ldg(fr + NJ - 1 - q), __ldg(fi + NJ - 1 - q), acc[q].h, acc[q].l);
+            }
             if constexpr (NJ % 2 == 1) leaf_real_factor_term<false>(er, __ldg(fr + NP), acc[NP].h, acc[NP].l);
         }
 #pragma unroll
-        for (int q = 0; q < (NJ + 1) / 2; ++q) leaf_fold(acc[q], sigma);
+        for (int q = 0; q < LEAF_SYM_NACC(NJ); ++q) leaf_fold(acc[q], sigma);
     }
 }
 
 template <int NJ>
 __device__ __forceinline__ dd leaf_level_sym(const double2 *Fr, const double2 *Fi, int kb, int kmain, int ks1,
                                              int k, const dd &pr, const dd &pim, double sigma) {
-    LeafAcc acc[(NJ + 1) / 2];
+    LeafAcc acc[LEAF_SYM_NACC(NJ)];
 #pragma unroll
-    for (int q = 0; q < (NJ + 1) / 2; ++q) acc[q] = LeafAcc{sigma, 0.0};   // biased accumulator
+    for (int q = 0; q < LEAF_SYM_NACC(NJ); ++q) acc[q] = LeafAcc{sigma, 0.0};   // biased accumulator
     leaf_rows_sym<NJ>(Fr, Fi, kb, min(kmain, ks1), k, true, pr, pim, sigma, acc);
     leaf_rows_sym<NJ>(Fr, Fi, max(kb, kmain), ks1, k, false, pr, pim, sigma, acc);
     dd s = {0.0, 0.0};
 #pragma unroll
-    for (int q = 0; q < (NJ + 1) / 2; ++q) s = dd_add(s, dd_norm(acc[q].h - sigma, acc[q].l));
+    for (int q = 0; q < LEAF_SYM_NACC(NJ); ++q) s = dd_add(s, dd_norm(acc[q].h - sigma, acc[q].l));
     return s;
 }
 
