@@ -23,7 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["sg_kernels.cu"]
 SOURCES_CPP = ["plan.cpp"]
-DEPS = ["dd.cuh", "plan.h"]
+DEPS = ["dd.cuh", "plan.h", "kernels_common.cuh", "k_factor.cuh", "k_tree.cuh", "k_sform.cuh",
+        "k_reduce.cuh", "k_collapse.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -1,0 +1,168 @@
+// k_factor.cuh — K0: per-(level, coordinate, node) factor tables, the base value and the suffix bounds of |F|
+// (included once, by sg_kernels.cu, after the shared definitions it uses)
+#pragma once
+
+// ---------------------------------------------------------------------------------------------
+// K0: factor table and base
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool dd_finite(dd a) { return isfinite(a.hi) && isfinite(a.lo); }
+
+__global__ void k_factor(const DevPlan P) {
+    const int n_ent = P.tab_off[P.L + 2];
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_ent) return;
+    int l = 2;
+    while (l < P.L + 1 && idx >= P.tab_off[l + 1]) ++l;
+    const int r = idx - P.tab_off[l], n = P.nl[l];
+    const int k = r / n, j = r - k * n;
+    const double x = P.X[P.entry_off[l] + j];
+    const dd wt = {P.Whi[P.entry_off[l] + j], P.Wlo[P.entry_off[l] + j]};
+    const double ck = P.c[k];
+    const dd xm = dd_from_sum(x, -0.5);   // x - 1/2 exactly
+    dd Er = {1.0, 0.0}, Ei = {0.0, 0.0};
+    switch (P.kind) {
+    case SG_F_EXP_LINEAR:
+        Er = dd_exp(dd_mul_d(xm, ck));
+        break;
+    case SG_F_OSCILLATORY: {
+        // sincos of |a| with the sign applied afterwards: nodes placed symmetrically about 1/2 get
+        // exactly conjugate factors (used by k_leaf2's symmetric-pair path)
+        dd a = dd_mul_d(xm, ck), s, co;
+        const bool neg = a.hi < 0.0;
+        dd_sincos(neg ? dd_neg(a) : a, s, co);
+        Er = co;
+        Ei = neg ? dd_neg(s) : s;
+        break;
+    }
+    case SG_F_GAUSSIAN: {
+        // -c^2 ((x-w)^2 - (1/2-w)^2) = -c^2 (x - 1/2)(x + 1/2 - 2w)
+        const double wk = P.w[k];
+        dd xp = dd_add(dd_from_sum(x, 0.5), dd{-2.0 * wk, 0.0});
+        dd arg = dd_mul(dd_mul(xm, xp), dd_from_prod(ck, ck));
+        Er = dd_exp(dd_neg(arg));
+        break;
+    }
+    case SG_F_PRODUCT_PEAK: {
+        // phi(x)/phi(1/2) = (c^-2 + (1/2-w)^2) / (c^-2 + (x-w)^2)
+        const double wk = P.w[k];
+        dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+        dd a = dd_from_sum(x, -wk), bm = dd_from_sum(0.5, -wk);
+        Er = dd_div(dd_add(ci2, dd_mul(bm, bm)), dd_add(ci2, dd_mul(a, a)));
+        break;
+    }
+    }
+    dd Fr = dd_mul(wt, Er);
+    P.Fre[idx] = make_double2(Fr.hi, Fr.lo);
+    bool ok = dd_finite(Fr);
+    if (P.kind == SG_F_OSCILLATORY) {
+        dd Fi = dd_mul(wt, Ei);
+        P.Fim[idx] = make_double2(Fi.hi, Fi.lo);
+        ok = ok && dd_finite(Fi);
+    }
+    if (!ok) atomicOr(P.status, 1);
+}
+
+__global__ void __launch_bounds__(256) k_base(const DevPlan P) {
+    // fixed-order strided partials, then a fixed CTA tree (sum; product for the peak kind)
+    const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
+    dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
+    for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
+        const double ck = P.c[k];
+        switch (P.kind) {
+        case SG_F_EXP_LINEAR:
+        case SG_F_OSCILLATORY:
+            acc = dd_add(acc, dd{0.5 * ck, 0.0});
+            break;
+        case SG_F_GAUSSIAN: {
+            dd bm = dd_from_sum(0.5, -P.w[k]);
+            acc = dd_add(acc, dd_mul(dd_mul(bm, bm), dd_from_prod(ck, ck)));
+            break;
+        }
+        case SG_F_PRODUCT_PEAK: {
+            dd bm = dd_from_sum(0.5, -P.w[k]);
+            dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+            acc = dd_mul(acc, dd_div(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
+            break;
+        }
+        }
+    }
+    __shared__ double2 sm[256];
+    sm[threadIdx.x] = make_double2(acc.hi, acc.lo);
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            dd a = {sm[threadIdx.x].x, sm[threadIdx.x].y}, b = {sm[threadIdx.x + s].x, sm[threadIdx.x + s].y};
+            dd r = prod ? dd_mul(a, b) : dd_add(a, b);
+            sm[threadIdx.x] = make_double2(r.hi, r.lo);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        dd s = {sm[0].x, sm[0].y};
+        dd Br = s, Bi = {0.0, 0.0};
+        switch (P.kind) {
+        case SG_F_EXP_LINEAR: Br = dd_exp(s); break;
+        case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(s)); break;
+        case SG_F_PRODUCT_PEAK: Br = s; break;
+        case SG_F_OSCILLATORY: {
+            const double u = P.u[0];
+            dd th = dd_add(dd_from_prod(DD_2PI_0, u), dd_from_prod(DD_2PI_1, u));
+            th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
+            th = dd_add(th, s);
+            dd sn, cs;
+            dd_sincos(th, sn, cs);
+            Br = cs;
+            Bi = sn;
+            break;
+        }
+        }
+        P.base[0] = Br.hi;
+        P.base[1] = Br.lo;
+        P.base[2] = Bi.hi;
+        P.base[3] = Bi.lo;
+        if (!dd_finite(Br) || !dd_finite(Bi)) atomicOr(P.status, 1);
+    }
+}
+
+// SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
+// One CTA per level: chunked row sums, a serial suffix scan over the 256 chunk sums, then each
+// thread writes the suffix values of its chunk (all loads in parallel; deterministic order).
+__global__ void __launch_bounds__(256) k_suffix_abs(const DevPlan P) {
+    const int l = 2 + blockIdx.x;
+    if (l > P.L + 1) return;
+    const int d = P.d, n = P.nl[l];
+    const double2 *Fr = P.Fre + P.tab_off[l];
+    const double2 *Fi = P.kind == SG_F_OSCILLATORY ? P.Fim + P.tab_off[l] : nullptr;
+    const int chunk = (d + blockDim.x - 1) / blockDim.x;
+    const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
+    auto row = [&](int k) {
+        double r = 0.0;
+        for (int j = 0; j < n; ++j) {
+            r += fabs(Fr[(long long)k * n + j].x);
+            if (Fi) r += fabs(Fi[(long long)k * n + j].x);
+        }
+        return r;
+    };
+    double cs = 0.0;
+    for (int k = k0; k < k1; ++k) cs += row(k);
+    __shared__ double suf[257];
+    suf[threadIdx.x] = cs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        suf[blockDim.x] = 0.0;
+        for (int i = blockDim.x - 1; i >= 0; --i) {
+            const double v = suf[i];
+            suf[i] = run;   // sum of the chunks after chunk i
+            run += v;
+        }
+    }
+    __syncthreads();
+    double s = suf[threadIdx.x];
+    if (threadIdx.x == 0) P.SA[(long long)l * (d + 1) + d] = 0.0;
+    for (int k = k1 - 1; k >= k0; --k) {
+        s += row(k);
+        P.SA[(long long)l * (d + 1) + k] = s;
+    }
+}
+

@@ -1,0 +1,108 @@
+// kernels_common.cuh — device-side plan/argument structs, warp/CTA dd reductions (K4) and the dd helpers shared by every kernel
+// (included once, by sg_kernels.cu, after the shared definitions it uses)
+#pragma once
+
+#define WPB 8                 // warps per CTA in the pass kernels
+#define PASS_THREADS (WPB * 32)
+#define META_KMASK ((1u << SG_META_KBITS) - 1u)
+
+struct DevPlan {
+    int d, L, kind, nfront;
+    int nl[SG_MAX_L + 3];
+    int entry_off[SG_MAX_L + 3];
+    int tab_off[SG_MAX_L + 3];
+    double coef[SG_MAX_L + 2];
+    long long M0;
+    const double *X, *Whi, *Wlo;
+    const double *c, *w, *u;
+    double2 *Fre, *Fim;
+    double *base;   // re.hi, re.lo, im.hi, im.lo
+    double *SA;     // [(L+2) x (d+1)] suffix sums of |F| per level (k_leaf's accumulation bound)
+    int *status;
+    int sform;      // 0 factor form; 1 SG_ARITH_SFORM_FP64, 2 SG_ARITH_SFORM_DD: base[0..1] = argument S
+    int symmask;    // bit l: level-l row symmetric about 1/2 (x_j = 1 - x_{n-1-j}, equal dd weights,
+                    // the midpoint at the centre if n is odd): oscillatory factors of a pair are
+                    // exact conjugates, the midpoint's is real (k_leaf's symmetric-row path)
+    const double2 *coefm;   // node coefficient (dd) per (depth t, excess b): [t * (L + 1) + b]
+};
+
+struct PassArgs {
+    long long nsrc, ntasks;
+    int nsplit;
+    int t;                         // depth of the source frontier (children have depth t + 1)
+    const double2 *src_re, *src_im;
+    const uint32_t *src_meta;
+    double2 *dst_re, *dst_im;
+    uint32_t *dst_meta;
+    const long long *offT, *NT, *CT, *TB;
+    double2 *partials;
+    unsigned long long *counter;   // dynamic task counter (persistent kernels), zeroed per launch
+};
+
+struct RootArgs {
+    long long lo, hi;
+    const long long *off1, *JS;
+    double2 *dst_re, *dst_im;
+    uint32_t *dst_meta;
+    double2 *partials;
+};
+
+// ---------------------------------------------------------------------------------------------
+// reductions (K4)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ dd warp_reduce_dd(dd v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dd w;
+        w.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+        w.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+        v = dd_add(v, w);
+    }
+    return v;
+}
+
+// same butterfly with the sloppy dd add (leaf task partials; fixed order, deterministic)
+__device__ __forceinline__ dd warp_reduce_dd_fast(dd v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dd w;
+        w.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+        w.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+        v = dd_add_fast(v, w);
+    }
+    return v;
+}
+
+// CTA sum in fixed order; result valid in thread 0.
+template <int NWARPS>
+__device__ __forceinline__ dd block_reduce_dd(dd v) {
+    __shared__ double2 sm[NWARPS];
+    v = warp_reduce_dd(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sm[wid] = make_double2(v.hi, v.lo);
+    __syncthreads();
+    dd s = {0.0, 0.0};
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NWARPS; ++i) s = dd_add(s, dd{sm[i].x, sm[i].y});
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// leaf arithmetic helpers
+// ---------------------------------------------------------------------------------------------
+// acc (hi, lo) += p + e  : TwoSum on the high parts, plain sum of the low parts.
+__device__ __forceinline__ void acc_add(double &ah, double &al, double p, double e) {
+    double s = ah + p;
+    double bb = s - ah;
+    double err = (ah - (s - bb)) + (p - bb);
+    al += err + e;
+    ah = s;
+}
+
+// v * C(t, b): the node coefficient of depth t and excess b (an exact integer double unless merged)
+__device__ __forceinline__ dd coef_mul(const DevPlan &P, dd v, int t, int b) {
+    const double2 c = P.coefm[t * (P.L + 1) + b];
+    return c.y == 0.0 ? dd_mul_d(v, c.x) : dd_mul(v, dd{c.x, c.y});
+}
+
