@@ -201,16 +201,16 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
 }
 
 // ---------------------------------------------------------------------------------------------
-// Leaf-only pass (no extendable children): the hot loop of configs 4-5 (>= 97% of the points).
+// Leaf-only pass (no extendable children), generic levels: k_leaf (config 5 pass 2: 7.2e8 points).
 //
-// Same task mapping as k_pass, but the accumulation is "grid-split": with sigma = 1.5 * 2^m and
-// 2^m >= 2 * (bound on sum |P F| over the lane's children, from the suffix table SA), the high part
-// h = fma(P.hi, F.hi, sigma) - sigma of every product is P.hi F.hi rounded once to the grid
-// u = ulp(sigma), so acc_hi += h is EXACT; the remainder and the cross terms are small and go to
-// acc_lo by FMAs (folded back onto the grid every FOLD rows).  7 FP64 instructions per real leaf
-// and 14 per oscillatory leaf, against 12 / 24 with TwoSum + dd products.
+// Same task mapping as k_pass; the accumulation is the biased grid accumulator (leaf_term): every
+// product P.hi F.hi is rounded once onto the grid of the lane's sigma and added exactly; the
+// remainder and the cross terms go to acc_lo by FMAs (folded back onto the grid every FOLD rows).
+// 6 FP64 instructions per real leaf and 12 per oscillatory leaf (symmetric rows: 7-8 via shared
+// conjugate-pair products), against 12 / 24 with TwoSum + dd products.
 // Children (k', j') are walked row by row (k'), NJ nodes per row unrolled with one accumulator pair
-// per node for ILP; rows with k' <= max lane k of the warp are predicated (segment boundaries).
+// per node (or per symmetric pair) for ILP; rows with k' <= max lane k of the warp are predicated
+// (segment boundaries).
 // ---------------------------------------------------------------------------------------------
 
 // Leaf term for a node whose factor is REAL (imaginary part exactly 0): the midpoint node x = 1/2 of
@@ -424,10 +424,10 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
 // ---------------------------------------------------------------------------------------------
 // k_leaf1: the last pass when every source prefix has excess L-1 (t = L-1), so every child has
 // level 2 and coefficient coef[L]: the dominant kernel of configs 4-5 (c4: 99.6%, c5: 97.4% of the
-// points).  Lean register budget (<= 64 -> 32 warps/SM), one accumulator pair per lane with short
-// dependency chains, two rows (k', k'+1) per iteration for ILP.  Oscillatory leaf = 14 FP64
-// instructions: h1, h2 (4), acc.h += h1 + h2 (2), remainder t1 + cross-term FMA chain (5),
-// remainder t2 (1), acc.l (2); real leaf = 7.
+// points) when the last two levels are not fused (SG_B200_NOFUSE=1 or plans that cannot fuse).
+// One biased accumulator pair per lane, LEAF1_ROWS rows per iteration for ILP.  Oscillatory leaf =
+// 12 FP64 instructions (two grid adds + their exact grid parts, remainder + cross-term FMA chain,
+// acc_lo), real leaf = 6.
 // ---------------------------------------------------------------------------------------------
 template <bool CPLX>
 __device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const double2 f, const double2 fi,
