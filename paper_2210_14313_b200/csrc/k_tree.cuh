@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
 #ifndef FOLD
-#define FOLD 32   // rows between folds of acc_lo onto the grid (A/B: 32 vs 16: c5 -0.8%, c4 -1.4%; rel. error 2.7e-20 vs 1e-20)
+#define FOLD 16   // rows between folds of acc_lo onto the grid (A/B: 32 is 0.8% faster on c5 but triples its error, 3e-20 vs 1e-20)
 #endif
 #ifndef LEAF_MINB
 #define LEAF_MINB 3
