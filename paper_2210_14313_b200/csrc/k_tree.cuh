@@ -298,6 +298,9 @@ __device__ __forceinline__ dd leaf_level(const double2 *Fr, const double2 *Fi, i
 // (leaf_sym_pair_terms, F_j = conj(F_{NJ-1-j})), the midpoint's factor (odd NJ) is real; one biased
 // accumulator pair per pair plus one for the midpoint.  8 FP64 instructions per point for even NJ
 // (midpoint-merged rows), 7.0 for NJ = 3, 7.4 for NJ = 5, instead of 12.
+#ifndef LEAF_SYM_FOLD
+#define LEAF_SYM_FOLD 4   // rows between folds in the symmetric-row path (A/B on c5: error 5.1e-21 at 4, 1.4e-20 at 16; time +0.2%)
+#endif
 #ifndef LEAF_SYM_SPLIT
 #define LEAF_SYM_SPLIT 0   // 1: the two nodes of a pair in separate accumulators (shorter chains)
 #endif
@@ -322,7 +325,7 @@ __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, co
                                               double sigma, LeafAcc (&acc)[LEAF_SYM_NACC(NJ)]) {
     constexpr int NP = NJ / 2;
     for (int kp = kp0; kp < kp1;) {
-        const int ke = min(kp1, kp + FOLD);
+        const int ke = min(kp1, kp + LEAF_SYM_FOLD);
         for (; kp < ke; ++kp) {
             const bool kv = !pred || kp > klane;
             const dd er = kv ? pr : dd{0.0, 0.0};

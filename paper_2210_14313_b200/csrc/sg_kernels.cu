@@ -244,7 +244,9 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             const int m = e0 + n - 1 - j;
             sym = (1.0 - hp.X[m] == hp.X[e0 + j]) && hp.Whi[m] == hp.Whi[e0 + j] && hp.Wlo[m] == hp.Wlo[e0 + j];
         }
+#ifndef LEAF_NO_SYMROWS
         if (sym) dp.symmask |= 1 << l;
+#endif
     }
     dp.X = (const double *)(base + oX);
     dp.Whi = (const double *)(base + oWh);

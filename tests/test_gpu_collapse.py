@@ -74,11 +74,13 @@ def test_collapse_delta_form(api, seed, d, L, rule, kind):
 
 @pytest.mark.parametrize("i", [2, 3, 4, 5])
 def test_collapse_equals_tree(api, i):
-    """Two different evaluation orders of the same Eq 2.6 sum agree to dd rounding."""
+    """Two different evaluation orders of the same Eq 2.6 sum agree to dd rounding: each is within
+    ~1e-20 of the 50-digit value on config 5 (the tree's FP64 low accumulators, amplified by the
+    combination sum's cancellation kappa <= 9.3e9; measured 5e-21), so 1e-19."""
     p = S.baseline_config(i)
     hi, lo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u)
     tree = mp.mpf(hi) + mp.mpf(lo)
-    assert rel(collapse_value(api, p), tree) <= 1e-20
+    assert rel(collapse_value(api, p), tree) <= 1e-19
 
 
 @pytest.mark.parametrize("d,L,rule,kind", [
