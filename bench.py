@@ -552,7 +552,8 @@ def bench_reference(p, args, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f128",
         "data": "synthetic",
-        "config": config_block(p, {"sample_points_per_step": pts, "sample_range": [lo, hi]}),
+        "config": config_block(p, {"sample_points_per_step": pts, "sample_range": [lo, hi],
+                                   "arith": "__float128, plain Eq 2.6/2.7 point enumeration (oracle/)"}),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
                          "sample": f"{p.name} depth-1 subtrees [{lo},{hi}) = {pts} points per step"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
