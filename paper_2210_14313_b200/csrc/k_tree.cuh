@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // Lane = one parent prefix, held in registers; the loop over its children (k', l', j') reads the
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
+#ifndef LEAF_SYM_FOLD
+#define LEAF_SYM_FOLD 4   // rows between folds in the symmetric-row path (A/B on c5: error 5.1e-21 at 4, 1.4e-20 at 16; time +0.2%)
+#endif
 #ifndef FOLD
 #define FOLD 16   // rows between folds of acc_lo onto the grid (A/B: 32 is 0.8% faster on c5 but triples its error, 3e-20 vs 1e-20)
 #endif
@@ -97,6 +100,153 @@ __device__ __forceinline__ void leaf_fold(LeafAcc &a, double sigma) {
     const double t = (a.l + sigma) - sigma;
     a.h += t;
     a.l -= t;
+}
+
+// Leaf term for a node whose factor is REAL (imaginary part exactly 0): the midpoint node x = 1/2 of
+// a level (E_k(1/2) = 1 for every kind, so F = w exactly real).  Re(P F) = P.re F: 7 FP64
+// instructions instead of 14 for the oscillatory kind; bitwise the same value the general formula
+// gives with F.im = 0 (every dropped term is an exact zero).
+// CZ: the factor's low part is exactly 0 (combination form: F = w * 1), its cross term drops.
+template <bool CZ = false>
+__device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double &ah, double &al) {
+    const double a1 = fma(er.hi, f.x, ah);   // biased accumulator (leaf_term)
+    const double h = a1 - ah;
+    ah = a1;
+    double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
+    if (!CZ) c = fma(er.hi, f.y, c);
+    al += c;
+}
+
+// Symmetric pair (x_0 = 1 - x_2, w_0 = w_2; oscillatory): F_0 = conj(F_2) exactly, so the two
+// points' terms Re(P F_0) = A + B and Re(P F_2) = A - B share the products A = P.re F_2.re and
+// B = P.im F_2.im (their grid parts, remainders and cross terms); each point's term is still formed
+// and accumulated on its own: node 0 adds the grid parts of A and B in turn (biased accumulator,
+// leaf_term), node 2 forms h_A - h_B and adds it.  16 FP64 instructions for the two points.
+__device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, const double2 f, const double2 g,
+                                                    double &ah, double &al) {
+    const double a1 = fma(er.hi, f.x, ah);
+    const double h1 = a1 - ah;
+    const double a2 = fma(ei.hi, g.x, a1);   // node 0: A + B
+    const double h2 = a2 - a1;
+    const double cA = fma(er.lo, f.x, fma(er.hi, f.y, fma(er.hi, f.x, -h1)));
+    const double cB = fma(ei.lo, g.x, fma(ei.hi, g.y, fma(ei.hi, g.x, -h2)));
+    al += cA + cB;
+    ah = a2 + (h1 - h2);                     // node 2: A - B
+    al += cA - cB;
+}
+
+
+// One level of the frontier writer's children for a lane: rows kp in [kb, ks1) (kp > k), the NJ
+// nodes of each row unrolled (NJ = 0: runtime n).  Every child is a Smolyak point (biased grid
+// accumulator term); children with excess bp <= L-1 and kp <= d-2 are also stored to frontier t+1
+// (dd product P F; coalesced: consecutive lanes = consecutive records of a segment).
+struct PassLevel {
+    int kb, ks1, k;
+    bool lv, wr;
+    int b, bp;
+    long long wbase, Nseg;
+    const double2 *Fr, *Fi;
+};
+
+template <bool CPLX, bool WRITE, int NJ>
+__device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
+                                           const dd &pim, double sigma, LeafAcc &acc, int nrt = 0) {
+    const int n = NJ > 0 ? NJ : nrt;
+    const int d = P.d, L = P.L;
+    int nfold = 0;
+    for (int kp = V.kb; kp < V.ks1; ++kp) {
+        const bool kv = V.lv && (kp > V.k);
+        const dd er = kv ? pr : dd{0.0, 0.0};
+        const dd ei = kv ? pim : dd{0.0, 0.0};
+        const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
+        long long tb = 0;
+        if (WRITE && wk) tb = A.TB[((long long)V.b * L + V.bp) * d + kp] + V.wbase;
+        const double2 *fr_row = V.Fr + (long long)kp * n;
+        const double2 *fi_row = CPLX ? V.Fi + (long long)kp * n : nullptr;
+#pragma unroll
+        for (int j = 0; j < (NJ > 0 ? NJ : n); ++j) {
+            const double2 f = __ldg(fr_row + j);
+            const double2 fi = CPLX ? __ldg(fi_row + j) : make_double2(0.0, 0.0);
+            leaf_term<CPLX>(er, ei, f, fi, acc);
+            if (WRITE && wk) {
+                // the stored child product P F in dd (complex for the oscillatory kind)
+                const long long o = tb + (long long)j * V.Nseg;
+                double p1, e1;
+                dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
+                if (!CPLX) {
+                    const dd ch = dd_norm(p1, e1);
+                    A.dst_re[o] = make_double2(ch.hi, ch.lo);
+                } else {
+                    double p2, e2, p3, e3, p4, e4;
+                    dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
+                    dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
+                    dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
+                    const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
+                    A.dst_re[o] = make_double2(cre.hi, cre.lo);
+                    A.dst_im[o] = make_double2(cim.hi, cim.lo);
+                }
+                A.dst_meta[o] = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
+            }
+        }
+        if (++nfold == FOLD) {
+            nfold = 0;
+            leaf_fold(acc, sigma);
+        }
+    }
+}
+
+// Symmetric oscillatory row (P.symmask): conjugate node pairs share the products of their terms
+// (leaf_sym_pair_terms) and of their stored child products (cdd_mul_conj_pair); the midpoint
+// (odd NJ) has a real factor.
+template <bool WRITE, int NJ>
+__device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
+                                               const dd &pim, double sigma, LeafAcc &acc) {
+    constexpr int NP = NJ / 2;
+    const int d = P.d, L = P.L;
+    int nfold = 0;
+    for (int kp = V.kb; kp < V.ks1; ++kp) {
+        const bool kv = V.lv && (kp > V.k);
+        const dd er = kv ? pr : dd{0.0, 0.0};
+        const dd ei = kv ? pim : dd{0.0, 0.0};
+        const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
+        long long tb = 0;
+        if (WRITE && wk) tb = A.TB[((long long)V.b * L + V.bp) * d + kp] + V.wbase;
+        const double2 *fr_row = V.Fr + (long long)kp * NJ;
+        const double2 *fi_row = V.Fi + (long long)kp * NJ;
+        const uint32_t meta = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const int ju = NJ - 1 - q;
+            const double2 f = __ldg(fr_row + ju), g = __ldg(fi_row + ju);
+            leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
+            if (WRITE && wk) {
+                cdd cu, cl;
+                cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
+                const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
+                A.dst_re[ou] = make_double2(cu.re.hi, cu.re.lo);
+                A.dst_im[ou] = make_double2(cu.im.hi, cu.im.lo);
+                A.dst_meta[ou] = meta;
+                A.dst_re[ol] = make_double2(cl.re.hi, cl.re.lo);
+                A.dst_im[ol] = make_double2(cl.im.hi, cl.im.lo);
+                A.dst_meta[ol] = meta;
+            }
+        }
+        if constexpr (NJ % 2 == 1) {
+            const double2 w = __ldg(fr_row + NP);
+            leaf_real_factor_term<false>(er, w, acc.h, acc.l);
+            if (WRITE && wk) {
+                const long long oc = tb + (long long)NP * V.Nseg;
+                const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
+                A.dst_re[oc] = make_double2(cr.hi, cr.lo);
+                A.dst_im[oc] = make_double2(ci.hi, ci.lo);
+                A.dst_meta[oc] = meta;
+            }
+        }
+        if (++nfold == LEAF_SYM_FOLD) {
+            nfold = 0;
+            leaf_fold(acc, sigma);
+        }
+    }
 }
 
 #ifndef PASS_MINB
@@ -154,44 +304,16 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             frexp(2.0 * bound, &ex);
             const double sigma = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
             LeafAcc acc = {sigma, 0.0};
-            int nfold = 0;
-            for (int kp = kb; kp < ks1; ++kp) {
-                const bool kv = lv && (kp > k);
-                const dd er = kv ? pr : dd{0.0, 0.0};
-                const dd ei = kv ? pim : dd{0.0, 0.0};
-                const bool wk = wr && kv && (kp <= d - 2);
-                long long tb = 0;
-                if (WRITE && wk) tb = A.TB[((long long)b * L + bp) * d + kp] + wbase;
-                const double2 *fr_row = Fr + kp * n;
-                const double2 *fi_row = CPLX ? Fi + kp * n : nullptr;
-                for (int j = 0; j < n; ++j) {
-                    const double2 f = __ldg(fr_row + j);
-                    const double2 fi = CPLX ? __ldg(fi_row + j) : make_double2(0.0, 0.0);
-                    leaf_term<CPLX>(er, ei, f, fi, acc);
-                    if (WRITE && wk) {
-                        // the stored child product P F in dd (complex for the oscillatory kind)
-                        const long long o = tb + (long long)j * Nseg;
-                        double p1, e1;
-                        dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
-                        if (!CPLX) {
-                            const dd ch = dd_norm(p1, e1);
-                            A.dst_re[o] = make_double2(ch.hi, ch.lo);
-                        } else {
-                            double p2, e2, p3, e3, p4, e4;
-                            dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
-                            dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
-                            dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
-                            const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
-                            A.dst_re[o] = make_double2(cre.hi, cre.lo);
-                            A.dst_im[o] = make_double2(cim.hi, cim.lo);
-                        }
-                        A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
-                    }
-                }
-                if (++nfold == FOLD) {
-                    nfold = 0;
-                    leaf_fold(acc, sigma);
-                }
+            PassLevel L0 = {kb, ks1, k, lv, wr, b, bp, wbase, Nseg, Fr, Fi};
+            const bool sym = CPLX && ((P.symmask >> lp) & 1);
+            if (sym && n == 3) pass_level_sym<WRITE, 3>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 5) pass_level_sym<WRITE, 5>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 2) pass_level_sym<WRITE, 2>(P, A, L0, pr, pim, sigma, acc);
+            else switch (n) {
+            case 2: pass_level<CPLX, WRITE, 2>(P, A, L0, pr, pim, sigma, acc); break;
+            case 3: pass_level<CPLX, WRITE, 3>(P, A, L0, pr, pim, sigma, acc); break;
+            case 5: pass_level<CPLX, WRITE, 5>(P, A, L0, pr, pim, sigma, acc); break;
+            default: pass_level<CPLX, WRITE, 0>(P, A, L0, pr, pim, sigma, acc, n); break;
             }
             if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(acc.h - sigma, acc.l), A.t + 1, bp));
         }
@@ -212,39 +334,6 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
 // per node (or per symmetric pair) for ILP; rows with k' <= max lane k of the warp are predicated
 // (segment boundaries).
 // ---------------------------------------------------------------------------------------------
-
-// Leaf term for a node whose factor is REAL (imaginary part exactly 0): the midpoint node x = 1/2 of
-// a level (E_k(1/2) = 1 for every kind, so F = w exactly real).  Re(P F) = P.re F: 7 FP64
-// instructions instead of 14 for the oscillatory kind; bitwise the same value the general formula
-// gives with F.im = 0 (every dropped term is an exact zero).
-// CZ: the factor's low part is exactly 0 (combination form: F = w * 1), its cross term drops.
-template <bool CZ = false>
-__device__ __forceinline__ void leaf_real_factor_term(const dd &er, const double2 f, double &ah, double &al) {
-    const double a1 = fma(er.hi, f.x, ah);   // biased accumulator (leaf_term)
-    const double h = a1 - ah;
-    ah = a1;
-    double c = fma(er.lo, f.x, fma(er.hi, f.x, -h));
-    if (!CZ) c = fma(er.hi, f.y, c);
-    al += c;
-}
-
-// Symmetric pair (x_0 = 1 - x_2, w_0 = w_2; oscillatory): F_0 = conj(F_2) exactly, so the two
-// points' terms Re(P F_0) = A + B and Re(P F_2) = A - B share the products A = P.re F_2.re and
-// B = P.im F_2.im (their grid parts, remainders and cross terms); each point's term is still formed
-// and accumulated on its own: node 0 adds the grid parts of A and B in turn (biased accumulator,
-// leaf_term), node 2 forms h_A - h_B and adds it.  16 FP64 instructions for the two points.
-__device__ __forceinline__ void leaf_sym_pair_terms(const dd &er, const dd &ei, const double2 f, const double2 g,
-                                                    double &ah, double &al) {
-    const double a1 = fma(er.hi, f.x, ah);
-    const double h1 = a1 - ah;
-    const double a2 = fma(ei.hi, g.x, a1);   // node 0: A + B
-    const double h2 = a2 - a1;
-    const double cA = fma(er.lo, f.x, fma(er.hi, f.y, fma(er.hi, f.x, -h1)));
-    const double cB = fma(ei.lo, g.x, fma(ei.hi, g.y, fma(ei.hi, g.x, -h2)));
-    al += cA + cB;
-    ah = a2 + (h1 - h2);                     // node 2: A - B
-    al += cA - cB;
-}
 
 template <bool CPLX, int NJ>
 __device__ __forceinline__ void leaf_rows(const double2 *__restrict__ Fr, const double2 *__restrict__ Fi,
@@ -298,9 +387,6 @@ __device__ __forceinline__ dd leaf_level(const double2 *Fr, const double2 *Fi, i
 // (leaf_sym_pair_terms, F_j = conj(F_{NJ-1-j})), the midpoint's factor (odd NJ) is real; one biased
 // accumulator pair per pair plus one for the midpoint.  8 FP64 instructions per point for even NJ
 // (midpoint-merged rows), 7.0 for NJ = 3, 7.4 for NJ = 5, instead of 12.
-#ifndef LEAF_SYM_FOLD
-#define LEAF_SYM_FOLD 4   // rows between folds in the symmetric-row path (A/B on c5: error 5.1e-21 at 4, 1.4e-20 at 16; time +0.2%)
-#endif
 #ifndef LEAF_SYM_SPLIT
 #define LEAF_SYM_SPLIT 0   // 1: the two nodes of a pair in separate accumulators (shorter chains)
 #endif
