@@ -234,3 +234,32 @@ def test_cuda_graph_replay_bitwise(api, i):
         r = plan.result().cpu().numpy()
         assert (float(r[0]), float(r[1])) == eager
     plan.close()
+
+
+@pytest.mark.parametrize("kind", [S.KIND_OSC, S.KIND_GAUSS])
+def test_update_integrand_host_pinned_device(api, kind):
+    """sg_update_integrand (the e2e leg's H2D path): new parameters from numpy, pinned host and
+    device tensors give bitwise the value of a fresh plan of the new problem, and match the oracle."""
+    import torch
+    a = S.random_problem(130, 25, 3, S.RULE_CC, kind)
+    b = S.random_problem(131, 25, 3, S.RULE_CC, kind)
+    fresh = api.Plan(b.d, b.q, b.rule, b.kind, b.c, b.w, b.u)
+    want = fresh.integrate_host()
+    fresh.close()
+    plan = api.Plan(a.d, a.q, a.rule, a.kind, a.c, a.w, a.u)
+    w_np = b.w if b.w is not None else None
+    for how in ("numpy", "pinned", "device"):
+        if how == "numpy":
+            c, w = b.c, w_np
+        elif how == "pinned":
+            c = torch.from_numpy(b.c.copy()).pin_memory()
+            w = None if w_np is None else torch.from_numpy(w_np.copy()).pin_memory()
+        else:
+            c = torch.from_numpy(b.c.copy()).cuda()
+            w = None if w_np is None else torch.from_numpy(w_np.copy()).cuda()
+        plan.sg_update_integrand(c, w, b.u)
+        assert plan.integrate_host() == want, how
+        plan.sg_update_integrand(a.c, a.w, a.u)   # back to a, then to b again
+    ref = oracle.integrate_problem(b, eval_mode=1)
+    assert rel(mp.mpf(want[0]) + mp.mpf(want[1]), mp.mpf(ref.text)) <= HEALTH
+    plan.close()
