@@ -263,3 +263,20 @@ def test_update_integrand_host_pinned_device(api, kind):
     ref = oracle.integrate_problem(b, eval_mode=1)
     assert rel(mp.mpf(want[0]) + mp.mpf(want[1]), mp.mpf(ref.text)) <= HEALTH
     plan.close()
+
+
+@pytest.mark.parametrize("i", [4, 5])
+def test_full_size_properties(api, i):
+    """Properties that hold at any size, checked at the full BASELINE sizes in the bench launch
+    configuration: the integral is invariant under a permutation of the coordinates (a different
+    prefix tree, shard order and task schedule) and the coordinate-wise difference form (reading R6)
+    gives the same value as Eq 2.6 — both against the stored full-size oracle value."""
+    p = S.baseline_config(i)
+    golden = mp.mpf(json.load(open(GOLDEN))["values"][p.name]["text"])
+    perm = np.random.default_rng(7).permutation(p.d)
+    q = S.Problem(p.name + "_perm", p.d, p.L, p.rule, p.kind, p.c[perm].copy(),
+                  None if p.w is None else p.w[perm].copy(), p.u)
+    v, _ = gpu_value(api, q)
+    assert rel(v, golden) <= HEALTH
+    v, _ = gpu_value(api, p, form=1)
+    assert rel(v, golden) <= HEALTH
