@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
             Cseg = A.CT[s];
         }
         const dd S = {P.base[0], P.base[1]};
+        const dd y0 = DDS ? dd_add(S, delta) : dd{0.0, 0.0};   // the lane's argument before its child
         const int kb = max(ks0, kmin + 1);
         for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
             const bool lv = valid && (lp <= L + 1 - b);
@@ -206,10 +207,13 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
                 for (int j = 0; j < n; ++j) {
                     const double2 wv = __ldg(Wt + kp * n + j), av = __ldg(At + kp * n + j);
                     // partial sum carried one coordinate further: dd (DDS) or FP64 (ablation)
-                    const dd dl = DDS ? dd_add(delta, dd{av.x, av.y}) : dd{delta.hi + av.x, 0.0};
+                    // dd: the point's argument (S + delta) + a (one dd add; the child's own delta
+                    // is only formed when it is stored); FP64 ablation: S + (delta + a)
+                    const dd dl = DDS ? ((WRITE && wk) ? dd_add(delta, dd{av.x, av.y}) : dd{0.0, 0.0})
+                                      : dd{delta.hi + av.x, 0.0};
                     const dd Wc = dd_mul(W, dd{wv.x, wv.y});
                     dd gv = {0.0, 0.0};
-                    if (kv) gv = sform_value<DDS>(P, DDS ? dd_add(S, dl) : dd{S.hi + dl.hi, 0.0});
+                    if (kv) gv = sform_value<DDS>(P, DDS ? dd_add(y0, dd{av.x, av.y}) : dd{S.hi + dl.hi, 0.0});
                     double p, e;
                     dd_mul_pe(Wc, gv, p, e);
                     acc_add(ah, al, p, e);
