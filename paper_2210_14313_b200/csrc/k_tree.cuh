@@ -688,7 +688,7 @@ struct Leaf2Args {
     const double2 *src_re, *src_im;   // frontier L-2
     long long base;                   // offset of segment (b = L-2, k = 0) in frontier L-2
     const long long *Cmid;            // C_{L-2}(L-2, k): parents of excess L-2 with k_last < k
-    const long long *T2;              // task descriptors: first parent, (ka << 32) | kb (plan.h)
+    const long long *T2;              // task descriptors: first parent, (ka << 32) | kb, (kp0 << 32) | kp1 (plan.h)
     long long ntasks;
     double2 *partials;             // one per task
     unsigned long long *counter;   // dynamic task counter, zeroed per launch
@@ -823,9 +823,11 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         utask = __shfl_sync(0xffffffffu, utask, 0);
         const long long task = (long long)utask;
         if (task >= A.ntasks) break;
-        // task = (chunk of 32 parents starting at `first`, k_mid range [ka, kb)), plan.h T2
-        const long long first = A.T2[2 * task], kk = A.T2[2 * task + 1];
+        // task = (chunk of 32 parents starting at `first`, k_mid range [ka, kb), rows [kp0, kp1)),
+        // plan.h T2
+        const long long first = A.T2[3 * task], kk = A.T2[3 * task + 1], rr = A.T2[3 * task + 2];
         const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
+        const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
         const long long i = first + lane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
@@ -892,9 +894,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 bh[jm] = sg[jm];
                 bl[jm] = 0.0;
             }
-            int kp = km + 1;
-            while (kp < d) {
-                const int ke = min(d, kp + FOLD);
+            int kp = max(km + 1, kp0);
+            while (kp < kp1) {
+                const int ke = min(kp1, kp + FOLD);
                 constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
                 for (; kp + RW - 1 < ke; kp += RW) {
 #pragma unroll

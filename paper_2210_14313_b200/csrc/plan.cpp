@@ -470,6 +470,30 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     hp.total_points = (uint64_t)total;
     const u128 root_w = counted(0) ? 1 : 0;
     auto item_weight = [&](int k1, int l1) -> u128 { return Sub[(size_t)(l1 - 1) * W + (k1 + 1)]; };
+    // Shard cost model (balances device time rather than points).  With the last two levels fused
+    // (k_leaf2), the subtree of a level-2 depth-1 prefix at coordinate k1 holds
+    //   leaf2 = C(d-1-k1, L-1) n2^(L-1)  points evaluated by k_leaf2 (cost 1 each),
+    //   mids  = C(d-1-k1, L-2) n2^(L-2)  depth-(L-1) prefixes, each a k_leaf2 row run with a fixed
+    //                                     prologue (mid products, bounds, lane fold) ~ LEAF2_MID_COST,
+    // and its other points are evaluated by the generic passes at ~GENERIC_POINT_COST each.
+    // Measured on config 5 (one B200): k_leaf2 4.6e-13 s/point, k_leaf 8.3e-13 s/point.
+    // (depends on the problem's structure only, never on fuse_mode / environment overrides: every
+    // rank of a world, and the host-only queries, must cut the same ranges)
+    const bool fusable_early = L >= 3 && std::min(L - 1, d - 1) == L - 1 && (hp.nl[2] == 2 || hp.nl[2] == 3);
+    auto binom = [](int64_t n, int r) -> double {
+        if (r < 0 || n < r) return 0.0;
+        double v = 1.0;
+        for (int i = 1; i <= r; ++i) v = v * (double)(n - r + i) / (double)i;
+        return v;
+    };
+    auto item_cost = [&](int k1, int l1) -> double {
+        const double pts = (double)item_weight(k1, l1);
+        if (!fusable_early || l1 != 2) return GENERIC_POINT_COST * pts;
+        const double n2 = (double)hp.nl[2];
+        const double leaf2 = binom(d - 1 - k1, L - 1) * std::pow(n2, L - 1);
+        const double mids = binom(d - 1 - k1, L - 2) * std::pow(n2, L - 2);
+        return leaf2 + GENERIC_POINT_COST * std::max(0.0, pts - leaf2) + LEAF2_MID_COST * mids;
+    };
 
     // ---- shard range in depth-1 rank space ----
     int64_t lo = 0, hi = nd1;
@@ -477,19 +501,24 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         lo = std::min<int64_t>(range_lo, nd1);
         hi = std::min<int64_t>(range_hi, nd1);
     } else if (world > 1) {
+        // cut points by the cost model above (double precision is ample: only balance depends on
+        // it; the points each rank evaluates are counted exactly below)
+        double total_cost = (double)root_w;
+        for (int k1 = 0; k1 < d; ++k1)
+            for (int l1 = 2; l1 <= L + 1; ++l1) total_cost += hp.nl[l1] * item_cost(k1, l1);
         auto cut = [&](int r) -> int64_t {
             if (r <= 0) return 0;
             if (r >= world) return nd1;
-            u128 target = total * (u128)r / (u128)world;   // total < 2^63, r < 2^31
-            u128 cum = root_w;
+            const double target = total_cost * (double)r / (double)world;
+            double cum = (double)root_w;
             if (cum >= target) return 0;
             int64_t pos = 0;
             for (int k1 = 0; k1 < d; ++k1)
                 for (int l1 = 2; l1 <= L + 1; ++l1) {
-                    u128 wgt = item_weight(k1, l1), n = (u128)hp.nl[l1];
-                    if (cum + n * wgt >= target) {
-                        u128 need = target - cum;
-                        return pos + (int64_t)((need + wgt - 1) / wgt);
+                    const double wgt = item_cost(k1, l1), n = (double)hp.nl[l1];
+                    if (wgt > 0.0 && cum + n * wgt >= target) {
+                        const int64_t take = (int64_t)std::ceil((target - cum) / wgt);
+                        return pos + std::min<int64_t>(std::max<int64_t>(take, 0), hp.nl[l1]);
                     }
                     cum += n * wgt;
                     pos += hp.nl[l1];
@@ -627,7 +656,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         const int64_t nchunks = (cmid(d - 2) + 31) / 32;
         struct Task {
             int64_t rows, first;
-            int ka, kb;
+            int ka, kb, kp0, kp1;   // k_mid range; row range (split tasks: one k_mid, [kp0, kp1))
         };
         std::vector<Task> tasks;
         int k0 = 0;
@@ -638,22 +667,44 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             for (int k = k0; k <= d - 2; ++k) {
                 acc += d - 1 - k;
                 if (acc >= LEAF2_TASK_ROWS || k == d - 2) {
-                    tasks.push_back(Task{acc, 32 * c, ka, k + 1});
+                    tasks.push_back(Task{acc, 32 * c, ka, k + 1, 0, d});
                     acc = 0;
                     ka = k + 1;
                 }
             }
         }
-        // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, chunk)
+        // Few tasks (a small shard: config 4 on 8 GPUs has ~10^4) leave the persistent grid's tail
+        // to a handful of long single-k_mid tasks: split their rows into pieces of
+        // LEAF2_TASK_ROWS so every resident warp gets >= 32 tasks (partials stay per task).
+        if ((int64_t)tasks.size() < LEAF2_MIN_TASKS) {
+            std::vector<Task> split;
+            for (const Task &tk : tasks) {
+                if (tk.kb - tk.ka != 1 || tk.rows <= LEAF2_TASK_ROWS) {
+                    split.push_back(tk);
+                    continue;
+                }
+                const int pieces = (int)((tk.rows + LEAF2_TASK_ROWS - 1) / LEAF2_TASK_ROWS);
+                const int r0 = tk.ka + 1;
+                for (int q = 0; q < pieces; ++q) {
+                    const int a = r0 + (int)((int64_t)tk.rows * q / pieces);
+                    const int b = r0 + (int)((int64_t)tk.rows * (q + 1) / pieces);
+                    split.push_back(Task{b - a, tk.first, tk.ka, tk.kb, a, b});
+                }
+            }
+            tasks.swap(split);
+        }
+        // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, rows, chunk)
         std::stable_sort(tasks.begin(), tasks.end(), [](const Task &a, const Task &b) {
             if (a.rows != b.rows) return a.rows > b.rows;
             if (a.ka != b.ka) return a.ka < b.ka;
+            if (a.kp0 != b.kp0) return a.kp0 < b.kp0;
             return a.first < b.first;
         });
-        hp.T2.resize(2 * tasks.size());
+        hp.T2.resize(3 * tasks.size());
         for (size_t i = 0; i < tasks.size(); ++i) {
-            hp.T2[2 * i] = tasks[i].first;
-            hp.T2[2 * i + 1] = ((int64_t)tasks[i].ka << 32) | (int64_t)tasks[i].kb;
+            hp.T2[3 * i] = tasks[i].first;
+            hp.T2[3 * i + 1] = ((int64_t)tasks[i].ka << 32) | (int64_t)tasks[i].kb;
+            hp.T2[3 * i + 2] = ((int64_t)tasks[i].kp0 << 32) | (int64_t)tasks[i].kp1;
         }
         const int t = hp.nfront;
         hp.pass_nsplit[t] = 1;

@@ -21,6 +21,15 @@
 #define SG_GP_MAX_K 6      // Gauss-Patterson rules up to 2^6 - 1 = 63 points (levels <= 48)
 #define SG_MAX_D ((1 << 20) - 1)
 #define SG_META_KBITS 20
+#ifndef GENERIC_POINT_COST
+#define GENERIC_POINT_COST 1.8    // shard cost model: a point of a generic pass vs a k_leaf2 point
+#endif
+#ifndef LEAF2_MID_COST
+#define LEAF2_MID_COST 20.0       // shard cost model: fixed cost of one k_leaf2 row run, in points
+#endif
+#ifndef LEAF2_MIN_TASKS
+#define LEAF2_MIN_TASKS (148 * 24 * 32)   // below this many fused tasks, long row runs are split
+#endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 #endif
@@ -66,7 +75,8 @@ struct HostPlan {
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.
-    // Two int64 per task: first parent index (chunk * 32), (ka << 32) | kb; sorted heavy-first.
+    // Three int64 per task: first parent index (chunk * 32), (ka << 32) | kb, (kp0 << 32) | kp1 (the
+    // row range; [0, d) unless a long single-k_mid task was split); sorted heavy-first.
     std::vector<int64_t> T2;
     // Sub[b * (d + 1) + (k + 1)] = Smolyak points (nonzero coefficient) in the subtree of a node
     // with excess b and last active coordinate k (k = -1: the root), the node itself included

@@ -97,8 +97,10 @@ def test_balanced_shards_partition(L, i, world):
     assert acc == total
     nd1 = p.d * sum(pins.node_count(p.rule, l) for l in range(2, p.L + 2))
     assert prev_hi == nd1
-    if total > 10 ** 8:     # big configs balance to a few percent (largest subtree < 1%)
-        assert max(sizes) / (total / world) < 1.05
+    if total > 10 ** 8:
+        # the cut balances the device-time cost model of plan.cpp (fused k_leaf2 points, generic-pass
+        # points, k_leaf2 row-run prologues), so points stay within a few percent, not exactly equal
+        assert max(sizes) / (total / world) < 1.10
 
 
 def test_explicit_range_counts(L):

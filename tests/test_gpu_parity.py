@@ -280,3 +280,21 @@ def test_full_size_properties(api, i):
     assert rel(v, golden) <= HEALTH
     v, _ = gpu_value(api, p, form=1)
     assert rel(v, golden) <= HEALTH
+
+
+def test_shard_ranges_independent_of_leaf_path(api, monkeypatch):
+    """Every rank must cut the same depth-1 ranges whatever leaf path its plan takes (fused or
+    stored frontier, factor or s-form arithmetic): the shard cost model depends on the problem only."""
+    p = S.baseline_config(5)
+    world = 4
+    ref = [api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=r, world=world).range()
+           for r in range(world)]
+    monkeypatch.setenv("SG_B200_NOFUSE", "1")
+    nofuse = [api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=r, world=world).range()
+              for r in range(world)]
+    monkeypatch.delenv("SG_B200_NOFUSE")
+    sform = [api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=r, world=world,
+                      arith=api.ARITH_SFORM_DD).range() for r in range(world)]
+    assert ref == nofuse == sform
+    assert ref[0][0] == 0 and ref[-1][1] == ref[-1][2]
+    assert all(a[1] == b[0] for a, b in zip(ref, ref[1:]))
