@@ -710,6 +710,9 @@ struct Leaf2Args {
 // CJ = index of the midpoint node in the level-2 row (-1: none), fixed per launch by the host;
 // SYM: nodes 0 and 2 form a symmetric pair (CJ == 1, NJ == 3, oscillatory), or nodes 0 and 1 do
 // (CJ == -1, NJ == 2: the midpoint-merged Clenshaw-Curtis level-2 row {0, 1}).
+#ifndef LEAF2_PREFETCH
+#define LEAF2_PREFETCH 1   // prefetch the next task's index and descriptor
+#endif
 #ifndef LEAF2_SPLITR
 #define LEAF2_SPLITR 0  // same split for the real kinds' NJ = 3 row with midpoint
 #endif
@@ -817,6 +820,31 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         Fi = CPLX ? fsm + n : nullptr;
     }
     (void)wib;
+#if LEAF2_PREFETCH
+    // software-pipelined task fetch: the next task's index and descriptor are requested before the
+    // current task's rows run, so their latency (atomic + L2 loads) is hidden behind the FP64 work
+    auto fetch = [&]() -> long long {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(A.counter, 1ull);
+        return (long long)__shfl_sync(0xffffffffu, u, 0);
+    };
+    long long task = fetch();
+    long long first = 0, kk = 0, rr = 0;
+    if (task < A.ntasks) {
+        first = A.T2[3 * task];
+        kk = A.T2[3 * task + 1];
+        rr = A.T2[3 * task + 2];
+    }
+    for (;;) {
+        if (task >= A.ntasks) break;
+        const long long next = fetch();
+        long long nfirst = 0, nkk = 0, nrr = 0;
+        if (next < A.ntasks) {
+            nfirst = A.T2[3 * next];
+            nkk = A.T2[3 * next + 1];
+            nrr = A.T2[3 * next + 2];
+        }
+#else
     for (;;) {
         unsigned long long utask = 0;
         if (lane == 0) utask = atomicAdd(A.counter, 1ull);
@@ -826,6 +854,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         // task = (chunk of 32 parents starting at `first`, k_mid range [ka, kb), rows [kp0, kp1)),
         // plan.h T2
         const long long first = A.T2[3 * task], kk = A.T2[3 * task + 1], rr = A.T2[3 * task + 2];
+#endif
         const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
         const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
         const long long i = first + lane;
@@ -939,6 +968,12 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             v = dd_mul_d(v, P.coef[P.L]);
             A.partials[task] = make_double2(v.hi, v.lo);
         }
+#if LEAF2_PREFETCH
+        task = next;
+        first = nfirst;
+        kk = nkk;
+        rr = nrr;
+#endif
     }
 }
 
