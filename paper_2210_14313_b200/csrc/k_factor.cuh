@@ -127,38 +127,43 @@ __global__ void __launch_bounds__(256) k_base(const DevPlan P) {
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.
 // One CTA per level: chunked row sums, a serial suffix scan over the 256 chunk sums, then each
 // thread writes the suffix values of its chunk (all loads in parallel; deterministic order).
-__global__ void __launch_bounds__(256) k_suffix_abs(const DevPlan P) {
+#define SUFFIX_THREADS 1024
+__global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) {
+    // latency-bound (a few us): one CTA per level; rows split into contiguous chunks per thread,
+    // row loads unrolled so they overlap, chunk suffix sums by a parallel (Hillis-Steele) scan.
+    // SA is only an upper bound for the leaf kernels' grid choice (used with a 1 + 2^-20 margin), so
+    // the summation order is free; it is fixed, so SA is deterministic.
     const int l = 2 + blockIdx.x;
     if (l > P.L + 1) return;
     const int d = P.d, n = P.nl[l];
     const double2 *Fr = P.Fre + P.tab_off[l];
     const double2 *Fi = P.kind == SG_F_OSCILLATORY ? P.Fim + P.tab_off[l] : nullptr;
-    const int chunk = (d + blockDim.x - 1) / blockDim.x;
+    const int chunk = (d + SUFFIX_THREADS - 1) / SUFFIX_THREADS;
     const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
     auto row = [&](int k) {
-        double r = 0.0;
+        double r0 = 0.0, r1 = 0.0;
+        const double2 *fr = Fr + (long long)k * n;
+        const double2 *fi = Fi ? Fi + (long long)k * n : nullptr;
+#pragma unroll 4
         for (int j = 0; j < n; ++j) {
-            r += fabs(Fr[(long long)k * n + j].x);
-            if (Fi) r += fabs(Fi[(long long)k * n + j].x);
+            r0 += fabs(__ldg(fr + j).x);
+            if (fi) r1 += fabs(__ldg(fi + j).x);
         }
-        return r;
+        return r0 + r1;
     };
     double cs = 0.0;
     for (int k = k0; k < k1; ++k) cs += row(k);
-    __shared__ double suf[257];
+    __shared__ double suf[SUFFIX_THREADS + 1];
     suf[threadIdx.x] = cs;
+    if (threadIdx.x == 0) suf[SUFFIX_THREADS] = 0.0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double run = 0.0;
-        suf[blockDim.x] = 0.0;
-        for (int i = blockDim.x - 1; i >= 0; --i) {
-            const double v = suf[i];
-            suf[i] = run;   // sum of the chunks after chunk i
-            run += v;
-        }
+    for (int off = 1; off < SUFFIX_THREADS; off <<= 1) {   // suf[i] = sum of chunks i.. end
+        const double t = (threadIdx.x + off < SUFFIX_THREADS) ? suf[threadIdx.x + off] : 0.0;
+        __syncthreads();
+        suf[threadIdx.x] += t;
+        __syncthreads();
     }
-    __syncthreads();
-    double s = suf[threadIdx.x];
+    double s = suf[threadIdx.x + 1];   // sum of the chunks after this thread's chunk
     if (threadIdx.x == 0) P.SA[(long long)l * (d + 1) + d] = 0.0;
     for (int k = k1 - 1; k >= k0; --k) {
         s += row(k);

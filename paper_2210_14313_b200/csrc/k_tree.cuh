@@ -692,6 +692,7 @@ struct Leaf2Args {
     long long ntasks;
     double2 *partials;             // one per task
     unsigned long long *counter;   // dynamic task counter, zeroed per launch
+    int prefetch;                  // software-pipelined task fetch (>= 16 tasks per resident warp)
 };
 
 #ifndef LEAF2_ROWS
@@ -837,12 +838,16 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
     }
     for (;;) {
         if (task >= A.ntasks) break;
-        const long long next = fetch();
-        long long nfirst = 0, nkk = 0, nrr = 0;
-        if (next < A.ntasks) {
-            nfirst = A.T2[3 * next];
-            nkk = A.T2[3 * next + 1];
-            nrr = A.T2[3 * next + 2];
+        // prefetch only with many tasks per warp: a reserved next task cannot be stolen by an idle
+        // warp, which lengthens the tail when each warp runs only a few tasks (config 3)
+        long long next = 0, nfirst = 0, nkk = 0, nrr = 0;
+        if (A.prefetch) {
+            next = fetch();
+            if (next < A.ntasks) {
+                nfirst = A.T2[3 * next];
+                nkk = A.T2[3 * next + 1];
+                nrr = A.T2[3 * next + 2];
+            }
         }
 #else
     for (;;) {
@@ -969,6 +974,14 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             A.partials[task] = make_double2(v.hi, v.lo);
         }
 #if LEAF2_PREFETCH
+        if (!A.prefetch) {
+            next = fetch();
+            if (next < A.ntasks) {
+                nfirst = A.T2[3 * next];
+                nkk = A.T2[3 * next + 1];
+                nrr = A.T2[3 * next + 2];
+            }
+        }
         task = next;
         first = nfirst;
         kk = nkk;

@@ -673,10 +673,15 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 }
             }
         }
-        // Few tasks (a small shard: config 4 on 8 GPUs has ~10^4) leave the persistent grid's tail
-        // to a handful of long single-k_mid tasks: split their rows into pieces of
-        // LEAF2_TASK_ROWS so every resident warp gets >= 32 tasks (partials stay per task).
-        if ((int64_t)tasks.size() < LEAF2_MIN_TASKS) {
+        // When the longest task is a large share of one resident warp's work (a small shard: config 4
+        // on 8 GPUs), the persistent grid's tail is a handful of long single-k_mid tasks: split
+        // their rows into pieces of LEAF2_TASK_ROWS (partials stay per task, order fixed).
+        int64_t total_rows = 0, max_rows = 0;
+        for (const Task &tk : tasks) {
+            total_rows += tk.rows;
+            max_rows = std::max(max_rows, tk.rows);
+        }
+        if (max_rows > LEAF2_TASK_ROWS && 4 * max_rows * (int64_t)LEAF2_RESIDENT_WARPS > total_rows) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {
                 if (tk.kb - tk.ka != 1 || tk.rows <= LEAF2_TASK_ROWS) {

@@ -27,8 +27,8 @@
 #ifndef LEAF2_MID_COST
 #define LEAF2_MID_COST 20.0       // shard cost model: fixed cost of one k_leaf2 row run, in points
 #endif
-#ifndef LEAF2_MIN_TASKS
-#define LEAF2_MIN_TASKS (148 * 24 * 32)   // below this many fused tasks, long row runs are split
+#ifndef LEAF2_RESIDENT_WARPS
+#define LEAF2_RESIDENT_WARPS (148 * 24)   // persistent k_leaf2 warps (B200: 148 SMs x 16-24 warps)
 #endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)

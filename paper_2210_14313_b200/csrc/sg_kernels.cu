@@ -521,7 +521,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             else k_factor_s<false><<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
         } else {
             k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-            k_suffix_abs<<<hp.L, 256, 0, st>>>(dp);
+            k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
         }
     }
     mark();
@@ -561,6 +561,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
             B.counter = p->d_counter;
+            B.prefetch = B.ntasks >= 16LL * p->leaf1_grid * WPB ? 1 : 0;
             if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
