@@ -50,6 +50,10 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // Lane = one parent prefix, held in registers; the loop over its children (k', l', j') reads the
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
+#ifndef LEAF_ROW_UNROLL
+#define LEAF_ROW_UNROLL 1   // row-loop unrolling in the generic k_leaf (A/B knob)
+#endif
+constexpr int kRowUnroll = LEAF_ROW_UNROLL;
 #ifndef LEAF_SYM_FOLD
 #define LEAF_SYM_FOLD 4   // rows between folds in the symmetric-row path (A/B on c5: error 5.1e-21 at 4, 1.4e-20 at 16; time +0.2%)
 #endif
@@ -342,6 +346,7 @@ __device__ __forceinline__ void leaf_rows(const double2 *__restrict__ Fr, const 
     const int nj = NJ > 0 ? NJ : n;
     for (int kp = kp0; kp < kp1;) {
         const int ke = min(kp1, kp + FOLD);
+        #pragma unroll kRowUnroll
         for (; kp < ke; ++kp) {
             const bool kv = !pred || kp > klane;
             const dd er = kv ? pr : dd{0.0, 0.0};
@@ -412,6 +417,7 @@ __device__ __forceinline__ void leaf_rows_sym(const double2 *__restrict__ Fr, co
     constexpr int NP = NJ / 2;
     for (int kp = kp0; kp < kp1;) {
         const int ke = min(kp1, kp + LEAF_SYM_FOLD);
+        #pragma unroll kRowUnroll
         for (; kp < ke; ++kp) {
             const bool kv = !pred || kp > klane;
             const dd er = kv ? pr : dd{0.0, 0.0};
