@@ -233,6 +233,17 @@ int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *op
 int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
               unsigned long long index, int *t, int *k, int *l, int *j, double *coef);
 
+/* Device K1 + per-point evaluation (validation path): for each of the n flat
+ * indices in index_dev (device, shard order of sg_unrank), enqueue on stream s the unranking and the
+ * point's term evaluated on its own — coefficient * Re(B * prod of its per-coordinate factors), in
+ * double-double, straight from the factor table (independent of the tree's partial products).
+ * Outputs (device): points_dev[n * (1 + 3L)] = t, then (k, l, j) for m < L (-1 past depth t);
+ * terms_dev[2n] = (hi, lo).  Indices outside the shard give t = -1 and a NaN term.  Builds device
+ * copies of the counting tables on first use (plan-owned).  Tree method with factor arithmetic only
+ * (else SG_EUNSUPPORTED). */
+int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long long *index_dev, long long n,
+                   int *points_dev, double *terms_dev);
+
 /* Host-only: the library's 1-D rule of `level` on [0,1] (n_l doubles each, ascending nodes),
  * rounded once from __float128 evaluations of Eq 2.11 / Eq 2.13.  Returns n_l, or a negative
  * status (SG_EINVAL bad rule/level, SG_EUNSUPPORTED above the table limits).  x, w: host arrays of

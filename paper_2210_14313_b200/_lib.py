@@ -23,8 +23,8 @@ SG_ENOWORKSPACE = -7
 SYMBOLS = ["sg_plan", "sg_workspace_size", "sg_set_workspace", "sg_update_integrand",
            "sg_integrate", "sg_finalize", "sg_integrate_host", "sg_status_word", "sg_plan_points",
            "sg_plan_range", "sg_plan_passes", "sg_plan_leaf_work", "sg_debug_tables", "sg_plan_query",
-           "sg_rule_table", "sg_profile_enable", "sg_profile_read", "sg_unrank", "sg_destroy",
-           "sg_strerror"]
+           "sg_rule_table", "sg_profile_enable", "sg_profile_read", "sg_unrank", "sg_eval_points",
+           "sg_destroy", "sg_strerror"]
 
 
 class SGError(RuntimeError):
@@ -85,6 +85,7 @@ def lib():
         ip = ctypes.POINTER(ctypes.c_int)
         L.sg_unrank.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.POINTER(sg_options), ctypes.c_ulonglong, ip, ip, ip, ip, dp]
+        L.sg_eval_points.argtypes = [vp, vp, vp, ctypes.c_longlong, vp, vp]
         L.sg_destroy.argtypes = [vp]
         L.sg_strerror.argtypes = [ctypes.c_int]
         L.sg_strerror.restype = ctypes.c_char_p

@@ -157,6 +157,19 @@ class Plan:
                                     base.ctypes.data_as(dp)), "sg_debug_tables")
         return buf.reshape(nd1, ncplx), base
 
+    def eval_points(self, index, stream=None):
+        """Device K1 + per-point terms (sg_eval_points): index = int64-compatible tensor/array of
+        flat point indices of this plan's shard.  Returns (points [n, 1 + 3L] int32 on device,
+        terms [n, 2] float64 on device: (hi, lo) of coefficient * Re(point value))."""
+        idx = torch.as_tensor(np.asarray(index, dtype=np.uint64).astype(np.int64), device=self.device)
+        n = int(idx.numel())
+        L = self.q - self.d
+        pts = torch.empty((max(n, 1), 1 + 3 * L), dtype=torch.int32, device=self.device)
+        terms = torch.empty((max(n, 1), 2), dtype=torch.float64, device=self.device)
+        check(lib().sg_eval_points(self._h, _stream_handle(stream), _dptr(idx), n, _dptr(pts),
+                                   _dptr(terms)), "sg_eval_points")
+        return pts[:n], terms[:n]
+
     def capture_graph(self):
         """Capture one whole step (sg_integrate + sg_finalize(world=1)) into a CUDA graph.
 

@@ -32,6 +32,7 @@
 #include "k_sform.cuh"
 #include "k_reduce.cuh"
 #include "k_collapse.cuh"
+#include "k_unrank.cuh"
 
 // ---------------------------------------------------------------------------------------------
 // plan object and C ABI
@@ -43,6 +44,8 @@ struct sg_plan_s {
     bool sform = false;        // s-form kernels (SG_ARITH_SFORM_FP64 or SG_ARITH_SFORM_DD)
     bool sform_dd = false;     // SG_ARITH_SFORM_DD: dd partial sums and outer function
     bool two = false;          // frontier layout with a second double2 array (complex or s-form)
+    void *d_unrank = nullptr;  // sg_eval_points: device Sub / SG / D1 tables (built on first use)
+    UnrankTabs utabs = {};
     bool collapse = false;     // SG_METHOD_COLLAPSE: O(d L^2) per-coordinate polynomial product
     int collapse_blocks = 0;   // CTAs of k_collapse_part (one partial polynomial each)
     bool collapse_emit = true; // rank 0 emits the value; other ranks contribute 0
@@ -813,9 +816,69 @@ extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
     return SG_OK;
 }
 
+extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long long *index_dev, long long n,
+                              int *points_dev, double *terms_dev) {
+    if (!p || n < 0 || (n > 0 && (!index_dev || !points_dev || !terms_dev))) return SG_EINVAL;
+    if (p->sform || p->collapse) return SG_EUNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)s;
+    const HostPlan &hp = p->hp;
+    if (!p->d_unrank) {
+        const int d = hp.d, L = hp.L, W = d + 1;
+        std::vector<unsigned long long> SG((size_t)(L + 1) * W, 0);
+        auto sub = [&](int b, int k) -> unsigned long long { return hp.Sub[(size_t)b * W + (k + 1)]; };
+        for (int b = 0; b <= L; ++b)
+            for (int k = d - 1; k >= 0; --k) {
+                unsigned long long g = 0;
+                for (int lp = 2; lp <= L + 1 - b; ++lp) g += (unsigned long long)hp.nl[lp] * sub(b + lp - 1, k);
+                SG[(size_t)b * W + k] = SG[(size_t)b * W + k + 1] + g;
+            }
+        const long long n1 = hp.range_hi - hp.range_lo;
+        std::vector<unsigned long long> D1((size_t)n1 + 1, 0);
+        for (long long i = 0; i < n1; ++i) {
+            const long long r1 = hp.range_lo + i;
+            const int k1 = (int)(r1 / hp.M0);
+            int rem = (int)(r1 - (long long)k1 * hp.M0), l1 = 2;
+            while (rem >= hp.nl[l1]) {
+                rem -= hp.nl[l1];
+                ++l1;
+            }
+            D1[(size_t)i + 1] = D1[(size_t)i] + sub(l1 - 1, k1);
+        }
+        const size_t nsub = hp.Sub.size(), nsg = SG.size(), nd1 = D1.size();
+        if (cudaMalloc(&p->d_unrank, sizeof(unsigned long long) * (nsub + nsg + nd1)) != cudaSuccess) {
+            cudaGetLastError();
+            p->d_unrank = nullptr;
+            return SG_ENOMEM;
+        }
+        unsigned long long *q = (unsigned long long *)p->d_unrank;
+        bool ok = cudaMemcpy(q, hp.Sub.data(), sizeof(unsigned long long) * nsub, cudaMemcpyHostToDevice) == cudaSuccess;
+        ok &= cudaMemcpy(q + nsub, SG.data(), sizeof(unsigned long long) * nsg, cudaMemcpyHostToDevice) == cudaSuccess;
+        ok &= cudaMemcpy(q + nsub + nsg, D1.data(), sizeof(unsigned long long) * nd1, cudaMemcpyHostToDevice) == cudaSuccess;
+        if (!ok) return SG_ECUDA;
+        p->utabs.Sub = q;
+        p->utabs.SG = q + nsub;
+        p->utabs.D1 = q + nsub + nsg;
+        p->utabs.lo = hp.range_lo;
+        p->utabs.n1 = n1;
+        p->utabs.include_root = hp.include_root ? 1 : 0;
+        p->utabs.merge = hp.merge;
+        p->utabs.shard_points = hp.shard_points;
+    }
+    // the factor table and base of the current parameters (K0), then one thread per index
+    if (cudaMemsetAsync(p->dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
+    if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(p->dp);
+    k_base<<<1, 256, 0, st>>>(p->dp);
+    if (n > 0)
+        k_eval_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p->dp, p->utabs, index_dev, n, points_dev,
+                                                                   terms_dev);
+    if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
+    return SG_OK;
+}
+
 extern "C" int sg_destroy(sg_plan_t p) {
     if (!p) return SG_EINVAL;
     for (auto &e : p->ev) cudaEventDestroy(e);
+    if (p->d_unrank) cudaFree(p->d_unrank);
     if (p->dev_block) cudaFree(p->dev_block);
     delete p;
     return SG_OK;
