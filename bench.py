@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
     ap.add_argument("--no-frontier", action="store_true",
                     help="skip the stored-frontier (unfused) leg that measures the HBM-bound frontier kernel")
+    ap.add_argument("--no-plain", action="store_true",
+                    help="skip the plain per-point SG ablation leg (SG_METHOD_PLAIN)")
     ap.add_argument("--no-corner", action="store_true",
                     help="skip the non-separable corner-peak leg (SG_ARITH_SFORM_DD)")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
@@ -417,6 +419,26 @@ def main():
                     "peak_gbs": hbm, "frac": (gbs / hbm) if hbm else None, "traffic": ftraffic}
         fplan.close()
 
+    # plain-SG ablation leg (SG_METHOD_PLAIN): the same integral with every point unranked and
+    # evaluated on its own (no dimension iteration) — what the MDI prefix reuse saves on this GPU
+    plain = None
+    if not args.no_plain:
+        pplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world, device=dev,
+                         method=api.METHOD_PLAIN)
+        pplan.profile_enable(True)
+        step(pplan)
+        torch.cuda.synchronize(dev)
+        p_times, _ = timed(lambda: step(pplan), 1, pplan, 0)
+        p_res = result.cpu().numpy()
+        plain = {"what": "every point unranked on the device and its term formed from its t factors "
+                         "(the paper's plain SG method), dd accumulation; 1 timed step",
+                 "time_to_integral_ms": p_times[0], "value": total_pts / (p_times[0] * 1e-3),
+                 "unit": "points/s", "mdi_speedup": p_times[0] / ms,
+                 "rel_diff_vs_tree": abs((float(p_res[0]) + float(p_res[1]))
+                                         - (float(value_res[0]) + float(value_res[1])))
+                                     / abs(float(value_res[0]))}
+        pplan.close()
+
     # corner-peak leg (SG_ARITH_SFORM_DD): the non-separable Genz corner peak on its own workload
     # (sg_configs.corner_config: d=100, L=4, CC), partial sums carried in dd, dd outer function per
     # point; sharded like the headline tree
@@ -496,6 +518,8 @@ def main():
             line["corner_peak"] = corner
         if frontier is not None:
             line["frontier_kernel"] = frontier
+        if plain is not None:
+            line["plain_sg"] = plain
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
         print(json.dumps(line), flush=True)

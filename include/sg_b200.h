@@ -128,7 +128,13 @@ typedef enum { SG_MERGE_NONE = 0, SG_MERGE_MIDPOINT = 1 } sg_merge;
  *                    every other rank a zero partial (so sg_finalize's sum is the value).  Requires
  *                    SG_MERGE_NONE (else SG_EINVAL) and SG_ARITH_FACTOR_DD (else SG_EUNSUPPORTED);
  *                    sg_plan_passes reports 0 passes. */
-typedef enum { SG_METHOD_TREE = 0, SG_METHOD_COLLAPSE = 1 } sg_method;
+/*  METHOD_PLAIN    = ablation: the paper's plain SG baseline on the GPU — no dimension iteration; every
+ *                    point of the shard is unranked (device K1) and its term formed from its t
+ *                    factors on its own (sg_eval_points' arithmetic), dd accumulation in a fixed
+ *                    order.  Same value; measures what the MDI prefix reuse saves.  Factor
+ *                    arithmetic only (else SG_EUNSUPPORTED); sg_plan_passes reports 0 passes;
+ *                    profiling launches [K0 factor, K0 base, k_plain, k_reduce]. */
+typedef enum { SG_METHOD_TREE = 0, SG_METHOD_COLLAPSE = 1, SG_METHOD_PLAIN = 2 } sg_method;
 
 /* Work partition.  The Smolyak points are split into the root (all-midpoint point) and the
  * subtrees of the depth-1 prefixes (k1, l1, j1) = (first active coordinate, its level >= 2, its node),
@@ -142,7 +148,7 @@ typedef struct {
     int rank, world;
     long long range_lo, range_hi;
     sg_merge merge;   /* SG_MERGE_NONE (default) or SG_MERGE_MIDPOINT */
-    sg_method method; /* SG_METHOD_TREE (default) or SG_METHOD_COLLAPSE */
+    sg_method method; /* SG_METHOD_TREE (default), SG_METHOD_COLLAPSE or SG_METHOD_PLAIN */
 } sg_options;
 
 typedef struct sg_plan_s *sg_plan_t;

@@ -24,7 +24,8 @@ FORM_COMBINATION, FORM_DELTA = 0, 1
 ARITH_FACTOR_DD, ARITH_SFORM_FP64, ARITH_SFORM_DD = 0, 1, 2   # s-forms: per-point outer function
                                                             # (FP64 ablation / dd, parity-grade)
 MERGE_NONE, MERGE_MIDPOINT = 0, 1          # midpoint-merged evaluation (sg_merge)
-METHOD_TREE, METHOD_COLLAPSE = 0, 1        # sg_method: prefix tree over the points / separable collapse
+METHOD_TREE, METHOD_COLLAPSE, METHOD_PLAIN = 0, 1, 2   # sg_method: prefix tree / separable collapse /
+                                                      # plain per-point SG baseline (ablation)
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:

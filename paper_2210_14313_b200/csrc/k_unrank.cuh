@@ -119,3 +119,32 @@ __global__ void __launch_bounds__(128) k_eval_points(const DevPlan P, const Unra
     out[2 * i] = term.hi;
     out[2 * i + 1] = term.lo;
 }
+
+// SG_METHOD_PLAIN: every point evaluated independently (the paper's plain SG baseline, no dimension
+// iteration): thread g handles the flat indices g, g + G, g + 2G, ... of the shard (fixed order),
+// unranks each one and forms its term from its t factors; dd accumulation, fixed CTA reduction.
+__global__ void __launch_bounds__(256) k_plain(const DevPlan P, const UnrankTabs U, double2 *partials) {
+    const unsigned long long G = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long g0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double ah = 0.0, al = 0.0;
+    int K[SG_MAX_L + 1], Lv[SG_MAX_L + 1], J[SG_MAX_L + 1];
+    const cdd B = {dd{P.base[0], P.base[1]}, dd{P.base[2], P.base[3]}};
+    for (unsigned long long i = g0; i < U.shard_points; i += G) {
+        int b = 0;
+        const int t = unrank_point(P, U, i, K, Lv, J, b);
+        if (t < 0) continue;
+        cdd v = B;
+        for (int m = 0; m < t; ++m) {
+            const int e = P.tab_off[Lv[m]] + K[m] * P.nl[Lv[m]] + J[m];
+            const double2 fr = P.Fre[e];
+            const double2 fi = P.Fim ? P.Fim[e] : make_double2(0.0, 0.0);
+            v = cdd_mul_fast(v, cdd{dd{fr.x, fr.y}, dd{fi.x, fi.y}});
+        }
+        const double2 c = P.coefm[t * (P.L + 1) + b];
+        double p, e;
+        dd_mul_pe(v.re, dd{c.x, c.y}, p, e);
+        acc_add(ah, al, p, e);
+    }
+    const dd s = block_reduce_dd<8>(dd_norm(ah, al));
+    if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(s.hi, s.lo);
+}

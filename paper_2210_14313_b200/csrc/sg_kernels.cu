@@ -46,6 +46,8 @@ struct sg_plan_s {
     bool two = false;          // frontier layout with a second double2 array (complex or s-form)
     void *d_unrank = nullptr;  // sg_eval_points: device Sub / SG / D1 tables (built on first use)
     UnrankTabs utabs = {};
+    bool plain = false;        // SG_METHOD_PLAIN: every point unranked and evaluated on its own
+    int plain_blocks = 0;
     bool collapse = false;     // SG_METHOD_COLLAPSE: O(d L^2) per-coordinate polynomial product
     int collapse_blocks = 0;   // CTAs of k_collapse_part (one partial polynomial each)
     bool collapse_emit = true; // rank 0 emits the value; other ranks contribute 0
@@ -77,6 +79,7 @@ struct sg_plan_s {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static int setup_leaf1(sg_plan_s *p);
+static int build_unrank_tables(sg_plan_s *p);
 
 static bool finite_array(const double *a, int n) {
     for (int i = 0; i < n; ++i)
@@ -139,7 +142,9 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     if (o.arith != SG_ARITH_FACTOR_DD && f->kind == SG_F_PRODUCT_PEAK) return SG_EUNSUPPORTED;
     if (o.merge != SG_MERGE_NONE && o.merge != SG_MERGE_MIDPOINT) return SG_EINVAL;
     if (o.merge != SG_MERGE_NONE && o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
-    if (o.method != SG_METHOD_TREE && o.method != SG_METHOD_COLLAPSE) return SG_EINVAL;
+    if (o.method != SG_METHOD_TREE && o.method != SG_METHOD_COLLAPSE && o.method != SG_METHOD_PLAIN)
+        return SG_EINVAL;
+    if (o.method == SG_METHOD_PLAIN && o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
     if (o.method == SG_METHOD_COLLAPSE) {
         if (o.merge != SG_MERGE_NONE) return SG_EINVAL;
         if (o.arith != SG_ARITH_FACTOR_DD) return SG_EUNSUPPORTED;
@@ -151,7 +156,8 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         // SG_B200_NOFUSE=1 / SG_B200_FUSE=1 override the automatic choice (tests, A/B runs)
         const char *nf = getenv("SG_B200_NOFUSE"), *fu = getenv("SG_B200_FUSE");
         int mode = (nf && nf[0] == '1') ? 0 : (fu && fu[0] == '1') ? 2 : 1;
-        if (o.arith != SG_ARITH_FACTOR_DD) mode = 0;
+        if (o.arith != SG_ARITH_FACTOR_DD || o.method == SG_METHOD_PLAIN) mode = 0;
+        p->plain = (o.method == SG_METHOD_PLAIN);
         if (o.method == SG_METHOD_COLLAPSE) {
             // whole problem on every rank (the collapse is not sharded); no tree passes run
             p->collapse = true;
@@ -286,12 +292,30 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         delete p;
         return SG_ECUDA;
     }
-    rc = p->collapse ? SG_OK : setup_leaf1(p);
+    rc = (p->collapse || p->plain) ? SG_OK : setup_leaf1(p);
     if (rc) {
         cudaGetLastError();
         cudaFree(p->dev_block);
         delete p;
         return rc;
+    }
+    if (p->plain) {
+        // ---- plain per-point method: unrank tables (plan-owned), one dd partial per CTA ----
+        rc = build_unrank_tables(p);
+        if (rc) {
+            cudaFree(p->dev_block);
+            delete p;
+            return rc;
+        }
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        p->plain_blocks = sms * 8;
+        p->ws_part_off = 0;
+        p->ws_red_off = align_up(sizeof(double2) * (size_t)p->plain_blocks, 256);
+        p->ws_need = p->ws_red_off + 256;
+        *out = p;
+        return SG_OK;
     }
     if (p->collapse) {
         // ---- collapse: workspace = the partial polynomials (re, im) of k_collapse_part ----
@@ -492,6 +516,19 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         if (p->prof && evi < (int)p->ev.size()) cudaEventRecord(p->ev[evi++], st);
     };
     mark();
+    if (p->plain) {
+        if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+        mark();
+        k_base<<<1, 256, 0, st>>>(dp);
+        mark();
+        double2 *part = (double2 *)(p->ws + p->ws_part_off);
+        k_plain<<<p->plain_blocks, 256, 0, st>>>(dp, p->utabs, part);
+        mark();
+        k_reduce<<<1, 1024, 0, st>>>(dp, part, p->plain_blocks, 0, out_dev);
+        mark();
+        if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
+        return SG_OK;
+    }
     if (p->collapse) {
         const int L = hp.L;
         if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
@@ -683,7 +720,7 @@ extern "C" int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long lon
 extern "C" int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
                               unsigned long long *written) {
     if (!p || !npass) return SG_EINVAL;
-    const int n = p->collapse ? 0 : p->hp.nfront + 1;   // the collapse runs no tree passes
+    const int n = (p->collapse || p->plain) ? 0 : p->hp.nfront + 1;   // no tree passes run
     if ((terms || written) && *npass < n) {
         *npass = n;
         return SG_EINVAL;
@@ -803,7 +840,7 @@ extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
     if (!p || !n) return SG_EINVAL;
     // launches: tree [K0 factor, K0 base, root, pass 1..nfront, reduce];
     //           collapse [K0 factor, K0 base, k_collapse_part, k_collapse_final]
-    const int nl = p->collapse ? 4 : 4 + p->hp.nfront;
+    const int nl = (p->collapse || p->plain) ? 4 : 4 + p->hp.nfront;
     if (!ms) {
         *n = nl;
         return SG_OK;
@@ -816,11 +853,7 @@ extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
     return SG_OK;
 }
 
-extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long long *index_dev, long long n,
-                              int *points_dev, double *terms_dev) {
-    if (!p || n < 0 || (n > 0 && (!index_dev || !points_dev || !terms_dev))) return SG_EINVAL;
-    if (p->sform || p->collapse) return SG_EUNSUPPORTED;
-    cudaStream_t st = (cudaStream_t)s;
+static int build_unrank_tables(sg_plan_s *p) {
     const HostPlan &hp = p->hp;
     if (!p->d_unrank) {
         const int d = hp.d, L = hp.L, W = d + 1;
@@ -864,6 +897,17 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
         p->utabs.merge = hp.merge;
         p->utabs.shard_points = hp.shard_points;
     }
+    return SG_OK;
+}
+
+extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long long *index_dev, long long n,
+                              int *points_dev, double *terms_dev) {
+    if (!p || n < 0 || (n > 0 && (!index_dev || !points_dev || !terms_dev))) return SG_EINVAL;
+    if (p->sform || p->collapse) return SG_EUNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)s;
+    const HostPlan &hp = p->hp;
+    int rc = build_unrank_tables(p);
+    if (rc) return rc;
     // the factor table and base of the current parameters (K0), then one thread per index
     if (cudaMemsetAsync(p->dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
     if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(p->dp);

@@ -93,3 +93,29 @@ def test_eval_points_out_of_range_and_errors(api):
     with pytest.raises(SGError):
         q.eval_points([0])
     q.close()
+
+
+@pytest.mark.parametrize("case", [("c1", None), ("c2", None), ("rand", (150, 12, 4, S.RULE_GP, S.KIND_GAUSS)),
+                                  ("merged", (151, 8, 5, S.RULE_CC, S.KIND_OSC)),
+                                  ("delta", (152, 30, 3, S.RULE_GL, S.KIND_PEAK))])
+def test_plain_method_vs_oracle(api, case):
+    """SG_METHOD_PLAIN (every point unranked and evaluated on its own, the paper's SG baseline)."""
+    p = S.baseline_config(int(case[0][1])) if case[1] is None else S.random_problem(*case[1])
+    kw = {"method": api.METHOD_PLAIN}
+    if case[0] == "merged":
+        kw["merge"] = api.MERGE_MIDPOINT
+    if case[0] == "delta":
+        kw["form"] = api.FORM_DELTA
+    hi, lo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u, **kw)
+    ref = mp.mpf(oracle.integrate_problem(p, eval_mode=1).text)
+    assert abs(mp.mpf(hi) + mp.mpf(lo) - ref) <= 1e-15 * abs(ref)
+
+
+def test_plain_method_config4_full_size(api):
+    import json
+    import os
+    p = S.baseline_config(4)
+    hi, lo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u, method=api.METHOD_PLAIN)
+    golden = os.path.join(os.path.dirname(__file__), "golden", "oracle_full.json")
+    ref = mp.mpf(json.load(open(golden))["values"]["c4"]["text"])
+    assert abs(mp.mpf(hi) + mp.mpf(lo) - ref) <= 1e-15 * abs(ref)
