@@ -298,3 +298,24 @@ def test_shard_ranges_independent_of_leaf_path(api, monkeypatch):
     assert ref == nofuse == sform
     assert ref[0][0] == 0 and ref[-1][1] == ref[-1][2]
     assert all(a[1] == b[0] for a, b in zip(ref, ref[1:]))
+
+
+@pytest.mark.parametrize("name,d,L,rule,kind,c,w,u", [
+    ("osc_huge_phase", 6, 4, S.RULE_CC, S.KIND_OSC, [0.7, 0.2, 0.9, 0.4, 0.1, 0.6], None, 1.0e6 + 0.3),
+    ("osc_big_c", 5, 4, S.RULE_GL, S.KIND_OSC, [40.0, -25.0, 10.0, 33.0, -7.0], None, 0.25),
+    ("exp_big_c", 5, 4, S.RULE_CC, S.KIND_EXP, [30.0, -20.0, 12.5, 40.0, -35.0], None, 0.0),
+    ("peak_sharp", 4, 5, S.RULE_GP, S.KIND_PEAK, [25.0, 18.0, 30.0, 22.0], [0.3, 0.7, 0.5, 0.05], 0.0),
+    ("peak_flat", 6, 3, S.RULE_CC, S.KIND_PEAK, [1e-3, 2e-3, 5e-4, 1e-3, 3e-3, 1e-3],
+     [0.1, 0.9, 0.5, 0.2, 0.8, 0.4], 0.0),
+    ("gauss_wide", 8, 3, S.RULE_TRAP, S.KIND_GAUSS, [5.0, 4.0, 6.0, 3.0, 5.5, 4.5, 2.0, 7.0],
+     [0.5, 0.1, 0.9, 0.3, 0.7, 0.2, 0.6, 0.4], 0.0),
+])
+def test_parameter_extremes(api, name, d, L, rule, kind, c, w, u):
+    """Large phases (dd range reduction of 2 pi u), large |c| (wide dynamic range of the factors),
+    sharp and flat product peaks, narrow Gaussians: tree, merged and collapse against the oracle."""
+    p = S.Problem(name, d, L, rule, kind, np.array(c, dtype=float),
+                  None if w is None else np.array(w, dtype=float), u)
+    ref = mp.mpf(oracle.integrate_problem(p, eval_mode=1).text)
+    for kw in ({}, {"merge": api.MERGE_MIDPOINT}, {"method": api.METHOD_COLLAPSE}):
+        v, _ = gpu_value(api, p, **kw)
+        assert rel(v, ref) <= HEALTH, (name, kw, float(rel(v, ref)))
