@@ -653,7 +653,16 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         // Cmid[k] = parents (excess L-2) whose last active coordinate is < k; chunk c of 32 parents
         // has a valid lane for every k_mid >= kstart(c) (Cmid is nondecreasing); k_mid <= d-2
         auto cmid = [&](int k) -> int64_t { return k <= d - 2 ? hp.C[tm][(size_t)(L - 2) * d + k] : 0; };
-        const int64_t nchunks = (cmid(d - 2) + 31) / 32;
+        // a level-2 row that is one conjugate pair (oscillatory, x_0 = 1 - x_1, equal weights:
+        // the midpoint-merged CC row) runs k_leaf2_pairs with LEAF2_PPL parents per lane
+        {
+            const int e0 = hp.entry_off[2];
+            const bool pair = kind == SG_F_OSCILLATORY && hp.nl[2] == 2 && 1.0 - hp.X[e0 + 1] == hp.X[e0] &&
+                              hp.Whi[e0] == hp.Whi[e0 + 1] && hp.Wlo[e0] == hp.Wlo[e0 + 1];
+            hp.leaf2_ppl = pair ? LEAF2_PPL : 1;
+        }
+        const int64_t CH = 32LL * hp.leaf2_ppl;   // parents per task chunk
+        const int64_t nchunks = (cmid(d - 2) + CH - 1) / CH;
         struct Task {
             int64_t rows, first;
             int ka, kb, kp0, kp1;   // k_mid range; row range (split tasks: one k_mid, [kp0, kp1))
@@ -661,13 +670,13 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         std::vector<Task> tasks;
         int k0 = 0;
         for (int64_t c = 0; c < nchunks; ++c) {
-            while (k0 <= d - 2 && cmid(k0) <= 32 * c) ++k0;   // kstart(c), nondecreasing in c
+            while (k0 <= d - 2 && cmid(k0) <= CH * c) ++k0;   // kstart(c), nondecreasing in c
             int64_t acc = 0;
             int ka = k0;
             for (int k = k0; k <= d - 2; ++k) {
                 acc += d - 1 - k;
                 if (acc >= LEAF2_TASK_ROWS || k == d - 2) {
-                    tasks.push_back(Task{acc, 32 * c, ka, k + 1, 0, d});
+                    tasks.push_back(Task{acc, CH * c, ka, k + 1, 0, d});
                     acc = 0;
                     ka = k + 1;
                 }

@@ -27,6 +27,10 @@
 #ifndef LEAF2_MID_COST
 #define LEAF2_MID_COST 20.0       // shard cost model: fixed cost of one k_leaf2 row run, in points
 #endif
+#ifndef LEAF2_PPL
+#define LEAF2_PPL 3   // parents per lane for a level-2 row that is one conjugate pair (k_leaf2_pairs;
+                      // A/B on merged config 5 at 1 CTA/SM: 1 -> 3.51 ms, 2 -> 3.39, 3 -> 3.23, 4 -> 3.37)
+#endif
 #ifndef LEAF2_RESIDENT_WARPS
 #define LEAF2_RESIDENT_WARPS (148 * 24)   // persistent k_leaf2 warps (B200: 148 SMs x 16-24 warps)
 #endif
@@ -72,6 +76,7 @@ struct HostPlan {
     // stored; the last pass builds each depth-(L-1) prefix from its depth-(L-2) parent (excess L-2,
     // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
     bool fuse = false;
+    int leaf2_ppl = 1;                 // parents per lane of the fused kernel (2: k_leaf2_pairs)
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.

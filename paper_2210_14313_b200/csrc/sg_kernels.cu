@@ -408,7 +408,13 @@ static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
     return (const void *)k_leaf2<CPLX, 2, SMEM, -1>;
 }
 template <bool CPLX>
-static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz) {
+static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz, int ppl = 1) {
+    if (CPLX && sym && nj == 2 && ppl == 2)
+        return smem ? (const void *)k_leaf2_pairs<2, true> : (const void *)k_leaf2_pairs<2, false>;
+    if (CPLX && sym && nj == 2 && ppl == 3)
+        return smem ? (const void *)k_leaf2_pairs<3, true> : (const void *)k_leaf2_pairs<3, false>;
+    if (CPLX && sym && nj == 2 && ppl == 4)
+        return smem ? (const void *)k_leaf2_pairs<4, true> : (const void *)k_leaf2_pairs<4, false>;
     return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz) : leaf2_fn<CPLX, false>(nj, center, sym, cz);
 }
 
@@ -447,7 +453,8 @@ static int setup_leaf1(sg_plan_s *p) {
     const bool sy = p->leaf2_sym;
     p->leaf2_cz = ct && hp.Wlo[hp.entry_off[2] + 1] == 0.0;
     const bool cz = p->leaf2_cz;
-    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy, cz) : leaf2_kernel<false>(nj, sm, ct, sy, cz))
+    const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy, cz, hp.leaf2_ppl)
+                                         : leaf2_kernel<false>(nj, sm, ct, sy, cz))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
@@ -474,7 +481,7 @@ template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
-    const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz);
+    const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz, p->hp.leaf2_ppl);
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
