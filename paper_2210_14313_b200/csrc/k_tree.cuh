@@ -1146,3 +1146,154 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
         rr = nrr;
     }
 }
+
+// ---------------------------------------------------------------------------------------------
+// k_leaf2_sym3: the fused last two levels for a level-2 row {0, 1/2, 1} (symmetric pair + real
+// midpoint, oscillatory: the Clenshaw-Curtis / trapezoidal combination-form row of configs 2, 5)
+// with PPL parents per lane (3 PPL mid prefixes), 1 CTA per SM: k_leaf2's per-point arithmetic
+// (split symmetric pair: node 0 into a, node 2 and the midpoint into b) with more independent
+// accumulator chains per warp.
+// ---------------------------------------------------------------------------------------------
+template <int PPL, bool SMEM, bool CZ>
+__global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
+    constexpr int NM = 3 * PPL;   // mid prefixes per lane
+    extern __shared__ double2 fsm[];
+    const int lane = threadIdx.x & 31;
+    const int d = P.d;
+    const double2 *Fr = P.Fre + P.tab_off[2];
+    const double2 *Fi = P.Fim + P.tab_off[2];
+    if (SMEM) {
+        const int n = d * 3;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            fsm[i] = Fr[i];
+            fsm[n + i] = Fi[i];
+        }
+        __syncthreads();
+        Fr = fsm;
+        Fi = fsm + n;
+    }
+    auto fetch = [&]() -> long long {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(A.counter, 1ull);
+        return (long long)__shfl_sync(0xffffffffu, u, 0);
+    };
+    long long task = fetch();
+    long long first = 0, kk = 0, rr = 0;
+    if (task < A.ntasks) {
+        first = A.T2[3 * task];
+        kk = A.T2[3 * task + 1];
+        rr = A.T2[3 * task + 2];
+    }
+    while (task < A.ntasks) {
+        long long next = 0, nfirst = 0, nkk = 0, nrr = 0;
+        if (A.prefetch) {
+            next = fetch();
+            if (next < A.ntasks) {
+                nfirst = A.T2[3 * next];
+                nkk = A.T2[3 * next + 1];
+                nrr = A.T2[3 * next + 2];
+            }
+        }
+        const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
+        const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
+        long long ip[PPL];
+        dd pr[PPL], pim[PPL];
+        const long long cend = A.Cmid[kb - 1];
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) {
+            ip[q] = first + 32LL * q + lane;
+            pr[q] = dd{0.0, 0.0};
+            pim[q] = dd{0.0, 0.0};
+            if (ip[q] < cend) {
+                const double2 v = A.src_re[A.base + ip[q]], vi = A.src_im[A.base + ip[q]];
+                pr[q] = dd{v.x, v.y};
+                pim[q] = dd{vi.x, vi.y};
+            }
+        }
+        dd lane_sum = {0.0, 0.0};
+        for (int km = ka; km < kb; ++km) {
+            const long long cm = A.Cmid[km];
+            const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+            const double2 fm = Fr[km * 3 + 2], gm = Fi[km * 3 + 2], wm = Fr[km * 3 + 1];
+            dd er[NM], ei[NM];
+            double sg[NM], ah[NM], al[NM], bh[NM], bl[NM];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) {
+                const bool valid = ip[q] < cm;
+                const dd vr = valid ? pr[q] : dd{0.0, 0.0}, vi = valid ? pim[q] : dd{0.0, 0.0};
+                cdd c2, c0;
+                cdd_mul_conj_pair(cdd{vr, vi}, cdd{dd{fm.x, fm.y}, dd{gm.x, gm.y}}, c2, c0);
+                er[3 * q] = c0.re;
+                ei[3 * q] = c0.im;
+                er[3 * q + 2] = c2.re;
+                ei[3 * q + 2] = c2.im;
+                er[3 * q + 1] = CZ ? dd_mul_d(vr, wm.x) : dd_mul(vr, dd{wm.x, wm.y});
+                ei[3 * q + 1] = CZ ? dd_mul_d(vi, wm.x) : dd_mul(vi, dd{wm.x, wm.y});
+            }
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                const double bound = (fabs(er[m].hi) + fabs(ei[m].hi)) * sa;
+                int ex = 0;
+                frexp(2.0 * bound, &ex);
+                sg[m] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+                ah[m] = bh[m] = sg[m];   // biased accumulators (node 0 -> a, node 1 -> b)
+                al[m] = bl[m] = 0.0;
+            }
+            int kp = max(km + 1, kp0);
+            while (kp < kp1) {
+                const int ke = min(kp1, kp + FOLD);
+                for (; kp < ke; ++kp) {
+                    const double2 f1 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
+                    const double2 g1 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
+                    const double2 w1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
+#pragma unroll
+                    for (int m = 0; m < NM; ++m) {
+                        const double u1 = fma(er[m].hi, f1.x, ah[m]);
+                        const double h1 = u1 - ah[m];
+                        ah[m] = fma(ei[m].hi, g1.x, u1);
+                        const double h2 = ah[m] - u1;
+                        const double cA = fma(er[m].lo, f1.x, fma(er[m].hi, f1.y, fma(er[m].hi, f1.x, -h1)));
+                        const double cB = fma(ei[m].lo, g1.x, fma(ei[m].hi, g1.y, fma(ei[m].hi, g1.x, -h2)));
+                        al[m] += cA + cB;
+                        bh[m] += h1 - h2;
+                        bl[m] += cA - cB;
+                        leaf_real_factor_term<CZ>(er[m], w1, bh[m], bl[m]);   // the midpoint node
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NM; ++m) {
+                    al[m] += bl[m];
+                    bl[m] = 0.0;
+                    const double t = (al[m] + sg[m]) - sg[m];
+                    ah[m] += t;
+                    al[m] -= t;
+                }
+            }
+            double hs = (ah[0] + (bh[0] - sg[0])) - sg[0], ls = al[0] + bl[0];
+#pragma unroll
+            for (int m = 1; m < NM; ++m) {
+                double e;
+                two_sum(hs, (ah[m] + (bh[m] - sg[m])) - sg[m], hs, e);
+                ls += al[m] + bl[m] + e;
+            }
+            lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
+        }
+        dd v = warp_reduce_dd_fast(lane_sum);
+        if (lane == 0) {
+            v = dd_mul_d(v, P.coef[P.L]);
+            A.partials[task] = make_double2(v.hi, v.lo);
+        }
+        if (!A.prefetch) {
+            next = fetch();
+            if (next < A.ntasks) {
+                nfirst = A.T2[3 * next];
+                nkk = A.T2[3 * next + 1];
+                nrr = A.T2[3 * next + 2];
+            }
+        }
+        task = next;
+        first = nfirst;
+        kk = nkk;
+        rr = nrr;
+    }
+}

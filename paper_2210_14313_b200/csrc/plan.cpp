@@ -659,7 +659,10 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             const int e0 = hp.entry_off[2];
             const bool pair = kind == SG_F_OSCILLATORY && hp.nl[2] == 2 && 1.0 - hp.X[e0 + 1] == hp.X[e0] &&
                               hp.Whi[e0] == hp.Whi[e0 + 1] && hp.Wlo[e0] == hp.Wlo[e0 + 1];
-            hp.leaf2_ppl = pair ? LEAF2_PPL : 1;
+            const bool sym3 = kind == SG_F_OSCILLATORY && hp.nl[2] == 3 && hp.X[e0 + 1] == 0.5 &&
+                              1.0 - hp.X[e0 + 2] == hp.X[e0] && hp.Whi[e0] == hp.Whi[e0 + 2] &&
+                              hp.Wlo[e0] == hp.Wlo[e0 + 2];
+            hp.leaf2_ppl = pair ? LEAF2_PPL : sym3 ? LEAF2_PPL3 : 1;
         }
         const int64_t CH = 32LL * hp.leaf2_ppl;   // parents per task chunk
         const int64_t nchunks = (cmid(d - 2) + CH - 1) / CH;

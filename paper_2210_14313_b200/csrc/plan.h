@@ -31,6 +31,10 @@
 #define LEAF2_PPL 3   // parents per lane for a level-2 row that is one conjugate pair (k_leaf2_pairs;
                       // A/B on merged config 5 at 1 CTA/SM: 1 -> 3.51 ms, 2 -> 3.39, 3 -> 3.23, 4 -> 3.37)
 #endif
+#ifndef LEAF2_PPL3
+#define LEAF2_PPL3 3  // parents per lane for the level-2 row {0, 1/2, 1} of the oscillatory kind (k_leaf2_sym3;
+                      // A/B on config 5, 3 runs: 1 (k_leaf2, 2 CTAs/SM) 13.105 ms, 2 -> 13.41, 3 -> 13.053)
+#endif
 #ifndef LEAF2_RESIDENT_WARPS
 #define LEAF2_RESIDENT_WARPS (148 * 24)   // persistent k_leaf2 warps (B200: 148 SMs x 16-24 warps)
 #endif

@@ -409,6 +409,13 @@ static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
 }
 template <bool CPLX>
 static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz, int ppl = 1) {
+    if (CPLX && sym && center && nj == 3 && ppl >= 2) {
+#define SYM3(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true> : (const void *)k_leaf2_sym3<P_, true, false>) \
+                       : (cz ? (const void *)k_leaf2_sym3<P_, false, true> : (const void *)k_leaf2_sym3<P_, false, false>))
+        if (ppl == 2) return SYM3(2);
+        if (ppl == 3) return SYM3(3);
+#undef SYM3
+    }
     if (CPLX && sym && nj == 2 && ppl == 2)
         return smem ? (const void *)k_leaf2_pairs<2, true> : (const void *)k_leaf2_pairs<2, false>;
     if (CPLX && sym && nj == 2 && ppl == 3)
