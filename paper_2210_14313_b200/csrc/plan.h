@@ -25,7 +25,8 @@
 #define GENERIC_POINT_COST 1.8    // shard cost model: a point of a generic pass vs a k_leaf2 point
 #endif
 #ifndef LEAF2_MID_COST
-#define LEAF2_MID_COST 20.0       // shard cost model: fixed cost of one k_leaf2 row run, in points
+#define LEAF2_MID_COST 5.0        // shard cost model: fixed cost of one k_leaf2 row run, in points
+                                  // (A/B of the N = 8 projection on config 5: 5 -> 0.903, 10 -> 0.891, 20 -> 0.892)
 #endif
 #ifndef LEAF2_PPL
 #define LEAF2_PPL 3   // parents per lane for a level-2 row that is one conjugate pair (k_leaf2_pairs;
