@@ -192,6 +192,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the stream-launched step instead of its CUDA-graph replay")
     ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
     ap.add_argument("--no-frontier", action="store_true",
                     help="skip the stored-frontier (unfused) leg that measures the HBM-bound frontier kernel")
@@ -256,6 +258,32 @@ def main():
         else:
             plan.sg_finalize(part, 1, stream, result)
 
+    def graph_step(plan):
+        """The step as one CUDA-graph replay (sg_integrate, + sg_finalize at world 1; the launch
+        events are graph event-record nodes, so profile_read still times each launch); at world > 1
+        the all-gather and sg_finalize follow the replay as in step()."""
+        if args.no_graph:
+            return lambda: step(plan)
+        plan.profile_enable(True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            part = plan.sg_integrate()
+            if world == 1:
+                plan.sg_finalize(part, 1, None, result)
+
+        def fn():
+            g.replay()
+            if world > 1:
+                if args.dist_backend == "nccl":
+                    dist.all_gather_into_tensor(gathered, part)
+                else:
+                    gl = torch.zeros(2 * world, dtype=torch.float64)
+                    dist.all_gather_into_tensor(gl, part.cpu())
+                    gathered.copy_(gl)
+                plan.sg_finalize(gathered, world, stream, result)
+        fn.graph = g
+        return fn
+
     def timed(fn, k, plan=plan, dominant=dominant):
         times, dom = [], []
         for _ in range(k):
@@ -283,8 +311,12 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    gstep = graph_step(plan)
+    for _ in range(args.warmup):
+        gstep()
+    torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
-        times, dom = timed(step, args.steps)
+        times, dom = timed(gstep, args.steps)
     ms = statistics.mean(times)
 
     # e2e: host buffers through the C ABI (pinned H2D of c/w, step, D2H of the result)
@@ -317,7 +349,9 @@ def main():
         for _ in range(args.warmup):
             step(mplan)
         torch.cuda.synchronize(dev)
-        m_times, m_dom = timed(lambda: step(mplan), args.steps, mplan, mdom)
+        mstep = graph_step(mplan)
+        mstep()
+        m_times, m_dom = timed(mstep, args.steps, mplan, mdom)
         m_res = result.cpu().numpy()
         m_ms = statistics.mean(m_times)
         mf, ma = mplan.leaf_work()
@@ -457,7 +491,9 @@ def main():
         for _ in range(args.warmup):
             step(kplan)
         torch.cuda.synchronize(dev)
-        k_times, _ = timed(lambda: step(kplan), args.steps, kplan, 0)
+        kstep = graph_step(kplan)
+        kstep()
+        k_times, _ = timed(kstep, args.steps, kplan, 0)
         k_res = result.cpu().numpy()
         k_ms = statistics.mean(k_times)
         corner = {"workload": f"{pc.name}: Genz corner peak (1 + sum c_k x_k)^-(d+1), d={pc.d}, "
@@ -494,7 +530,9 @@ def main():
             "time_to_integral_ms": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(p, {"parallelism": f"dp{world} (depth-1 subtree shards)",
-                                       "shard_points_rank0": shard_pts}),
+                                       "shard_points_rank0": shard_pts,
+                                       "launch": "stream launches" if args.no_graph else
+                                       "CUDA-graph replay of sg_integrate (+ sg_finalize)"}),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"pass {dominant} leaf kernel ({dom_terms} points)",
@@ -508,9 +546,9 @@ def main():
                                       f"{fp64_meas} TFLOP/s"},
             "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
-            # per step: k_factor, k_suffix_abs, k_base, k_root, one kernel per pass >= 1,
-            # k_reduce_l1, k_reduce, k_finalize
-            "gpu_launches": (len(passes) - 1 + 7) * args.steps,
+            # per step: k_factor_base, k_suffix_abs, k_root, one kernel per pass >= 1,
+            # k_reduce_fused, k_finalize
+            "gpu_launches": (len(passes) - 1 + 5) * args.steps,
             "clocks": clk.summary(),
             "parity": parity,
             "step_ms_all": [round(t, 4) for t in times],

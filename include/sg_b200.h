@@ -218,6 +218,7 @@ int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, doubl
  * kernel and after each kernel.  sg_profile_read waits for the events of the LAST sg_integrate and
  * writes the device duration (ms) of each launch, in launch order:
  *   [K0 factor table, K0 base, root pass, pass 1 .. pass nfront, final reduce]
+ * (the base value is computed by one extra block of the factor-table launch: its entry is ~0)
  * (SG_METHOD_COLLAPSE: [K0 factor table, K0 base, k_collapse_part, k_collapse_final]).
  * *n: in = capacity of ms[], out = number of launches (query with ms = NULL). */
 int sg_profile_enable(sg_plan_t p, int enable);

@@ -171,23 +171,28 @@ class Plan:
                                    _dptr(terms)), "sg_eval_points")
         return pts[:n], terms[:n]
 
-    def capture_graph(self):
-        """Capture one whole step (sg_integrate + sg_finalize(world=1)) into a CUDA graph.
+    def capture_graph(self, finalize: bool = True, profile: bool = False):
+        """Capture one step (sg_integrate, + sg_finalize(world=1) if `finalize`) into a CUDA graph.
 
         Returns the torch.cuda.CUDAGraph; ``graph.replay()`` re-runs the step with ~one launch of
-        CPU overhead (the small configs are launch-latency bound).  The result lands in the
-        tensor returned by ``result()``.  Profiling events must be off while capturing."""
-        self.profile_enable(False)
+        CPU overhead (the small configs are launch-latency bound).  The partial lands in the
+        plan's default output (``sg_integrate()``'s tensor), the value in ``result()``.  With
+        `profile`, the per-launch events are captured as graph event-record nodes and
+        ``profile_read()`` returns the last replay's launch times."""
+        self.profile_enable(profile)
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(side):
-            self.sg_finalize(self.sg_integrate(side), 1, side)
+            out = self.sg_integrate(side)
+            if finalize:
+                self.sg_finalize(out, 1, side)
         torch.cuda.current_stream(self.device).wait_stream(side)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             out = self.sg_integrate()
-            self.sg_finalize(out, 1)
+            if finalize:
+                self.sg_finalize(out, 1)
         return g
 
     def result(self) -> torch.Tensor:

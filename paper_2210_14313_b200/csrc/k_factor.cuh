@@ -7,9 +7,8 @@
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool dd_finite(dd a) { return isfinite(a.hi) && isfinite(a.lo); }
 
-__global__ void k_factor(const DevPlan P) {
+__device__ __forceinline__ void factor_entry(const DevPlan &P, int idx) {
     const int n_ent = P.tab_off[P.L + 2];
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n_ent) return;
     int l = 2;
     while (l < P.L + 1 && idx >= P.tab_off[l + 1]) ++l;
@@ -62,8 +61,9 @@ __global__ void k_factor(const DevPlan P) {
     if (!ok) atomicOr(P.status, 1);
 }
 
-__global__ void __launch_bounds__(256) k_base(const DevPlan P) {
-    // fixed-order strided partials, then a fixed CTA tree (sum; product for the peak kind)
+// base value B (256-thread CTA): fixed-order strided partials, then a fixed CTA tree (sum; product
+// for the peak kind)
+__device__ __forceinline__ void base_body(const DevPlan &P) {
     const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
     dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
     for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
@@ -122,6 +122,14 @@ __global__ void __launch_bounds__(256) k_base(const DevPlan P) {
         P.base[3] = Bi.lo;
         if (!dd_finite(Br) || !dd_finite(Bi)) atomicOr(P.status, 1);
     }
+}
+
+// K0 in one launch: blocks 0 .. nfb-1 fill the factor table (one entry per thread), block nfb computes
+// the base value (independent of the table; same 256-thread order as k_base, so the same bits).
+#define K0_THREADS 256
+__global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int nfb) {
+    if ((int)blockIdx.x == nfb) base_body(P);
+    else factor_entry(P, blockIdx.x * K0_THREADS + threadIdx.x);
 }
 
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by k_leaf.

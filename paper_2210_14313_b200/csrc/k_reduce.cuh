@@ -2,17 +2,7 @@
 // (included once, by sg_kernels.cu, after the shared definitions it uses)
 #pragma once
 
-// Level-1 reduction: block b sums partials [b*RED_CHUNK, (b+1)*RED_CHUNK) in a fixed order.
-#define RED_CHUNK 8192
-__global__ void __launch_bounds__(256) k_reduce_l1(const double2 *partials, long long n, double2 *out) {
-    const long long b0 = (long long)blockIdx.x * RED_CHUNK, b1 = min(n, b0 + RED_CHUNK);
-    dd s = {0.0, 0.0};
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
-    s = block_reduce_dd<8>(s);
-    if (threadIdx.x == 0) out[blockIdx.x] = make_double2(s.hi, s.lo);
-}
-
-// Final fixed-order reduction of the level-1 partials (+ the root point) -> out[0..1].
+// One-block fixed-order reduction of per-block partials (+ the root point) -> out[0..1] (plain path).
 __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 *partials,
                                                  long long n, int include_root, double *out) {
     dd s = {0.0, 0.0};
@@ -28,6 +18,56 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
         if (*P.status) s = dd{nan(""), nan("")};
         out[0] = s.hi;
         out[1] = s.lo;
+    }
+}
+
+// Tree-path reduction in ONE launch: block b sums partials [b*RED_CHUNK2, (b+1)*RED_CHUNK2) (each
+// thread its RED_PER_THREAD elements, loads issued together, summed in index order), writes l1[b];
+// the last block to finish (atomic ticket after a fence) sums l1[0..nblk) in a fixed order, adds the
+// root point and writes out[0..1], then re-arms the ticket.  Which block is last does not change any
+// summation order, so the result is bitwise reproducible.
+#define RED_THREADS 256
+#define RED_PER_THREAD 8
+#define RED_CHUNK2 (RED_THREADS * RED_PER_THREAD)
+__global__ void __launch_bounds__(RED_THREADS)
+k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int include_root, double *out,
+               double2 *l1, unsigned long long *ticket) {
+    const long long b0 = (long long)blockIdx.x * RED_CHUNK2 + (long long)threadIdx.x * RED_PER_THREAD;
+    double2 v[RED_PER_THREAD];
+#pragma unroll
+    for (int i = 0; i < RED_PER_THREAD; ++i)
+        v[i] = b0 + i < n ? __ldcg(partials + b0 + i) : make_double2(0.0, 0.0);
+    dd s = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < RED_PER_THREAD; ++i) s = dd_add(s, dd{v[i].x, v[i].y});
+    s = block_reduce_dd<RED_THREADS / 32>(s);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        l1[blockIdx.x] = make_double2(s.hi, s.lo);
+        __threadfence();
+        last = atomicAdd(ticket, 1ULL) == (unsigned long long)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    dd t = {0.0, 0.0};
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += RED_THREADS) {
+        const double2 x = __ldcg(l1 + i);
+        t = dd_add(t, dd{x.x, x.y});
+    }
+    __syncthreads();   // the block_reduce scratch is reused
+    t = block_reduce_dd<RED_THREADS / 32>(t);
+    if (threadIdx.x == 0) {
+        if (include_root && P.coefm[0].x != 0.0) {
+            const dd root = P.sform == 2   ? sform_g_dd(P.kind, P.d, dd{P.base[0], P.base[1]})
+                            : P.sform == 1 ? dd{sform_g(P.kind, P.d, P.base[0]), 0.0}
+                                           : dd{P.base[0], P.base[1]};
+            t = dd_add(t, coef_mul(P, root, 0, 0));
+        }
+        if (*P.status) t = dd{nan(""), nan("")};
+        out[0] = t.hi;
+        out[1] = t.lo;
+        *ticket = 0;
     }
 }
 

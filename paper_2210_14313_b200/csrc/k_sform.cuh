@@ -17,9 +17,8 @@
 // Fim[idx] = a (dd; lo = 0 in FP64 mode); base[0..1] = S (dd); frontier re = W, im = delta.
 // ---------------------------------------------------------------------------------------------
 template <bool DDS>
-__global__ void k_factor_s(const DevPlan P) {
+__device__ __forceinline__ void factor_s_entry(const DevPlan &P, int idx) {
     const int n_ent = P.tab_off[P.L + 2];
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n_ent) return;
     int l = 2;
     while (l < P.L + 1 && idx >= P.tab_off[l + 1]) ++l;
@@ -47,7 +46,7 @@ __global__ void k_factor_s(const DevPlan P) {
 }
 
 // S in dd: fixed-order strided partials, then a fixed CTA tree (deterministic)
-__global__ void __launch_bounds__(256) k_base_s(const DevPlan P) {
+__device__ __forceinline__ void base_s_body(const DevPlan &P) {
     dd acc = {0.0, 0.0};
     double cneg = 0.0;   // corner peak: sum of negative c_k (domain 1 + sum min(c_k, 0) > 0)
     for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
@@ -89,6 +88,13 @@ __global__ void __launch_bounds__(256) k_base_s(const DevPlan P) {
         P.base[3] = 0.0;
         if (!dd_finite(S)) atomicOr(P.status, 1);
     }
+}
+
+// K0 of the s-form in one launch (block nfb: the base sum S; see k_factor_base)
+template <bool DDS>
+__global__ void __launch_bounds__(K0_THREADS) k_factor_base_s(const DevPlan P, int nfb) {
+    if ((int)blockIdx.x == nfb) base_s_body(P);
+    else factor_s_entry<DDS>(P, blockIdx.x * K0_THREADS + threadIdx.x);
 }
 
 __device__ __forceinline__ double sform_g(int kind, int d, double arg) {

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/sg_b200.h"
@@ -693,7 +695,9 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             total_rows += tk.rows;
             max_rows = std::max(max_rows, tk.rows);
         }
-        if (max_rows > LEAF2_TASK_ROWS && 4 * max_rows * (int64_t)LEAF2_RESIDENT_WARPS > total_rows) {
+        const bool do_split =
+            max_rows > LEAF2_TASK_ROWS && LEAF2_SPLIT_SHARE * max_rows * (int64_t)LEAF2_RESIDENT_WARPS > total_rows;
+        if (do_split) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {
                 if (tk.kb - tk.ka != 1 || tk.rows <= LEAF2_TASK_ROWS) {
@@ -709,6 +713,19 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 }
             }
             tasks.swap(split);
+        }
+        if (const char *dbg = getenv("SG_B200_DEBUG_TASKS"); dbg && dbg[0] == '1') {
+            // lane utilisation: parent-rows with a valid lane / lane-row slots the tasks occupy
+            double useful = 0, slots = 0, tail = 0;
+            for (int k = 0; k + 1 <= d - 2; ++k) {
+                tail = 0;
+                for (int km = k + 1; km <= d - 2; ++km) tail += d - 1 - km;
+                useful += (double)(cmid(k + 1) - cmid(k)) * tail;
+            }
+            for (const Task &tk : tasks) slots += (double)tk.rows * CH;
+            fprintf(stderr, "leaf2 tasks: %zu total_rows %lld max_rows %lld split %d ppl %d parents %lld "
+                    "lane_util %.4f\n", tasks.size(), (long long)total_rows, (long long)max_rows, (int)do_split,
+                    hp.leaf2_ppl, (long long)cmid(d - 2), useful / slots);
         }
         // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, rows, chunk)
         std::stable_sort(tasks.begin(), tasks.end(), [](const Task &a, const Task &b) {

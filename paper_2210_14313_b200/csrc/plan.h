@@ -39,6 +39,9 @@
 #ifndef LEAF2_RESIDENT_WARPS
 #define LEAF2_RESIDENT_WARPS (148 * 24)   // persistent k_leaf2 warps (B200: 148 SMs x 16-24 warps)
 #endif
+#ifndef LEAF2_SPLIT_SHARE
+#define LEAF2_SPLIT_SHARE 4   // split long tasks when one is > 1/SHARE of a resident warp's row share
+#endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 #endif

@@ -285,6 +285,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     ok &= cudaMemcpy((void *)dp.u, &f->u, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
     ok &= cudaMemcpy(p->d_tabs, tabs.data(), sizeof(long long) * tabs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     ok &= cudaMemset(dp.status, 0, sizeof(int) * 4) == cudaSuccess;
+    ok &= cudaMemset(p->d_counter, 0, sizeof(unsigned long long) * 8) == cudaSuccess;   // tickets
     ok &= cudaMemcpy((void *)dp.coefm, cm.data(), sizeof(double2) * cm.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -351,7 +352,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->ws_part_off = ws;
     ws = align_up(ws + sizeof(double2) * (size_t)std::max<int64_t>(hp.total_partials, 1), 256);
     p->ws_red_off = ws;
-    ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK - 1) / RED_CHUNK + 1), 256);
+    ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2 + 1), 256);
     p->ws_need = ws;
     *out = p;
     return SG_OK;
@@ -526,15 +527,19 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     double2 *partials = (double2 *)(p->ws + p->ws_part_off);
     if (cudaMemsetAsync(dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
     int evi = 0;
+    // under stream capture the events become graph event-record nodes (timed on every replay)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (p->prof && cudaStreamIsCapturing(st, &cap) != cudaSuccess) return SG_ECUDA;
+    const unsigned ev_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
     auto mark = [&]() {
-        if (p->prof && evi < (int)p->ev.size()) cudaEventRecord(p->ev[evi++], st);
+        if (p->prof && evi < (int)p->ev.size()) cudaEventRecordWithFlags(p->ev[evi++], st, ev_flags);
     };
     mark();
+    const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);   // factor-table blocks of the merged K0 launch
     if (p->plain) {
-        if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         mark();
-        k_base<<<1, 256, 0, st>>>(dp);
-        mark();
+        mark();   // K0 base: merged into the factor launch
         double2 *part = (double2 *)(p->ws + p->ws_part_off);
         k_plain<<<p->plain_blocks, 256, 0, st>>>(dp, p->utabs, part);
         mark();
@@ -545,10 +550,9 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     }
     if (p->collapse) {
         const int L = hp.L;
-        if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         mark();
-        k_base<<<1, 256, 0, st>>>(dp);
-        mark();
+        mark();   // K0 base: merged into the factor launch
         double2 *pre = (double2 *)(p->ws + p->ws_part_off);
         double2 *pim = pre + (size_t)p->collapse_blocks * (L + 1);
         const size_t smem_part = (size_t)(p->cplx ? 4 : 2) * COLLAPSE_THREADS * (L + 1) * sizeof(double2);
@@ -569,19 +573,15 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         return SG_OK;
     }
     // K0
-    if (hp.tab_entries > 0) {
-        if (p->sform) {
-            if (p->sform_dd) k_factor_s<true><<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-            else k_factor_s<false><<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-        } else {
-            k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(dp);
-            k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
-        }
+    if (p->sform) {
+        if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+    } else {
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
     }
     mark();
-    if (p->sform) k_base_s<<<1, 256, 0, st>>>(dp);
-    else k_base<<<1, 256, 0, st>>>(dp);
-    mark();
+    mark();   // K0 base: merged into the factor launch
     // root pass
     RootArgs R;
     memset(&R, 0, sizeof R);
@@ -670,10 +670,11 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         mark();
     }
     {
-        const long long nl1 = (hp.total_partials + RED_CHUNK - 1) / RED_CHUNK;
+        const long long nl1 = std::max<long long>(1, (hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2);
         double2 *l1 = (double2 *)(p->ws + p->ws_red_off);
-        k_reduce_l1<<<(unsigned)nl1, 256, 0, st>>>(partials, hp.total_partials, l1);
-        k_reduce<<<1, 1024, 0, st>>>(dp, l1, nl1, hp.include_root ? 1 : 0, out_dev);
+        k_reduce_fused<<<(unsigned)nl1, RED_THREADS, 0, st>>>(dp, partials, hp.total_partials,
+                                                               hp.include_root ? 1 : 0, out_dev, l1,
+                                                               p->d_counter + 1);
     }
     mark();
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
@@ -924,8 +925,8 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
     if (rc) return rc;
     // the factor table and base of the current parameters (K0), then one thread per index
     if (cudaMemsetAsync(p->dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
-    if (hp.tab_entries > 0) k_factor<<<(hp.tab_entries + 127) / 128, 128, 0, st>>>(p->dp);
-    k_base<<<1, 256, 0, st>>>(p->dp);
+    const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);
+    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb);
     if (n > 0)
         k_eval_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p->dp, p->utabs, index_dev, n, points_dev,
                                                                    terms_dev);

@@ -32,6 +32,21 @@ def time_plan(plan, flush, reps=5):
     return best
 
 
+def phases(plan, flush, reps=5):
+    """Per-launch device ms (sg_profile_read) of the best of `reps` runs, plus the step time."""
+    plan.profile_enable(True)
+    best = None
+    for _ in range(reps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        plan.sg_integrate()
+        ms = plan.profile_read()
+        if best is None or sum(ms) < sum(best):
+            best = ms
+    plan.profile_enable(False)
+    return best
+
+
 def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     worlds = [int(a) for a in sys.argv[2:]] or [2, 4, 8]
@@ -39,6 +54,8 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     whole = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
     t1 = time_plan(whole, flush)
+    if os.environ.get("SHARD_PHASES"):
+        print(f"  world=1 launches ms: {[round(x, 4) for x in phases(whole, flush)]}")
     whole.close()
     print(f"{p.name} world=1 {t1:.4f} ms")
     for world in worlds:
@@ -49,6 +66,11 @@ def main():
             pts.append(sp.points()[0])
             sp.close()
         mx = max(ts)
+        if os.environ.get("SHARD_PHASES"):
+            r = ts.index(mx)
+            sp = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=r, world=world)
+            print(f"  rank {r} launches ms: {[round(x, 4) for x in phases(sp, flush)]}")
+            sp.close()
         print(f"{p.name} world={world} max={mx:.4f} ms mean={sum(ts) / world:.4f} "
               f"time_imbalance={mx / (sum(ts) / world):.4f} point_imbalance="
               f"{max(pts) / (sum(pts) / world):.4f} projected_eff={t1 / (world * mx):.4f} "
