@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
 // factor table at warp-uniform addresses (one broadcast transaction per load).
 // ---------------------------------------------------------------------------------------------
 #ifndef LEAF_ROW_UNROLL
-#define LEAF_ROW_UNROLL 1   // row-loop unrolling in the generic k_leaf (A/B knob)
+#define LEAF_ROW_UNROLL 2   // row-loop unrolling in k_leaf (A/B: c5 pass 2 0.629 -> 0.602 ms with NJ = 5)
 #endif
 constexpr int kRowUnroll = LEAF_ROW_UNROLL;
 #ifndef LEAF_SYM_FOLD
@@ -504,9 +504,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
             else switch (n) {
             case 2: s = leaf_level<CPLX, 2>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             case 3: s = leaf_level<CPLX, 3>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
-#ifdef LEAF_NJ5
             case 5: s = leaf_level<CPLX, 5>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
-#endif
             default: s = leaf_level<CPLX, 0>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             }
             if (lv) tot = dd_add(tot, coef_mul(P, s, A.t + 1, b + lp - 1));
