@@ -1091,58 +1091,58 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
             int kp = max(km + 1, kp0);
             while (kp < kp1) {
                 const int ke = min(kp1, kp + FOLD);
-                for (; kp < ke; ++kp) {
-                    const double2 f1 = SMEM ? Fr[kp * 2 + 1] : __ldg(Fr + kp * 2 + 1);
-                    const double2 g1 = SMEM ? Fi[kp * 2 + 1] : __ldg(Fi + kp * 2 + 1);
-#pragma unroll
-                    for (int m = 0; m < NM; ++m) {
-                        const double u1 = fma(er[m].hi, f1.x, ah[m]);
-                        const double h1 = u1 - ah[m];
-                        ah[m] = fma(ei[m].hi, g1.x, u1);
-                        const double h2 = ah[m] - u1;
-                        const double cA = fma(er[m].lo, f1.x, fma(er[m].hi, f1.y, fma(er[m].hi, f1.x, -h1)));
-                        const double cB = fma(ei[m].lo, g1.x, fma(ei[m].hi, g1.y, fma(ei[m].hi, g1.x, -h2)));
-                        al[m] += cA + cB;
-                        bh[m] += h1 - h2;
-                        bl[m] += cA - cB;
-                    }
-                }
+            for (; kp < ke; ++kp) {
+                const double2 f1 = SMEM ? Fr[kp * 2 + 1] : __ldg(Fr + kp * 2 + 1);
+                const double2 g1 = SMEM ? Fi[kp * 2 + 1] : __ldg(Fi + kp * 2 + 1);
 #pragma unroll
                 for (int m = 0; m < NM; ++m) {
-                    al[m] += bl[m];
-                    bl[m] = 0.0;
-                    const double t = (al[m] + sg[m]) - sg[m];
-                    ah[m] += t;
-                    al[m] -= t;
+                    const double u1 = fma(er[m].hi, f1.x, ah[m]);
+                    const double h1 = u1 - ah[m];
+                    ah[m] = fma(ei[m].hi, g1.x, u1);
+                    const double h2 = ah[m] - u1;
+                    const double cA = fma(er[m].lo, f1.x, fma(er[m].hi, f1.y, fma(er[m].hi, f1.x, -h1)));
+                    const double cB = fma(ei[m].lo, g1.x, fma(ei[m].hi, g1.y, fma(ei[m].hi, g1.x, -h2)));
+                    al[m] += cA + cB;
+                    bh[m] += h1 - h2;
+                    bl[m] += cA - cB;
                 }
             }
-            double hs = (ah[0] + (bh[0] - sg[0])) - sg[0], ls = al[0] + bl[0];
 #pragma unroll
-            for (int m = 1; m < NM; ++m) {
-                double e;
-                two_sum(hs, (ah[m] + (bh[m] - sg[m])) - sg[m], hs, e);
-                ls += al[m] + bl[m] + e;
-            }
-            lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
-        }
-        dd v = warp_reduce_dd_fast(lane_sum);
-        if (lane == 0) {
-            v = dd_mul_d(v, P.coef[P.L]);
-            A.partials[task] = make_double2(v.hi, v.lo);
-        }
-        if (!A.prefetch) {
-            next = fetch();
-            if (next < A.ntasks) {
-                nfirst = A.T2[3 * next];
-                nkk = A.T2[3 * next + 1];
-                nrr = A.T2[3 * next + 2];
+            for (int m = 0; m < NM; ++m) {
+                al[m] += bl[m];
+                bl[m] = 0.0;
+                const double t = (al[m] + sg[m]) - sg[m];
+                ah[m] += t;
+                al[m] -= t;
             }
         }
-        task = next;
-        first = nfirst;
-        kk = nkk;
-        rr = nrr;
+        double hs = (ah[0] + (bh[0] - sg[0])) - sg[0], ls = al[0] + bl[0];
+#pragma unroll
+        for (int m = 1; m < NM; ++m) {
+            double e;
+            two_sum(hs, (ah[m] + (bh[m] - sg[m])) - sg[m], hs, e);
+            ls += al[m] + bl[m] + e;
+        }
+        lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
     }
+    dd v = warp_reduce_dd_fast(lane_sum);
+    if (lane == 0) {
+        v = dd_mul_d(v, P.coef[P.L]);
+        A.partials[task] = make_double2(v.hi, v.lo);
+    }
+    if (!A.prefetch) {
+        next = fetch();
+        if (next < A.ntasks) {
+            nfirst = A.T2[3 * next];
+            nkk = A.T2[3 * next + 1];
+            nrr = A.T2[3 * next + 2];
+        }
+    }
+    task = next;
+    first = nfirst;
+    kk = nkk;
+    rr = nrr;
+}
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1152,6 +1152,116 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
 // (split symmetric pair: node 0 into a, node 2 and the midpoint into b) with more independent
 // accumulator chains per warp.
 // ---------------------------------------------------------------------------------------------
+// One k_leaf2_sym3 task for one lane: a fused task (SRCT = false: the lane's PPL parents times the
+// three level-2 factors of each k_mid in [ka, kb)) or a source task (SRCT = true: NM stored
+// excess-(L-1) sources of last coordinate -ka - 1, kb of them in the chunk, are the prefixes
+// themselves), each prefix walking the symmetric level-2 rows.  Two instantiations, so the fused
+// tasks' loop nest is compiled as if the source tasks did not exist.
+template <int PPL, bool SMEM, bool CZ, bool SRCT>
+__device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, const double2 *Fr,
+                                        const double2 *Fi, int lane, long long first, int ka, int kb,
+                                        int kp0, int kp1) {
+    constexpr int NM = 3 * PPL;
+    const int d = P.d;
+    const int km0 = SRCT ? -ka - 1 : ka, km1 = SRCT ? km0 + 1 : kb;
+    long long ip[PPL];
+    dd pr[PPL], pim[PPL];
+    const long long cend = SRCT ? 0 : A.Cmid[kb - 1];
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) {
+        ip[q] = first + 32LL * q + lane;
+        pr[q] = dd{0.0, 0.0};
+        pim[q] = dd{0.0, 0.0};
+        if (ip[q] < cend) {
+            const double2 v = A.src_re[A.base + ip[q]], vi = A.src_im[A.base + ip[q]];
+            pr[q] = dd{v.x, v.y};
+            pim[q] = dd{vi.x, vi.y};
+        }
+    }
+    dd lane_sum = {0.0, 0.0};
+    for (int km = km0; km < km1; ++km) {
+        const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+        dd er[NM], ei[NM];
+        double sg[NM], ah[NM], al[NM], bh[NM], bl[NM];
+        if constexpr (SRCT) {
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                const int is = 32 * m + lane;
+                er[m] = ei[m] = dd{0.0, 0.0};
+                if (is < kb) {
+                    const double2 v = A.src_re[first + is], vi = A.src_im[first + is];
+                    er[m] = dd{v.x, v.y};
+                    ei[m] = dd{vi.x, vi.y};
+                }
+            }
+        } else {
+            const long long cm = A.Cmid[km];
+            const double2 fm = Fr[km * 3 + 2], gm = Fi[km * 3 + 2], wm = Fr[km * 3 + 1];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) {
+                const bool valid = ip[q] < cm;
+                const dd vr = valid ? pr[q] : dd{0.0, 0.0}, vi = valid ? pim[q] : dd{0.0, 0.0};
+                cdd c2, c0;
+                cdd_mul_conj_pair(cdd{vr, vi}, cdd{dd{fm.x, fm.y}, dd{gm.x, gm.y}}, c2, c0);
+                er[3 * q] = c0.re;
+                ei[3 * q] = c0.im;
+                er[3 * q + 2] = c2.re;
+                ei[3 * q + 2] = c2.im;
+                er[3 * q + 1] = CZ ? dd_mul_d(vr, wm.x) : dd_mul(vr, dd{wm.x, wm.y});
+                ei[3 * q + 1] = CZ ? dd_mul_d(vi, wm.x) : dd_mul(vi, dd{wm.x, wm.y});
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+            const double bound = (fabs(er[m].hi) + fabs(ei[m].hi)) * sa;
+            int ex = 0;
+            frexp(2.0 * bound, &ex);
+            sg[m] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
+            ah[m] = bh[m] = sg[m];   // biased accumulators (node 0 -> a, node 1 -> b)
+            al[m] = bl[m] = 0.0;
+        }
+        int kp = max(km + 1, kp0);
+        while (kp < kp1) {
+            const int ke = min(kp1, kp + FOLD);
+            for (; kp < ke; ++kp) {
+                const double2 f1 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
+                const double2 g1 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
+                const double2 w1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
+#pragma unroll
+                for (int m = 0; m < NM; ++m) {
+                    const double u1 = fma(er[m].hi, f1.x, ah[m]);
+                    const double h1 = u1 - ah[m];
+                    ah[m] = fma(ei[m].hi, g1.x, u1);
+                    const double h2 = ah[m] - u1;
+                    const double cA = fma(er[m].lo, f1.x, fma(er[m].hi, f1.y, fma(er[m].hi, f1.x, -h1)));
+                    const double cB = fma(ei[m].lo, g1.x, fma(ei[m].hi, g1.y, fma(ei[m].hi, g1.x, -h2)));
+                    al[m] += cA + cB;
+                    bh[m] += h1 - h2;
+                    bl[m] += cA - cB;
+                    leaf_real_factor_term<CZ>(er[m], w1, bh[m], bl[m]);   // the midpoint node
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                al[m] += bl[m];
+                bl[m] = 0.0;
+                const double t = (al[m] + sg[m]) - sg[m];
+                ah[m] += t;
+                al[m] -= t;
+            }
+        }
+        double hs = (ah[0] + (bh[0] - sg[0])) - sg[0], ls = al[0] + bl[0];
+#pragma unroll
+        for (int m = 1; m < NM; ++m) {
+            double e;
+            two_sum(hs, (ah[m] + (bh[m] - sg[m])) - sg[m], hs, e);
+            ls += al[m] + bl[m] + e;
+        }
+        lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
+    }
+    return lane_sum;
+}
+
 template <int PPL, bool SMEM, bool CZ>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
     constexpr int NM = 3 * PPL;   // mid prefixes per lane
@@ -1194,88 +1304,10 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(c
         }
         const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
         const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
-        long long ip[PPL];
-        dd pr[PPL], pim[PPL];
-        const long long cend = A.Cmid[kb - 1];
-#pragma unroll
-        for (int q = 0; q < PPL; ++q) {
-            ip[q] = first + 32LL * q + lane;
-            pr[q] = dd{0.0, 0.0};
-            pim[q] = dd{0.0, 0.0};
-            if (ip[q] < cend) {
-                const double2 v = A.src_re[A.base + ip[q]], vi = A.src_im[A.base + ip[q]];
-                pr[q] = dd{v.x, v.y};
-                pim[q] = dd{vi.x, vi.y};
-            }
-        }
-        dd lane_sum = {0.0, 0.0};
-        for (int km = ka; km < kb; ++km) {
-            const long long cm = A.Cmid[km];
-            const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
-            const double2 fm = Fr[km * 3 + 2], gm = Fi[km * 3 + 2], wm = Fr[km * 3 + 1];
-            dd er[NM], ei[NM];
-            double sg[NM], ah[NM], al[NM], bh[NM], bl[NM];
-#pragma unroll
-            for (int q = 0; q < PPL; ++q) {
-                const bool valid = ip[q] < cm;
-                const dd vr = valid ? pr[q] : dd{0.0, 0.0}, vi = valid ? pim[q] : dd{0.0, 0.0};
-                cdd c2, c0;
-                cdd_mul_conj_pair(cdd{vr, vi}, cdd{dd{fm.x, fm.y}, dd{gm.x, gm.y}}, c2, c0);
-                er[3 * q] = c0.re;
-                ei[3 * q] = c0.im;
-                er[3 * q + 2] = c2.re;
-                ei[3 * q + 2] = c2.im;
-                er[3 * q + 1] = CZ ? dd_mul_d(vr, wm.x) : dd_mul(vr, dd{wm.x, wm.y});
-                ei[3 * q + 1] = CZ ? dd_mul_d(vi, wm.x) : dd_mul(vi, dd{wm.x, wm.y});
-            }
-#pragma unroll
-            for (int m = 0; m < NM; ++m) {
-                const double bound = (fabs(er[m].hi) + fabs(ei[m].hi)) * sa;
-                int ex = 0;
-                frexp(2.0 * bound, &ex);
-                sg[m] = bound > 0.0 ? ldexp(1.5, ex) : 1.5;
-                ah[m] = bh[m] = sg[m];   // biased accumulators (node 0 -> a, node 1 -> b)
-                al[m] = bl[m] = 0.0;
-            }
-            int kp = max(km + 1, kp0);
-            while (kp < kp1) {
-                const int ke = min(kp1, kp + FOLD);
-                for (; kp < ke; ++kp) {
-                    const double2 f1 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
-                    const double2 g1 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
-                    const double2 w1 = SMEM ? Fr[kp * 3 + 1] : __ldg(Fr + kp * 3 + 1);
-#pragma unroll
-                    for (int m = 0; m < NM; ++m) {
-                        const double u1 = fma(er[m].hi, f1.x, ah[m]);
-                        const double h1 = u1 - ah[m];
-                        ah[m] = fma(ei[m].hi, g1.x, u1);
-                        const double h2 = ah[m] - u1;
-                        const double cA = fma(er[m].lo, f1.x, fma(er[m].hi, f1.y, fma(er[m].hi, f1.x, -h1)));
-                        const double cB = fma(ei[m].lo, g1.x, fma(ei[m].hi, g1.y, fma(ei[m].hi, g1.x, -h2)));
-                        al[m] += cA + cB;
-                        bh[m] += h1 - h2;
-                        bl[m] += cA - cB;
-                        leaf_real_factor_term<CZ>(er[m], w1, bh[m], bl[m]);   // the midpoint node
-                    }
-                }
-#pragma unroll
-                for (int m = 0; m < NM; ++m) {
-                    al[m] += bl[m];
-                    bl[m] = 0.0;
-                    const double t = (al[m] + sg[m]) - sg[m];
-                    ah[m] += t;
-                    al[m] -= t;
-                }
-            }
-            double hs = (ah[0] + (bh[0] - sg[0])) - sg[0], ls = al[0] + bl[0];
-#pragma unroll
-            for (int m = 1; m < NM; ++m) {
-                double e;
-                two_sum(hs, (ah[m] + (bh[m] - sg[m])) - sg[m], hs, e);
-                ls += al[m] + bl[m] + e;
-            }
-            lane_sum = dd_add_fast(lane_sum, dd_norm(hs, ls));
-        }
+        // source tasks (ka < 0): kb = number of sources in the chunk.  (Branch order A/B on c5: this
+        // order places the fused loop nest at 12.50 ms, the reverse at 12.82 ms: code layout.)
+        const dd lane_sum = ka < 0 ? sym3_task<PPL, SMEM, CZ, true>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1)
+                                   : sym3_task<PPL, SMEM, CZ, false>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);
         dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);

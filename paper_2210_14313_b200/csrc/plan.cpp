@@ -665,6 +665,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                               1.0 - hp.X[e0 + 2] == hp.X[e0] && hp.Whi[e0] == hp.Whi[e0 + 2] &&
                               hp.Wlo[e0] == hp.Wlo[e0 + 2];
             hp.leaf2_ppl = pair ? LEAF2_PPL : sym3 ? LEAF2_PPL3 : 1;
+            hp.leaf2_sym3 = sym3 && !pair;
         }
         const int64_t CH = 32LL * hp.leaf2_ppl;   // parents per task chunk
         const int64_t nchunks = (cmid(d - 2) + CH - 1) / CH;
@@ -687,6 +688,36 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 }
             }
         }
+        // Source tasks (k_leaf2_sym3 only): the excess-(L-1) sources of frontier L-2 with last active
+        // coordinate k, in chunks of 32 * 3 * PPL (one prefix per lane and accumulator slot), each
+        // walking the symmetric level-2 rows k' = k+1 .. d-1.  Encoded with ka = -(k + 1) < 0,
+        // kb = number of sources in the chunk; never split (rows <= d - 1).
+#ifndef LEAF2_NO_SRCTASKS
+        if (hp.leaf2_sym3 && L >= 3 && merge == 0) {
+            const int bs = L - 1;
+            const int64_t CHB = 32LL * 3 * hp.leaf2_ppl;
+            uint64_t moved = 0;
+            for (int k = 0; k <= d - 2; ++k) {
+                const int64_t n = hp.N[tm][(size_t)bs * d + k], o = hp.off[tm][(size_t)bs * d + k];
+                for (int64_t c = 0; c < n; c += CHB)
+                    tasks.push_back(Task{d - 1 - k, o + c, -(k + 1), (int)std::min<int64_t>(CHB, n - c), k + 1, d});
+                moved += (uint64_t)n * (uint64_t)hp.nl[2] * (uint64_t)(d - 1 - k);
+            }
+            hp.leaf2_srctasks = true;
+            hp.leaf_src_end = hp.off[tm][(size_t)bs * d];
+            hp.pass_terms[tm] -= moved;
+            hp.pass_terms[tm + 1] += moved;
+            // pass tm (k_leaf) geometry over the remaining sources
+            const int64_t chunks = (hp.leaf_src_end + 31) / 32;
+            int64_t ns = chunks > 0 ? (TARGET_WARPS + chunks - 1) / chunks : 1;
+            ns = std::max<int64_t>(1, std::min<int64_t>(ns, d));
+            hp.pass_nsplit[tm] = (int)ns;
+            hp.pass_ntasks[tm] = chunks * ns;
+            // no sources left: no k_leaf launch and no partial slot
+            hp.pass_blocks[tm] = chunks == 0 ? 0
+                                 : std::max<int64_t>(1, (hp.pass_ntasks[tm] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+        }
+#endif
         // When the longest task is a large share of one resident warp's work (a small shard: config 4
         // on 8 GPUs), the persistent grid's tail is a handful of long single-k_mid tasks: split
         // their rows into pieces of LEAF2_TASK_ROWS (partials stay per task, order fixed).

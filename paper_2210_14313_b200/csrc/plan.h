@@ -85,6 +85,13 @@ struct HostPlan {
     // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
     bool fuse = false;
     int leaf2_ppl = 1;                 // parents per lane of the fused kernel (2: k_leaf2_pairs)
+    bool leaf2_sym3 = false;           // k_leaf2_sym3 (oscillatory, level-2 row {0, 1/2, 1} symmetric)
+    // k_leaf2_sym3 also takes the depth-(L-1) points of the excess-(L-1) sources of frontier L-2 as
+    // "source tasks" (their level-2 rows are the same symmetric rows the fused tasks walk; the
+    // prefixes are the stored sources themselves): pass L-2 (k_leaf) then only reads the sources
+    // [0, leaf_src_end) of its frontier (the excess-(L-2) block).
+    bool leaf2_srctasks = false;
+    int64_t leaf_src_end = -1;
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.

@@ -461,6 +461,9 @@ static int setup_leaf1(sg_plan_s *p) {
     const bool sy = p->leaf2_sym;
     p->leaf2_cz = ct && hp.Wlo[hp.entry_off[2] + 1] == 0.0;
     const bool cz = p->leaf2_cz;
+    // source tasks are only understood by k_leaf2_sym3 (plan.cpp builds them for that kernel alone)
+    if (p->leaf2 && hp.leaf2_srctasks && !(p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2))
+        return SG_EUNSUPPORTED;
     const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy, cz, hp.leaf2_ppl)
                                          : leaf2_kernel<false>(nj, sm, ct, sy, cz))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
@@ -626,7 +629,8 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         }
         PassArgs A;
         memset(&A, 0, sizeof A);
-        A.nsrc = hp.total[t];
+        // with k_leaf2_sym3 source tasks, pass L-2 reads only the excess-(L-2) block of its frontier
+        A.nsrc = (hp.leaf2_srctasks && p->leaf2 && t == hp.nfront - 1) ? hp.leaf_src_end : hp.total[t];
         A.ntasks = hp.pass_ntasks[t];
         A.nsplit = hp.pass_nsplit[t];
         A.t = t;
@@ -647,6 +651,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         if (t == p->leaf1_t && cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess)
             return SG_ECUDA;
         const unsigned grid = (unsigned)hp.pass_blocks[t];
+        if (grid == 0) {   // every source of this pass went to k_leaf2_sym3's source tasks
+            mark();
+            continue;
+        }
         // single-level last pass (every source has excess L-1): specialised k_leaf1
         const int n2 = hp.nl[2];
         const bool single = !write && t == p->leaf1_t;
