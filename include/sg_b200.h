@@ -198,14 +198,16 @@ int sg_plan_points(sg_plan_t p, unsigned long long *shard_points,
 int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long long *n_depth1);
 
 /* Per-pass launch statistics of the last plan: number of passes, and for pass i the number of
- * tree nodes (leaf terms) it evaluates and the frontier nodes it writes.  Arrays of length >=
+ * tree nodes (leaf terms) it evaluates and the frontier nodes it writes (the depth-(L-1) points that
+ * k_leaf2_sym3's source tasks evaluate are counted in the last pass, whose kernel runs them).  Arrays of length >=
  * *npass (query with NULL arrays first). */
 int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
                    unsigned long long *written);
 
 /* Host-only measurement helper: the FP64 instructions per Smolyak point of the leaf kernel variant
  * this plan runs for its dominant (last) pass — DFMA and DADD thread-instructions per point,
- * averaged over one level-2 row (midpoint, symmetric-pair and zero-tail specialisations included).
+ * averaged over one level-2 row (midpoint, symmetric-pair and zero-tail specialisations included)
+ * and, for k_leaf2_sym3, weighted with its level-3 source-task points (general oscillatory terms).
  * Used by bench.py to turn the measured kernel time into achieved FLOP/s (DFMA = 2 flops).
  * Both pointers must be non-NULL (else SG_EINVAL). */
 int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_point);

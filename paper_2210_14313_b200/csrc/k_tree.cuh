@@ -1152,15 +1152,17 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
 // (split symmetric pair: node 0 into a, node 2 and the midpoint into b) with more independent
 // accumulator chains per warp.
 // ---------------------------------------------------------------------------------------------
-// One k_leaf2_sym3 task for one lane: a fused task (SRCT = false: the lane's PPL parents times the
-// three level-2 factors of each k_mid in [ka, kb)) or a source task (SRCT = true: NM stored
-// excess-(L-1) sources of last coordinate -ka - 1, kb of them in the chunk, are the prefixes
-// themselves), each prefix walking the symmetric level-2 rows.  Two instantiations, so the fused
-// tasks' loop nest is compiled as if the source tasks did not exist.
-template <int PPL, bool SMEM, bool CZ, bool SRCT>
+// One k_leaf2_sym3 task for one lane.  MODE 0: a fused task (the lane's PPL parents times the three
+// level-2 factors of each k_mid in [ka, kb), each prefix walking the symmetric level-2 rows).
+// MODE 1 / 2: a source task: NM stored sources of frontier L-2 with last coordinate -ka - 1 (kb of
+// them in the chunk) are the prefixes themselves; MODE 1 walks their symmetric level-2 rows, MODE 2
+// their level-3 rows (SYM3_N3 nodes, general complex leaf terms).  One instantiation per mode, so the
+// fused tasks' loop nest is compiled as if the source tasks did not exist.
+template <int PPL, bool SMEM, bool CZ, int MODE>
 __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, const double2 *Fr,
                                         const double2 *Fi, int lane, long long first, int ka, int kb,
                                         int kp0, int kp1) {
+    constexpr bool SRCT = MODE != 0;
     constexpr int NM = 3 * PPL;
     const int d = P.d;
     const int km0 = SRCT ? -ka - 1 : ka, km1 = SRCT ? km0 + 1 : kb;
@@ -1180,7 +1182,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
     }
     dd lane_sum = {0.0, 0.0};
     for (int km = km0; km < km1; ++km) {
-        const double sa = P.SA[2LL * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+        const double sa = P.SA[(MODE == 2 ? 3LL : 2LL) * (d + 1) + km + 1] * (1.0 + 0x1p-20);
         dd er[NM], ei[NM];
         double sg[NM], ah[NM], al[NM], bh[NM], bl[NM];
         if constexpr (SRCT) {
@@ -1223,6 +1225,23 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
         int kp = max(km + 1, kp0);
         while (kp < kp1) {
             const int ke = min(kp1, kp + FOLD);
+            if constexpr (MODE == 2) {
+                const double2 *F3r = P.Fre + P.tab_off[3], *F3i = P.Fim + P.tab_off[3];
+                for (; kp < ke; ++kp) {
+#pragma unroll
+                    for (int j = 0; j < SYM3_N3; ++j) {
+                        const double2 f = __ldg(F3r + kp * SYM3_N3 + j), g = __ldg(F3i + kp * SYM3_N3 + j);
+#pragma unroll
+                        for (int m = 0; m < NM; ++m) {
+                            LeafAcc a = {ah[m], al[m]};
+                            leaf_term<true>(er[m], ei[m], f, g, a);
+                            ah[m] = a.h;
+                            al[m] = a.l;
+                        }
+                    }
+                }
+            }
+            if constexpr (MODE != 2) {
             for (; kp < ke; ++kp) {
                 const double2 f1 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
                 const double2 g1 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
@@ -1240,6 +1259,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
                     bl[m] += cA - cB;
                     leaf_real_factor_term<CZ>(er[m], w1, bh[m], bl[m]);   // the midpoint node
                 }
+            }
             }
 #pragma unroll
             for (int m = 0; m < NM; ++m) {
@@ -1304,13 +1324,16 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(c
         }
         const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
         const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
-        // source tasks (ka < 0): kb = number of sources in the chunk.  (Branch order A/B on c5: this
-        // order places the fused loop nest at 12.50 ms, the reverse at 12.82 ms: code layout.)
-        const dd lane_sum = ka < 0 ? sym3_task<PPL, SMEM, CZ, true>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1)
-                                   : sym3_task<PPL, SMEM, CZ, false>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);
+        // source tasks (ka < 0): kb = chunk size | SRC_L3 | SRC_CPREV.  (Branch order A/B on c5: the
+        // fused loop nest 12.50 ms with the source branches first, 12.82 ms the other way: layout.)
+        const int cnt = kb & 0xffff;
+        const dd lane_sum =
+            ka < 0 ? ((kb & SRC_L3) ? sym3_task<PPL, SMEM, CZ, 2>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1)
+                                    : sym3_task<PPL, SMEM, CZ, 1>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1))
+                   : sym3_task<PPL, SMEM, CZ, 0>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);
         dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
-            v = dd_mul_d(v, P.coef[P.L]);
+            v = dd_mul_d(v, P.coef[ka < 0 && (kb & SRC_CPREV) ? P.L - 1 : P.L]);
             A.partials[task] = make_double2(v.hi, v.lo);
         }
         if (!A.prefetch) {

@@ -86,12 +86,17 @@ struct HostPlan {
     bool fuse = false;
     int leaf2_ppl = 1;                 // parents per lane of the fused kernel (2: k_leaf2_pairs)
     bool leaf2_sym3 = false;           // k_leaf2_sym3 (oscillatory, level-2 row {0, 1/2, 1} symmetric)
-    // k_leaf2_sym3 also takes the depth-(L-1) points of the excess-(L-1) sources of frontier L-2 as
-    // "source tasks" (their level-2 rows are the same symmetric rows the fused tasks walk; the
-    // prefixes are the stored sources themselves): pass L-2 (k_leaf) then only reads the sources
-    // [0, leaf_src_end) of its frontier (the excess-(L-2) block).
+    // k_leaf2_sym3 also takes the depth-(L-1) points of frontier L-2's sources as "source tasks"
+    // (the prefixes are the stored sources themselves): the excess-(L-1) sources' level-2 rows (the
+    // same symmetric rows the fused tasks walk) and, when level 3 has SYM3_N3 nodes, the
+    // excess-(L-2) sources' level-2 rows (coefficient coef[L-1]) and level-3 rows.  Pass L-2
+    // (k_leaf) then reads only the sources [0, leaf_src_end) of its frontier (none: no launch).
     bool leaf2_srctasks = false;
+#define SRC_L3 (1 << 16)      // source task flag: walk the level-3 rows (SYM3_N3 nodes)
+#define SRC_CPREV (1 << 17)   // source task flag: children have excess L-1 (coefficient coef[L-1])
+#define SYM3_N3 5             // level-3 row length of the level-3 source tasks
     int64_t leaf_src_end = -1;
+    uint64_t leaf2_l3_points = 0;      // points of the level-3 source tasks (general complex terms)
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.

@@ -777,6 +777,12 @@ extern "C" int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *da
             a = (2.0 * a + ca) / 3.0;
         }
     }
+    if (p->leaf2 && p->hp.leaf2_l3_points > 0 && p->hp.pass_terms[p->hp.nfront] > 0) {
+        // k_leaf2_sym3's level-3 source tasks: general oscillatory terms (8 DFMA + 4 DADD)
+        const double w = (double)p->hp.leaf2_l3_points / (double)p->hp.pass_terms[p->hp.nfront];
+        f = (1.0 - w) * f + w * 8.0;
+        a = (1.0 - w) * a + w * 4.0;
+    }
     *dfma_per_point = f;
     *dadd_per_point = a;
     return SG_OK;
