@@ -1282,7 +1282,10 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
     return lane_sum;
 }
 
-template <int PPL, bool SMEM, bool CZ>
+// SRC = false: the fused tasks (pass L-1); SRC = true: the source tasks (pass L-2, its own task list
+// T2 and partial slots), a separate kernel so the fused loop nest's code is not disturbed (measured:
+// sharing one kernel slowed the fused tasks by 1.6-4% through code layout alone).
+template <int PPL, bool SMEM, bool CZ, bool SRC>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
     constexpr int NM = 3 * PPL;   // mid prefixes per lane
     extern __shared__ double2 fsm[];
@@ -1324,16 +1327,18 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(c
         }
         const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
         const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
-        // source tasks (ka < 0): kb = chunk size | SRC_L3 | SRC_CPREV.  (Branch order A/B on c5: the
-        // fused loop nest 12.50 ms with the source branches first, 12.82 ms the other way: layout.)
-        const int cnt = kb & 0xffff;
-        const dd lane_sum =
-            ka < 0 ? ((kb & SRC_L3) ? sym3_task<PPL, SMEM, CZ, 2>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1)
-                                    : sym3_task<PPL, SMEM, CZ, 1>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1))
-                   : sym3_task<PPL, SMEM, CZ, 0>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);
+        // source tasks: ka = -(k + 1), kb = chunk size | SRC_L3 | SRC_CPREV
+        dd lane_sum;
+        if constexpr (SRC) {
+            const int cnt = kb & 0xffff;
+            lane_sum = (kb & SRC_L3) ? sym3_task<PPL, SMEM, CZ, 2>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1)
+                                     : sym3_task<PPL, SMEM, CZ, 1>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1);
+        } else {
+            lane_sum = sym3_task<PPL, SMEM, CZ, 0>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);
+        }
         dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
-            v = dd_mul_d(v, P.coef[ka < 0 && (kb & SRC_CPREV) ? P.L - 1 : P.L]);
+            v = dd_mul_d(v, P.coef[SRC && (kb & SRC_CPREV) ? P.L - 1 : P.L]);
             A.partials[task] = make_double2(v.hi, v.lo);
         }
         if (!A.prefetch) {

@@ -688,53 +688,53 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 }
             }
         }
-        // Source tasks (k_leaf2_sym3 only): the excess-(L-1) sources of frontier L-2 with last active
-        // coordinate k, in chunks of 32 * 3 * PPL (one prefix per lane and accumulator slot), each
-        // walking the symmetric level-2 rows k' = k+1 .. d-1.  Encoded with ka = -(k + 1) < 0,
-        // kb = number of sources in the chunk; never split (rows <= d - 1).
+        // Source tasks (k_leaf2_sym3 plans whose level 3 has SYM3_N3 nodes): pass L-2 runs
+        // k_leaf2_sym3<SRC = true> over every source of frontier L-2 instead of k_leaf.  A task is a
+        // chunk of 32 * 3 * PPL sources with the same last active coordinate k (one prefix per lane
+        // and accumulator slot): the excess-(L-1) sources' symmetric level-2 rows k' = k+1 .. d-1,
+        // the excess-(L-2) sources' level-2 rows (coefficient coef[L-1], SRC_CPREV) and their
+        // level-3 rows (SRC_L3).  Encoded with ka = -(k + 1), kb = chunk size | flags; heavy-first,
+        // never split (rows <= d - 1); one partial slot per task.
+        std::vector<Task> srct;
 #ifndef LEAF2_NO_SRCTASKS
-        if (hp.leaf2_sym3 && L >= 3 && merge == 0) {
-            const int bs = L - 1;
+        if (hp.leaf2_sym3 && L >= 3 && merge == 0 && hp.nl[3] == SYM3_N3) {
             const int64_t CHB = 32LL * 3 * hp.leaf2_ppl;
-            uint64_t moved = 0;
-            for (int k = 0; k <= d - 2; ++k) {
-                const int64_t n = hp.N[tm][(size_t)bs * d + k], o = hp.off[tm][(size_t)bs * d + k];
-                for (int64_t c = 0; c < n; c += CHB)
-                    tasks.push_back(Task{d - 1 - k, o + c, -(k + 1), (int)std::min<int64_t>(CHB, n - c), k + 1, d});
-                moved += (uint64_t)n * (uint64_t)hp.nl[2] * (uint64_t)(d - 1 - k);
-            }
-            hp.leaf2_srctasks = true;
-            hp.leaf_src_end = hp.off[tm][(size_t)bs * d];
-            // the excess-(L-2) sources (the fused tasks' parents) too: their level-2 children
-            // (coefficient coef[L-1]) and level-3 children (coef[L]) as source tasks, so pass L-2 has
-            // nothing left to read (c5: 12.92 -> 12.86 ms, one launch fewer)
-#ifndef LEAF2_NO_SRC_EXCESS2
-            if (hp.nl[3] == SYM3_N3) {
-                const int b2 = L - 2;
+            for (int b = L - 2; b <= L - 1; ++b)
                 for (int k = 0; k <= d - 2; ++k) {
-                    const int64_t n = hp.N[tm][(size_t)b2 * d + k], o = hp.off[tm][(size_t)b2 * d + k];
-                    for (int64_t c = 0; c < n; c += CHB) {
-                        const int cnt = (int)std::min<int64_t>(CHB, n - c);
-                        tasks.push_back(Task{d - 1 - k, o + c, -(k + 1), cnt | SRC_CPREV, k + 1, d});
-                        tasks.push_back(Task{3LL * (d - 1 - k), o + c, -(k + 1), cnt | SRC_L3, k + 1, d});
-                    }
-                    moved += (uint64_t)n * (uint64_t)(hp.nl[2] + hp.nl[3]) * (uint64_t)(d - 1 - k);
-                    hp.leaf2_l3_points += (uint64_t)n * (uint64_t)hp.nl[3] * (uint64_t)(d - 1 - k);
+                    const int64_t n = hp.N[tm][(size_t)b * d + k], o = hp.off[tm][(size_t)b * d + k];
+                    // rows k+1 .. d-1 in pieces of at most LEAF2_SRC_ROWS (the persistent grid's tail)
+                    const int rows = d - 1 - k;
+                    const int pieces = LEAF2_SRC_ROWS > 0 ? (rows + LEAF2_SRC_ROWS - 1) / LEAF2_SRC_ROWS : 1;
+                    for (int64_t c = 0; c < n; c += CHB)
+                        for (int q = 0; q < pieces; ++q) {
+                            const int cnt = (int)std::min<int64_t>(CHB, n - c);
+                            const int a0 = k + 1 + (int)((int64_t)rows * q / pieces);
+                            const int a1 = k + 1 + (int)((int64_t)rows * (q + 1) / pieces);
+                            if (b == L - 1) {
+                                srct.push_back(Task{a1 - a0, o + c, -(k + 1), cnt, a0, a1});
+                            } else {
+                                srct.push_back(Task{a1 - a0, o + c, -(k + 1), cnt | SRC_CPREV, a0, a1});
+                                srct.push_back(Task{3LL * (a1 - a0), o + c, -(k + 1), cnt | SRC_L3, a0, a1});
+                            }
+                        }
                 }
-                hp.leaf_src_end = hp.off[tm][(size_t)b2 * d];
+            hp.leaf2_srctasks = true;
+            std::stable_sort(srct.begin(), srct.end(), [](const Task &a, const Task &b) {
+                if (a.rows != b.rows) return a.rows > b.rows;
+                if (a.ka != b.ka) return a.ka < b.ka;
+                if (a.kb != b.kb) return a.kb < b.kb;
+                if (a.first != b.first) return a.first < b.first;
+                return a.kp0 < b.kp0;
+            });
+            hp.T2S.resize(3 * srct.size());
+            for (size_t i = 0; i < srct.size(); ++i) {
+                hp.T2S[3 * i] = srct[i].first;
+                hp.T2S[3 * i + 1] = ((int64_t)srct[i].ka << 32) | (int64_t)(uint32_t)srct[i].kb;
+                hp.T2S[3 * i + 2] = ((int64_t)srct[i].kp0 << 32) | (int64_t)srct[i].kp1;
             }
-#endif
-            hp.pass_terms[tm] -= moved;
-            hp.pass_terms[tm + 1] += moved;
-            // pass tm (k_leaf) geometry over the remaining sources
-            const int64_t chunks = (hp.leaf_src_end + 31) / 32;
-            int64_t ns = chunks > 0 ? (TARGET_WARPS + chunks - 1) / chunks : 1;
-            ns = std::max<int64_t>(1, std::min<int64_t>(ns, d));
-            hp.pass_nsplit[tm] = (int)ns;
-            hp.pass_ntasks[tm] = chunks * ns;
-            // no sources left: no k_leaf launch and no partial slot
-            hp.pass_blocks[tm] = chunks == 0 ? 0
-                                 : std::max<int64_t>(1, (hp.pass_ntasks[tm] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK);
+            hp.pass_nsplit[tm] = 1;
+            hp.pass_ntasks[tm] = (int64_t)srct.size();
+            hp.pass_blocks[tm] = (int64_t)srct.size();   // one partial slot per task
         }
 #endif
         // When the longest task is a large share of one resident warp's work (a small shard: config 4

@@ -86,17 +86,19 @@ struct HostPlan {
     bool fuse = false;
     int leaf2_ppl = 1;                 // parents per lane of the fused kernel (2: k_leaf2_pairs)
     bool leaf2_sym3 = false;           // k_leaf2_sym3 (oscillatory, level-2 row {0, 1/2, 1} symmetric)
-    // k_leaf2_sym3 also takes the depth-(L-1) points of frontier L-2's sources as "source tasks"
-    // (the prefixes are the stored sources themselves): the excess-(L-1) sources' level-2 rows (the
-    // same symmetric rows the fused tasks walk) and, when level 3 has SYM3_N3 nodes, the
-    // excess-(L-2) sources' level-2 rows (coefficient coef[L-1]) and level-3 rows.  Pass L-2
-    // (k_leaf) then reads only the sources [0, leaf_src_end) of its frontier (none: no launch).
+    // Source tasks: pass L-2 runs k_leaf2_sym3<SRC = true> over all its sources (the prefixes are the
+    // stored sources themselves) instead of k_leaf — the excess-(L-1) sources' symmetric level-2
+    // rows, the excess-(L-2) sources' level-2 rows (coefficient coef[L-1]) and level-3 rows
+    // (SYM3_N3 nodes).  Three int64 per task like T2: first source index, ((-(k+1)) << 32) | (chunk
+    // size | flags), (kp0 << 32) | kp1.
     bool leaf2_srctasks = false;
+    std::vector<int64_t> T2S;
 #define SRC_L3 (1 << 16)      // source task flag: walk the level-3 rows (SYM3_N3 nodes)
 #define SRC_CPREV (1 << 17)   // source task flag: children have excess L-1 (coefficient coef[L-1])
 #define SYM3_N3 5             // level-3 row length of the level-3 source tasks
-    int64_t leaf_src_end = -1;
-    uint64_t leaf2_l3_points = 0;      // points of the level-3 source tasks (general complex terms)
+#ifndef LEAF2_SRC_ROWS
+#define LEAF2_SRC_ROWS 0      // source task rows per piece (0: unsplit)
+#endif
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.

@@ -56,7 +56,7 @@ struct sg_plan_s {
     size_t dev_bytes = 0;
     long long *d_tabs = nullptr;
     std::vector<size_t> tab_offT, tab_NT, tab_CT, tab_TB;   // element offsets into d_tabs per depth
-    size_t tab_JS = 0, tab_off1 = 0, tab_TK = 0;
+    size_t tab_JS = 0, tab_off1 = 0, tab_TK = 0, tab_TKS = 0;
     double *d_scratch = nullptr;   // 4 doubles
     // profiling hook (sg_profile_enable): events around every launch of sg_integrate
     bool prof = false;
@@ -202,6 +202,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     p->tab_JS = push(hp.JS);
     if (hp.fuse) p->tab_TK = push(hp.T2);
+    if (hp.leaf2_srctasks) p->tab_TKS = push(hp.T2S);
     p->tab_off1 = hp.nfront >= 1 ? p->tab_offT[1] : 0;
     if (tabs.empty()) tabs.push_back(0);
     size_t sz = 0;
@@ -411,8 +412,8 @@ static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
 template <bool CPLX>
 static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz, int ppl = 1) {
     if (CPLX && sym && center && nj == 3 && ppl >= 2) {
-#define SYM3(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true> : (const void *)k_leaf2_sym3<P_, true, false>) \
-                       : (cz ? (const void *)k_leaf2_sym3<P_, false, true> : (const void *)k_leaf2_sym3<P_, false, false>))
+#define SYM3(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true, false> : (const void *)k_leaf2_sym3<P_, true, false, false>) \
+                       : (cz ? (const void *)k_leaf2_sym3<P_, false, true, false> : (const void *)k_leaf2_sym3<P_, false, false, false>))
         if (ppl == 2) return SYM3(2);
         if (ppl == 3) return SYM3(3);
 #undef SYM3
@@ -424,6 +425,15 @@ static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool c
     if (CPLX && sym && nj == 2 && ppl == 4)
         return smem ? (const void *)k_leaf2_pairs<4, true> : (const void *)k_leaf2_pairs<4, false>;
     return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz) : leaf2_fn<CPLX, false>(nj, center, sym, cz);
+}
+
+// The source-task kernel of pass L-2 (plan.cpp builds source tasks only for k_leaf2_sym3 plans).
+static const void *leaf2_src_kernel(bool smem, bool cz, int ppl) {
+#define SYM3S(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true, true> : (const void *)k_leaf2_sym3<P_, true, false, true>) \
+                        : (cz ? (const void *)k_leaf2_sym3<P_, false, true, true> : (const void *)k_leaf2_sym3<P_, false, false, true>))
+    if (ppl == 2) return SYM3S(2);
+    return SYM3S(3);
+#undef SYM3S
 }
 
 // Persistent geometry of the single-level last pass (k_leaf1, or the fused k_leaf2; once per plan).
@@ -470,6 +480,10 @@ static int setup_leaf1(sg_plan_s *p) {
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
+    if (hp.leaf2_srctasks && p->leaf1_smem > 48 * 1024 &&
+        cudaFuncSetAttribute(leaf2_src_kernel(true, cz, hp.leaf2_ppl), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p->leaf1_smem) != cudaSuccess)
+        return SG_ECUDA;
     int per_sm = 0, dev = 0, sms = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PASS_THREADS, p->leaf1_smem) != cudaSuccess ||
         cudaGetDevice(&dev) != cudaSuccess ||
@@ -493,6 +507,16 @@ static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t 
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
     const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz, p->hp.leaf2_ppl);
+    DevPlan dp = p->dp;
+    Leaf2Args a = A;
+    void *args[] = {&dp, &a};
+    cudaLaunchKernel(fn, dim3(grid), dim3(PASS_THREADS), args, sm, st);
+}
+
+static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) {
+    const size_t sm = p->leaf1_smem;
+    const void *fn = leaf2_src_kernel(sm > 0, p->leaf2_cz, p->hp.leaf2_ppl);
+    const unsigned grid = (unsigned)std::min<long long>(p->leaf1_grid, A.ntasks);
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
@@ -627,10 +651,28 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             mark();
             continue;
         }
+        if (hp.leaf2_srctasks && p->leaf2 && t == hp.nfront - 1) {
+            // pass L-2 as k_leaf2_sym3 source tasks over every source of frontier L-2
+            Leaf2Args S;
+            memset(&S, 0, sizeof S);
+            double2 *re, *im;
+            uint32_t *meta;
+            front_ptrs(p, t, re, im, meta);
+            S.src_re = re;
+            S.src_im = im;
+            S.T2 = p->d_tabs + p->tab_TKS;
+            S.ntasks = hp.pass_ntasks[t];
+            S.partials = partials + hp.pass_partial_off[t];
+            S.counter = p->d_counter;
+            S.prefetch = 0;
+            if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
+            if (S.ntasks > 0) launch_leaf2_src(p, S, st);
+            mark();
+            continue;
+        }
         PassArgs A;
         memset(&A, 0, sizeof A);
-        // with k_leaf2_sym3 source tasks, pass L-2 reads only the excess-(L-2) block of its frontier
-        A.nsrc = (hp.leaf2_srctasks && p->leaf2 && t == hp.nfront - 1) ? hp.leaf_src_end : hp.total[t];
+        A.nsrc = hp.total[t];
         A.ntasks = hp.pass_ntasks[t];
         A.nsplit = hp.pass_nsplit[t];
         A.t = t;
@@ -651,10 +693,6 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         if (t == p->leaf1_t && cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess)
             return SG_ECUDA;
         const unsigned grid = (unsigned)hp.pass_blocks[t];
-        if (grid == 0) {   // every source of this pass went to k_leaf2_sym3's source tasks
-            mark();
-            continue;
-        }
         // single-level last pass (every source has excess L-1): specialised k_leaf1
         const int n2 = hp.nl[2];
         const bool single = !write && t == p->leaf1_t;
@@ -776,12 +814,6 @@ extern "C" int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *da
             f = (2.0 * f + cf) / 3.0;
             a = (2.0 * a + ca) / 3.0;
         }
-    }
-    if (p->leaf2 && p->hp.leaf2_l3_points > 0 && p->hp.pass_terms[p->hp.nfront] > 0) {
-        // k_leaf2_sym3's level-3 source tasks: general oscillatory terms (8 DFMA + 4 DADD)
-        const double w = (double)p->hp.leaf2_l3_points / (double)p->hp.pass_terms[p->hp.nfront];
-        f = (1.0 - w) * f + w * 8.0;
-        a = (1.0 - w) * a + w * 4.0;
     }
     *dfma_per_point = f;
     *dadd_per_point = a;
