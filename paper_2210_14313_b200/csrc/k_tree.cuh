@@ -1002,6 +1002,12 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 // instructions instead of 32 and the warp has twice the independent accumulator chains.  Same
 // arithmetic per point as k_leaf2's split symmetric pair (node 0 into a, node 1 into b).
 // ---------------------------------------------------------------------------------------------
+#ifndef SYM3_THREADS
+#define SYM3_THREADS 256   // k_leaf2_sym3 CTA size (A/B knob)
+#endif
+#ifndef SYM3_MINB
+#define SYM3_MINB 1        // k_leaf2_sym3 CTAs per SM bound (A/B knob)
+#endif
 #ifndef LEAF2_PAIRS_MINB
 #define LEAF2_PAIRS_MINB 1   // 1 CTA (8 warps) per SM, up to 255 registers: ILP over occupancy
 #endif
@@ -1286,7 +1292,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
 // T2 and partial slots), a separate kernel so the fused loop nest's code is not disturbed (measured:
 // sharing one kernel slowed the fused tasks by 1.6-4% through code layout alone).
 template <int PPL, bool SMEM, bool CZ, bool SRC>
-__global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
+__global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
     constexpr int NM = 3 * PPL;   // mid prefixes per lane
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31;

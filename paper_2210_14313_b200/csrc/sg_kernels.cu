@@ -70,6 +70,7 @@ struct sg_plan_s {
     bool leaf2_cz = false;     // midpoint factor has an exactly zero low part (combination form)
     unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
+    int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     std::vector<cudaEvent_t> ev;
     // workspace
     char *ws = nullptr;
@@ -484,13 +485,16 @@ static int setup_leaf1(sg_plan_s *p) {
         cudaFuncSetAttribute(leaf2_src_kernel(true, cz, hp.leaf2_ppl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
+    // k_leaf2_sym3 has its own CTA size; every other leaf kernel runs PASS_THREADS
+    p->leaf2_threads = (p->leaf2 && p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2) ? SYM3_THREADS : PASS_THREADS;
+    const int wpb = p->leaf2_threads / 32;
     int per_sm = 0, dev = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PASS_THREADS, p->leaf1_smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->leaf2_threads, p->leaf1_smem) != cudaSuccess ||
         cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         return SG_ECUDA;
     const long long ntasks = hp.pass_ntasks[t];
-    p->leaf1_grid = std::max<long long>(1, std::min<long long>((ntasks + WPB - 1) / WPB, (long long)sms * per_sm));
+    p->leaf1_grid = std::max<long long>(1, std::min<long long>((ntasks + wpb - 1) / wpb, (long long)sms * per_sm));
     hp.pass_blocks[t] = ntasks;   // partial slots: one per task (0 tasks -> no slot, no launch)
     int64_t poff = hp.root_blocks;
     for (int u = 1; u <= hp.nfront; ++u) {
@@ -510,7 +514,7 @@ static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t 
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
-    cudaLaunchKernel(fn, dim3(grid), dim3(PASS_THREADS), args, sm, st);
+    cudaLaunchKernel(fn, dim3(grid), dim3(p->leaf2_threads), args, sm, st);
 }
 
 static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) {
@@ -520,7 +524,7 @@ static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) 
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
-    cudaLaunchKernel(fn, dim3(grid), dim3(PASS_THREADS), args, sm, st);
+    cudaLaunchKernel(fn, dim3(grid), dim3(SYM3_THREADS), args, sm, st);
 }
 
 template <bool CPLX>
@@ -642,7 +646,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
             B.counter = p->d_counter;
-            B.prefetch = B.ntasks >= 16LL * p->leaf1_grid * WPB ? 1 : 0;
+            B.prefetch = B.ntasks >= 16LL * p->leaf1_grid * (p->leaf2_threads / 32) ? 1 : 0;
             if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);

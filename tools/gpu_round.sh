@@ -1,5 +1,6 @@
 #!/bin/bash
-# One GPU-box session: tests, smoke, bench, ncu launch list + one full capture of the top kernel.
+# One GPU-box session: tests, smoke, bench, ncu launch list + full captures of the leaf kernels
+# (config 5: pass 2's source-task launch and pass 3's fused launch of k_leaf2_sym3; config 4: k_leaf2).
 # usage: bash tools/gpu_round.sh <tag> [what...]   what in {test,smoke,bench,ncu,ncufull}
 tag=${1:-r01}; shift
 what=${@:-test smoke bench ncu ncufull}
@@ -19,7 +20,7 @@ for w in $what; do
              --log-file gpurun_out/${tag}_launches_c4.csv python tools/prof_step.py 4 2 > gpurun_out/${tag}_ncu2.log 2>&1 ;;
     ncufull) timeout 300 python tools/prof_step.py 5 1 > gpurun_out/${tag}_plain5.log 2>&1 && \
            timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-             -k regex:k_leaf2 -c 1 -o gpurun_out/${tag}_c5_leaf2 python tools/prof_step.py 5 1 > gpurun_out/${tag}_ncu3.log 2>&1 ;
+             -k regex:k_leaf2 -c 2 -o gpurun_out/${tag}_c5_leaf2 python tools/prof_step.py 5 1 > gpurun_out/${tag}_ncu3.log 2>&1 ;
            timeout 300 python tools/prof_step.py 4 1 > gpurun_out/${tag}_plain4b.log 2>&1 && \
            timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
              -k regex:k_leaf2 -c 1 -o gpurun_out/${tag}_c4_leaf2 python tools/prof_step.py 4 1 > gpurun_out/${tag}_ncu4.log 2>&1 ;;

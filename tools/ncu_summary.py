@@ -70,7 +70,10 @@ def main():
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
     for rep in reps:
-        for d in raw(rep):
+        ds = raw(rep)
+        # traffic.json: the dominant (longest) captured launch of each config
+        top = max(ds, key=lambda d: float(d["gpu__time_duration.sum"][0])) if ds else None
+        for d in ds:
             name = d.get("Kernel Name", ("?", ""))[0]
             lines.append(f"## {os.path.basename(rep)} — `{name}`")
             lines.append("")
@@ -82,7 +85,7 @@ def main():
             lines.append("")
             base = os.path.basename(rep)
             for cfg in ("c4", "c5", "c3"):
-                if f"_{cfg}_" in base and "leaf" in base:
+                if f"_{cfg}_" in base and "leaf" in base and d is top:
                     rb = to_bytes(*d["dram__bytes_read.sum"])
                     wb = to_bytes(*d["dram__bytes_write.sum"])
                     traffic[cfg] = rb + wb
