@@ -699,12 +699,29 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
 #ifndef LEAF2_NO_SRCTASKS
         if (hp.leaf2_sym3 && L >= 3 && merge == 0 && hp.nl[3] == SYM3_N3) {
             const int64_t CHB = 32LL * 3 * hp.leaf2_ppl;
+            // task weight = rows (level-3 rows: 3 rows); when the longest task exceeds one resident
+            // warp's share of the total (a small shard), rows are split into pieces of about half a
+            // share (measured, config 5 unsplit at N = 1 and split at N = 8: 0.43 / ~0.06 ms)
+            double wsum = 0.0, wmax = 0.0;
+            for (int b = L - 2; b <= L - 1; ++b)
+                for (int k = 0; k <= d - 2; ++k) {
+                    const int64_t chunks = (hp.N[tm][(size_t)b * d + k] + CHB - 1) / CHB;
+                    const double w = (double)(d - 1 - k) * (b == L - 1 ? 1.0 : 4.0);
+                    wsum += (double)chunks * w;
+                    if (chunks > 0) wmax = std::max(wmax, (double)(d - 1 - k) * (b == L - 1 ? 1.0 : 3.0));
+                }
+            const double share = wsum / (double)SYM3_RESIDENT_WARPS;
+            int rmax = d;   // rows per piece (weight-1 rows; level-3 pieces get a third)
+            if (LEAF2_SRC_ROWS > 0) rmax = LEAF2_SRC_ROWS;
+            else if (wmax > share) rmax = std::max(8, (int)(share / 2.0));
             for (int b = L - 2; b <= L - 1; ++b)
                 for (int k = 0; k <= d - 2; ++k) {
                     const int64_t n = hp.N[tm][(size_t)b * d + k], o = hp.off[tm][(size_t)b * d + k];
-                    // rows k+1 .. d-1 in pieces of at most LEAF2_SRC_ROWS (the persistent grid's tail)
                     const int rows = d - 1 - k;
-                    const int pieces = LEAF2_SRC_ROWS > 0 ? (rows + LEAF2_SRC_ROWS - 1) / LEAF2_SRC_ROWS : 1;
+                    // level-2 pieces of <= rmax rows; the level-3 tasks of excess-(L-2) sources use
+                    // pieces of <= rmax / 3 rows (their rows cost three level-2 rows)
+                    const int r2 = rmax, r3 = rmax >= d ? d : std::max(4, rmax / 3);
+                    const int pieces = b == L - 1 ? (rows + r2 - 1) / r2 : (rows + r3 - 1) / r3;
                     for (int64_t c = 0; c < n; c += CHB)
                         for (int q = 0; q < pieces; ++q) {
                             const int cnt = (int)std::min<int64_t>(CHB, n - c);

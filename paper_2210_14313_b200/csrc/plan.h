@@ -97,8 +97,9 @@ struct HostPlan {
 #define SRC_CPREV (1 << 17)   // source task flag: children have excess L-1 (coefficient coef[L-1])
 #define SYM3_N3 5             // level-3 row length of the level-3 source tasks
 #ifndef LEAF2_SRC_ROWS
-#define LEAF2_SRC_ROWS 0      // source task rows per piece (0: unsplit)
+#define LEAF2_SRC_ROWS 0      // source task rows per piece (0: automatic, see plan.cpp)
 #endif
+#define SYM3_RESIDENT_WARPS (148 * 8)   // persistent k_leaf2_sym3 warps (1 CTA of 8 warps per SM)
     // Fused tasks: (chunk of 32 parents, k_mid range [ka, kb)).  A chunk's k_mid values whose rows
     // (d - 1 - k_mid each) are short are grouped until a task holds >= LEAF2_TASK_ROWS rows, so the
     // per-task fixed cost (task fetch, parent load, warp reduction, partial store) is amortised.
