@@ -1188,7 +1188,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
     }
     dd lane_sum = {0.0, 0.0};
     for (int km = km0; km < km1; ++km) {
-        const double sa = P.SA[(MODE == 2 ? 3LL : 2LL) * (d + 1) + km + 1] * (1.0 + 0x1p-20);
+        const double sa = P.SA[(MODE >= 2 ? 3LL : 2LL) * (d + 1) + km + 1] * (1.0 + 0x1p-20);
         dd er[NM], ei[NM];
         double sg[NM], ah[NM], al[NM], bh[NM], bl[NM];
         if constexpr (SRCT) {
@@ -1247,7 +1247,37 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
                     }
                 }
             }
-            if constexpr (MODE != 2) {
+            if constexpr (MODE >= 3) {
+                // level-3 row {0, x1, 1/2, x3, 1} with x = 0 and 1 an exactly conjugate pair and an
+                // exactly real midpoint (MODE 3: nodes x1, x3 general terms; MODE 4: x1 = 1 - x3
+                // exactly, a second conjugate pair): 46 resp. 38 FP64 per 5 points instead of 60
+                const double2 *F3r = P.Fre + P.tab_off[3], *F3i = P.Fim + P.tab_off[3];
+                for (; kp < ke; ++kp) {
+                    const double2 f4 = __ldg(F3r + kp * 5 + 4), g4 = __ldg(F3i + kp * 5 + 4);
+                    const double2 f3 = __ldg(F3r + kp * 5 + 3), g3 = __ldg(F3i + kp * 5 + 3);
+                    const double2 f2 = __ldg(F3r + kp * 5 + 2);
+                    double2 f1 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+                    if constexpr (MODE == 3) {
+                        f1 = __ldg(F3r + kp * 5 + 1);
+                        g1 = __ldg(F3i + kp * 5 + 1);
+                    }
+#pragma unroll
+                    for (int m = 0; m < NM; ++m) {
+                        leaf_sym_pair_terms(er[m], ei[m], f4, g4, ah[m], al[m]);   // nodes 0 and 4
+                        if constexpr (MODE == 4) {
+                            leaf_sym_pair_terms(er[m], ei[m], f3, g3, bh[m], bl[m]);   // nodes 1 and 3
+                        } else {
+                            LeafAcc b = {bh[m], bl[m]};
+                            leaf_term<true>(er[m], ei[m], f1, g1, b);
+                            leaf_term<true>(er[m], ei[m], f3, g3, b);
+                            bh[m] = b.h;
+                            bl[m] = b.l;
+                        }
+                        leaf_real_factor_term<false>(er[m], f2, ah[m], al[m]);   // the midpoint
+                    }
+                }
+            }
+            if constexpr (MODE < 2) {
             for (; kp < ke; ++kp) {
                 const double2 f1 = SMEM ? Fr[kp * 3 + 2] : __ldg(Fr + kp * 3 + 2);
                 const double2 g1 = SMEM ? Fi[kp * 3 + 2] : __ldg(Fi + kp * 3 + 2);
@@ -1291,7 +1321,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
 // SRC = false: the fused tasks (pass L-1); SRC = true: the source tasks (pass L-2, its own task list
 // T2 and partial slots), a separate kernel so the fused loop nest's code is not disturbed (measured:
 // sharing one kernel slowed the fused tasks by 1.6-4% through code layout alone).
-template <int PPL, bool SMEM, bool CZ, bool SRC>
+template <int PPL, bool SMEM, bool CZ, bool SRC, int L3S = 0>
 __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
     constexpr int NM = 3 * PPL;   // mid prefixes per lane
     extern __shared__ double2 fsm[];
@@ -1337,7 +1367,7 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
         dd lane_sum;
         if constexpr (SRC) {
             const int cnt = kb & 0xffff;
-            lane_sum = (kb & SRC_L3) ? sym3_task<PPL, SMEM, CZ, 2>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1)
+            lane_sum = (kb & SRC_L3) ? sym3_task<PPL, SMEM, CZ, 2 + L3S>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1)
                                      : sym3_task<PPL, SMEM, CZ, 1>(P, A, Fr, Fi, lane, first, ka, cnt, kp0, kp1);
         } else {
             lane_sum = sym3_task<PPL, SMEM, CZ, 0>(P, A, Fr, Fi, lane, first, ka, kb, kp0, kp1);

@@ -71,6 +71,7 @@ struct sg_plan_s {
     unsigned long long *d_counter = nullptr;   // dynamic task counter (plan-owned)
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
+    int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
     std::vector<cudaEvent_t> ev;
     // workspace
     char *ws = nullptr;
@@ -428,13 +429,18 @@ static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool c
     return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz) : leaf2_fn<CPLX, false>(nj, center, sym, cz);
 }
 
-// The source-task kernel of pass L-2 (plan.cpp builds source tasks only for k_leaf2_sym3 plans).
-static const void *leaf2_src_kernel(bool smem, bool cz, int ppl) {
-#define SYM3S(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true, true> : (const void *)k_leaf2_sym3<P_, true, false, true>) \
-                        : (cz ? (const void *)k_leaf2_sym3<P_, false, true, true> : (const void *)k_leaf2_sym3<P_, false, false, true>))
-    if (ppl == 2) return SYM3S(2);
-    return SYM3S(3);
-#undef SYM3S
+// The source-task kernel of pass L-2 (plan.cpp builds source tasks only for k_leaf2_sym3 plans, with
+// LEAF2_PPL3 parents per lane); l3s = symmetry of the level-3 row (0 none, 1 nodes 0/4 + midpoint,
+// 2 all pairs + midpoint).
+template <bool SMEM, bool CZ>
+static const void *leaf2_src_kernel_l3(int l3s) {
+    if (l3s == 2) return (const void *)k_leaf2_sym3<LEAF2_PPL3, SMEM, CZ, true, 2>;
+    if (l3s == 1) return (const void *)k_leaf2_sym3<LEAF2_PPL3, SMEM, CZ, true, 1>;
+    return (const void *)k_leaf2_sym3<LEAF2_PPL3, SMEM, CZ, true, 0>;
+}
+static const void *leaf2_src_kernel(bool smem, bool cz, int l3s) {
+    return smem ? (cz ? leaf2_src_kernel_l3<true, true>(l3s) : leaf2_src_kernel_l3<true, false>(l3s))
+                : (cz ? leaf2_src_kernel_l3<false, true>(l3s) : leaf2_src_kernel_l3<false, false>(l3s));
 }
 
 // Persistent geometry of the single-level last pass (k_leaf1, or the fused k_leaf2; once per plan).
@@ -481,8 +487,22 @@ static int setup_leaf1(sg_plan_s *p) {
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
+    if (hp.leaf2_srctasks) {
+        // exactly conjugate level-3 pairs (x_j = 1 - x_{4-j}, equal weights) and an exactly real
+        // midpoint (x_2 = 1/2): shared products in the source tasks' level-3 rows
+        const int e3 = hp.entry_off[3];
+        auto pair = [&](int a, int b) {
+            return 1.0 - hp.X[e3 + b] == hp.X[e3 + a] && hp.Whi[e3 + a] == hp.Whi[e3 + b] &&
+                   hp.Wlo[e3 + a] == hp.Wlo[e3 + b];
+        };
+        const bool p04 = pair(0, 4) && hp.X[e3 + 2] == 0.5, p13 = pair(1, 3);
+        p->leaf2_l3s = p04 ? (p13 ? 2 : 1) : 0;
+#ifdef LEAF2_NO_L3SYM
+        p->leaf2_l3s = 0;
+#endif
+    }
     if (hp.leaf2_srctasks && p->leaf1_smem > 48 * 1024 &&
-        cudaFuncSetAttribute(leaf2_src_kernel(true, cz, hp.leaf2_ppl), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(leaf2_src_kernel(true, cz, p->leaf2_l3s), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
     // k_leaf2_sym3 has its own CTA size; every other leaf kernel runs PASS_THREADS
@@ -519,7 +539,7 @@ static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t 
 
 static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) {
     const size_t sm = p->leaf1_smem;
-    const void *fn = leaf2_src_kernel(sm > 0, p->leaf2_cz, p->hp.leaf2_ppl);
+    const void *fn = leaf2_src_kernel(sm > 0, p->leaf2_cz, p->leaf2_l3s);
     const unsigned grid = (unsigned)std::min<long long>(p->leaf1_grid, A.ntasks);
     DevPlan dp = p->dp;
     Leaf2Args a = A;
