@@ -125,7 +125,7 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
 }
 
 // K0 in one launch: blocks 0 .. nfb-1 fill the factor table (one entry per thread), block nfb computes
-// the base value (independent of the table; same 256-thread order as k_base, so the same bits).
+// the base value (independent of the table; base_body needs a 256-thread block).
 #define K0_THREADS 256
 __global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int nfb) {
     if ((int)blockIdx.x == nfb) base_body(P);

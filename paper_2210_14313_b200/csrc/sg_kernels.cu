@@ -6,9 +6,11 @@
 //                      suffix bounds of |F| for the leaf kernels' grid accumulators
 //  k_tree.cuh          K2+K3: level-synchronous prefix-tree passes (Eqs 3.8-3.11,
 //                      the multilevel dimension iteration): root pass, frontier writer k_pass,
-//                      leaf kernels k_leaf (generic), k_leaf1 (single level), k_leaf2 (fused last two
-//                      levels, the hot loop)
+//                      leaf kernels k_leaf (generic), k_leaf1 (single level), k_leaf2 / _pairs /
+//                      _sym3 (fused last two levels, the hot loop; k_leaf2_sym3<SRC> also runs
+//                      pass L-2 as source tasks)
 //  k_sform.cuh         s-form passes (partial sums of the argument, outer function per point)
+//  k_unrank.cuh        device unranker (sg_eval_points) and the plain per-point SG ablation
 //  k_reduce.cuh        K4/K5: task partials -> fixed-order dd sum; cross-rank finalize
 //  k_collapse.cuh      separable collapse (SG_METHOD_COLLAPSE)
 #include <cuda_runtime.h>
