@@ -77,3 +77,17 @@ def test_source_pass_terms_and_launch(api):
     ms = plan.profile_read()
     assert ms[3 + 2 - 1] > 0.05          # pass 2: ~0.43 ms of source tasks on a B200
     plan.close()
+
+
+@pytest.mark.parametrize("d,L,rule", [(2500, 3, S.RULE_CC), (700, 4, S.RULE_TRAP)])
+def test_source_tasks_large_d_no_smem(api, d, L, rule):
+    """d large enough that the level-2 factor slice no longer fits shared memory (the fused and the
+    source-task launches read it through L1): 1e11-1e12 points, against the 50-digit DP value and the
+    separable collapse (an independent evaluation order of the same Eq 2.6 sum)."""
+    import pins
+    p = S.random_problem(308, d, L, rule, S.KIND_OSC)
+    hi, lo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u)
+    v = mp.mpf(hi) + mp.mpf(lo)
+    assert rel(v, pins.dp_value(p)) <= HEALTH
+    chi, clo = api.integrate(p.d, p.L, p.rule, p.kind, p.c, p.w, p.u, method=api.METHOD_COLLAPSE)
+    assert rel(v, mp.mpf(chi) + mp.mpf(clo)) <= 1e-18
