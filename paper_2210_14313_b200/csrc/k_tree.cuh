@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
             else switch (n) {
             case 2: s = leaf_level<CPLX, 2>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             case 3: s = leaf_level<CPLX, 3>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
+            case 4: s = leaf_level<CPLX, 4>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             case 5: s = leaf_level<CPLX, 5>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             default: s = leaf_level<CPLX, 0>(Fr, Fi, n, kb, kmain, ks1, k, er, ei, sigma); break;
             }
