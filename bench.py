@@ -3,7 +3,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
     torchrun --nproc-per-node N ... bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-Workload (default): BASELINE.json configs[4] — d=300, q=d+4, Clenshaw-Curtis, oscillatory Genz
+Workload (headline): BASELINE.json configs[4] — d=300, q=d+4, Clenshaw-Curtis, oscillatory Genz
 integrand (seed 4), 27,521,113,876 Smolyak points: the configuration BASELINE.json ties to the
 1/2/4/8-GPU scaling run; it fits one GPU.  A step = the whole hot path:
 K0 factor tables, root pass, all prefix-tree passes, deterministic reduction, the cross-rank
@@ -13,6 +13,12 @@ the start of the timed region; L2 is flushed (256 MiB write) between timed steps
 events.  Times: CUDA events on the launching stream, barrier + synchronize on both sides, max over
 ranks.  The "e2e" leg times the same step through the C ABI with HOST buffers: pinned H2D of the
 parameters (sg_update_integrand), the step, and the D2H read of the 16-byte result.
+
+The "configs" block repeats the measurement for every BASELINE config c1-c5 (Eq 2.6 over each config,
+PAPER.md:65-75): sg_plan time, time-to-integral best / median / mean, points/s, relative error against
+the stored __float128 oracle value (tests/golden, written by oracle/ only) and, for c3-c5, the FP64
+fraction of the dominant leaf kernel.  FP64 work per point comes from the ncu counters committed in
+profiles/ (sm__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on of that launch).
 """
 from __future__ import annotations
 
@@ -21,6 +27,7 @@ import ctypes
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -28,18 +35,16 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
 import sg_configs as S  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-# Algorithmic FP64 work per Smolyak point of the dominant leaf kernel comes from the library
-# (sg_plan_leaf_work: DFMA and DADD thread-instructions per point of the variant the plan runs;
-# DESIGN.md §6): flops = 2 DFMA + DADD, pipe slots = DFMA + DADD.
-# FP64 peak derived from the unit count and clock (DESIGN.md): 148 SMs x 64 FP64 FMA/clk x 2 flops
-# x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz) = 37.2 TFLOP/s.
+# FP64 peak derived from the unit count and clock (DESIGN.md §6): 148 SMs x 64 FP64 FMA/clk x 2 flops
+# x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz) = 37.2 TFLOP/s.  MEASURED_PEAKS.json has no FP64 figure;
+# the DFMA burst measured in this run (tools/fp64_peak.cu) is reported beside it.
 SM_COUNT = 148
 FP64_FMA_PER_SM_CLK = 64
+COUNTERS = os.path.join(ROOT, "profiles", "fp64_counters.json")   # written by tools/fp64_counters.py
+GOLDEN = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
 
 
 def peak_fp64_tflops():
@@ -49,6 +54,22 @@ def peak_fp64_tflops():
     except Exception:
         pass
     return SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * mhz * 1e6 / 1e12, mhz
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def stats(times):
+    return {"best": min(times), "median": statistics.median(times), "mean": statistics.mean(times)}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -110,79 +131,88 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------
-# CPU oracle sample (cpu_baseline and --impl reference)
+# CPU oracle (cpu_baseline and --impl reference): oracle/ only, never the product library
 # ----------------------------------------------------------------------------------------------
-def oracle_sample_range(p: S.Problem, target_points: int):
-    """Depth-1 range [lo, nd1) of the workload whose subtrees hold about target_points points
-    (host-only library query; the range is the sample the oracle times)."""
-    from paper_2210_14313_b200._lib import lib, sg_options
-    L = lib()
-
-    def pts(lo, hi):
-        o = sg_options(0, 0, 0, 1, lo, hi)
-        sp = ctypes.c_ulonglong()
-        rc = L.sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), ctypes.byref(sp), None,
-                             None, None, None)
-        assert rc == 0
-        return sp.value
-
-    o = sg_options(0, 0, 0, 1, 0, -1)
-    nd1 = ctypes.c_longlong()
-    hi_ = ctypes.c_longlong()
-    L.sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), None, None, None,
-                    ctypes.byref(hi_), None)
-    nd1 = hi_.value
-    a, b = 1, nd1
-    while a < b:   # smallest lo such that points(lo, nd1) <= target
-        m = (a + b) // 2
-        if pts(m, nd1) > target_points:
-            a = m + 1
-        else:
-            b = m
-    return a, nd1, pts(a, nd1)
-
-
-def run_oracle_sample(p, lo, hi):
+def oracle_sample(p, target_points, fp64=False):
     import oracle
     # all host cores, explicitly: torchrun sets OMP_NUM_THREADS=1 for its ranks
-    r = oracle.integrate_problem(p, lo=lo, hi=hi, include_root=False, eval_mode=1,
-                                 nthreads=os.cpu_count())
-    return r
+    return oracle.timing_sample(p, int(target_points), nthreads=os.cpu_count(), fp64=fp64)
 
 
-def cpu_baseline(p, target_points=int(1.2e8)):
-    lo, hi, npts = oracle_sample_range(p, target_points)
-    r = run_oracle_sample(p, lo, hi)
-    cores = os.cpu_count()
-    return {"value": r.npoints / r.seconds, "unit": "points/s", "cores": cores, "kind": "oracle",
-            "sample": f"{p.name} depth-1 subtrees [{lo},{hi}) = {r.npoints} of "
-                      f"{S_total_points(p)} Smolyak points, __float128 oracle (eval_mode=1), "
-                      f"OpenMP {cores} threads, {r.seconds:.2f} s",
+def sample_text(p, r, stride, total, what):
+    return (f"{p.name}: every {stride}-th depth-2 multi-index subtree of the whole tree (lexicographic, "
+            f"oracle.timing_sample) = {r.npoints} of {total} Smolyak points, {what}, eval_mode=1 "
+            f"(active-coordinate form), OpenMP {os.cpu_count()} threads, {r.seconds:.2f} s")
+
+
+def cpu_baseline(p, target_points=int(6e7)):
+    r, stride, total = oracle_sample(p, target_points)
+    return {"value": r.npoints / r.seconds, "unit": "points/s", "cores": os.cpu_count(),
+            "cpu": cpu_model(), "kind": "oracle",
+            "sample": sample_text(p, r, stride, total, "__float128 oracle"),
             "seconds": r.seconds, "points": r.npoints}
 
 
-def S_total_points(p):
-    from paper_2210_14313_b200._lib import lib, sg_options
-    o = sg_options(0, 0, 0, 1, 0, -1)
-    tp = ctypes.c_ulonglong()
-    lib().sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), None, ctypes.byref(tp), None,
-                        None, None)
-    return tp.value
-
-
-def config_block(p, extra=None):
-    c = {"workload": f"BASELINE.json configs[{int(p.name[1:]) - 1}] ({p.name}): d={p.d}, "
-                     f"q=d+{p.L}, {S.RULE_NAMES[p.rule]}, {S.KIND_NAMES[p.kind]} integrand",
-         "d": p.d, "q": p.q, "L": p.L, "rule": S.RULE_NAMES[p.rule],
-         "integrand": S.KIND_NAMES[p.kind], "points": S_total_points(p),
-         "form": "combination (Eq 2.6)", "arith": "factor-form double-double",
-         "l2": "flushed between timed steps (256 MiB write, outside the events)"}
-    if extra:
-        c.update(extra)
-    return c
+def cpu_baseline_fp64(full_configs=(1, 2, 3, 4), sample_config=5, target_points=int(1e9)):
+    """The FP64 instantiation of the same plain oracle (oracle/sg_oracle.c -DSGO_FP64): a CPU speed
+    baseline that is not parity-grade; its error against the stored quad value shows the
+    conditioning of Eq 2.6.  Full size for c1-c4, a sample for c5 (its full-size
+    error is committed in profiles/ by tools/oracle_fp64.py)."""
+    import mpmath as mp
+    import oracle
+    gold = json.load(open(GOLDEN))["values"] if os.path.exists(GOLDEN) else {}
+    rows = {}
+    with mp.workdps(40):
+        for i in full_configs:
+            p = S.baseline_config(i)
+            r = oracle.integrate_problem(p, eval_mode=1, nthreads=os.cpu_count(), fp64=True)
+            row = {"points": r.npoints, "seconds": r.seconds, "points_per_s": r.npoints / max(r.seconds, 1e-9)}
+            if p.name in gold:
+                ref = mp.mpf(gold[p.name]["text"])
+                row["rel_err_vs_quad_oracle"] = float(abs((mp.mpf(r.hi) + mp.mpf(r.lo) - ref) / ref))
+            rows[p.name] = row
+    p = S.baseline_config(sample_config)
+    r, stride, total = oracle_sample(p, target_points, fp64=True)
+    rows[p.name] = {"points": r.npoints, "seconds": r.seconds, "points_per_s": r.npoints / r.seconds,
+                    "sample": sample_text(p, r, stride, total, "FP64 oracle")}
+    committed = os.path.join(ROOT, "profiles", "r02_oracle_fp64_container.json")
+    if os.path.exists(committed):
+        c = json.load(open(committed))["configs"].get(p.name)
+        if c:
+            rows[p.name]["full_size_rel_err_vs_quad_oracle"] = c["rel_err_vs_quad_oracle"]
+            rows[p.name]["full_size_note"] = "profiles/r02_oracle_fp64_container.json (tools/oracle_fp64.py)"
+    return {"kind": "oracle (FP64 instantiation, not parity-grade)", "cores": os.cpu_count(),
+            "cpu": cpu_model(), "configs": rows}
 
 
 # ----------------------------------------------------------------------------------------------
+def fp64_counters(cfg, variant="tree"):
+    """Committed ncu FP64 counters of config `cfg`'s dominant leaf launch (tools/fp64_counters.py)."""
+    if not os.path.exists(COUNTERS):
+        return None
+    return json.load(open(COUNTERS)).get("launches", {}).get(f"c{cfg}_{variant}")
+
+
+def roofline_from(points, kernel_ms, ctr, plan, peak, mhz, burst):
+    """achieved FP64 FLOP/s of the dominant launch: points x (flops per point from the committed ncu
+    counters of that launch; the plan's inner-loop count if none) / its live CUDA-event time."""
+    if ctr is not None and ctr.get("points") == points:
+        fpp, ipp = ctr["flops_per_point"], ctr["fp64_inst_per_point"]
+        src = f"ncu counters {ctr['source']}"
+    else:
+        fma, add = plan.leaf_work()
+        fpp, ipp = 2 * fma + add, fma + add
+        src = "sg_plan_leaf_work (inner loop only; no committed ncu counters for this launch)"
+    ach = points * fpp / (kernel_ms * 1e-3) / 1e12
+    out = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+           "flops_per_point": round(fpp, 4), "fp64_inst_per_point": round(ipp, 4),
+           "work_source": src, "kernel_ms": kernel_ms,
+           "pipe_frac": points * ipp / (kernel_ms * 1e-3) / (SM_COUNT * FP64_FMA_PER_SM_CLK * mhz * 1e6)}
+    if isinstance(burst, (int, float)) and burst > 0:
+        out["frac_of_measured_dfma_burst"] = ach / burst
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,14 +221,16 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config block (c1-c5)")
     ap.add_argument("--no-merged", action="store_true", help="skip the SG_MERGE_MIDPOINT leg")
     ap.add_argument("--no-graph", action="store_true",
                     help="time the stream-launched step instead of its CUDA-graph replay")
     ap.add_argument("--no-collapse", action="store_true", help="skip the SG_METHOD_COLLAPSE leg")
     ap.add_argument("--no-frontier", action="store_true",
                     help="skip the stored-frontier (unfused) leg that measures the HBM-bound frontier kernel")
-    ap.add_argument("--no-plain", action="store_true",
-                    help="skip the plain per-point SG ablation leg (SG_METHOD_PLAIN)")
+    ap.add_argument("--plain-ablation", action="store_true",
+                    help="also run the plain per-point SG ablation leg (SG_METHOD_PLAIN: the paper's "
+                         "comparison system, out of the hot-path scope; off by default)")
     ap.add_argument("--no-corner", action="store_true",
                     help="skip the non-separable corner-peak leg (SG_ARITH_SFORM_DD)")
     # testing aids for the multi-rank path on a 1-GPU box: gloo carries the 16-byte collective
@@ -206,6 +238,9 @@ def main():
     # inside a kernel, so sharing is safe); the product configuration is nccl + one GPU per rank
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--device-index", type=int, default=None)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise the process group and run the all-gather even at world 1 "
+                         "(exercises the NCCL branch on a 1-GPU box)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -227,7 +262,8 @@ def main():
         B.build()
     local = local if args.device_index is None else args.device_index
     torch.cuda.set_device(local)
-    if world > 1:
+    dist_on = world > 1 or args.force_dist
+    if dist_on:
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -235,60 +271,65 @@ def main():
         dist.barrier()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-
-    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world, device=dev)
-    plan.profile_enable(True)
-    shard_pts, total_pts = plan.points()
-    passes = plan.passes()
-    dominant = max(range(1, len(passes)), key=lambda i: passes[i].terms) if len(passes) > 1 else 0
     gathered = torch.zeros(2 * world, dtype=torch.float64, device=dev)
     result = torch.zeros(2, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(plan=plan):
+    def make_plan(q, **kw):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        pl = api.Plan(q.d, q.q, q.rule, q.kind, q.c, q.w, q.u, rank=rank, world=world, device=dev, **kw)
+        torch.cuda.synchronize(dev)
+        return pl, (time.perf_counter() - t0) * 1e3
+
+    def gather_finalize(plan, part):
+        if args.dist_backend == "nccl":
+            dist.all_gather_into_tensor(gathered, part)
+        else:
+            g = torch.zeros(2 * world, dtype=torch.float64)
+            dist.all_gather_into_tensor(g, part.cpu())
+            gathered.copy_(g)
+        plan.sg_finalize(gathered, world, stream, result)
+
+    def step(plan):
         part = plan.sg_integrate(stream)
-        if world > 1:
-            if args.dist_backend == "nccl":
-                dist.all_gather_into_tensor(gathered, part)
-            else:
-                g = torch.zeros(2 * world, dtype=torch.float64)
-                dist.all_gather_into_tensor(g, part.cpu())
-                gathered.copy_(g)
-            plan.sg_finalize(gathered, world, stream, result)
+        if dist_on:
+            gather_finalize(plan, part)
         else:
             plan.sg_finalize(part, 1, stream, result)
 
     def graph_step(plan):
         """The step as one CUDA-graph replay (sg_integrate, + sg_finalize at world 1; the launch
-        events are graph event-record nodes, so profile_read still times each launch); at world > 1
-        the all-gather and sg_finalize follow the replay as in step()."""
+        events are graph event-record nodes, so profile_read still times each launch); with a
+        process group the all-gather and sg_finalize follow the replay as in step()."""
         if args.no_graph:
             return lambda: step(plan)
         plan.profile_enable(True)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             part = plan.sg_integrate()
-            if world == 1:
+            if not dist_on:
                 plan.sg_finalize(part, 1, None, result)
 
         def fn():
             g.replay()
-            if world > 1:
-                if args.dist_backend == "nccl":
-                    dist.all_gather_into_tensor(gathered, part)
-                else:
-                    gl = torch.zeros(2 * world, dtype=torch.float64)
-                    dist.all_gather_into_tensor(gl, part.cpu())
-                    gathered.copy_(gl)
-                plan.sg_finalize(gathered, world, stream, result)
+            if dist_on:
+                gather_finalize(plan, part)
         fn.graph = g
         return fn
 
-    def timed(fn, k, plan=plan, dominant=dominant):
+    def maxrank(ms):
+        if not dist_on:
+            return ms
+        t = torch.tensor([ms], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, k, plan=None, dominant=None):
         times, dom = [], []
         for _ in range(k):
             flush.fill_(1.0)
-            if world > 1:
+            if dist_on:
                 dist.barrier()
             torch.cuda.synchronize(dev)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -297,27 +338,42 @@ def main():
             fn()
             e1.record(stream)
             torch.cuda.synchronize(dev)
-            ms = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([ms], dtype=torch.float64,
-                                 device=dev if args.dist_backend == "nccl" else "cpu")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = float(t.item())
-            times.append(ms)
-            prof = plan.profile_read()
-            dom.append(prof[3 + dominant - 1] if dominant > 0 else prof[2])
+            times.append(maxrank(e0.elapsed_time(e1)))
+            if plan is not None and dominant is not None:
+                prof = plan.profile_read()
+                dom.append(prof[3 + dominant - 1] if dominant > 0 else prof[2])
         return times, dom
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    gstep = graph_step(plan)
-    for _ in range(args.warmup):
-        gstep()
-    torch.cuda.synchronize(dev)
+    def dominant_pass(plan):
+        passes = plan.passes()
+        return (max(range(1, len(passes)), key=lambda i: passes[i].terms) if len(passes) > 1 else 0), passes
+
+    def measure(q, k, w, **kw):
+        """plan + warm-up + k timed graph replays of problem q."""
+        plan, plan_ms = make_plan(q, **kw)
+        plan.profile_enable(True)
+        dom, passes = dominant_pass(plan)
+        for _ in range(w):
+            step(plan)
+        torch.cuda.synchronize(dev)
+        g = graph_step(plan)
+        for _ in range(w):
+            g()
+        torch.cuda.synchronize(dev)
+        times, dom_ms = timed(g, k, plan, dom)
+        res = result.cpu().numpy().copy()
+        return plan, plan_ms, dom, passes, times, dom_ms, res, g
+
+    peak, mhz = peak_fp64_tflops()
+
+    # ---- headline config -------------------------------------------------------------------------
+    plan, plan_ms, dominant, passes, _, _, _, gstep = measure(p, 0, args.warmup)
+    shard_pts, total_pts = plan.points()
     with ClockSampler(local) as clk:
-        times, dom = timed(gstep, args.steps)
-    ms = statistics.mean(times)
+        times, dom = timed(gstep, args.steps, plan, dominant)
+    st = stats(times)
+    ms = st["mean"]
+    value_res = result.cpu().numpy().copy()
 
     # e2e: host buffers through the C ABI (pinned H2D of c/w, step, D2H of the result)
     c_host = torch.from_numpy(p.c.copy()).pin_memory()
@@ -326,7 +382,7 @@ def main():
 
     def e2e_step():
         plan.sg_update_integrand(c_host, w_host, p.u, stream)
-        step()
+        step(plan)
         res_host.copy_(result, non_blocking=True)
 
     for _ in range(2):
@@ -334,44 +390,50 @@ def main():
     e2e_times, _ = timed(e2e_step, args.steps)
     e2e_ms = statistics.mean(e2e_times)
     h2d = 8 * p.d * (2 if p.w is not None else 1) + 8
-    value_res = result.cpu().numpy()
+
+    # ---- every BASELINE config (c1-c5) -----------------------------------------------------------
+    configs = None
+    if not args.no_configs:
+        configs = {}
+        for i in range(1, 6):
+            q = S.baseline_config(i)
+            if i == args.config:
+                cplan, c_plan_ms, cdom, cpasses, ctimes, cdom_ms, cres = (plan, plan_ms, dominant, passes,
+                                                                          times, dom, value_res)
+            else:
+                cplan, c_plan_ms, cdom, cpasses, ctimes, cdom_ms, cres, _ = measure(q, args.steps, args.warmup)
+            cst = stats(ctimes)
+            npts = cplan.points()[1]
+            row = {"d": q.d, "q": q.q, "rule": S.RULE_NAMES[q.rule], "integrand": S.KIND_NAMES[q.kind],
+                   "points": npts, "plan_ms": c_plan_ms, "time_to_integral_ms": cst,
+                   "points_per_s": npts / (cst["mean"] * 1e-3), "points_per_s_best": npts / (cst["best"] * 1e-3),
+                   "parity": parity_block(q, cres, brief=True)}
+            if i >= 3 and cdom > 0:
+                row["dominant_kernel"] = roofline_from(cpasses[cdom].terms, statistics.mean(cdom_ms),
+                                                       fp64_counters(i), cplan, peak, mhz, None)
+                row["dominant_kernel"]["points"] = cpasses[cdom].terms
+            configs[q.name] = row
+            if cplan is not plan:
+                cplan.close()
 
     # merged leg (SG_MERGE_MIDPOINT): the same integral with the midpoint copies of
     # every point summed into merged coefficients, each remaining point evaluated once
     merged = None
     if not args.no_merged:
-        mplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
-                         device=dev, merge=api.MERGE_MIDPOINT)
-        mplan.profile_enable(True)
-        m_shard, m_total = mplan.points()
-        mpasses = mplan.passes()
-        mdom = max(range(1, len(mpasses)), key=lambda i: mpasses[i].terms) if len(mpasses) > 1 else 0
-        for _ in range(args.warmup):
-            step(mplan)
-        torch.cuda.synchronize(dev)
-        mstep = graph_step(mplan)
-        mstep()
-        m_times, m_dom = timed(mstep, args.steps, mplan, mdom)
-        m_res = result.cpu().numpy()
-        m_ms = statistics.mean(m_times)
-        mf, ma = mplan.leaf_work()
-        m_dom_ms = statistics.mean(m_dom)
-        peak_, mhz_ = peak_fp64_tflops()
-        m_ach = mpasses[mdom].terms * (2 * mf + ma) / (m_dom_ms * 1e-3) / 1e12
+        mplan, _, mdom, mpasses, m_times, m_dom, m_res, _ = measure(p, args.steps, args.warmup,
+                                                                    merge=api.MERGE_MIDPOINT)
+        m_total = mplan.points()[1]
+        mst = stats(m_times)
         merged = {
-            "time_to_integral_ms": m_ms, "points": m_total,
-            "value": m_total / (m_ms * 1e-3), "unit": "points/s",
-            "eq26_points_per_s": total_pts / (m_ms * 1e-3),
-            "speedup_vs_combination": ms / m_ms,
-            "result": float(m_res[0]),
+            "time_to_integral_ms": mst["mean"], "time_to_integral_stats_ms": mst, "points": m_total,
+            "value": m_total / (mst["mean"] * 1e-3), "unit": "points/s",
+            "eq26_points_per_s": total_pts / (mst["mean"] * 1e-3),
+            "speedup_vs_combination": ms / mst["mean"], "result": float(m_res[0]),
             "rel_diff_vs_combination": abs((float(m_res[0]) + float(m_res[1]))
                                            - (float(value_res[0]) + float(value_res[1])))
                                        / abs(float(value_res[0])),
-            "roofline": {"bound": "alu", "achieved": m_ach, "peak": peak_, "unit": "TFLOP/s",
-                         "frac": m_ach / peak_, "kernel": f"pass {mdom} ({mpasses[mdom].terms} points)",
-                         "kernel_ms": m_dom_ms, "fp64_inst_per_point": mf + ma,
-                         "pipe_frac": mpasses[mdom].terms * (mf + ma) / (m_dom_ms * 1e-3)
-                                      / (SM_COUNT * FP64_FMA_PER_SM_CLK * mhz_ * 1e6)},
+            "roofline": roofline_from(mpasses[mdom].terms, statistics.mean(m_dom),
+                                      fp64_counters(args.config, "merged"), mplan, peak, mhz, None),
             "step_ms_all": [round(t, 4) for t in m_times],
         }
         mplan.close()
@@ -381,41 +443,22 @@ def main():
     # emits the value, the other ranks a zero partial; the all-gather + finalize are unchanged)
     collapse = None
     if not args.no_collapse:
-        cplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
-                         device=dev, method=api.METHOD_COLLAPSE)
+        cplan, _ = make_plan(p, method=api.METHOD_COLLAPSE)
         for _ in range(args.warmup):
             step(cplan)
         torch.cuda.synchronize(dev)
-        c_times = []
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize(dev)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step(cplan)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            c_ms_i = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([c_ms_i], dtype=torch.float64,
-                                 device=dev if args.dist_backend == "nccl" else "cpu")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                c_ms_i = float(t.item())
-            c_times.append(c_ms_i)
+        c_times, _ = timed(lambda: step(cplan), args.steps)
         c_res = result.cpu().numpy()
         c_ms = statistics.mean(c_times)
         collapse = {
-            "time_to_integral_ms": c_ms, "eq26_points_per_s": total_pts / (c_ms * 1e-3),
+            "time_to_integral_ms": c_ms, "time_to_integral_stats_ms": stats(c_times),
+            "eq26_points_per_s": total_pts / (c_ms * 1e-3),
             "speedup_vs_combination": ms / c_ms, "result": float(c_res[0]),
             "rel_diff_vs_combination": abs((float(c_res[0]) + float(c_res[1]))
                                            - (float(value_res[0]) + float(value_res[1])))
                                        / abs(float(value_res[0])),
             "work": f"d*(L+1) = {p.d * (p.L + 1)} level sums + d truncated polynomial products "
                     f"of degree {p.L} (dd); launch-latency bound",
-            "step_ms_all": [round(t, 4) for t in c_times],
         }
         cplan.close()
 
@@ -427,13 +470,11 @@ def main():
     if not args.no_frontier:
         os.environ["SG_B200_NOFUSE"] = "1"
         try:
-            fplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world,
-                             device=dev)
+            fplan, _ = make_plan(p)
         finally:
             del os.environ["SG_B200_NOFUSE"]
         fplan.profile_enable(True)
         fpasses = fplan.passes()
-        # the pass writing the largest frontier
         wpass = max(range(1, len(fpasses)), key=lambda i: fpasses[i].written) if len(fpasses) > 1 else 0
         for _ in range(min(args.warmup, 2)):
             step(fplan)
@@ -458,19 +499,17 @@ def main():
                     "peak_gbs": hbm, "frac": (gbs / hbm) if hbm else None, "traffic": ftraffic}
         fplan.close()
 
-    # plain-SG ablation leg (SG_METHOD_PLAIN): the same integral with every point unranked and
-    # evaluated on its own (no dimension iteration) — what the MDI prefix reuse saves on this GPU
+    # plain-SG ablation leg (opt-in; SG_METHOD_PLAIN): the paper's comparison system on the GPU
     plain = None
-    if not args.no_plain:
-        pplan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u, rank=rank, world=world, device=dev,
-                         method=api.METHOD_PLAIN)
-        pplan.profile_enable(True)
+    if args.plain_ablation:
+        pplan, _ = make_plan(p, method=api.METHOD_PLAIN)
         step(pplan)
         torch.cuda.synchronize(dev)
-        p_times, _ = timed(lambda: step(pplan), 1, pplan, 0)
+        p_times, _ = timed(lambda: step(pplan), 1)
         p_res = result.cpu().numpy()
-        plain = {"what": "every point unranked on the device and its term formed from its t factors "
-                         "(the paper's plain SG method), dd accumulation; 1 timed step",
+        plain = {"what": "opt-in ablation (comparison system, out of the hot-path scope): every point "
+                         "unranked on the device and its term formed from its t factors, dd "
+                         "accumulation; 1 timed step",
                  "time_to_integral_ms": p_times[0], "value": total_pts / (p_times[0] * 1e-3),
                  "unit": "points/s", "mdi_speedup": p_times[0] / ms,
                  "rel_diff_vs_tree": abs((float(p_res[0]) + float(p_res[1]))
@@ -484,27 +523,17 @@ def main():
     corner = None
     if not args.no_corner:
         pc = S.corner_config()
-        kplan = api.Plan(pc.d, pc.q, pc.rule, pc.kind, pc.c, pc.w, pc.u, rank=rank, world=world,
-                         device=dev, arith=api.ARITH_SFORM_DD)
-        kplan.profile_enable(True)
-        k_shard, k_total = kplan.points()
-        for _ in range(args.warmup):
-            step(kplan)
-        torch.cuda.synchronize(dev)
-        kstep = graph_step(kplan)
-        kstep()
-        k_times, _ = timed(kstep, args.steps, kplan, 0)
-        k_res = result.cpu().numpy()
-        k_ms = statistics.mean(k_times)
+        kplan, _, _, _, k_times, _, k_res, _ = measure(pc, args.steps, args.warmup, arith=api.ARITH_SFORM_DD)
+        k_total = kplan.points()[1]
+        kst = stats(k_times)
         corner = {"workload": f"{pc.name}: Genz corner peak (1 + sum c_k x_k)^-(d+1), d={pc.d}, "
                               f"q=d+{pc.L}, {S.RULE_NAMES[pc.rule]}, c~U(0,1) seed 5, sum c = 1",
                   "arith": "s-form double-double (dd partial sums, dd power per point)",
-                  "points": k_total, "time_to_integral_ms": k_ms,
-                  "value": k_total / (k_ms * 1e-3), "unit": "points/s",
-                  "result": float(k_res[0]), "step_ms_all": [round(t, 4) for t in k_times]}
-        gfile = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
-        if os.path.exists(gfile):
-            vals = json.load(open(gfile))["values"]
+                  "points": k_total, "time_to_integral_ms": kst["mean"], "time_to_integral_stats_ms": kst,
+                  "value": k_total / (kst["mean"] * 1e-3), "unit": "points/s",
+                  "result": float(k_res[0])}
+        if os.path.exists(GOLDEN):
+            vals = json.load(open(GOLDEN))["values"]
             if pc.name in vals:
                 ref = float(vals[pc.name]["hi"]) + float(vals[pc.name]["lo"])
                 corner["rel_err_vs_oracle"] = abs(float(k_res[0]) + float(k_res[1]) - ref) / abs(ref)
@@ -512,47 +541,52 @@ def main():
 
     # rank-0 report
     if rank == 0:
-        peak, mhz = peak_fp64_tflops()
+        with ClockSampler(local) as bclk:
+            fp64_meas = measure_fp64_peak()
         dom_ms = statistics.mean(dom)
         dom_terms = passes[dominant].terms
-        fma_pp, add_pp = plan.leaf_work()
-        fpp, ipp = 2 * fma_pp + add_pp, fma_pp + add_pp
-        achieved = dom_terms * fpp / (dom_ms * 1e-3) / 1e12
+        roof = roofline_from(dom_terms, dom_ms, fp64_counters(args.config), plan, peak, mhz,
+                             fp64_meas if isinstance(fp64_meas, float) else None)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
             traffic = json.load(open(tfile)).get(f"c{args.config}")
-        parity = parity_block(p, value_res)
-        fp64_meas = measure_fp64_peak()
+        roof.update({"traffic": traffic, "kernel": f"pass {dominant} leaf kernel ({dom_terms} points)",
+                     "max_flop_frac_of_mix": roof["flops_per_point"] / (2 * roof["fp64_inst_per_point"]),
+                     "peak_note": f"FP64 peak derived: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} DFMA/clk x 2 x "
+                                  f"{mhz:.0f} MHz (MEASURED_PEAKS.json has no FP64 entry); measured DFMA "
+                                  f"burst {fp64_meas} TFLOP/s (tools/fp64_peak.cu, clocks in "
+                                  f"roofline.burst_clocks)",
+                     "burst_tflops": fp64_meas, "burst_clocks": bclk.summary(),
+                     "flops_note": "flops per point = (2 DFMA + DADD + DMUL) thread-instructions of this "
+                                   "launch / its points (ncu counters, profiles/fp64_counters.json); "
+                                   "DESIGN.md §6 explains why SURVEY.md §8d's textbook-dd 68 flops per "
+                                   "point are not this kernel's work"})
         line = {
             "metric": METRIC, "value": total_pts / (ms * 1e-3), "unit": "points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "time_to_integral_ms": ms, "higher_is_better": True, "scaling": "strong",
+            "time_to_integral_ms": ms, "time_to_integral_stats_ms": st,
+            "points_per_s_best": total_pts / (st["best"] * 1e-3),
+            "plan_ms": plan_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(p, {"parallelism": f"dp{world} (depth-1 subtree shards)",
-                                       "shard_points_rank0": shard_pts,
-                                       "launch": "stream launches" if args.no_graph else
-                                       "CUDA-graph replay of sg_integrate (+ sg_finalize)"}),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"pass {dominant} leaf kernel ({dom_terms} points)",
-                         "kernel_ms": dom_ms, "flops_per_point": round(fpp, 4),
-                         "fp64_inst_per_point": round(ipp, 4),
-                         "pipe_frac": dom_terms * ipp / (dom_ms * 1e-3)
-                                      / (SM_COUNT * FP64_FMA_PER_SM_CLK * mhz * 1e6),
-                         "max_flop_frac_of_mix": fpp / (2 * ipp),
-                         "peak_note": f"FP64 peak derived: {SM_COUNT} SMs x {FP64_FMA_PER_SM_CLK} "
-                                      f"DFMA/clk x 2 x {mhz:.0f} MHz; measured DFMA burst "
-                                      f"{fp64_meas} TFLOP/s"},
+            "config": config_block(p, total_pts, {
+                "parallelism": f"dp{world} (depth-1 subtree shards)", "shard_points_rank0": shard_pts,
+                "collective": ("nccl all_gather_into_tensor" if dist_on and args.dist_backend == "nccl"
+                               else "gloo (test aid)" if dist_on else "none (world 1)"),
+                "launch": "stream launches" if args.no_graph else
+                          "CUDA-graph replay of sg_integrate (+ sg_finalize)"}),
+            "roofline": roof,
             "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
             # per step: k_factor_base, k_suffix_abs, k_root, one kernel per pass >= 1,
             # k_reduce_fused, k_finalize
             "gpu_launches": (len(passes) - 1 + 5) * args.steps,
             "clocks": clk.summary(),
-            "parity": parity,
+            "parity": parity_block(p, value_res),
             "step_ms_all": [round(t, 4) for t in times],
         }
+        if configs is not None:
+            line["configs"] = configs
         if merged is not None:
             line["merged"] = merged
         if collapse is not None:
@@ -565,11 +599,24 @@ def main():
             line["plain_sg"] = plain
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(p)
+            line["cpu_baseline_fp64"] = cpu_baseline_fp64()
         print(json.dumps(line), flush=True)
     plan.close()
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def config_block(p, total_points, extra=None):
+    c = {"workload": f"BASELINE.json configs[{int(p.name[1:]) - 1}] ({p.name}): d={p.d}, "
+                     f"q=d+{p.L}, {S.RULE_NAMES[p.rule]}, {S.KIND_NAMES[p.kind]} integrand",
+         "d": p.d, "q": p.q, "L": p.L, "rule": S.RULE_NAMES[p.rule],
+         "integrand": S.KIND_NAMES[p.kind], "points": total_points,
+         "form": "combination (Eq 2.6)", "arith": "factor-form double-double",
+         "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+    if extra:
+        c.update(extra)
+    return c
 
 
 def closed_form(p):
@@ -592,24 +639,25 @@ def closed_form(p):
     return None
 
 
-def parity_block(p, res):
+def parity_block(p, res, brief=False):
     """GPU value against the stored full-size oracle value (tests/golden, written by oracle/ only)
     in 40-digit arithmetic, and the absolute / relative quadrature error against the closed form."""
     import mpmath as mp
     out = {"value": float(res[0])}
     with mp.workdps(40):
         got = mp.mpf(float(res[0])) + mp.mpf(float(res[1]))
-        gfile = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
-        if os.path.exists(gfile):
-            vals = json.load(open(gfile))["values"]
+        if os.path.exists(GOLDEN):
+            vals = json.load(open(GOLDEN))["values"]
             if p.name in vals:
                 ref = mp.mpf(vals[p.name]["text"])
-                out.update({"oracle": vals[p.name]["text"],
-                            "rel_err_vs_oracle": float(abs((got - ref) / ref)),
-                            "gate": 1e-12})
+                if not brief:
+                    out["oracle"] = vals[p.name]["text"]
+                out.update({"rel_err_vs_oracle": float(abs((got - ref) / ref)), "gate": 1e-12})
         cf = closed_form(p)
         if cf is not None:
-            out.update({"closed_form": mp.nstr(cf, 20), "abs_err_vs_closed_form": float(abs(got - cf)),
+            if not brief:
+                out["closed_form"] = mp.nstr(cf, 20)
+            out.update({"abs_err_vs_closed_form": float(abs(got - cf)),
                         "rel_err_vs_closed_form": float(abs((got - cf) / cf))})
     return out
 
@@ -618,7 +666,6 @@ def measure_fp64_peak():
     lib_path = os.path.join(ROOT, "tools", "libfp64peak.so")
     try:
         if not os.path.exists(lib_path):
-            import subprocess
             subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode",
                                    "arch=compute_100a,code=sm_100a", "-O3", "-shared",
                                    "-Xcompiler", "-fPIC", os.path.join(ROOT, "tools", "fp64_peak.cu"),
@@ -634,15 +681,18 @@ def measure_fp64_peak():
 
 
 def bench_reference(p, args, world):
-    """--impl reference: the CPU oracle (oracle/, __float128, OpenMP) as it stands, each step a
-    bounded sample of the workload (a fixed depth-1 subtree range)."""
-    target = int(4e7)
-    lo, hi, npts = oracle_sample_range(p, target)
-    for _ in range(args.warmup):
-        run_oracle_sample(p, lo, hi)
-    secs, pts = [], 0
+    """--impl reference: the CPU oracle (oracle/, __float128, OpenMP) as it stands on the box's host
+    cores, each step the same bounded sample of the workload (every s-th depth-2 multi-index subtree
+    of the whole tree, oracle.timing_sample).  Loads only oracle/ (never the product library)."""
+    import oracle
+    target = int(1e7)
+    total = oracle.n_points(p)
+    r0, stride, _ = oracle_sample(p, target)
+    for _ in range(max(0, args.warmup - 1)):
+        oracle.integrate_problem(p, stride=stride, include_root=False, eval_mode=1, nthreads=os.cpu_count())
+    secs, pts = [], r0.npoints
     for _ in range(args.steps):
-        r = run_oracle_sample(p, lo, hi)
+        r = oracle.integrate_problem(p, stride=stride, include_root=False, eval_mode=1, nthreads=os.cpu_count())
         secs.append(r.seconds)
         pts = r.npoints
     ms = statistics.mean(secs) * 1e3
@@ -653,10 +703,11 @@ def bench_reference(p, args, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f128",
         "data": "synthetic",
-        "config": config_block(p, {"sample_points_per_step": pts, "sample_range": [lo, hi],
-                                   "arith": "__float128, plain Eq 2.6/2.7 point enumeration (oracle/)"}),
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{p.name} depth-1 subtrees [{lo},{hi}) = {pts} points per step"},
+        "config": config_block(p, total, {"sample_points_per_step": pts, "sample_stride": stride,
+                                          "arith": "__float128, plain Eq 2.6/2.7 point enumeration (oracle/)"}),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "cpu": cpu_model(),
+                         "kind": "oracle", "sample": sample_text(p, r0, stride, total, "__float128 oracle")
+                         + " per step"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

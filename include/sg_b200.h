@@ -128,7 +128,10 @@ typedef enum { SG_MERGE_NONE = 0, SG_MERGE_MIDPOINT = 1 } sg_merge;
  *                    every other rank a zero partial (so sg_finalize's sum is the value).  Requires
  *                    SG_MERGE_NONE (else SG_EINVAL) and SG_ARITH_FACTOR_DD (else SG_EUNSUPPORTED);
  *                    sg_plan_passes reports 0 passes. */
-/*  METHOD_PLAIN    = ablation: the paper's plain SG baseline on the GPU — no dimension iteration; every
+/*  METHOD_PLAIN    = opt-in ablation, not part of the hot path: the paper's plain SG comparison
+ *                    system (SURVEY.md §2a P25 marks it out of scope), kept only to
+ *                    measure what the MDI reuse saves (bench.py --plain-ablation; off by default)
+ *                    on the GPU — no dimension iteration; every
  *                    point of the shard is unranked (device K1) and its term formed from its t
  *                    factors on its own (sg_eval_points' arithmetic), dd accumulation in a fixed
  *                    order.  Same value; measures what the MDI prefix reuse saves.  Factor
@@ -153,58 +156,79 @@ typedef struct {
 
 typedef struct sg_plan_s *sg_plan_t;
 
-/* Build a plan: validates arguments, builds the 1-D rule tables (double, correctly rounded from
+/* Defined by: the problem Q_d^q(f) of PAPER.md:65-67 (Eq 2.6, accuracy level q, d dimensions) with
+ * the tensor rules of PAPER.md:69-71 (Eq 2.7) and the 1-D rules of PAPER.md:103-147 (Eqs 2.10-2.13);
+ * errors after SPEC.md:66 (UnsupportedLevel), 194 (Overflow), 347 (BudgetTooSmall).
+ * Build a plan: validates arguments, builds the 1-D rule tables (double, correctly rounded from
  * quad evaluations of Eqs 2.11/2.13 on [0,1]), the counting tables of the prefix tree and the
  * shard range; allocates plan-owned device tables and copies the integrand parameters (H2D,
  * synchronous).  q = d + L.  On success *out owns device memory until sg_destroy. */
 int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, const sg_options *opt,
             sg_plan_t *out);
 
-/* Bytes of caller-provided device workspace (frontier ping-pong buffers + reduction partials). */
+/* Defined by: DESIGN.md §5 (no paper passage: the frontier of the level-synchronous walk of
+ * PAPER.md:248-295 needs scratch that the caller owns).
+ * Bytes of caller-provided device workspace (frontier ping-pong buffers + reduction partials). */
 int sg_workspace_size(sg_plan_t p, size_t *bytes);
 
-/* Attach caller-owned device workspace of at least sg_workspace_size bytes (256-byte aligned). */
+/* Defined by: DESIGN.md §5 (ownership contract of SURVEY.md §8b).
+ * Attach caller-owned device workspace of at least sg_workspace_size bytes (256-byte aligned). */
 int sg_set_workspace(sg_plan_t p, void *dev_ptr, size_t bytes);
 
-/* Replace the integrand parameters (same kind and d) by an async copy from `f` on stream s.
+/* Defined by: the integrand parameters of the BASELINE configs / Genz families (PAPER.md:619 Test 8
+ * kinds; BASELINE.json configs); f only, the quadrature Q_d^q is unchanged.
+ * Replace the integrand parameters (same kind and d) by an async copy from `f` on stream s.
  * f->c / f->w may be host memory (pinned for true asynchrony) or device memory. */
 int sg_update_integrand(sg_plan_t p, sg_stream_t s, const sg_integrand_desc *f);
 
-/* Enqueue the whole hot path on stream s: factor tables (K0), root pass, level-synchronous
+/* Defined by: Q_d^q(f) = Eq 2.6 with Eq 2.7, evaluated by the multilevel dimension
+ * iteration of PAPER.md:248-295 (Eqs 3.8-3.11, Algorithm 3.3: partial results carried one coordinate
+ * at a time, "the function evaluation at any integration point is not completed until the last
+ * step").
+ * Enqueue the whole hot path on stream s: factor tables (K0), root pass, level-synchronous
  * frontier/leaf passes (K2/K3), deterministic reduction (K4).  out_dev (device, 2 doubles) receives
  * this plan's partial sum as a double-double (hi, lo).  Bitwise reproducible for a fixed plan. */
 int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev);
 
-/* Fixed-order double-double sum of `world` gathered partials (device, 2*world doubles, rank order)
+/* Defined by: the outer sum of Eq 2.6 split over disjoint point sets (the shards of
+ * sg_options); summation order fixed after SPEC.md:204-207 (determinism).
+ * Fixed-order double-double sum of `world` gathered partials (device, 2*world doubles, rank order)
  * into result_dev (device, 2 doubles: value rounded to double, and the residual).  Writes NaN if
  * the plan's non-finite flag is set. */
 int sg_finalize(sg_plan_t p, sg_stream_t s, const double *gathered_dev, int world,
                 double *result_dev);
 
-/* Synchronous convenience: H2D of nothing, runs sg_integrate + sg_finalize(world=1) on s,
+/* Defined by: Q_d^q(f), PAPER.md:65-67 (Eq 2.6), as sg_integrate + sg_finalize at world 1.
+ * Synchronous convenience: H2D of nothing, runs sg_integrate + sg_finalize(world=1) on s,
  * copies the 2-double result into result_host and synchronises s. Returns SG_ENONFINITE if
  * the result is not finite. */
 int sg_integrate_host(sg_plan_t p, sg_stream_t s, double *result_host);
 
-/* Synchronously read the device status word (SG_OK or SG_ENONFINITE). */
+/* Defined by: NonFiniteIntegrand.
+ * Synchronously read the device status word (SG_OK or SG_ENONFINITE). */
 int sg_status_word(sg_plan_t p, int *status);
 
-/* Number of Smolyak points n_d^q this plan evaluates (its shard), and of the whole problem. */
+/* Defined by: n_d^q = sum_{q-d+1 <= |l| <= q} n_{l_1} ... n_{l_d}.
+ * Number of Smolyak points n_d^q this plan evaluates (its shard), and of the whole problem. */
 int sg_plan_points(sg_plan_t p, unsigned long long *shard_points,
                    unsigned long long *total_points);
 
-/* Shard range actually used: [lo, hi) in depth-1 rank space, and M0 * d (= number of depth-1
+/* Defined by: DESIGN.md reading R15 (the paper does not partition work across devices).
+ * Shard range actually used: [lo, hi) in depth-1 rank space, and M0 * d (= number of depth-1
  * prefixes). */
 int sg_plan_range(sg_plan_t p, long long *lo, long long *hi, long long *n_depth1);
 
-/* Per-pass launch statistics of the last plan: number of passes, and for pass i the number of
+/* Defined by: the per-step partial functions f_{t-m} of PAPER.md:268-295 (Eqs 3.9-3.11): pass t
+ * carries the prefixes with t active coordinates.
+ * Per-pass launch statistics of the last plan: number of passes, and for pass i the number of
  * tree nodes (leaf terms) it evaluates and the frontier nodes it writes (the depth-(L-1) points that
  * k_leaf2_sym3's source tasks evaluate are counted in the last pass, whose kernel runs them).  Arrays of length >=
  * *npass (query with NULL arrays first). */
 int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
                    unsigned long long *written);
 
-/* Host-only measurement helper: the FP64 instructions per Smolyak point of the leaf kernel variant
+/* Defined by: DESIGN.md §6 (measurement), no paper passage.
+ * Host-only measurement helper: the FP64 instructions per Smolyak point of the leaf kernel variant
  * this plan runs for its dominant (last) pass — DFMA and DADD thread-instructions per point,
  * averaged over one level-2 row (midpoint, symmetric-pair and zero-tail specialisations included)
  * and, for k_leaf2_sym3, weighted with its level-3 source-task points (general oscillatory terms).
@@ -212,11 +236,14 @@ int sg_plan_passes(sg_plan_t p, int *npass, unsigned long long *terms,
  * Both pointers must be non-NULL (else SG_EINVAL). */
 int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_point);
 
-/* Debug/test hook: copy the device factor table (per level l = 2..L+1, coordinate k, node j;
+/* Defined by: the per-coordinate weights and nodes of Eq 2.7 times the
+ * integrand's per-coordinate factor.
+ * Debug/test hook: copy the device factor table (per level l = 2..L+1, coordinate k, node j;
  * doubles per entry: 2 real dd or 4 complex dd) and the base value to host memory. */
 int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host);
 
-/* Profiling hook.  When enabled, sg_integrate records a CUDA event on its stream before its first
+/* Defined by: DESIGN.md §6 (measurement), no paper passage.
+ * Profiling hook.  When enabled, sg_integrate records a CUDA event on its stream before its first
  * kernel and after each kernel.  sg_profile_read waits for the events of the LAST sg_integrate and
  * writes the device duration (ms) of each launch, in launch order:
  *   [K0 factor table, K0 base, root pass, pass 1 .. pass nfront, final reduce]
@@ -226,13 +253,16 @@ int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, doubl
 int sg_profile_enable(sg_plan_t p, int enable);
 int sg_profile_read(sg_plan_t p, float *ms, int *n);
 
-/* Host-only (no device touched): the plan's counts and shard range for (d, q, rule, kind, opt).
+/* Defined by: n_d^q and the shard partition of DESIGN.md reading R15.
+ * Host-only (no device touched): the plan's counts and shard range for (d, q, rule, kind, opt).
  * Any output pointer may be NULL.  Same validation and error codes as sg_plan. */
 int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
                   unsigned long long *shard_points, unsigned long long *total_points,
                   long long *range_lo, long long *range_hi, int *n_passes);
 
-/* Host-only K1 unranker (north-star subsystem 1): the `index`-th Smolyak point of the shard
+/* Defined by: the bijection k -> (x_{j_1}^{l_1}, ..., x_{j_d}^{l_d}) of PAPER.md:77-79 between the
+ * n_d^q points and their multi-index / node tuples, with the Eq 2.6 coefficient.
+ * Host-only K1 unranker (north-star subsystem 1): the `index`-th Smolyak point of the shard
  * described by (d, q, rule, kind, opt) in canonical order — the root (all-midpoint point) if the
  * shard includes it and its coefficient is nonzero, then the depth-1 subtrees r1 = lo .. hi-1, each
  * in preorder with children ordered by (k', l', j').  Outputs (host arrays of >= L entries): *t =
@@ -242,7 +272,9 @@ int sg_plan_query(int d, int q, sg_rule rule, sg_kind kind, const sg_options *op
 int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
               unsigned long long index, int *t, int *k, int *l, int *j, double *coef);
 
-/* Device K1 + per-point evaluation (validation path): for each of the n flat
+/* Defined by: PAPER.md:77-79 (point bijection) and Eq 2.7's summand w_{j_1}^{l_1}...w_{j_d}^{l_d}
+ * f(x) times the Eq 2.6 coefficient.
+ * Device K1 + per-point evaluation (validation path): for each of the n flat
  * indices in index_dev (device, shard order of sg_unrank), enqueue on stream s the unranking and the
  * point's term evaluated on its own — coefficient * Re(B * prod of its per-coordinate factors), in
  * double-double, straight from the factor table (independent of the tree's partial products).
@@ -253,13 +285,16 @@ int sg_unrank(int d, int q, sg_rule rule, sg_kind kind, const sg_options *opt,
 int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long long *index_dev, long long n,
                    int *points_dev, double *terms_dev);
 
-/* Host-only: the library's 1-D rule of `level` on [0,1] (n_l doubles each, ascending nodes),
+/* Defined by: PAPER.md:103-147 (Eqs 2.10-2.13: trapezoidal, Clenshaw-Curtis, Gauss-Patterson,
+ * Gauss-Legendre), mapped to [0,1] (reading R2).
+ * Host-only: the library's 1-D rule of `level` on [0,1] (n_l doubles each, ascending nodes),
  * rounded once from __float128 evaluations of Eq 2.11 / Eq 2.13.  Returns n_l, or a negative
  * status (SG_EINVAL bad rule/level, SG_EUNSUPPORTED above the table limits).  x, w: host arrays of
  * at least n_l doubles. */
 int sg_rule_table(sg_rule rule, int level, double *x, double *w);
 
-/* Free plan-owned device memory.  The stream the plan was used on must be idle. */
+/* Defined by: the ownership contract of SURVEY.md §8b.
+ * Free plan-owned device memory.  The stream the plan was used on must be idle. */
 int sg_destroy(sg_plan_t p);
 
 /* Static string for a status code. */

@@ -26,6 +26,24 @@
 
 typedef __float128 quad;
 
+/* Summation / integrand arithmetic.  Default: __float128 (the parity oracle).  Compiled with
+ * -DSGO_FP64 (liboracle_sg_fp64.so) the SAME program sums and evaluates f in double: the plain FP64
+ * oracle, a CPU speed baseline that is not parity-grade.  The 1-D rule tables are
+ * generated in quad and rounded to double in both builds (identical inputs). */
+#ifdef SGO_FP64
+typedef double sreal;
+#define SR_EXP exp
+#define SR_COS cos
+#define SR_POW pow
+#define SR_PI M_PI
+#else
+typedef quad sreal;
+#define SR_EXP expq
+#define SR_COS cosq
+#define SR_POW powq
+#define SR_PI M_PIq
+#endif
+
 enum { SGO_RULE_TRAP = 1, SGO_RULE_CC = 2, SGO_RULE_GP = 3, SGO_RULE_GL = 4 };
 enum { SGO_EXP = 0, SGO_OSC = 1, SGO_PEAK = 2, SGO_GAUSS = 3, SGO_CORNER = 4, SGO_MONOMIAL = 9 };
 #define SGO_MAX_LEVEL 20
@@ -294,82 +312,82 @@ typedef struct {
     int d, kind;
     const double *c, *w;
     double u;
-    quad two_pi_u;     /* 2 pi u, quad */
-    quad *cinv2;       /* c_k^-2, quad (peak) */
-    quad s_mid;        /* sum_k c_k / 2 (exp/osc) or sum_k c_k^2 (1/2 - w_k)^2 (gauss) */
-    quad peak_mid;     /* prod_k 1/(c_k^-2 + (1/2 - w_k)^2) */
+    sreal two_pi_u;     /* 2 pi u */
+    sreal *cinv2;       /* c_k^-2 (peak) */
+    sreal s_mid;        /* sum_k c_k / 2 (exp/osc) or sum_k c_k^2 (1/2 - w_k)^2 (gauss) */
+    sreal peak_mid;     /* prod_k 1/(c_k^-2 + (1/2 - w_k)^2) */
 } integrand;
 
 /* Plain O(d) evaluation: f(x_1..x_d) exactly as written in BASELINE.json. */
-static quad f_plain(const integrand *F, const double *x) {
+static sreal f_plain(const integrand *F, const double *x) {
     const int d = F->d;
-    quad s = 0, p = 1;
+    sreal s = 0, p = 1;
     switch (F->kind) {
     case SGO_EXP:
-        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
-        return expq(s);
+        for (int k = 0; k < d; ++k) s += (sreal)F->c[k] * (sreal)x[k];
+        return SR_EXP(s);
     case SGO_OSC:
-        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
-        return cosq(F->two_pi_u + s);
+        for (int k = 0; k < d; ++k) s += (sreal)F->c[k] * (sreal)x[k];
+        return SR_COS(F->two_pi_u + s);
     case SGO_PEAK:
         for (int k = 0; k < d; ++k) {
-            quad t = (quad)x[k] - (quad)F->w[k];
+            sreal t = (sreal)x[k] - (sreal)F->w[k];
             p *= 1 / (F->cinv2[k] + t * t);
         }
         return p;
     case SGO_GAUSS:
         for (int k = 0; k < d; ++k) {
-            quad t = (quad)x[k] - (quad)F->w[k];
-            s += (quad)F->c[k] * (quad)F->c[k] * t * t;
+            sreal t = (sreal)x[k] - (sreal)F->w[k];
+            s += (sreal)F->c[k] * (sreal)F->c[k] * t * t;
         }
-        return expq(-s);
+        return SR_EXP(-s);
     case SGO_CORNER: /* Genz corner peak: (1 + sum_k c_k x_k)^-(d+1) */
-        for (int k = 0; k < d; ++k) s += (quad)F->c[k] * (quad)x[k];
-        return powq(1 + s, -(quad)(d + 1));
+        for (int k = 0; k < d; ++k) s += (sreal)F->c[k] * (sreal)x[k];
+        return SR_POW(1 + s, -(sreal)(d + 1));
     case SGO_MONOMIAL: /* test-only: prod x_k^{alpha_k}, alpha_k = (int) w[k] */
         for (int k = 0; k < d; ++k) {
             int a = (int)F->w[k];
-            for (int e = 0; e < a; ++e) p *= (quad)x[k];
+            for (int e = 0; e < a; ++e) p *= (sreal)x[k];
         }
         return p;
     }
-    return nanq("");
+    return (sreal)NAN;
 }
 
 /* "Active" evaluation: the same f, using that every inactive coordinate sits at the midpoint 1/2
  * (level 1, reading R3), so sum_k c_k x_k = sum_k c_k/2 + sum_active c_k (x_k - 1/2) exactly in
  * real arithmetic (and the analogues for gauss/peak).  O(#active) per point; cross-checked
  * against f_plain in tests. */
-static quad f_active(const integrand *F, int t, const int *ak, const double *ax) {
-    quad s = 0, p;
+static sreal f_active(const integrand *F, int t, const int *ak, const double *ax) {
+    sreal s = 0, p;
     switch (F->kind) {
     case SGO_EXP:
-        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
-        return expq(F->s_mid + s);
+        for (int m = 0; m < t; ++m) s += (sreal)F->c[ak[m]] * ((sreal)ax[m] - (sreal)0.5);
+        return SR_EXP(F->s_mid + s);
     case SGO_OSC:
-        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
-        return cosq(F->two_pi_u + F->s_mid + s);
+        for (int m = 0; m < t; ++m) s += (sreal)F->c[ak[m]] * ((sreal)ax[m] - (sreal)0.5);
+        return SR_COS(F->two_pi_u + F->s_mid + s);
     case SGO_CORNER:
-        for (int m = 0; m < t; ++m) s += (quad)F->c[ak[m]] * ((quad)ax[m] - 0.5Q);
-        return powq(1 + F->s_mid + s, -(quad)(F->d + 1));
+        for (int m = 0; m < t; ++m) s += (sreal)F->c[ak[m]] * ((sreal)ax[m] - (sreal)0.5);
+        return SR_POW(1 + F->s_mid + s, -(sreal)(F->d + 1));
     case SGO_GAUSS:
         for (int m = 0; m < t; ++m) {
             int k = ak[m];
-            quad c2 = (quad)F->c[k] * (quad)F->c[k];
-            quad a = (quad)ax[m] - (quad)F->w[k], b = 0.5Q - (quad)F->w[k];
+            sreal c2 = (sreal)F->c[k] * (sreal)F->c[k];
+            sreal a = (sreal)ax[m] - (sreal)F->w[k], b = (sreal)0.5 - (sreal)F->w[k];
             s += c2 * (a * a - b * b);
         }
-        return expq(-(F->s_mid + s));
+        return SR_EXP(-(F->s_mid + s));
     case SGO_PEAK:
         p = F->peak_mid;
         for (int m = 0; m < t; ++m) {
             int k = ak[m];
-            quad a = (quad)ax[m] - (quad)F->w[k], b = 0.5Q - (quad)F->w[k];
+            sreal a = (sreal)ax[m] - (sreal)F->w[k], b = (sreal)0.5 - (sreal)F->w[k];
             p *= (F->cinv2[k] + b * b) / (F->cinv2[k] + a * a);
         }
         return p;
     }
-    return nanq("");
+    return (sreal)NAN;
 }
 
 /* ---------------------------------------------------------------------------------------------
@@ -388,16 +406,18 @@ typedef struct {
     const integrand *F;
     int nl[SGO_MAX_LEVEL + 2];
     double *X[SGO_MAX_LEVEL + 2], *W[SGO_MAX_LEVEL + 2];
-    quad coef[SGO_MAX_LEVEL + 2];
+    sreal coef[SGO_MAX_LEVEL + 2];
     int64_t M0;                      /* number of depth-1 (k1,l1,j1) triples per coordinate */
     int64_t lo, hi;                  /* shard: depth-1 lexicographic range [lo, hi) */
+    int64_t stride;                  /* sample: every stride-th depth-2 subtree of each top-level item */
+    int count_only;                  /* count the selected points, evaluate nothing */
 } problem;
 
 typedef struct {
     int t;                           /* number of active coordinates */
     int ak[SGO_MAX_LEVEL + 2], al[SGO_MAX_LEVEL + 2];
     double *xfull;                   /* full point for the plain evaluator */
-    quad sum;
+    sreal sum;
     int64_t npoints;
 } walker;
 
@@ -421,16 +441,22 @@ static void tensor_sum(const problem *P, walker *Wk, int e) {
         if (b < jhi0) jhi0 = (int)(b > jlo0 ? b : jlo0);
         if (jlo0 >= jhi0) return;
     }
+    if (P->count_only) {
+        int64_t n = t > 0 ? jhi0 - jlo0 : 1;
+        for (int m = 1; m < t; ++m) n *= P->nl[Wk->al[m]];
+        Wk->npoints += n;
+        return;
+    }
     for (int m = 0; m < t; ++m) j[m] = 0;
     if (t > 0) j[0] = jlo0;
-    quad acc = 0;
+    sreal acc = 0;
     for (;;) {
-        quad wprod = 1;
+        sreal wprod = 1;
         for (int m = 0; m < t; ++m) {
-            wprod *= (quad)P->W[Wk->al[m]][j[m]];
+            wprod *= (sreal)P->W[Wk->al[m]][j[m]];
             ax[m] = P->X[Wk->al[m]][j[m]];
         }
-        quad fx;
+        sreal fx;
         if (P->eval_mode == 0) {
             for (int m = 0; m < t; ++m) Wk->xfull[Wk->ak[m]] = ax[m];
             fx = f_plain(P->F, Wk->xfull);
@@ -474,10 +500,17 @@ static void walk(const problem *P, walker *Wk, int kstart, int e) {
  * Outputs: out_hilo[0] + out_hilo[1] = quad result rounded to a double pair; out_str = "%.36Qe";
  * out_npoints = tensor points evaluated; out_seconds = wall time of the summation.
  * Returns 0, or -1 on bad arguments.
+ * sgo_integrate_ex adds: stride (> 1: only the points of every stride-th depth-2 multi-index subtree
+ * (k1, l1, k2, l2, ...) of each top-level item (k1, l1), in walk order, the counter starting at the
+ * item's index: an evenly spread sample of the whole tree for CPU timing; the root and the depth-1
+ * multi-indices are not sampled) and count_only (return the number of selected points in
+ * out_npoints, evaluate nothing).
  */
-int sgo_integrate(int d, int L, int rule, int kind, const double *c, const double *w, double u,
-                  long long lo, long long hi, int include_root, int eval_mode, int nthreads,
-                  double *out_hilo, char *out_str, long long *out_npoints, double *out_seconds) {
+int sgo_integrate_ex(int d, int L, int rule, int kind, const double *c, const double *w, double u,
+                     long long lo, long long hi, long long stride, int include_root, int eval_mode,
+                     int nthreads, int count_only, double *out_hilo, char *out_str,
+                     long long *out_npoints, double *out_seconds) {
+    if (stride < 1) return -1;
     if (d < 1 || L < 0 || L + 1 > SGO_MAX_LEVEL || !c) return -1;
     if ((kind == SGO_PEAK || kind == SGO_GAUSS || kind == SGO_MONOMIAL) && !w) return -1;
     if (kind == SGO_MONOMIAL && eval_mode != 0) return -1;
@@ -500,41 +533,93 @@ int sgo_integrate(int d, int L, int rule, int kind, const double *c, const doubl
     }
     for (int e = 0; e <= L; ++e) {
         quad b = binom_q(d - 1, L - e);
-        P.coef[e] = ((L - e) % 2 ? -b : b);
+        P.coef[e] = (sreal)((L - e) % 2 ? -b : b);   /* exact in double too: |C| < 2^53 (plan limits) */
     }
     P.M0 = 0;
     for (int l = 2; l <= L + 1; ++l) P.M0 += P.nl[l];
     P.lo = lo; P.hi = hi < 0 ? (int64_t)d * P.M0 + 1 : hi;
+    P.stride = stride; P.count_only = count_only;
 
     integrand F;
     memset(&F, 0, sizeof F);
     F.d = d; F.kind = kind; F.c = c; F.w = w; F.u = u;
-    F.two_pi_u = 2 * M_PIq * (quad)u;
-    F.cinv2 = (quad *)malloc(sizeof(quad) * d);
+    F.two_pi_u = 2 * SR_PI * (sreal)u;
+    F.cinv2 = (sreal *)malloc(sizeof(sreal) * d);
     F.s_mid = 0; F.peak_mid = 1;
     for (int k = 0; k < d; ++k) {
-        F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
-        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (quad)c[k] / 2;
+        F.cinv2[k] = 1 / ((sreal)c[k] * (sreal)c[k]);
+        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (sreal)c[k] / 2;
         if (kind == SGO_GAUSS) {
-            quad b = 0.5Q - (quad)w[k];
-            F.s_mid += (quad)c[k] * (quad)c[k] * b * b;
+            sreal b = (sreal)0.5 - (sreal)w[k];
+            F.s_mid += (sreal)c[k] * (sreal)c[k] * b * b;
         }
         if (kind == SGO_PEAK) {
-            quad b = 0.5Q - (quad)w[k];
+            sreal b = (sreal)0.5 - (sreal)w[k];
             F.peak_mid *= 1 / (F.cinv2[k] + b * b);
         }
     }
     P.F = &F;
 
+    if (stride > 1) {
+        /* Timing sample: the depth-2 multi-index subtrees (k1, l1, k2, l2) in lexicographic order,
+         * numbered 0, 1, 2, ...; every stride-th one, starting at stride / 2; OpenMP over the
+         * selected subtrees, partial sums added in list order.  The root and the depth-1
+         * multi-indices are not part of the sample. */
+        int64_t nsel = 0, cap = 1024, cnt = 0;
+        int *U = (int *)malloc(sizeof(int) * 4 * cap);
+        for (int k1 = 0; k1 < d; ++k1)
+            for (int l1 = 2; l1 <= L + 1; ++l1) {
+                for (int k2 = k1 + 1; k2 < d; ++k2)
+                    for (int l2 = 2; l2 <= L + 1 - (l1 - 1); ++l2, ++cnt) {
+                        if (cnt % stride != stride / 2) continue;
+                        if (nsel == cap) { cap *= 2; U = (int *)realloc(U, sizeof(int) * 4 * cap); }
+                        U[4 * nsel] = k1; U[4 * nsel + 1] = l1; U[4 * nsel + 2] = k2; U[4 * nsel + 3] = l2;
+                        ++nsel;
+                    }
+            }
+        sreal *usum = (sreal *)calloc(nsel > 0 ? nsel : 1, sizeof(sreal));
+        int64_t *upts = (int64_t *)calloc(nsel > 0 ? nsel : 1, sizeof(int64_t));
+        if (nthreads > 0) omp_set_num_threads(nthreads);
+        struct timespec s0, s1;
+        clock_gettime(CLOCK_MONOTONIC, &s0);
+#pragma omp parallel
+        {
+            walker Wk;
+            memset(&Wk, 0, sizeof Wk);
+            Wk.xfull = (double *)malloc(sizeof(double) * d);
+            for (int k = 0; k < d; ++k) Wk.xfull[k] = 0.5;
+#pragma omp for schedule(dynamic, 1)
+            for (int64_t i = 0; i < nsel; ++i) {
+                Wk.sum = 0; Wk.npoints = 0; Wk.t = 2;
+                Wk.ak[0] = U[4 * i]; Wk.al[0] = U[4 * i + 1]; Wk.ak[1] = U[4 * i + 2]; Wk.al[1] = U[4 * i + 3];
+                walk(&P, &Wk, Wk.ak[1] + 1, Wk.al[0] - 1 + Wk.al[1] - 1);
+                usum[i] = Wk.sum; upts[i] = Wk.npoints;
+            }
+            free(Wk.xfull);
+        }
+        sreal tot = 0;
+        int64_t np = 0;
+        for (int64_t i = 0; i < nsel; ++i) { tot += usum[i]; np += upts[i]; }
+        clock_gettime(CLOCK_MONOTONIC, &s1);
+        double hd = (double)tot;
+        if (out_hilo) { out_hilo[0] = hd; out_hilo[1] = (double)(tot - (sreal)hd); }
+        if (out_str) quadmath_snprintf(out_str, 64, "%.36Qe", (quad)tot);
+        if (out_npoints) *out_npoints = np;
+        if (out_seconds) *out_seconds = (s1.tv_sec - s0.tv_sec) + 1e-9 * (s1.tv_nsec - s0.tv_nsec);
+        for (int l = 1; l <= L + 1; ++l) { free(P.X[l]); free(P.W[l]); }
+        free(F.cinv2); free(U); free(usum); free(upts);
+        return 0;
+    }
+
     /* top-level items: (k1, l1) for k1 in [0,d), l1 in [2, L+1]; item sums added in order */
     const int nitems = d * L;
-    quad *item_sum = (quad *)calloc(nitems > 0 ? nitems : 1, sizeof(quad));
+    sreal *item_sum = (sreal *)calloc(nitems > 0 ? nitems : 1, sizeof(sreal));
     int64_t *item_pts = (int64_t *)calloc(nitems > 0 ? nitems : 1, sizeof(int64_t));
     if (nthreads > 0) omp_set_num_threads(nthreads);
     struct timespec t0, t1;
     clock_gettime(CLOCK_MONOTONIC, &t0);
 
-    quad root_sum = 0;
+    sreal root_sum = 0;
     int64_t root_pts = 0;
     if (include_root && P.emin == 0) {
         walker Wk;
@@ -564,20 +649,27 @@ int sgo_integrate(int d, int L, int rule, int kind, const double *c, const doubl
         }
         free(Wk.xfull);
     }
-    quad total = root_sum;
+    sreal total = root_sum;
     int64_t npts = root_pts;
     for (int it = 0; it < nitems; ++it) { total += item_sum[it]; npts += item_pts[it]; }
     clock_gettime(CLOCK_MONOTONIC, &t1);
 
     double hi_d = (double)total;
-    double lo_d = (double)(total - (quad)hi_d);
+    double lo_d = (double)(total - (sreal)hi_d);
     if (out_hilo) { out_hilo[0] = hi_d; out_hilo[1] = lo_d; }
-    if (out_str) quadmath_snprintf(out_str, 64, "%.36Qe", total);
+    if (out_str) quadmath_snprintf(out_str, 64, "%.36Qe", (quad)total);
     if (out_npoints) *out_npoints = npts;
     if (out_seconds) *out_seconds = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
     for (int l = 1; l <= L + 1; ++l) { free(P.X[l]); free(P.W[l]); }
     free(F.cinv2); free(item_sum); free(item_pts);
     return 0;
+}
+
+int sgo_integrate(int d, int L, int rule, int kind, const double *c, const double *w, double u,
+                  long long lo, long long hi, int include_root, int eval_mode, int nthreads,
+                  double *out_hilo, char *out_str, long long *out_npoints, double *out_seconds) {
+    return sgo_integrate_ex(d, L, rule, kind, c, w, u, lo, hi, 1, include_root, eval_mode, nthreads, 0,
+                            out_hilo, out_str, out_npoints, out_seconds);
 }
 
 /* Single-point evaluation (test hook): f at a full point x, plain and active forms. */
@@ -586,23 +678,23 @@ int sgo_eval_point(int d, int kind, const double *c, const double *w, double u, 
     integrand F;
     memset(&F, 0, sizeof F);
     F.d = d; F.kind = kind; F.c = c; F.w = w; F.u = u;
-    F.two_pi_u = 2 * M_PIq * (quad)u;
-    F.cinv2 = (quad *)malloc(sizeof(quad) * d);
+    F.two_pi_u = 2 * SR_PI * (sreal)u;
+    F.cinv2 = (sreal *)malloc(sizeof(sreal) * d);
     F.peak_mid = 1;
     int *ak = (int *)malloc(sizeof(int) * d);
     double *ax = (double *)malloc(sizeof(double) * d);
     int t = 0;
     for (int k = 0; k < d; ++k) {
-        F.cinv2[k] = 1 / ((quad)c[k] * (quad)c[k]);
-        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (quad)c[k] / 2;
-        if (kind == SGO_GAUSS) { quad b = 0.5Q - (quad)w[k]; F.s_mid += (quad)c[k] * (quad)c[k] * b * b; }
-        if (kind == SGO_PEAK) { quad b = 0.5Q - (quad)w[k]; F.peak_mid *= 1 / (F.cinv2[k] + b * b); }
+        F.cinv2[k] = 1 / ((sreal)c[k] * (sreal)c[k]);
+        if (kind == SGO_EXP || kind == SGO_OSC || kind == SGO_CORNER) F.s_mid += (sreal)c[k] / 2;
+        if (kind == SGO_GAUSS) { sreal b = (sreal)0.5 - (sreal)w[k]; F.s_mid += (sreal)c[k] * (sreal)c[k] * b * b; }
+        if (kind == SGO_PEAK) { sreal b = (sreal)0.5 - (sreal)w[k]; F.peak_mid *= 1 / (F.cinv2[k] + b * b); }
         if (x[k] != 0.5) { ak[t] = k; ax[t] = x[k]; ++t; }
     }
-    quad a = f_plain(&F, x);
-    quad b = kind == SGO_MONOMIAL ? a : f_active(&F, t, ak, ax);
-    out_plain[0] = (double)a; out_plain[1] = (double)(a - (quad)out_plain[0]);
-    out_active[0] = (double)b; out_active[1] = (double)(b - (quad)out_active[0]);
+    sreal a = f_plain(&F, x);
+    sreal b = kind == SGO_MONOMIAL ? a : f_active(&F, t, ak, ax);
+    out_plain[0] = (double)a; out_plain[1] = (double)(a - (sreal)out_plain[0]);
+    out_active[0] = (double)b; out_active[1] = (double)(b - (sreal)out_active[0]);
     free(F.cinv2); free(ak); free(ax);
     return 0;
 }

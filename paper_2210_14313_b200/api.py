@@ -54,6 +54,8 @@ class Plan:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2210_14313_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.d, self.q, self.rule, self.kind = int(d), int(q), int(rule), int(kind)
         self._c = np.ascontiguousarray(c, dtype=np.float64)
         self._w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
@@ -94,16 +96,28 @@ class Plan:
         return result
 
     def sg_update_integrand(self, c, w=None, u: float | None = None, stream=None):
-        """Async parameter refresh.  c/w: numpy (host) or torch tensors (pinned host or device)."""
+        """Async parameter refresh.  c/w: numpy (host) or torch tensors (pinned host or device).
+
+        Tensors must be float64, contiguous, with d elements, on the CPU or on this plan's device
+        (else ValueError: the C side reads exactly 8 d bytes from each pointer).  Host arrays are
+        staged by the CUDA runtime before the call returns (pageable memory) or read by the copy
+        engine in stream order (pinned tensors: keep them alive until the stream reaches the copy)."""
         dp = ctypes.POINTER(ctypes.c_double)
+        keep = []
 
         def ptr(a):
             if a is None:
                 return None
             if isinstance(a, torch.Tensor):
+                if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != self.d:
+                    raise ValueError("parameters must be contiguous float64 tensors of d elements")
+                if a.device.type != "cpu" and a.device != self.device:
+                    raise ValueError(f"parameter tensor on {a.device}, plan on {self.device}")
                 return ctypes.cast(ctypes.c_void_p(a.data_ptr()), dp)
             a = np.ascontiguousarray(a, dtype=np.float64)
-            self._keep = getattr(self, "_keep", []) + [a]
+            if a.size != self.d:
+                raise ValueError("parameters must have d elements")
+            keep.append(a)   # alive until sg_update_integrand returns (pageable: staged by then)
             return a.ctypes.data_as(dp)
 
         desc = sg_integrand_desc(self.kind, self.d, ptr(c), ptr(w), float(self.u if u is None else u))

@@ -859,8 +859,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         // plan.h T2
         const long long first = A.T2[3 * task], kk = A.T2[3 * task + 1], rr = A.T2[3 * task + 2];
 #endif
-        const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
-        const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
+        const int ka = task_hi32(kk), kb = task_lo32(kk);
+        const int kp0 = task_hi32(rr), kp1 = task_lo32(rr);
         const long long i = first + lane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
@@ -1047,8 +1047,8 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
                 nrr = A.T2[3 * next + 2];
             }
         }
-        const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
-        const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
+        const int ka = task_hi32(kk), kb = task_lo32(kk);
+        const int kp0 = task_hi32(rr), kp1 = task_lo32(rr);
         long long ip[PPL];
         dd pr[PPL], pim[PPL];
         const long long cend = A.Cmid[kb - 1];
@@ -1357,8 +1357,8 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
                 nrr = A.T2[3 * next + 2];
             }
         }
-        const int ka = (int)(kk >> 32), kb = (int)(kk & 0xffffffffLL);
-        const int kp0 = (int)(rr >> 32), kp1 = (int)(rr & 0xffffffffLL);
+        const int ka = task_hi32(kk), kb = task_lo32(kk);
+        const int kp0 = task_hi32(rr), kp1 = task_lo32(rr);
         // source tasks: ka = -(k + 1), kb = chunk size | SRC_L3 | SRC_CPREV
         dd lane_sum;
         if constexpr (SRC) {

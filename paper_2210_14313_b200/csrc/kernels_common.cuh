@@ -6,6 +6,10 @@
 #define PASS_THREADS (WPB * 32)
 #define META_KMASK ((1u << SG_META_KBITS) - 1u)
 
+// task descriptor words (plan.cpp pack32): two int32 fields, the high one possibly negative
+__device__ __forceinline__ int task_hi32(long long v) { return (int)(int32_t)(uint32_t)((unsigned long long)v >> 32); }
+__device__ __forceinline__ int task_lo32(long long v) { return (int)(int32_t)(uint32_t)((unsigned long long)v & 0xffffffffull); }
+
 struct DevPlan {
     int d, L, kind, nfront;
     int nl[SG_MAX_L + 3];

@@ -281,6 +281,12 @@ int host_rule(int rule, int l, double *x, double *w) {
     return n;
 }
 
+// task descriptor word: two int32 fields (the high one may be negative: source tasks store
+// -(k + 1)) packed through unsigned arithmetic; decoded by task_hi32 / task_lo32 (kernels_common.cuh)
+static int64_t pack32(int hi, int lo) {
+    return (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo);
+}
+
 static u128 sat_add(u128 a, u128 b) {
     u128 r = a + b;
     const u128 cap = (u128)1 << 100;
@@ -499,7 +505,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
 
     // ---- shard range in depth-1 rank space ----
     int64_t lo = 0, hi = nd1;
-    if (range_hi > range_lo && range_lo >= 0) {
+    const bool explicit_range = range_hi > range_lo && range_lo >= 0;
+    if (explicit_range) {
         lo = std::min<int64_t>(range_lo, nd1);
         hi = std::min<int64_t>(range_hi, nd1);
     } else if (world > 1) {
@@ -532,7 +539,9 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     }
     hp.range_lo = lo;
     hp.range_hi = hi;
-    hp.include_root = (lo == 0);
+    // the root point belongs to exactly one shard: rank 0 of a world partition (cut() may give
+    // several ranks an empty range starting at 0), or an explicit range that starts at 0
+    hp.include_root = explicit_range ? (lo == 0) : (rank == 0);
     {
         u128 sp = hp.include_root ? root_w : 0;
         int64_t pos = 0;
@@ -746,8 +755,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             hp.T2S.resize(3 * srct.size());
             for (size_t i = 0; i < srct.size(); ++i) {
                 hp.T2S[3 * i] = srct[i].first;
-                hp.T2S[3 * i + 1] = ((int64_t)srct[i].ka << 32) | (int64_t)(uint32_t)srct[i].kb;
-                hp.T2S[3 * i + 2] = ((int64_t)srct[i].kp0 << 32) | (int64_t)srct[i].kp1;
+                hp.T2S[3 * i + 1] = pack32(srct[i].ka, srct[i].kb);
+                hp.T2S[3 * i + 2] = pack32(srct[i].kp0, srct[i].kp1);
             }
             hp.pass_nsplit[tm] = 1;
             hp.pass_ntasks[tm] = (int64_t)srct.size();
@@ -804,8 +813,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         hp.T2.resize(3 * tasks.size());
         for (size_t i = 0; i < tasks.size(); ++i) {
             hp.T2[3 * i] = tasks[i].first;
-            hp.T2[3 * i + 1] = ((int64_t)tasks[i].ka << 32) | (int64_t)tasks[i].kb;
-            hp.T2[3 * i + 2] = ((int64_t)tasks[i].kp0 << 32) | (int64_t)tasks[i].kp1;
+            hp.T2[3 * i + 1] = pack32(tasks[i].ka, tasks[i].kb);
+            hp.T2[3 * i + 2] = pack32(tasks[i].kp0, tasks[i].kp1);
         }
         const int t = hp.nfront;
         hp.pass_nsplit[t] = 1;

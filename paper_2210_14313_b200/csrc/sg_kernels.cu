@@ -181,10 +181,11 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->sform = (o.arith == SG_ARITH_SFORM_FP64 || o.arith == SG_ARITH_SFORM_DD);
     p->sform_dd = (o.arith == SG_ARITH_SFORM_DD);
     p->two = p->cplx || p->sform;
-    if (p->sform) p->leaf1 = false;
     {
+        // specialised single-level / fused leaf kernels: factor form only; SG_B200_GENERIC_LEAF=1
+        // forces the generic k_leaf (tests)
         const char *g = getenv("SG_B200_GENERIC_LEAF");
-        p->leaf1 = !(g && g[0] == '1');
+        p->leaf1 = !p->sform && !(g && g[0] == '1');
     }
     // ---- device tables: one allocation ----
     const int L = hp.L, nent = (int)hp.X.size();

@@ -103,6 +103,34 @@ def test_balanced_shards_partition(L, i, world):
         assert max(sizes) / (total / world) < 1.10
 
 
+@pytest.mark.parametrize("d,Lv,rule,form", [(5, 0, S.RULE_CC, 0), (1, 1, S.RULE_CC, 1), (1, 0, S.RULE_GL, 0),
+                                           (2, 1, S.RULE_GL, 1), (3, 2, S.RULE_CC, 0), (1, 3, S.RULE_CC, 1),
+                                           (4, 4, S.RULE_CC, 0), (2, 5, S.RULE_TRAP, 1)])
+@pytest.mark.parametrize("world", [2, 3, 5, 8])
+def test_shards_partition_tiny(L, d, Lv, rule, form, world):
+    """Every world partition of a tiny problem (L = 0: only the root; d = 1; fewer depth-1 prefixes
+    than ranks) counts each Smolyak point exactly once: the shard points add up to the total, the
+    root sits on rank 0 only (several ranks may get an empty range starting at 0), and the host
+    unranker enumerates each shard's points without duplicates across ranks."""
+    from paper_2210_14313_b200 import api
+    q = d + Lv
+    whole = _query(L, d, q, rule, form=form)
+    assert whole[0] == 0
+    total = whole[2]
+    acc, seen = 0, set()
+    for r in range(world):
+        rc, sp, tp, lo, hi, _ = _query(L, d, q, rule, form=form, rank=r, world=world)
+        assert rc == 0 and tp == total
+        acc += sp
+        for idx in range(sp):
+            cf, pt = api.sg_unrank(d, q, rule, 0, idx, form=form, rank=r, world=world)
+            key = tuple(pt)
+            assert key not in seen, (r, idx, key)
+            seen.add(key)
+    assert acc == total
+    assert len(seen) == total
+
+
 def test_explicit_range_counts(L):
     p = S.baseline_config(2)
     # subtree points of a depth-1 range must equal the oracle's point count for the same range

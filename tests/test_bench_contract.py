@@ -58,3 +58,20 @@ def test_gpu_arm_contract():
     assert line["parity"]["rel_err_vs_oracle"] <= 1e-12
     for leg in ("merged", "collapse", "corner_peak", "frontier_kernel"):
         assert leg in line, leg
+
+
+def test_reference_arm_loads_only_the_oracle():
+    """--impl reference runs the CPU oracle alone: the product library must not be mapped into the
+    process (the arm's sample is chosen by oracle/ itself)."""
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--config', '5', "
+            "'--steps', '1', '--warmup', '1']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "assert 'libsg_b200' not in maps, 'product library loaded'; "
+            "assert 'liboracle_sg' in maps; print('MAPS_OK')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "MAPS_OK" in out.stdout
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    assert line["config"]["points"] == 27521113876
+    assert 0.5e7 < line["config"]["sample_points_per_step"] < 2e7

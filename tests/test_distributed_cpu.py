@@ -53,7 +53,7 @@ def _worker(rank, world, port, cfg, out_q):
     rc = lib().sg_plan_query(p.d, p.q, p.rule, p.kind, ctypes.byref(o), ctypes.byref(sp), None,
                              ctypes.byref(lo), ctypes.byref(hi), None)
     assert rc == 0
-    r = oracle.integrate_problem(p, lo=lo.value, hi=hi.value, include_root=(lo.value == 0),
+    r = oracle.integrate_problem(p, lo=lo.value, hi=hi.value, include_root=(rank == 0),
                                  eval_mode=1, nthreads=2)
     assert r.npoints == sp.value
     part = torch.tensor([r.hi, r.lo], dtype=torch.float64)

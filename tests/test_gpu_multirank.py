@@ -30,6 +30,8 @@ def test_torchrun_bench_shards_match_oracle(nproc, cfg):
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py",
            "--gpus", str(nproc), "--steps", "3", "--warmup", "3", "--config", str(cfg),
            "--dist-backend", "gloo", "--device-index", "0", "--no-cpu-baseline"]
+    if nproc > 2:
+        cmd.append("--no-configs")
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]

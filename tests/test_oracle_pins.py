@@ -490,3 +490,49 @@ def test_corner_peak_special_cases():
     # outside the domain (1 + sum min(c, 0) <= 0): rejected
     with pytest.raises(Exception):
         oracle.integrate(3, 2, S.RULE_CC, S.KIND_CORNER, np.array([-0.6, -0.5, 0.3]))
+
+
+# ----------------------------------------------------------------------------------------------
+# oracle measurement helpers (bench.py's CPU legs): point counts, timing samples, FP64 build
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("i", [1, 2, 3, 4, 5])
+def test_count_only_walk_equals_generating_function(i):
+    """count_only walks the same multi-indices as the evaluation without evaluating: its count is
+    n_d^q = [z^e] G(z)^d summed over the band, and oracle.n_points (bench's total)
+    is the same number."""
+    p = S.baseline_config(i)
+    n = oracle.count_points(p)
+    assert n == pins.n_points(p.rule, p.d, p.L) == oracle.n_points(p)
+    if i <= 2:
+        assert n == oracle.integrate_problem(p, eval_mode=1).npoints
+
+
+def test_timing_sample_is_a_subset_spread_over_the_tree():
+    """The CPU timing sample (every s-th depth-2 subtree) evaluates exactly the points count_only
+    selects, far fewer than the whole, from subtrees across the whole depth-1 range."""
+    p = S.baseline_config(5)
+    r, stride, total = oracle.timing_sample(p, int(2e6))
+    assert stride > 1 and total == 27521113876
+    assert r.npoints == oracle.count_points(p, stride=stride, include_root=False)
+    assert 0.5e6 < r.npoints < 8e6
+    # the sample reaches the tail of the depth-1 range as well as its head: a shard that holds only
+    # the last third of the depth-1 prefixes still contains sampled points
+    nd1 = oracle.depth1_count(p)
+    assert oracle.count_points(p, stride=stride, lo=2 * nd1 // 3, hi=nd1, include_root=False) > 0
+    assert oracle.count_points(p, stride=stride, lo=0, hi=nd1 // 3, include_root=False) > 0
+    # stride 1 is the ordinary (unsampled) evaluation
+    q = S.baseline_config(1)
+    assert oracle.integrate_problem(q, stride=1).text == oracle.integrate_problem(q).text
+
+
+@pytest.mark.parametrize("i,bound", [(1, 1e-14), (2, 1e-11)])
+def test_fp64_build_is_the_same_sum_in_double(i, bound):
+    """The FP64 instantiation (-DSGO_FP64) sums the same points in double: it agrees with the quad
+    oracle to the conditioning of Eq 2.6 (kappa * 2^-53: c1 kappa 128, c2 kappa <= 1.2e5, SURVEY.md
+    §8c) and reports the same point count."""
+    p = S.baseline_config(i)
+    a = oracle.integrate_problem(p, eval_mode=1)
+    b = oracle.integrate_problem(p, eval_mode=1, fp64=True)
+    assert a.npoints == b.npoints
+    assert b.lo == 0.0 or abs(b.lo) <= abs(b.hi) * 2 ** -52
+    assert abs((mp.mpf(b.hi) - qval(a)) / qval(a)) < bound
