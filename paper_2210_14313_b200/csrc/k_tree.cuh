@@ -802,10 +802,17 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
         }
 }
 
-template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false>
+// G (lane groups, small shards): a task's chunk holds 32 / G parents and lane = (parent lane % (32/G),
+// k_mid group lane / (32/G)); group g walks the task's k_mids ka + g, ka + g + G, ... < kb (rows
+// [max(k_mid + 1, kp0), kp1) each), so a shard with few parents (config 4 on 8 GPUs: 132 on rank 0)
+// fills its lanes.  G = 1 is the lane = parent mapping (every k_mid of the task on every lane).
+template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false, int G = 1>
 __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
+    static_assert(G == 1 || G == 2 || G == 4 || G == 8, "lane groups");
+    constexpr int PCH = 32 / G;   // parents per task chunk
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int plane = G == 1 ? lane : lane % PCH, lgrp = G == 1 ? 0 : lane / PCH;
     const int d = P.d;
     const double2 *Fr = P.Fre + P.tab_off[2];
     const double2 *Fi = CPLX ? P.Fim + P.tab_off[2] : nullptr;
@@ -861,7 +868,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 #endif
         const int ka = task_hi32(kk), kb = task_lo32(kk);
         const int kp0 = task_hi32(rr), kp1 = task_lo32(rr);
-        const long long i = first + lane;
+        const long long i = first + plane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
             const double2 v = A.src_re[A.base + i];
@@ -872,7 +879,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             }
         }
         dd lane_sum = {0.0, 0.0};
-        for (int km = ka; km < kb; ++km) {
+        for (int km = ka + lgrp; km < kb; km += G) {
             const bool valid = i < A.Cmid[km];
             const dd prv = valid ? pr : dd{0.0, 0.0};
             const dd pimv = valid ? pim : dd{0.0, 0.0};

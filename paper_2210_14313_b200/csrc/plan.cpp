@@ -676,25 +676,63 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             hp.leaf2_ppl = pair ? LEAF2_PPL : sym3 ? LEAF2_PPL3 : 1;
             hp.leaf2_sym3 = sym3 && !pair;
         }
-        const int64_t CH = 32LL * hp.leaf2_ppl;   // parents per task chunk
+        // Lane groups (real kinds, one parent per lane): with few parents (a small shard) the last
+        // chunk of 32 is mostly empty lanes (config 4, rank 0 of 8: 132 parents -> 0.82 of the lanes
+        // busy); 32 / G parents per chunk and G k_mid groups per warp fill them.  The smallest G whose
+        // lane fill is >= 0.95 (1 on every full-size problem; the plan depends on the problem and
+        // the shard only, so every rank and the host queries agree).
+        hp.leaf2_groups = 1;
+        if (kind != SG_F_OSCILLATORY && hp.leaf2_ppl == 1) {
+            const int64_t np = cmid(d - 2);
+            auto fill = [&](int g) {
+                const int64_t pc = 32 / g;
+                return np > 0 ? (double)np / (double)(((np + pc - 1) / pc) * pc) : 1.0;
+            };
+            int best = 1;
+            for (int g : {1, 2, 4, 8}) {
+                if (fill(g) >= 0.95) {
+                    best = g;
+                    break;
+                }
+                if (fill(g) > fill(best) + 1e-9) best = g;
+            }
+            if (const char *e = getenv("SG_B200_LEAF2_GROUPS"); e && e[0]) best = atoi(e);   // A/B runs
+            if (best == 1 || best == 2 || best == 4 || best == 8) hp.leaf2_groups = best;
+        }
+        const int G = hp.leaf2_groups;
+        const int64_t CH = 32LL * hp.leaf2_ppl / G;   // parents per task chunk
         const int64_t nchunks = (cmid(d - 2) + CH - 1) / CH;
         struct Task {
             int64_t rows, first;
-            int ka, kb, kp0, kp1;   // k_mid range; row range (split tasks: one k_mid, [kp0, kp1))
+            int ka, kb, kp0, kp1;   // k_mid range; row range (split tasks: one k_mid block, [kp0, kp1))
         };
         std::vector<Task> tasks;
         int k0 = 0;
         for (int64_t c = 0; c < nchunks; ++c) {
             while (k0 <= d - 2 && cmid(k0) <= CH * c) ++k0;   // kstart(c), nondecreasing in c
-            int64_t acc = 0;
-            int ka = k0;
-            for (int k = k0; k <= d - 2; ++k) {
-                acc += d - 1 - k;
-                if (acc >= LEAF2_TASK_ROWS || k == d - 2) {
-                    tasks.push_back(Task{acc, CH * c, ka, k + 1, 0, d});
-                    acc = 0;
-                    ka = k + 1;
+            if (G == 1) {
+                int64_t acc = 0;
+                int ka = k0;
+                for (int k = k0; k <= d - 2; ++k) {
+                    acc += d - 1 - k;
+                    if (acc >= LEAF2_TASK_ROWS || k == d - 2) {
+                        tasks.push_back(Task{acc, CH * c, ka, k + 1, 0, d});
+                        acc = 0;
+                        ka = k + 1;
+                    }
                 }
+                continue;
+            }
+            // G > 1: blocks of G consecutive k_mids (one per lane group), grouped until the first
+            // group's rows (the longest) reach LEAF2_TASK_ROWS; rows = that group's row count
+            for (int km = k0; km <= d - 2;) {
+                const int ka = km;
+                int64_t grows = 0;
+                while (km <= d - 2 && grows < LEAF2_TASK_ROWS) {
+                    grows += d - 1 - km;
+                    km += G;
+                }
+                tasks.push_back(Task{grows, CH * c, ka, std::min(km, d - 1), 0, d});
             }
         }
         // Source tasks (k_leaf2_sym3 plans whose level 3 has SYM3_N3 nodes): pass L-2 runs
@@ -776,7 +814,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         if (do_split) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {
-                if (tk.kb - tk.ka != 1 || tk.rows <= LEAF2_TASK_ROWS) {
+                if (tk.kb - tk.ka > G || tk.rows <= LEAF2_TASK_ROWS) {   // one k_mid block only
                     split.push_back(tk);
                     continue;
                 }
@@ -798,10 +836,10 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                 for (int km = k + 1; km <= d - 2; ++km) tail += d - 1 - km;
                 useful += (double)(cmid(k + 1) - cmid(k)) * tail;
             }
-            for (const Task &tk : tasks) slots += (double)tk.rows * CH;
+            for (const Task &tk : tasks) slots += (double)tk.rows * CH * G;
             fprintf(stderr, "leaf2 tasks: %zu total_rows %lld max_rows %lld split %d ppl %d parents %lld "
-                    "lane_util %.4f\n", tasks.size(), (long long)total_rows, (long long)max_rows, (int)do_split,
-                    hp.leaf2_ppl, (long long)cmid(d - 2), useful / slots);
+                    "lane_util %.4f groups %d\n", tasks.size(), (long long)total_rows, (long long)max_rows, (int)do_split,
+                    hp.leaf2_ppl, (long long)cmid(d - 2), useful / slots, G);
         }
         // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, rows, chunk)
         std::stable_sort(tasks.begin(), tasks.end(), [](const Task &a, const Task &b) {

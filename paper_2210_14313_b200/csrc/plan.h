@@ -85,6 +85,8 @@ struct HostPlan {
     // all actives at level 2) on the fly.  Tasks: (k_mid, chunk of 32 parents with k < k_mid).
     bool fuse = false;
     int leaf2_ppl = 1;                 // parents per lane of the fused kernel (2: k_leaf2_pairs)
+    int leaf2_groups = 1;              // lane groups of k_leaf2 (real kinds, few parents: 32 / G parents
+                                       // per chunk, G k_mid groups per warp); 1 = lane per parent
     bool leaf2_sym3 = false;           // k_leaf2_sym3 (oscillatory, level-2 row {0, 1/2, 1} symmetric)
     // Source tasks: pass L-2 runs k_leaf2_sym3<SRC = true> over all its sources (the prefixes are the
     // stored sources themselves) instead of k_leaf — the excess-(L-1) sources' symmetric level-2

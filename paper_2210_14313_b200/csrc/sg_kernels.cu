@@ -403,8 +403,20 @@ static const void *leaf1_kernel(int nj, bool smem) {
 
 // Variant of k_leaf2 for this plan: NJ level-2 nodes, factor rows in smem or L1, midpoint index
 // (center), symmetric pair (sym, oscillatory only), midpoint factor with zero low part (cz).
+// Real kinds with few parents per shard: lane groups (k_leaf2 G = 2, 4, 8; plan.cpp leaf2_groups)
+template <bool SMEM, int G>
+static const void *leaf2_fn_groups(int nj, bool center, bool cz) {
+    if (nj == 3 && center)
+        return cz ? (const void *)k_leaf2<false, 3, SMEM, 1, false, true, G> : (const void *)k_leaf2<false, 3, SMEM, 1, false, false, G>;
+    if (nj == 3) return (const void *)k_leaf2<false, 3, SMEM, -1, false, false, G>;
+    return (const void *)k_leaf2<false, 2, SMEM, -1, false, false, G>;
+}
+
 template <bool CPLX, bool SMEM>
-static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
+static const void *leaf2_fn(int nj, bool center, bool sym, bool cz, int groups = 1) {
+    if (!CPLX && groups == 2) return leaf2_fn_groups<SMEM, 2>(nj, center, cz);
+    if (!CPLX && groups == 4) return leaf2_fn_groups<SMEM, 4>(nj, center, cz);
+    if (!CPLX && groups == 8) return leaf2_fn_groups<SMEM, 8>(nj, center, cz);
     if (nj == 3 && center) {
         if (CPLX && sym) return cz ? (const void *)k_leaf2<CPLX, 3, SMEM, 1, true, true>
                                    : (const void *)k_leaf2<CPLX, 3, SMEM, 1, true, false>;
@@ -415,7 +427,7 @@ static const void *leaf2_fn(int nj, bool center, bool sym, bool cz) {
     return (const void *)k_leaf2<CPLX, 2, SMEM, -1>;
 }
 template <bool CPLX>
-static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz, int ppl = 1) {
+static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool cz, int ppl = 1, int groups = 1) {
     if (CPLX && sym && center && nj == 3 && ppl >= 2) {
 #define SYM3(P_) (smem ? (cz ? (const void *)k_leaf2_sym3<P_, true, true, false> : (const void *)k_leaf2_sym3<P_, true, false, false>) \
                        : (cz ? (const void *)k_leaf2_sym3<P_, false, true, false> : (const void *)k_leaf2_sym3<P_, false, false, false>))
@@ -429,7 +441,7 @@ static const void *leaf2_kernel(int nj, bool smem, bool center, bool sym, bool c
         return smem ? (const void *)k_leaf2_pairs<3, true> : (const void *)k_leaf2_pairs<3, false>;
     if (CPLX && sym && nj == 2 && ppl == 4)
         return smem ? (const void *)k_leaf2_pairs<4, true> : (const void *)k_leaf2_pairs<4, false>;
-    return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz) : leaf2_fn<CPLX, false>(nj, center, sym, cz);
+    return smem ? leaf2_fn<CPLX, true>(nj, center, sym, cz, groups) : leaf2_fn<CPLX, false>(nj, center, sym, cz, groups);
 }
 
 // The source-task kernel of pass L-2 (plan.cpp builds source tasks only for k_leaf2_sym3 plans, with
@@ -484,8 +496,9 @@ static int setup_leaf1(sg_plan_s *p) {
     // source tasks are only understood by k_leaf2_sym3 (plan.cpp builds them for that kernel alone)
     if (p->leaf2 && hp.leaf2_srctasks && !(p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2))
         return SG_EUNSUPPORTED;
+    if (hp.leaf2_groups > 1 && (p->cplx || hp.leaf2_ppl != 1)) return SG_EUNSUPPORTED;   // plan.cpp never does this
     const void *fn = p->leaf2 ? (p->cplx ? leaf2_kernel<true>(nj, sm, ct, sy, cz, hp.leaf2_ppl)
-                                         : leaf2_kernel<false>(nj, sm, ct, sy, cz))
+                                         : leaf2_kernel<false>(nj, sm, ct, sy, cz, 1, hp.leaf2_groups))
                               : (p->cplx ? leaf1_kernel<true>(nj, sm) : leaf1_kernel<false>(nj, sm));
     if (p->leaf1_smem > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->leaf1_smem) != cudaSuccess)
@@ -533,7 +546,8 @@ template <bool CPLX>
 static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t st) {
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
-    const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz, p->hp.leaf2_ppl);
+    const void *fn = leaf2_kernel<CPLX>(nj, sm > 0, p->leaf2_center, p->leaf2_sym, p->leaf2_cz, p->hp.leaf2_ppl,
+                                        p->hp.leaf2_groups);
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};

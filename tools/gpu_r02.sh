@@ -11,15 +11,12 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${tag}_gpu.txt
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${tag}_build.log 2>&1 || { tail -20 gpurun_out/${tag}_build.log; exit 3; }
 NCU_M=sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum
-ctr_runs() {   # $1 = "" (plain) or "ncu"
+ctr_runs() {   # plain run && the same command under ncu (FP64 counters of the dominant launch)
   for cv in "3 tree" "4 tree" "5 tree" "5 merged"; do
     set -- $cv
-    if [ "$MODE" = ncu ]; then
-      timeout 900 ncu --metrics $NCU_M --clock-control none --csv --log-file gpurun_out/ctr_c$1_$2.csv \
-        python tools/fp64_counters.py --run --config $1 --variant $2 > gpurun_out/ctr_c$1_$2.json 2> gpurun_out/ctr_c$1_$2.err
-    else
-      timeout 300 python tools/fp64_counters.py --run --config $1 --variant $2 > gpurun_out/${tag}_plainctr_c$1_$2.json 2>&1 || echo "plain ctr $cv failed"
-    fi
+    timeout 300 python tools/fp64_counters.py --run --config $1 --variant $2 > gpurun_out/${tag}_plainctr_c$1_$2.json 2>&1 && \
+    timeout 900 ncu --metrics $NCU_M --clock-control none --csv --log-file gpurun_out/ctr_c$1_$2.csv \
+      python tools/fp64_counters.py --run --config $1 --variant $2 > gpurun_out/ctr_c$1_$2.json 2> gpurun_out/ctr_c$1_$2.err
   done
 }
 for s in $steps; do
@@ -29,16 +26,19 @@ for s in $steps; do
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1 ;;
     bench) timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err ;;
     plainruns)
-      MODE=plain ctr_runs
       timeout 600 python tools/sanitize_cases.py > gpurun_out/${tag}_sanitize_plain.log 2>&1 || echo "sanitize plain failed"
       timeout 300 python tools/prof_step.py 5 2 > gpurun_out/${tag}_plain5.log 2>&1
       timeout 300 python tools/prof_step.py 4 2 > gpurun_out/${tag}_plain4.log 2>&1 ;;
     ctr)
-      MODE=ncu ctr_runs
+      ctr_runs
+      timeout 300 python tools/prof_step.py 5 2 > gpurun_out/${tag}_plain5.log 2>&1 && \
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/${tag}_launches_c5.csv python tools/prof_step.py 5 2 > /dev/null 2>&1
+      timeout 300 python tools/prof_step.py 4 2 > gpurun_out/${tag}_plain4.log 2>&1 && \
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/${tag}_launches_c4.csv python tools/prof_step.py 4 2 > /dev/null 2>&1 ;;
+    shards) for c in 4 5; do SHARD_PHASES=1 timeout 900 python tools/shard_times.py $c 2 4 8 > gpurun_out/${tag}_shards_c$c.txt 2>&1; done ;;
+    pyt) timeout 1800 python -m pytest $PYT -q -x --tb=long 2>&1 | tail -150 > gpurun_out/${tag}_pyt.log ;;
     memcheck|racecheck|synccheck|initcheck)
       timeout 2400 compute-sanitizer --tool $s --error-exitcode 9 --print-limit 50 \
         python tools/sanitize_cases.py > gpurun_out/${tag}_san_$s.log 2>&1

@@ -4,7 +4,8 @@
 
 The shards are independent (no data-path exchange), so the slowest shard's time is the N-GPU
 step time up to the 16-byte all-gather; this projects strong-scaling efficiency t1 / (N max_r t_r)
-from one device.  Times: CUDA events around sg_integrate, best of 5, L2 flushed in between.
+from one device.  Times: CUDA events around a CUDA-graph replay of sg_integrate (bench.py's launch
+configuration), best of 5, L2 flushed in between.
 """
 import os
 import sys
@@ -18,13 +19,17 @@ from paper_2210_14313_b200 import api  # noqa: E402
 
 
 def time_plan(plan, flush, reps=5):
+    """Best of `reps` CUDA-graph replays of sg_integrate (the launch configuration bench.py times)."""
+    for _ in range(2):
+        plan.sg_integrate()
+    g = plan.capture_graph(finalize=False)
     best = None
     for _ in range(reps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        plan.sg_integrate()
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
