@@ -183,3 +183,14 @@ def timing_sample(p, target_points: int, nthreads: int = 0, fp64: bool = False, 
     r = integrate_problem(p, stride=stride, include_root=False, eval_mode=eval_mode,
                           nthreads=nthreads, fp64=fp64)
     return r, stride, total
+
+
+def eval_point(kind: int, c, w, u: float, x):
+    """f at one full point, (plain, active) forms, each as a (hi, lo) pair of doubles."""
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    a = np.zeros(2)
+    b = np.zeros(2)
+    _load().sgo_eval_point(len(c), kind, _ptr(c), _ptr(w), float(u), _ptr(x), _ptr(a), _ptr(b))
+    return (a[0], a[1]), (b[0], b[1])
