@@ -129,12 +129,11 @@ __global__ void __launch_bounds__(COLLAPSE_THREADS) k_collapse_final(const DevPl
         const dd Br = {P.base[0], P.base[1]}, Bi = {P.base[2], P.base[3]};
         dd a = CPLX ? dd_sub(dd_mul(Br, sr), dd_mul(Bi, si)) : dd_mul(Br, sr);
         if (!emit) a = dd{0.0, 0.0};   // ranks != 0 contribute nothing (the collapse is not sharded)
-        if (*P.status || !dd_finite(a)) {
-            atomicOr(P.status, 1);
-            a = dd{nan(""), nan("")};
-        }
+        const int st = *P.status || !dd_finite(a);
+        if (st) a = dd{nan(""), nan("")};
         out[0] = a.hi;
         out[1] = a.lo;
+        step_close_status(P, st);
     }
 }
 

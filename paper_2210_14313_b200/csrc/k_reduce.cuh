@@ -15,9 +15,11 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
                                            : dd{P.base[0], P.base[1]};
             s = dd_add(s, coef_mul(P, root, 0, 0));
         }
-        if (*P.status) s = dd{nan(""), nan("")};
+        const int st = *P.status;
+        if (st) s = dd{nan(""), nan("")};
         out[0] = s.hi;
         out[1] = s.lo;
+        step_close_status(P, st);
     }
 }
 
@@ -31,7 +33,7 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
 #define RED_CHUNK2 (RED_THREADS * RED_PER_THREAD)
 __global__ void __launch_bounds__(RED_THREADS)
 k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int include_root, double *out,
-               double2 *l1, unsigned long long *ticket) {
+               double2 *l1, unsigned long long *ticket, unsigned long long *task_counters) {
     const long long b0 = (long long)blockIdx.x * RED_CHUNK2 + (long long)threadIdx.x * RED_PER_THREAD;
     double2 v[RED_PER_THREAD];
 #pragma unroll
@@ -64,18 +66,25 @@ k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int includ
                                            : dd{P.base[0], P.base[1]};
             t = dd_add(t, coef_mul(P, root, 0, 0));
         }
-        if (*P.status) t = dd{nan(""), nan("")};
+        const int st = *P.status;
+        if (st) t = dd{nan(""), nan("")};
         out[0] = t.hi;
         out[1] = t.lo;
         *ticket = 0;
+        // re-arm the persistent leaf kernels' task counters for the next step (all of this step's
+        // passes finished before this launch)
+        task_counters[0] = 0;
+        task_counters[2] = 0;
+        step_close_status(P, st);
     }
 }
 
+// status = the plan's status words; status[1] holds the flag of the last completed sg_integrate
 __global__ void k_finalize(const double *gathered, int world, const int *status, double *result) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     dd s = {0.0, 0.0};
     for (int r = 0; r < world; ++r) s = dd_add(s, dd{gathered[2 * r], gathered[2 * r + 1]});
-    if (*status || !isfinite(s.hi)) s = dd{nan(""), nan("")};
+    if (status[1] || !isfinite(s.hi)) s = dd{nan(""), nan("")};
     result[0] = s.hi;
     result[1] = s.lo;
 }

@@ -51,6 +51,15 @@ struct RootArgs {
     double2 *partials;
 };
 
+// Status words: status[0] is the live NonFiniteIntegrand flag of the running step (atomicOr by any
+// kernel), status[1] the flag of the last completed sg_integrate (read by k_finalize and
+// sg_status_word).  The step's final kernel publishes status[0] to status[1] and clears status[0],
+// so every sg_integrate starts with a clear flag without a memset node.
+__device__ __forceinline__ void step_close_status(const DevPlan &P, int st) {
+    P.status[1] = st ? 1 : 0;
+    P.status[0] = 0;
+}
+
 // ---------------------------------------------------------------------------------------------
 // reductions (K4)
 // ---------------------------------------------------------------------------------------------

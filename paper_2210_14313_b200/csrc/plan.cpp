@@ -679,7 +679,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         // Lane groups (real kinds, one parent per lane): with few parents (a small shard) the last
         // chunk of 32 is mostly empty lanes (config 4, rank 0 of 8: 132 parents -> 0.82 of the lanes
         // busy); 32 / G parents per chunk and G k_mid groups per warp fill them.  The smallest G whose
-        // lane fill is >= 0.95 (1 on every full-size problem; the plan depends on the problem and
+        // lane fill is >= 0.97 (1 on every full-size problem; the plan depends on the problem and
         // the shard only, so every rank and the host queries agree).
         hp.leaf2_groups = 1;
         if (kind != SG_F_OSCILLATORY && hp.leaf2_ppl == 1) {
@@ -690,7 +690,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             };
             int best = 1;
             for (int g : {1, 2, 4, 8}) {
-                if (fill(g) >= 0.95) {
+                if (fill(g) >= 0.97) {
                     best = g;
                     break;
                 }
@@ -811,14 +811,20 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         }
         const bool do_split =
             max_rows > LEAF2_TASK_ROWS && LEAF2_SPLIT_SHARE * max_rows * (int64_t)LEAF2_RESIDENT_WARPS > total_rows;
+        // piece length: about LEAF2_PIECES_PER_WARP pieces per resident warp (the dynamic schedule's
+        // tail is about one piece), at most LEAF2_TASK_ROWS and at least LEAF2_MIN_PIECE rows (each
+        // piece repeats its k_mid prologue)
+        const int64_t piece = std::max<int64_t>(
+            LEAF2_MIN_PIECE,
+            std::min<int64_t>(LEAF2_TASK_ROWS, total_rows / ((int64_t)LEAF2_RESIDENT_WARPS * LEAF2_PIECES_PER_WARP)));
         if (do_split) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {
-                if (tk.kb - tk.ka > G || tk.rows <= LEAF2_TASK_ROWS) {   // one k_mid block only
+                if (tk.kb - tk.ka > G || tk.rows <= piece) {   // one k_mid block only
                     split.push_back(tk);
                     continue;
                 }
-                const int pieces = (int)((tk.rows + LEAF2_TASK_ROWS - 1) / LEAF2_TASK_ROWS);
+                const int pieces = (int)((tk.rows + piece - 1) / piece);
                 const int r0 = tk.ka + 1;
                 for (int q = 0; q < pieces; ++q) {
                     const int a = r0 + (int)((int64_t)tk.rows * q / pieces);

@@ -42,6 +42,12 @@
 #ifndef LEAF2_SPLIT_SHARE
 #define LEAF2_SPLIT_SHARE 4   // split long tasks when one is > 1/SHARE of a resident warp's row share
 #endif
+#ifndef LEAF2_PIECES_PER_WARP
+#define LEAF2_PIECES_PER_WARP 8   // split pieces per resident warp on small shards (tail ~ one piece)
+#endif
+#ifndef LEAF2_MIN_PIECE
+#define LEAF2_MIN_PIECE 32        // shortest split piece (rows)
+#endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 #endif

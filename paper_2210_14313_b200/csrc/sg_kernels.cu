@@ -75,6 +75,10 @@ struct sg_plan_s {
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
     std::vector<cudaEvent_t> ev;
+    std::vector<std::pair<int, int>> prof_pairs;   // per launch of the last sg_integrate: (start, end) event
+    // fused plans: pass nfront-1 runs on a plan-owned side stream, concurrently with the fused pass
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
@@ -360,6 +364,16 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->ws_red_off = ws;
     ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2 + 1), 256);
     p->ws_need = ws;
+    if (p->leaf2 && hp.nfront >= 2 && !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
+        // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
+        if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            sg_destroy(p);
+            return SG_ECUDA;
+        }
+    }
     *out = p;
     return SG_OK;
 }
@@ -586,6 +600,31 @@ static void front_ptrs(sg_plan_s *p, int t, double2 *&re, double2 *&im, uint32_t
     meta = (uint32_t *)(b + (p->two ? 2 : 1) * sizeof(double2) * cap);
 }
 
+// Profiling: sg_integrate records CUDA events (plan-owned) and, per launch, the pair (start event,
+// end event) whose difference sg_profile_read reports.  Sequential launches chain (the end of one is
+// the start of the next); the two concurrent passes (fork/join below) both start at the fork event.
+struct ProfRec {
+    sg_plan_s *p;
+    cudaStream_t st;
+    unsigned flags;
+    int nev = 0;
+    int last = -1;   // index of the most recent event on the main stream
+    int rec(cudaStream_t on) {
+        if (!p->prof || nev >= (int)p->ev.size()) return -1;
+        cudaEventRecordWithFlags(p->ev[nev], on, flags);
+        return nev++;
+    }
+    void launch_done(int start, int end) {
+        if (p->prof) p->prof_pairs.push_back({start, end});
+    }
+    // a sequential launch just issued on the main stream
+    void seq() {
+        const int e = rec(st);
+        launch_done(last, e);
+        last = e;
+    }
+};
+
 extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     if (!p || !out_dev) return SG_EINVAL;
     if (!p->ws) return SG_ENOWORKSPACE;
@@ -593,63 +632,64 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     const HostPlan &hp = p->hp;
     const DevPlan &dp = p->dp;
     double2 *partials = (double2 *)(p->ws + p->ws_part_off);
-    if (cudaMemsetAsync(dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
-    int evi = 0;
     // under stream capture the events become graph event-record nodes (timed on every replay)
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (p->prof && cudaStreamIsCapturing(st, &cap) != cudaSuccess) return SG_ECUDA;
-    const unsigned ev_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
-    auto mark = [&]() {
-        if (p->prof && evi < (int)p->ev.size()) cudaEventRecordWithFlags(p->ev[evi++], st, ev_flags);
-    };
-    mark();
+    ProfRec pr{p, st, cap == cudaStreamCaptureStatusActive ? (unsigned)cudaEventRecordExternal : 0u};
+    p->prof_pairs.clear();
+    pr.last = pr.rec(st);
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);   // factor-table blocks of the merged K0 launch
+    if (p->plain || p->collapse) {
+        // status words: these paths' final kernels also close the step (step_close_status)
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb, nullptr);
+        pr.seq();
+        pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
+    }
     if (p->plain) {
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        mark();
-        mark();   // K0 base: merged into the factor launch
         double2 *part = (double2 *)(p->ws + p->ws_part_off);
         k_plain<<<p->plain_blocks, 256, 0, st>>>(dp, p->utabs, part);
-        mark();
+        pr.seq();
         k_reduce<<<1, 1024, 0, st>>>(dp, part, p->plain_blocks, 0, out_dev);
-        mark();
+        pr.seq();
         if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
         return SG_OK;
     }
     if (p->collapse) {
         const int L = hp.L;
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        mark();
-        mark();   // K0 base: merged into the factor launch
         double2 *pre = (double2 *)(p->ws + p->ws_part_off);
         double2 *pim = pre + (size_t)p->collapse_blocks * (L + 1);
         const size_t smem_part = (size_t)(p->cplx ? 4 : 2) * COLLAPSE_THREADS * (L + 1) * sizeof(double2);
         const size_t smem_fin = (size_t)(p->cplx ? 2 : 1) * COLLAPSE_THREADS * (L + 1) * sizeof(double2);
         if (p->cplx) {
             k_collapse_part<true><<<p->collapse_blocks, COLLAPSE_THREADS, smem_part, st>>>(dp, pre, pim);
-            mark();
+            pr.seq();
             k_collapse_final<true><<<1, COLLAPSE_THREADS, smem_fin, st>>>(dp, pre, pim, p->collapse_blocks,
                                                                          p->collapse_emit ? 1 : 0, out_dev);
         } else {
             k_collapse_part<false><<<p->collapse_blocks, COLLAPSE_THREADS, smem_part, st>>>(dp, pre, pim);
-            mark();
+            pr.seq();
             k_collapse_final<false><<<1, COLLAPSE_THREADS, smem_fin, st>>>(dp, pre, pim, p->collapse_blocks,
                                                                           p->collapse_emit ? 1 : 0, out_dev);
         }
-        mark();
+        pr.seq();
         if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
         return SG_OK;
     }
-    // K0
+    // Task counters (plan-owned, zero at the start of every step; re-armed by k_reduce_fused):
+    // [0] the persistent last-pass kernel, [1] the reduction ticket, [2] the source-task kernel,
+    // [3] K0's suffix ticket.
+    unsigned long long *cnt_leaf = p->d_counter, *cnt_src = p->d_counter + 2;
+    // K0 (factor table + base; with a small table also the suffix bounds, by its last block)
+    const bool k0_suffix = !p->sform && hp.tab_entries > 0 && hp.tab_entries <= K0_SUFFIX_MAX;
     if (p->sform) {
         if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
     } else {
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb, k0_suffix ? p->d_counter + 3 : nullptr);
+        if (hp.tab_entries > 0 && !k0_suffix) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
     }
-    mark();
-    mark();   // K0 base: merged into the factor launch
+    pr.seq();
+    pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
     // root pass
     RootArgs R;
     memset(&R, 0, sizeof R);
@@ -665,9 +705,22 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
     else
         k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-    mark();
+    pr.seq();
+    // Fused plans: pass nfront-1 writes no frontier (its children are the fused kernel's business),
+    // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
+    // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).
+    // The persistent fused kernel takes the SMs the shorter pass leaves or frees (its tail fill).
+    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2;
+    int ev_fork = -1;
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
+        cudaStream_t sx = st;
+        if (fork && t == hp.nfront - 1) {
+            if (cudaEventRecord(p->ev_fork, st) != cudaSuccess) return SG_ECUDA;
+            if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
+            ev_fork = pr.last;
+            sx = p->side;
+        }
         if (p->leaf2 && t == hp.nfront) {
             // fused last two levels: read the stored depth-(L-2) parents of excess L-2
             Leaf2Args B;
@@ -682,14 +735,19 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.T2 = p->d_tabs + p->tab_TK;
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
-            B.counter = p->d_counter;
+            B.counter = cnt_leaf;
             B.prefetch = B.ntasks >= 16LL * p->leaf1_grid * (p->leaf2_threads / 32) ? 1 : 0;
-            if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
                 else launch_leaf2<false>(p, B, hp.nl[2], st);
             }
-            mark();
+            if (fork) {
+                const int e = pr.rec(st);
+                pr.launch_done(ev_fork, e);
+                pr.last = e;
+            } else {
+                pr.seq();
+            }
             continue;
         }
         if (hp.leaf2_srctasks && p->leaf2 && t == hp.nfront - 1) {
@@ -704,66 +762,73 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             S.T2 = p->d_tabs + p->tab_TKS;
             S.ntasks = hp.pass_ntasks[t];
             S.partials = partials + hp.pass_partial_off[t];
-            S.counter = p->d_counter;
+            S.counter = cnt_src;
             S.prefetch = 0;
-            if (cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
-            if (S.ntasks > 0) launch_leaf2_src(p, S, st);
-            mark();
-            continue;
-        }
-        PassArgs A;
-        memset(&A, 0, sizeof A);
-        A.nsrc = hp.total[t];
-        A.ntasks = hp.pass_ntasks[t];
-        A.nsplit = hp.pass_nsplit[t];
-        A.t = t;
-        double2 *re, *im;
-        uint32_t *meta;
-        front_ptrs(p, t, re, im, meta);
-        A.src_re = re;
-        A.src_im = im;
-        A.src_meta = meta;
-        const bool write = (t + 1 <= hp.nfront) && !(p->leaf2 && t + 1 == hp.nfront);
-        if (write) front_ptrs(p, t + 1, A.dst_re, A.dst_im, A.dst_meta);
-        A.offT = p->d_tabs + p->tab_offT[t];
-        A.NT = p->d_tabs + p->tab_NT[t];
-        A.CT = p->d_tabs + p->tab_CT[t];
-        A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
-        A.partials = partials + hp.pass_partial_off[t];
-        A.counter = p->d_counter;
-        if (t == p->leaf1_t && cudaMemsetAsync(p->d_counter, 0, sizeof(unsigned long long), st) != cudaSuccess)
-            return SG_ECUDA;
-        const unsigned grid = (unsigned)hp.pass_blocks[t];
-        // single-level last pass (every source has excess L-1): specialised k_leaf1
-        const int n2 = hp.nl[2];
-        const bool single = !write && t == p->leaf1_t;
-        if (p->sform) {
-            if (p->sform_dd) {
-                if (write) k_pass_s<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-                else k_pass_s<true, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            } else {
-                if (write) k_pass_s<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-                else k_pass_s<false, false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            }
-        } else if (p->cplx) {
-            if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, st); }
-            else k_leaf<true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            if (S.ntasks > 0) launch_leaf2_src(p, S, sx);
         } else {
-            if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A);
-            else if (single) { if (A.ntasks > 0) launch_leaf1<false>(p, A, n2, st); }
-            else k_leaf<false><<<grid, PASS_THREADS, 0, st>>>(dp, A);
+            PassArgs A;
+            memset(&A, 0, sizeof A);
+            A.nsrc = hp.total[t];
+            A.ntasks = hp.pass_ntasks[t];
+            A.nsplit = hp.pass_nsplit[t];
+            A.t = t;
+            double2 *re, *im;
+            uint32_t *meta;
+            front_ptrs(p, t, re, im, meta);
+            A.src_re = re;
+            A.src_im = im;
+            A.src_meta = meta;
+            const bool write = (t + 1 <= hp.nfront) && !(p->leaf2 && t + 1 == hp.nfront);
+            if (write) front_ptrs(p, t + 1, A.dst_re, A.dst_im, A.dst_meta);
+            A.offT = p->d_tabs + p->tab_offT[t];
+            A.NT = p->d_tabs + p->tab_NT[t];
+            A.CT = p->d_tabs + p->tab_CT[t];
+            A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
+            A.partials = partials + hp.pass_partial_off[t];
+            A.counter = cnt_leaf;   // k_leaf1 (the last pass of an unfused plan)
+            const unsigned grid = (unsigned)hp.pass_blocks[t];
+            // single-level last pass (every source has excess L-1): specialised k_leaf1
+            const int n2 = hp.nl[2];
+            const bool single = !write && t == p->leaf1_t;
+            if (p->sform) {
+                if (p->sform_dd) {
+                    if (write) k_pass_s<true, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                    else k_pass_s<true, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                } else {
+                    if (write) k_pass_s<false, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                    else k_pass_s<false, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                }
+            } else if (p->cplx) {
+                if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, sx); }
+                else k_leaf<true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+            } else {
+                if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                else if (single) { if (A.ntasks > 0) launch_leaf1<false>(p, A, n2, sx); }
+                else k_leaf<false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+            }
         }
-        mark();
+        if (sx != st) {
+            const int e = pr.rec(sx);
+            pr.launch_done(ev_fork, e);
+            if (cudaEventRecord(p->ev_join, sx) != cudaSuccess) return SG_ECUDA;
+        } else {
+            pr.seq();
+        }
     }
+    if (fork && cudaStreamWaitEvent(st, p->ev_join, 0) != cudaSuccess) return SG_ECUDA;
     {
         const long long nl1 = std::max<long long>(1, (hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2);
         double2 *l1 = (double2 *)(p->ws + p->ws_red_off);
         k_reduce_fused<<<(unsigned)nl1, RED_THREADS, 0, st>>>(dp, partials, hp.total_partials,
                                                                hp.include_root ? 1 : 0, out_dev, l1,
-                                                               p->d_counter + 1);
+                                                               p->d_counter + 1, p->d_counter);
     }
-    mark();
+    {
+        // the reduction starts when both branches are done: time it from the later of the two ends
+        const int e = pr.rec(st);
+        pr.launch_done(pr.last, e);
+    }
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
 }
@@ -792,8 +857,8 @@ extern "C" int sg_integrate_host(sg_plan_t p, sg_stream_t s, double *result_host
 
 extern "C" int sg_status_word(sg_plan_t p, int *status) {
     if (!p || !status) return SG_EINVAL;
-    int v = 0;
-    if (cudaMemcpy(&v, p->dp.status, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return SG_ECUDA;
+    int v = 0;   // status[1]: the flag of the last completed sg_integrate (k_finalize reads the same)
+    if (cudaMemcpy(&v, p->dp.status + 1, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return SG_ECUDA;
     *status = v ? SG_ENONFINITE : SG_OK;
     return SG_OK;
 }
@@ -930,7 +995,7 @@ extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
 extern "C" int sg_profile_enable(sg_plan_t p, int enable) {
     if (!p) return SG_EINVAL;
     if (enable && p->ev.empty()) {
-        p->ev.resize(5 + p->hp.nfront);
+        p->ev.resize(6 + p->hp.nfront);
         for (auto &e : p->ev)
             if (cudaEventCreate(&e) != cudaSuccess) return SG_ECUDA;
     }
@@ -947,10 +1012,20 @@ extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
         *n = nl;
         return SG_OK;
     }
-    if (*n < nl || p->ev.empty()) return SG_EINVAL;
-    if (cudaEventSynchronize(p->ev[nl]) != cudaSuccess) return SG_ECUDA;
-    for (int i = 0; i < nl; ++i)
-        if (cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess) return SG_ECUDA;
+    if (*n < nl || p->ev.empty() || (int)p->prof_pairs.size() != nl) return SG_EINVAL;
+    int emax = 0;
+    for (auto &pr : p->prof_pairs) emax = std::max(emax, std::max(pr.first, pr.second));
+    if (cudaEventSynchronize(p->ev[emax]) != cudaSuccess) return SG_ECUDA;
+    for (int i = 0; i < nl; ++i) {
+        const int a = p->prof_pairs[i].first, b = p->prof_pairs[i].second;
+        if (a < 0 || b < 0) return SG_EINVAL;
+        if (a == b) {
+            ms[i] = 0.0f;
+            continue;
+        }
+        if (cudaEventSynchronize(p->ev[b]) != cudaSuccess) return SG_ECUDA;
+        if (cudaEventElapsedTime(&ms[i], p->ev[a], p->ev[b]) != cudaSuccess) return SG_ECUDA;
+    }
     *n = nl;
     return SG_OK;
 }
@@ -1011,12 +1086,13 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
     int rc = build_unrank_tables(p);
     if (rc) return rc;
     // the factor table and base of the current parameters (K0), then one thread per index
-    if (cudaMemsetAsync(p->dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);
-    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb);
+    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb, nullptr);
     if (n > 0)
         k_eval_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p->dp, p->utabs, index_dev, n, points_dev,
                                                                    terms_dev);
+    // keep the invariant "status[0] is clear when a step starts" (non-finite factors show as NaN terms)
+    if (cudaMemsetAsync(p->dp.status, 0, sizeof(int), st) != cudaSuccess) return SG_ECUDA;
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
 }
@@ -1024,6 +1100,9 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
 extern "C" int sg_destroy(sg_plan_t p) {
     if (!p) return SG_EINVAL;
     for (auto &e : p->ev) cudaEventDestroy(e);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->side) cudaStreamDestroy(p->side);
     if (p->d_unrank) cudaFree(p->d_unrank);
     if (p->dev_block) cudaFree(p->dev_block);
     delete p;
