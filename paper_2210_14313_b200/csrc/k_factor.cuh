@@ -124,17 +124,29 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
     }
 }
 
+// K0 in one launch: blocks 0 .. nfb-1 fill the factor table (one entry per thread), block nfb computes
+// the base value (independent of the table; base_body needs a 256-thread block).
+#define K0_THREADS 256
+__global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int nfb) {
+    if ((int)blockIdx.x == nfb) base_body(P);
+    else factor_entry(P, blockIdx.x * K0_THREADS + threadIdx.x);
+}
+
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by the leaf
-// kernels' grid accumulators.  One level per call by an NT-thread CTA: chunked row sums, a parallel
-// (Hillis-Steele) suffix scan over the NT chunk sums, then each thread writes the suffix values of its
-// chunk.  SA is only an upper bound for the grid choice (used with a 1 + 2^-20 margin), so the
-// summation order is free; it is fixed, so SA is deterministic.
-template <int NT>
-__device__ __forceinline__ void suffix_level(const DevPlan &P, int l, double *suf) {
+// kernels' grid accumulators.  One CTA per level: chunked row sums, a parallel (Hillis-Steele)
+// suffix scan over the chunk sums, then each thread writes the suffix values of its chunk.  SA is
+// only an upper bound for the grid choice (used with a 1 + 2^-20 margin), so the summation order is
+// free; it is fixed, so SA is deterministic.  (Tried: the same scan in K0's last block (atomic
+// ticket) to save the launch: 21 us slower on config 4 — one 256-thread CTA walking the levels in
+// turn is latency-bound; reverted.)
+#define SUFFIX_THREADS 1024
+__global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) {
+    const int l = 2 + blockIdx.x;
+    if (l > P.L + 1) return;
     const int d = P.d, n = P.nl[l];
     const double2 *Fr = P.Fre + P.tab_off[l];
     const double2 *Fi = P.kind == SG_F_OSCILLATORY ? P.Fim + P.tab_off[l] : nullptr;
-    const int chunk = (d + NT - 1) / NT;
+    const int chunk = (d + SUFFIX_THREADS - 1) / SUFFIX_THREADS;
     const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
     auto row = [&](int k) {
         double r0 = 0.0, r1 = 0.0;
@@ -142,18 +154,19 @@ __device__ __forceinline__ void suffix_level(const DevPlan &P, int l, double *su
         const double2 *fi = Fi ? Fi + (long long)k * n : nullptr;
 #pragma unroll 4
         for (int j = 0; j < n; ++j) {
-            r0 += fabs(__ldcg(fr + j).x);
-            if (fi) r1 += fabs(__ldcg(fi + j).x);
+            r0 += fabs(__ldg(fr + j).x);
+            if (fi) r1 += fabs(__ldg(fi + j).x);
         }
         return r0 + r1;
     };
     double cs = 0.0;
     for (int k = k0; k < k1; ++k) cs += row(k);
+    __shared__ double suf[SUFFIX_THREADS + 1];
     suf[threadIdx.x] = cs;
-    if (threadIdx.x == 0) suf[NT] = 0.0;
+    if (threadIdx.x == 0) suf[SUFFIX_THREADS] = 0.0;
     __syncthreads();
-    for (int off = 1; off < NT; off <<= 1) {   // suf[i] = sum of chunks i.. end
-        const double t = (threadIdx.x + off < NT) ? suf[threadIdx.x + off] : 0.0;
+    for (int off = 1; off < SUFFIX_THREADS; off <<= 1) {   // suf[i] = sum of chunks i.. end
+        const double t = (threadIdx.x + off < SUFFIX_THREADS) ? suf[threadIdx.x + off] : 0.0;
         __syncthreads();
         suf[threadIdx.x] += t;
         __syncthreads();
@@ -164,39 +177,4 @@ __device__ __forceinline__ void suffix_level(const DevPlan &P, int l, double *su
         sacc += row(k);
         P.SA[(long long)l * (d + 1) + k] = sacc;
     }
-    __syncthreads();   // suf is reused by the next level
-}
-
-// K0 in one launch: blocks 0 .. nfb-1 fill the factor table (one entry per thread), block nfb computes
-// the base value (independent of the table; base_body needs a 256-thread block).  With a ticket
-// (small tables, K0_SUFFIX_MAX entries), the last block to finish (atomic ticket after a fence, the
-// same pattern as k_reduce_fused) also computes the suffix bounds SA of every level — one launch
-// fewer per step; which block is last changes no summation order.
-#define K0_THREADS 256
-#define K0_SUFFIX_MAX 65536
-__global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int nfb, unsigned long long *ticket) {
-    if ((int)blockIdx.x == nfb) base_body(P);
-    else factor_entry(P, blockIdx.x * K0_THREADS + threadIdx.x);
-    if (ticket == nullptr) return;
-    __shared__ int last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(ticket, 1ULL) == (unsigned long long)gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    __shared__ double suf[K0_THREADS + 1];
-    for (int l = 2; l <= P.L + 1; ++l) suffix_level<K0_THREADS>(P, l, suf);
-    if (threadIdx.x == 0) *ticket = 0;   // re-armed for the next step
-}
-
-#define SUFFIX_THREADS 1024
-// Standalone suffix bounds (large tables): one CTA per level.
-__global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) {
-    const int l = 2 + blockIdx.x;
-    if (l > P.L + 1) return;
-    __shared__ double suf[SUFFIX_THREADS + 1];
-    suffix_level<SUFFIX_THREADS>(P, l, suf);
 }

@@ -366,7 +366,12 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->ws_need = ws;
     if (p->leaf2 && hp.nfront >= 2 && !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
-        if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
+        // fills the rest of the GPU and takes over the SMs the short pass frees (graph kernel nodes
+        // keep the capturing stream's priority)
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        if (cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
@@ -641,7 +646,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);   // factor-table blocks of the merged K0 launch
     if (p->plain || p->collapse) {
         // status words: these paths' final kernels also close the step (step_close_status)
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb, nullptr);
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         pr.seq();
         pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
     }
@@ -676,17 +681,15 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         return SG_OK;
     }
     // Task counters (plan-owned, zero at the start of every step; re-armed by k_reduce_fused):
-    // [0] the persistent last-pass kernel, [1] the reduction ticket, [2] the source-task kernel,
-    // [3] K0's suffix ticket.
+    // [0] the persistent last-pass kernel, [1] the reduction ticket, [2] the source-task kernel.
     unsigned long long *cnt_leaf = p->d_counter, *cnt_src = p->d_counter + 2;
-    // K0 (factor table + base; with a small table also the suffix bounds, by its last block)
-    const bool k0_suffix = !p->sform && hp.tab_entries > 0 && hp.tab_entries <= K0_SUFFIX_MAX;
+    // K0 (factor table + base), then the suffix bounds of |F|
     if (p->sform) {
         if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
     } else {
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb, k0_suffix ? p->d_counter + 3 : nullptr);
-        if (hp.tab_entries > 0 && !k0_suffix) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
     }
     pr.seq();
     pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
@@ -1087,7 +1090,7 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
     if (rc) return rc;
     // the factor table and base of the current parameters (K0), then one thread per index
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);
-    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb, nullptr);
+    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb);
     if (n > 0)
         k_eval_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p->dp, p->utabs, index_dev, n, points_dev,
                                                                    terms_dev);

@@ -38,13 +38,14 @@ def time_plan(plan, flush, reps=5):
 
 
 def phases(plan, flush, reps=5):
-    """Per-launch device ms (sg_profile_read) of the best of `reps` runs, plus the step time."""
-    plan.profile_enable(True)
+    """Per-launch device ms (sg_profile_read: events captured as graph nodes) of the best of `reps`
+    CUDA-graph replays."""
+    g = plan.capture_graph(finalize=False, profile=True)
     best = None
     for _ in range(reps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
-        plan.sg_integrate()
+        g.replay()
         ms = plan.profile_read()
         if best is None or sum(ms) < sum(best):
             best = ms
