@@ -814,9 +814,10 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         // piece length: about LEAF2_PIECES_PER_WARP pieces per resident warp (the dynamic schedule's
         // tail is about one piece), at most LEAF2_TASK_ROWS and at least LEAF2_MIN_PIECE rows (each
         // piece repeats its k_mid prologue)
+        int64_t ppw = LEAF2_PIECES_PER_WARP;
+        if (const char *e = getenv("SG_B200_PIECES"); e && e[0]) ppw = std::max(1, atoi(e));   // A/B runs
         const int64_t piece = std::max<int64_t>(
-            LEAF2_MIN_PIECE,
-            std::min<int64_t>(LEAF2_TASK_ROWS, total_rows / ((int64_t)LEAF2_RESIDENT_WARPS * LEAF2_PIECES_PER_WARP)));
+            LEAF2_MIN_PIECE, std::min<int64_t>(LEAF2_TASK_ROWS, total_rows / ((int64_t)LEAF2_RESIDENT_WARPS * ppw)));
         if (do_split) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {
@@ -854,6 +855,23 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             if (a.kp0 != b.kp0) return a.kp0 < b.kp0;
             return a.first < b.first;
         });
+        if (const char *dbg = getenv("SG_B200_DEBUG_TASKS"); dbg && dbg[0] == '1') {
+            // list schedule of the sorted tasks on the resident warps (cost = rows + 2 per k_mid of the
+            // task's group for its prologue): makespan against the perfect balance (tail loss)
+            std::vector<double> wq(LEAF2_RESIDENT_WARPS, 0.0);
+            std::make_heap(wq.begin(), wq.end(), std::greater<double>());
+            double tot = 0.0;
+            for (const Task &tk : tasks) {
+                const double c = (double)tk.rows + 2.0 * (double)((tk.kb - tk.ka + G - 1) / G);
+                std::pop_heap(wq.begin(), wq.end(), std::greater<double>());
+                wq.back() += c;
+                std::push_heap(wq.begin(), wq.end(), std::greater<double>());
+                tot += c;
+            }
+            const double mk = *std::max_element(wq.begin(), wq.end());
+            fprintf(stderr, "leaf2 schedule: makespan %.0f avg %.0f efficiency %.4f\n", mk,
+                    tot / LEAF2_RESIDENT_WARPS, tot / LEAF2_RESIDENT_WARPS / mk);
+        }
         hp.T2.resize(3 * tasks.size());
         for (size_t i = 0; i < tasks.size(); ++i) {
             hp.T2[3 * i] = tasks[i].first;

@@ -74,6 +74,8 @@ struct sg_plan_s {
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
+    int prefetch_min = 16;              // fused kernel prefetches the next task with >= this many
+                                        // tasks per resident warp (SG_B200_PREFETCH_MIN: A/B runs)
     std::vector<cudaEvent_t> ev;
     std::vector<std::pair<int, int>> prof_pairs;   // per launch of the last sg_integrate: (start, end) event
     // fused plans: pass nfront-1 runs on a plan-owned side stream, concurrently with the fused pass
@@ -303,6 +305,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         delete p;
         return SG_ECUDA;
     }
+    if (const char *e = getenv("SG_B200_PREFETCH_MIN"); e && e[0]) p->prefetch_min = atoi(e);
     rc = (p->collapse || p->plain) ? SG_OK : setup_leaf1(p);
     if (rc) {
         cudaGetLastError();
@@ -739,7 +742,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.ntasks = hp.pass_ntasks[t];
             B.partials = partials + hp.pass_partial_off[t];
             B.counter = cnt_leaf;
-            B.prefetch = B.ntasks >= 16LL * p->leaf1_grid * (p->leaf2_threads / 32) ? 1 : 0;
+            B.prefetch = B.ntasks >= (long long)p->prefetch_min * p->leaf1_grid * (p->leaf2_threads / 32) ? 1 : 0;
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
                 else launch_leaf2<false>(p, B, hp.nl[2], st);
