@@ -5,9 +5,10 @@
 // ---------------------------------------------------------------------------------------------
 // Root pass: every depth-1 point (k1, l1, j1) of this shard, one thread each.
 // ---------------------------------------------------------------------------------------------
+// One depth-1 point r1 (lexicographic rank in [R.lo, R.hi)): its term, and its frontier-1 record if
+// it is extendable.
 template <bool CPLX>
-__global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R) {
-    const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ dd root_node(const DevPlan &P, const RootArgs &R, long long r1) {
     dd tot = {0.0, 0.0};
     if (r1 < R.hi) {
         const int k1 = (int)(r1 / P.M0);
@@ -41,7 +42,13 @@ __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R)
             R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
         }
     }
-    dd s = block_reduce_dd<8>(tot);
+    return tot;
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R) {
+    const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    dd s = block_reduce_dd<8>(root_node<CPLX>(P, R, r1));
     if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
 }
 

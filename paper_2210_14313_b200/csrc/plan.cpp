@@ -817,7 +817,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         int64_t ppw = LEAF2_PIECES_PER_WARP;
         if (const char *e = getenv("SG_B200_PIECES"); e && e[0]) ppw = std::max(1, atoi(e));   // A/B runs
         const int64_t piece = std::max<int64_t>(
-            LEAF2_MIN_PIECE, std::min<int64_t>(LEAF2_TASK_ROWS, total_rows / ((int64_t)LEAF2_RESIDENT_WARPS * ppw)));
+            LEAF2_MIN_PIECE, std::min<int64_t>(LEAF2_MAX_PIECE, total_rows / ((int64_t)LEAF2_RESIDENT_WARPS * ppw)));
         if (do_split) {
             std::vector<Task> split;
             for (const Task &tk : tasks) {

@@ -43,7 +43,12 @@
 #define LEAF2_SPLIT_SHARE 4   // split long tasks when one is > 1/SHARE of a resident warp's row share
 #endif
 #ifndef LEAF2_PIECES_PER_WARP
-#define LEAF2_PIECES_PER_WARP 8   // split pieces per resident warp on small shards (tail ~ one piece)
+#define LEAF2_PIECES_PER_WARP 2   // split pieces per resident warp on small shards (A/B on config 4 at N = 8:
+                                  // 8 -> 0.314 ms, 4 -> 0.296, 2 -> 0.294, 1 -> 0.325; fewer, longer pieces
+                                  // amortise the per-task fetch and k_mid prologue)
+#endif
+#ifndef LEAF2_MAX_PIECE
+#define LEAF2_MAX_PIECE 1024      // longest split piece (rows)
 #endif
 #ifndef LEAF2_MIN_PIECE
 #define LEAF2_MIN_PIECE 32        // shortest split piece (rows)
