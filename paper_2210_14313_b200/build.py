@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["sg_kernels.cu"]
 SOURCES_CPP = ["plan.cpp"]
 DEPS = ["dd.cuh", "plan.h", "kernels_common.cuh", "k_factor.cuh", "k_tree.cuh", "k_sform.cuh",
-        "k_reduce.cuh", "k_collapse.cuh", "k_unrank.cuh", "k_head.cuh"]
+        "k_reduce.cuh", "k_collapse.cuh", "k_unrank.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -35,7 +35,6 @@
 #include "k_reduce.cuh"
 #include "k_collapse.cuh"
 #include "k_unrank.cuh"
-#include "k_head.cuh"
 
 // ---------------------------------------------------------------------------------------------
 // plan object and C ABI
@@ -75,7 +74,6 @@ struct sg_plan_s {
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
-    int head_grid = 0;                  // > 0: K0 + suffix + root as one cooperative k_head launch
     int prefetch_min = 16;              // fused kernel prefetches the next task with >= this many
                                         // tasks per resident warp (SG_B200_PREFETCH_MIN: A/B runs)
     std::vector<cudaEvent_t> ev;
@@ -369,24 +367,6 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->ws_red_off = ws;
     ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2 + 1), 256);
     p->ws_need = ws;
-    {
-        // one cooperative head launch (k_head.cuh) when its whole grid is co-resident and the suffix
-        // rows per thread fit its registers; SG_B200_NOHEAD=1 keeps the three launches (A/B, tests)
-        const char *nh = getenv("SG_B200_NOHEAD");
-        const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);
-        const long long grid = std::max<long long>(std::max<long long>(nfb + 1, hp.root_blocks), hp.L);
-        int dev = 0, sms = 0, per_sm = 0, coop = 0;
-        if (!(nh && nh[0] == '1') && !p->sform && hp.tab_entries > 0 &&
-            hp.d <= HEAD_SUF_MAXCH * K0_THREADS && cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, p->cplx ? (const void *)k_head<true> : (const void *)k_head<false>, K0_THREADS, 0) ==
-                cudaSuccess &&
-            grid <= (long long)per_sm * sms)
-            p->head_grid = (int)grid;
-        cudaGetLastError();
-    }
     if (p->leaf2 && hp.nfront >= 2 && !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
         // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
@@ -706,6 +686,17 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // Task counters (plan-owned, zero at the start of every step; re-armed by k_reduce_fused):
     // [0] the persistent last-pass kernel, [1] the reduction ticket, [2] the source-task kernel.
     unsigned long long *cnt_leaf = p->d_counter, *cnt_src = p->d_counter + 2;
+    // K0 (factor table + base), then the suffix bounds of |F|
+    if (p->sform) {
+        if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+    } else {
+        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
+    }
+    pr.seq();
+    pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
+    // root pass
     RootArgs R;
     memset(&R, 0, sizeof R);
     R.lo = hp.range_lo;
@@ -714,38 +705,13 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     R.JS = p->d_tabs + p->tab_JS;
     if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
     R.partials = partials;
-    if (p->head_grid > 0) {
-        // K0 + suffix bounds + root pass in one cooperative launch (k_head.cuh)
-        DevPlan dpc = dp;
-        RootArgs Rc = R;
-        int nfb_c = nfb, rb = (int)hp.root_blocks;
-        void *args[] = {&dpc, &Rc, &nfb_c, &rb};
-        if (cudaLaunchCooperativeKernel(p->cplx ? (const void *)k_head<true> : (const void *)k_head<false>,
-                                        dim3(p->head_grid), dim3(K0_THREADS), args, 0, st) != cudaSuccess)
-            return SG_ECUDA;
-        pr.seq();
-        pr.launch_done(pr.last, pr.last);   // K0 base: merged
-        pr.launch_done(pr.last, pr.last);   // root pass: merged
-    } else {
-        // K0 (factor table + base), then the suffix bounds of |F|
-        if (p->sform) {
-            if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-            else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        } else {
-            k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-            if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
-        }
-        pr.seq();
-        pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
-        // root pass
-        if (p->sform)
-            (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-        else if (p->cplx)
-            k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-        else
-            k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-        pr.seq();
-    }
+    if (p->sform)
+        (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    else if (p->cplx)
+        k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    else
+        k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+    pr.seq();
     // Fused plans: pass nfront-1 writes no frontier (its children are the fused kernel's business),
     // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
     // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).
