@@ -7,7 +7,12 @@
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool dd_finite(dd a) { return isfinite(a.hi) && isfinite(a.lo); }
 
-__device__ __forceinline__ void factor_entry(const DevPlan &P, int idx) {
+struct FactorOut {
+    int l, k, j;   // level, coordinate, node of the entry
+    dd Fr, Fi;     // its factor w E (imaginary part: oscillatory kind)
+};
+
+__device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOut *outp = nullptr) {
     const int n_ent = P.tab_off[P.L + 2];
     if (idx >= n_ent) return;
     int l = 2;
@@ -50,15 +55,38 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx) {
         break;
     }
     }
-    dd Fr = dd_mul(wt, Er);
+    dd Fr = dd_mul(wt, Er), Fi = {0.0, 0.0};
     P.Fre[idx] = make_double2(Fr.hi, Fr.lo);
     bool ok = dd_finite(Fr);
     if (P.kind == SG_F_OSCILLATORY) {
-        dd Fi = dd_mul(wt, Ei);
+        Fi = dd_mul(wt, Ei);
         P.Fim[idx] = make_double2(Fi.hi, Fi.lo);
         ok = ok && dd_finite(Fi);
     }
     if (!ok) atomicOr(P.status, 1);
+    if (outp) *outp = FactorOut{l, k, j, Fr, Fi};
+}
+
+// per-coordinate bound b_k >= max over x in [0,1] of |E_k(x)| (|Re| + |Im| for the oscillatory kind),
+// evaluated in FP64 with a relative margin of 2^-40 over the library exp's error: the analytic
+// suffix bounds SA (k_head) use it instead of summing the table's |F|
+__device__ __forceinline__ double coord_bound(const DevPlan &P, int k) {
+    const double ck = P.c[k];
+    switch (P.kind) {
+    case SG_F_EXP_LINEAR: return exp(0.5 * fabs(ck)) * (1.0 + 0x1p-40);
+    case SG_F_OSCILLATORY: return 1.4142135623730951 * (1.0 + 0x1p-40);
+    case SG_F_GAUSSIAN: {
+        // exp(-c^2 ((x - w)^2 - (1/2 - w)^2)) is largest where (x - w)^2 is smallest on [0, 1]
+        const double wk = P.w[k], dist = wk < 0.0 ? -wk : (wk > 1.0 ? wk - 1.0 : 0.0), bm = 0.5 - wk;
+        return exp(ck * ck * (bm * bm - dist * dist)) * (1.0 + 0x1p-40);
+    }
+    case SG_F_PRODUCT_PEAK: {
+        const double wk = P.w[k], dist = wk < 0.0 ? -wk : (wk > 1.0 ? wk - 1.0 : 0.0), bm = 0.5 - wk;
+        const double ci2 = 1.0 / (ck * ck);
+        return (ci2 + bm * bm) / (ci2 + dist * dist) * (1.0 + 0x1p-40);
+    }
+    }
+    return 1.0;
 }
 
 // base value B (256-thread CTA): fixed-order strided partials, then a fixed CTA tree (sum; product
@@ -176,5 +204,158 @@ __global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) 
     for (int k = k1 - 1; k >= k0; --k) {
         sacc += row(k);
         P.SA[(long long)l * (d + 1) + k] = sacc;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_head: the head of a tree step in ONE launch, no grid barrier — K0's factor entries, the base B
+// (every block computes it redundantly from the d coefficients: the same fixed-order arithmetic, so
+// the same bits; block 0 stores it), the root pass for the block's own entries (the depth-1 point of
+// entry (l, k, j) is rank r1 = k M0 + sum_{l'<l} n_l' + j; its factor is the thread's own, so no
+// cross-block dependency), and, in block 0, the analytic suffix bounds SA[l][k] = W_l sum_{k'>=k}
+// b_k' (W_l = sum_j |w_j^l|, b_k = coord_bound) — upper bounds of the table sums k_suffix_abs takes.
+// Replaces k_factor_base + k_suffix_abs + k_root (three graph nodes) for d <= HEAD_MAX_D, where the
+// redundant per-block base loop (d / 256 coordinates per thread) stays short.  Root partial slot =
+// the block (plan.cpp sizes root_blocks to the K0 grid).
+// ---------------------------------------------------------------------------------------------
+#define HEAD_MAX_D 2048
+template <bool CPLX>
+__global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const RootArgs R) {
+    const int idx = blockIdx.x * K0_THREADS + threadIdx.x;
+    FactorOut fo;
+    fo.l = -1;
+    factor_entry(P, idx, &fo);
+    // B, block-wide (base_body's arithmetic; every thread gets the value through shared memory)
+    __shared__ double2 bsm[4];
+    {
+        const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
+        dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
+        for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
+            const double ck = P.c[k];
+            switch (P.kind) {
+            case SG_F_EXP_LINEAR:
+            case SG_F_OSCILLATORY:
+                acc = dd_add(acc, dd{0.5 * ck, 0.0});
+                break;
+            case SG_F_GAUSSIAN: {
+                dd bm = dd_from_sum(0.5, -P.w[k]);
+                acc = dd_add(acc, dd_mul(dd_mul(bm, bm), dd_from_prod(ck, ck)));
+                break;
+            }
+            case SG_F_PRODUCT_PEAK: {
+                dd bm = dd_from_sum(0.5, -P.w[k]);
+                dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+                acc = dd_mul(acc, dd_div(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
+                break;
+            }
+            }
+        }
+        __shared__ double2 sm[K0_THREADS];
+        sm[threadIdx.x] = make_double2(acc.hi, acc.lo);
+        __syncthreads();
+        for (int s2 = K0_THREADS / 2; s2 > 0; s2 >>= 1) {
+            if (threadIdx.x < s2) {
+                dd a = {sm[threadIdx.x].x, sm[threadIdx.x].y}, b = {sm[threadIdx.x + s2].x, sm[threadIdx.x + s2].y};
+                dd r = prod ? dd_mul(a, b) : dd_add(a, b);
+                sm[threadIdx.x] = make_double2(r.hi, r.lo);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            dd sv = {sm[0].x, sm[0].y};
+            dd Br = sv, Bi = {0.0, 0.0};
+            switch (P.kind) {
+            case SG_F_EXP_LINEAR: Br = dd_exp(sv); break;
+            case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(sv)); break;
+            case SG_F_PRODUCT_PEAK: Br = sv; break;
+            case SG_F_OSCILLATORY: {
+                const double u = P.u[0];
+                dd th = dd_add(dd_from_prod(DD_2PI_0, u), dd_from_prod(DD_2PI_1, u));
+                th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
+                th = dd_add(th, sv);
+                dd sn, cs;
+                dd_sincos(th, sn, cs);
+                Br = cs;
+                Bi = sn;
+                break;
+            }
+            }
+            bsm[0] = make_double2(Br.hi, Br.lo);
+            bsm[1] = make_double2(Bi.hi, Bi.lo);
+            if (blockIdx.x == 0) {
+                P.base[0] = Br.hi;
+                P.base[1] = Br.lo;
+                P.base[2] = Bi.hi;
+                P.base[3] = Bi.lo;
+                if (!dd_finite(Br) || !dd_finite(Bi)) atomicOr(P.status, 1);
+            }
+        }
+        __syncthreads();
+    }
+    // root pass for this thread's entry (k_root's arithmetic)
+    dd tot = {0.0, 0.0};
+    if (fo.l >= 2) {
+        long long r1 = (long long)fo.k * P.M0 + fo.j;
+        for (int l = 2; l < fo.l; ++l) r1 += P.nl[l];
+        if (r1 >= R.lo && r1 < R.hi) {
+            const dd Br = {bsm[0].x, bsm[0].y};
+            dd cr, ci = {0.0, 0.0};
+            if (CPLX) {
+                const dd Bi = {bsm[1].x, bsm[1].y};
+                cdd ch = cdd_mul(cdd{Br, Bi}, cdd{fo.Fr, fo.Fi});
+                cr = ch.re;
+                ci = ch.im;
+            } else {
+                cr = dd_mul(Br, fo.Fr);
+            }
+            const int b1 = fo.l - 1, k1 = fo.k;
+            tot = coef_mul(P, cr, 1, b1);
+            if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
+                const long long seg = (long long)b1 * P.d + k1;
+                const long long o = R.off1[seg] + fo.j - R.JS[seg];
+                R.dst_re[o] = make_double2(cr.hi, cr.lo);
+                if (CPLX) R.dst_im[o] = make_double2(ci.hi, ci.lo);
+                R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+            }
+        }
+    }
+    dd sblk = block_reduce_dd<K0_THREADS / 32>(tot);
+    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(sblk.hi, sblk.lo);
+    // block 0: analytic suffix bounds of every level
+    if (blockIdx.x == 0) {
+        const int d = P.d, chunk = (d + K0_THREADS - 1) / K0_THREADS;   // <= HEAD_MAX_D / K0_THREADS
+        const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
+        double bk[HEAD_MAX_D / K0_THREADS];
+        double cs = 0.0;
+#pragma unroll
+        for (int c = 0; c < HEAD_MAX_D / K0_THREADS; ++c) {
+            bk[c] = (k0 + c < k1) ? coord_bound(P, k0 + c) : 0.0;
+            cs += bk[c];
+        }
+        __shared__ double suf[K0_THREADS + 1];
+        __syncthreads();
+        suf[threadIdx.x] = cs;
+        if (threadIdx.x == 0) suf[K0_THREADS] = 0.0;
+        __syncthreads();
+        for (int off = 1; off < K0_THREADS; off <<= 1) {   // suf[i] = sum of chunks i.. end
+            const double t = (threadIdx.x + off < K0_THREADS) ? suf[threadIdx.x + off] : 0.0;
+            __syncthreads();
+            suf[threadIdx.x] += t;
+            __syncthreads();
+        }
+        double sacc = suf[threadIdx.x + 1];
+        double sk[HEAD_MAX_D / K0_THREADS];
+#pragma unroll
+        for (int c = HEAD_MAX_D / K0_THREADS - 1; c >= 0; --c) {
+            sacc += bk[c];
+            sk[c] = sacc;
+        }
+        for (int l = 2; l <= P.L + 1; ++l) {
+            const double wl = P.wabs[l] * (1.0 + 0x1p-40);
+            if (threadIdx.x == 0) P.SA[(long long)l * (d + 1) + d] = 0.0;
+#pragma unroll
+            for (int c = 0; c < HEAD_MAX_D / K0_THREADS; ++c)
+                if (k0 + c < k1) P.SA[(long long)l * (d + 1) + k0 + c] = wl * sk[c];
+        }
     }
 }

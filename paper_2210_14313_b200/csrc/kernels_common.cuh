@@ -28,6 +28,7 @@ struct DevPlan {
                     // the midpoint at the centre if n is odd): oscillatory factors of a pair are
                     // exact conjugates, the midpoint's is real (k_leaf's symmetric-row path)
     const double2 *coefm;   // node coefficient (dd) per (depth t, excess b): [t * (L + 1) + b]
+    double wabs[SG_MAX_L + 3];   // sum_j |w_j^l| (+ |lo|) per level: k_head's analytic suffix bounds
 };
 
 struct PassArgs {

@@ -631,7 +631,10 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     hp.pass_partial_off.assign(hp.nfront + 1, 0);
     hp.pass_terms[0] = (uint64_t)(hi - lo);
     hp.pass_written[0] = hp.nfront >= 1 ? (uint64_t)hp.total[1] : 0;
-    hp.root_blocks = std::max<int64_t>(1, (hi - lo + 255) / 256);
+    // root partial slots: one per 256 depth-1 prefixes of the WHOLE rank space, i.e. one per K0 block
+    // (k_head computes each depth-1 point in the K0 thread of its factor entry; the separate k_root
+    // launches the same number of blocks, those past the shard range write zero)
+    hp.root_blocks = std::max<int64_t>(1, (nd1 + 255) / 256);
     int64_t poff = hp.root_blocks;
     for (int t = 1; t <= hp.nfront; ++t) {
         u128 terms = 0;

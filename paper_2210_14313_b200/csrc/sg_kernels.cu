@@ -74,6 +74,7 @@ struct sg_plan_s {
     size_t leaf1_smem = 0;     // its dynamic shared memory (0 = factor rows read through L1)
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
+    bool head = false;                  // K0 + base + root + suffix bounds as one k_head launch
     int prefetch_min = 16;              // fused kernel prefetches the next task with >= this many
                                         // tasks per resident warp (SG_B200_PREFETCH_MIN: A/B runs)
     std::vector<cudaEvent_t> ev;
@@ -256,6 +257,11 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         dp.tab_off[l] = hp.tab_off[l];
     }
     for (int e = 0; e < SG_MAX_L + 2; ++e) dp.coef[e] = hp.coef[e];
+    for (int l = 2; l <= L + 1; ++l) {   // sum_j |w_j^l| of the level's table entries (k_head's SA bound)
+        double a = 0.0;
+        for (int j = 0; j < hp.nl[l]; ++j) a += fabs(hp.Whi[hp.entry_off[l] + j]) + fabs(hp.Wlo[hp.entry_off[l] + j]);
+        dp.wabs[l] = a;
+    }
     dp.M0 = hp.M0;
     dp.symmask = 0;
     for (int l = 2; l <= L + 1; ++l) {
@@ -367,6 +373,12 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     p->ws_red_off = ws;
     ws = align_up(ws + sizeof(double2) * (size_t)((hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2 + 1), 256);
     p->ws_need = ws;
+    {
+        // one head launch for the factor form at d <= HEAD_MAX_D; SG_B200_NOHEAD=1 keeps the three
+        // launches (A/B, tests)
+        const char *nh = getenv("SG_B200_NOHEAD");
+        p->head = !p->sform && hp.d <= HEAD_MAX_D && !(nh && nh[0] == '1');
+    }
     if (p->leaf2 && hp.nfront >= 2 && !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
         // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
@@ -686,17 +698,6 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // Task counters (plan-owned, zero at the start of every step; re-armed by k_reduce_fused):
     // [0] the persistent last-pass kernel, [1] the reduction ticket, [2] the source-task kernel.
     unsigned long long *cnt_leaf = p->d_counter, *cnt_src = p->d_counter + 2;
-    // K0 (factor table + base), then the suffix bounds of |F|
-    if (p->sform) {
-        if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-    } else {
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
-        if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
-    }
-    pr.seq();
-    pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
-    // root pass
     RootArgs R;
     memset(&R, 0, sizeof R);
     R.lo = hp.range_lo;
@@ -705,13 +706,33 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     R.JS = p->d_tabs + p->tab_JS;
     if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
     R.partials = partials;
-    if (p->sform)
-        (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-    else if (p->cplx)
-        k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-    else
-        k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
-    pr.seq();
+    if (p->head) {
+        // K0 + base + root pass + analytic suffix bounds in one launch (k_head, k_factor.cuh)
+        if (p->cplx) k_head<true><<<(unsigned)hp.root_blocks, K0_THREADS, 0, st>>>(dp, R);
+        else k_head<false><<<(unsigned)hp.root_blocks, K0_THREADS, 0, st>>>(dp, R);
+        pr.seq();
+        pr.launch_done(pr.last, pr.last);   // K0 base: merged
+        pr.launch_done(pr.last, pr.last);   // root pass: merged
+    } else {
+        // K0 (factor table + base), then the suffix bounds of |F|
+        if (p->sform) {
+            if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+            else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        } else {
+            k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+            if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
+        }
+        pr.seq();
+        pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
+        // root pass
+        if (p->sform)
+            (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+        else if (p->cplx)
+            k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+        else
+            k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
+        pr.seq();
+    }
     // Fused plans: pass nfront-1 writes no frontier (its children are the fused kernel's business),
     // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
     // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).

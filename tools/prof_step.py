@@ -20,7 +20,8 @@ def main():
     plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u,
                     merge=int(os.environ.get("QUICK_MERGE", "0")),
                     method=int(os.environ.get("QUICK_METHOD", "0")),
-                    arith=int(os.environ.get("QUICK_ARITH", "0")))
+                    arith=int(os.environ.get("QUICK_ARITH", "0")),
+                    rank=int(os.environ.get("QUICK_RANK", "0")), world=int(os.environ.get("QUICK_WORLD", "1")))
     for _ in range(steps):
         out = plan.sg_integrate()
         plan.sg_finalize(out, 1)
