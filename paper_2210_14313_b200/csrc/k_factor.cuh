@@ -12,6 +12,7 @@ struct FactorOut {
     dd Fr, Fi;     // its factor w E (imaginary part: oscillatory kind)
 };
 
+template <int KIND>
 __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOut *outp = nullptr) {
     const int n_ent = P.tab_off[P.L + 2];
     if (idx >= n_ent) return;
@@ -24,7 +25,7 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOu
     const double ck = P.c[k];
     const dd xm = dd_from_sum(x, -0.5);   // x - 1/2 exactly
     dd Er = {1.0, 0.0}, Ei = {0.0, 0.0};
-    switch (P.kind) {
+    switch (KIND) {
     case SG_F_EXP_LINEAR:
         Er = dd_exp(dd_mul_d(xm, ck));
         break;
@@ -58,7 +59,7 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOu
     dd Fr = dd_mul(wt, Er), Fi = {0.0, 0.0};
     P.Fre[idx] = make_double2(Fr.hi, Fr.lo);
     bool ok = dd_finite(Fr);
-    if (P.kind == SG_F_OSCILLATORY) {
+    if (KIND == SG_F_OSCILLATORY) {
         Fi = dd_mul(wt, Ei);
         P.Fim[idx] = make_double2(Fi.hi, Fi.lo);
         ok = ok && dd_finite(Fi);
@@ -70,9 +71,10 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOu
 // per-coordinate bound b_k >= max over x in [0,1] of |E_k(x)| (|Re| + |Im| for the oscillatory kind),
 // evaluated in FP64 with a relative margin of 2^-40 over the library exp's error: the analytic
 // suffix bounds SA (k_head) use it instead of summing the table's |F|
+template <int KIND>
 __device__ __forceinline__ double coord_bound(const DevPlan &P, int k) {
     const double ck = P.c[k];
-    switch (P.kind) {
+    switch (KIND) {
     case SG_F_EXP_LINEAR: return exp(0.5 * fabs(ck)) * (1.0 + 0x1p-40);
     case SG_F_OSCILLATORY: return 1.4142135623730951 * (1.0 + 0x1p-40);
     case SG_F_GAUSSIAN: {
@@ -91,12 +93,13 @@ __device__ __forceinline__ double coord_bound(const DevPlan &P, int k) {
 
 // base value B (256-thread CTA): fixed-order strided partials, then a fixed CTA tree (sum; product
 // for the peak kind)
+template <int KIND>
 __device__ __forceinline__ void base_body(const DevPlan &P) {
-    const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
+    const bool prod = (KIND == SG_F_PRODUCT_PEAK);
     dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
     for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
         const double ck = P.c[k];
-        switch (P.kind) {
+        switch (KIND) {
         case SG_F_EXP_LINEAR:
         case SG_F_OSCILLATORY:
             acc = dd_add(acc, dd{0.5 * ck, 0.0});
@@ -128,7 +131,7 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
     if (threadIdx.x == 0) {
         dd s = {sm[0].x, sm[0].y};
         dd Br = s, Bi = {0.0, 0.0};
-        switch (P.kind) {
+        switch (KIND) {
         case SG_F_EXP_LINEAR: Br = dd_exp(s); break;
         case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(s)); break;
         case SG_F_PRODUCT_PEAK: Br = s; break;
@@ -155,9 +158,12 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
 // K0 in one launch: blocks 0 .. nfb-1 fill the factor table (one entry per thread), block nfb computes
 // the base value (independent of the table; base_body needs a 256-thread block).
 #define K0_THREADS 256
+// KIND: the integrand kind (one instantiation each: the others' dd exp / sincos / division code would
+// only cost instruction fetches in this latency-bound launch)
+template <int KIND>
 __global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int nfb) {
-    if ((int)blockIdx.x == nfb) base_body(P);
-    else factor_entry(P, blockIdx.x * K0_THREADS + threadIdx.x);
+    if ((int)blockIdx.x == nfb) base_body<KIND>(P);
+    else factor_entry<KIND>(P, blockIdx.x * K0_THREADS + threadIdx.x);
 }
 
 // SA[l][k] = sum_{k' >= k} sum_j (|Fre[l][k'][j].hi| + |Fim[l][k'][j].hi|): bound used by the leaf
@@ -219,20 +225,21 @@ __global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) 
 // the block (plan.cpp sizes root_blocks to the K0 grid).
 // ---------------------------------------------------------------------------------------------
 #define HEAD_MAX_D 2048
-template <bool CPLX>
+template <int KIND>
 __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const RootArgs R) {
+    constexpr bool CPLX = (KIND == SG_F_OSCILLATORY);
     const int idx = blockIdx.x * K0_THREADS + threadIdx.x;
     FactorOut fo;
     fo.l = -1;
-    factor_entry(P, idx, &fo);
+    factor_entry<KIND>(P, idx, &fo);
     // B, block-wide (base_body's arithmetic; every thread gets the value through shared memory)
     __shared__ double2 bsm[4];
     {
-        const bool prod = (P.kind == SG_F_PRODUCT_PEAK);
+        const bool prod = (KIND == SG_F_PRODUCT_PEAK);
         dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
         for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
             const double ck = P.c[k];
-            switch (P.kind) {
+            switch (KIND) {
             case SG_F_EXP_LINEAR:
             case SG_F_OSCILLATORY:
                 acc = dd_add(acc, dd{0.5 * ck, 0.0});
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
         if (threadIdx.x == 0) {
             dd sv = {sm[0].x, sm[0].y};
             dd Br = sv, Bi = {0.0, 0.0};
-            switch (P.kind) {
+            switch (KIND) {
             case SG_F_EXP_LINEAR: Br = dd_exp(sv); break;
             case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(sv)); break;
             case SG_F_PRODUCT_PEAK: Br = sv; break;
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
         double cs = 0.0;
 #pragma unroll
         for (int c = 0; c < HEAD_MAX_D / K0_THREADS; ++c) {
-            bk[c] = (k0 + c < k1) ? coord_bound(P, k0 + c) : 0.0;
+            bk[c] = (k0 + c < k1) ? coord_bound<KIND>(P, k0 + c) : 0.0;
             cs += bk[c];
         }
         __shared__ double suf[K0_THREADS + 1];

@@ -31,6 +31,9 @@ __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 
 #define RED_THREADS 256
 #define RED_PER_THREAD 8
 #define RED_CHUNK2 (RED_THREADS * RED_PER_THREAD)
+// SF = DevPlan::sform (0 factor form, 1 / 2 s-forms): the root point's value; one instantiation each
+// keeps the s-forms' per-point outer functions out of the factor-form launch (instruction fetch)
+template <int SF>
 __global__ void __launch_bounds__(RED_THREADS)
 k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int include_root, double *out,
                double2 *l1, unsigned long long *ticket, unsigned long long *task_counters) {
@@ -61,9 +64,9 @@ k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int includ
     t = block_reduce_dd<RED_THREADS / 32>(t);
     if (threadIdx.x == 0) {
         if (include_root && P.coefm[0].x != 0.0) {
-            const dd root = P.sform == 2   ? sform_g_dd(P.kind, P.d, dd{P.base[0], P.base[1]})
-                            : P.sform == 1 ? dd{sform_g(P.kind, P.d, P.base[0]), 0.0}
-                                           : dd{P.base[0], P.base[1]};
+            const dd root = SF == 2   ? sform_g_dd(P.kind, P.d, dd{P.base[0], P.base[1]})
+                            : SF == 1 ? dd{sform_g(P.kind, P.d, P.base[0]), 0.0}
+                                      : dd{P.base[0], P.base[1]};
             t = dd_add(t, coef_mul(P, root, 0, 0));
         }
         const int st = *P.status;

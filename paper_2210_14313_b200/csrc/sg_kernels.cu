@@ -611,6 +611,25 @@ static void launch_leaf1(sg_plan_s *p, const PassArgs &A, int nj, cudaStream_t s
     }
 }
 
+// K0 / head launches, one instantiation per integrand kind (factor form: kinds 0-3)
+static void launch_factor_base(const DevPlan &dp, int nfb, cudaStream_t st) {
+    const unsigned g = (unsigned)(nfb + 1);
+    switch (dp.kind) {
+    case SG_F_EXP_LINEAR: k_factor_base<SG_F_EXP_LINEAR><<<g, K0_THREADS, 0, st>>>(dp, nfb); break;
+    case SG_F_OSCILLATORY: k_factor_base<SG_F_OSCILLATORY><<<g, K0_THREADS, 0, st>>>(dp, nfb); break;
+    case SG_F_PRODUCT_PEAK: k_factor_base<SG_F_PRODUCT_PEAK><<<g, K0_THREADS, 0, st>>>(dp, nfb); break;
+    case SG_F_GAUSSIAN: k_factor_base<SG_F_GAUSSIAN><<<g, K0_THREADS, 0, st>>>(dp, nfb); break;
+    }
+}
+static void launch_head(const DevPlan &dp, const RootArgs &R, unsigned grid, cudaStream_t st) {
+    switch (dp.kind) {
+    case SG_F_EXP_LINEAR: k_head<SG_F_EXP_LINEAR><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_OSCILLATORY: k_head<SG_F_OSCILLATORY><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_PRODUCT_PEAK: k_head<SG_F_PRODUCT_PEAK><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_GAUSSIAN: k_head<SG_F_GAUSSIAN><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
+    }
+}
+
 static void front_ptrs(sg_plan_s *p, int t, double2 *&re, double2 *&im, uint32_t *&meta) {
     const int par = t % 2;
     const int64_t cap = p->hp.ws_front_cap[par];
@@ -661,7 +680,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);   // factor-table blocks of the merged K0 launch
     if (p->plain || p->collapse) {
         // status words: these paths' final kernels also close the step (step_close_status)
-        k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+        launch_factor_base(dp, nfb, st);
         pr.seq();
         pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
     }
@@ -708,8 +727,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     R.partials = partials;
     if (p->head) {
         // K0 + base + root pass + analytic suffix bounds in one launch (k_head, k_factor.cuh)
-        if (p->cplx) k_head<true><<<(unsigned)hp.root_blocks, K0_THREADS, 0, st>>>(dp, R);
-        else k_head<false><<<(unsigned)hp.root_blocks, K0_THREADS, 0, st>>>(dp, R);
+        launch_head(dp, R, (unsigned)hp.root_blocks, st);
         pr.seq();
         pr.launch_done(pr.last, pr.last);   // K0 base: merged
         pr.launch_done(pr.last, pr.last);   // root pass: merged
@@ -719,7 +737,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
             else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         } else {
-            k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
+            launch_factor_base(dp, nfb, st);
             if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
         }
         pr.seq();
@@ -847,9 +865,9 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     {
         const long long nl1 = std::max<long long>(1, (hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2);
         double2 *l1 = (double2 *)(p->ws + p->ws_red_off);
-        k_reduce_fused<<<(unsigned)nl1, RED_THREADS, 0, st>>>(dp, partials, hp.total_partials,
-                                                               hp.include_root ? 1 : 0, out_dev, l1,
-                                                               p->d_counter + 1, p->d_counter);
+        auto red = dp.sform == 2 ? k_reduce_fused<2> : dp.sform == 1 ? k_reduce_fused<1> : k_reduce_fused<0>;
+        red<<<(unsigned)nl1, RED_THREADS, 0, st>>>(dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev,
+                                                  l1, p->d_counter + 1, p->d_counter);
     }
     {
         // the reduction starts when both branches are done: time it from the later of the two ends
@@ -1114,7 +1132,7 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
     if (rc) return rc;
     // the factor table and base of the current parameters (K0), then one thread per index
     const int nfb = (int)((hp.tab_entries + K0_THREADS - 1) / K0_THREADS);
-    k_factor_base<<<nfb + 1, K0_THREADS, 0, st>>>(p->dp, nfb);
+    launch_factor_base(p->dp, nfb, st);
     if (n > 0)
         k_eval_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p->dp, p->utabs, index_dev, n, points_dev,
                                                                    terms_dev);
