@@ -494,13 +494,16 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         for (int i = 1; i <= r; ++i) v = v * (double)(n - r + i) / (double)i;
         return v;
     };
+    double cost_generic = GENERIC_POINT_COST, cost_mid = LEAF2_MID_COST;
+    if (const char *e = getenv("SG_B200_COST_GENERIC"); e && e[0]) cost_generic = atof(e);   // A/B runs
+    if (const char *e = getenv("SG_B200_COST_MID"); e && e[0]) cost_mid = atof(e);
     auto item_cost = [&](int k1, int l1) -> double {
         const double pts = (double)item_weight(k1, l1);
-        if (!fusable_early || l1 != 2) return GENERIC_POINT_COST * pts;
+        if (!fusable_early || l1 != 2) return cost_generic * pts;
         const double n2 = (double)hp.nl[2];
         const double leaf2 = binom(d - 1 - k1, L - 1) * std::pow(n2, L - 1);
         const double mids = binom(d - 1 - k1, L - 2) * std::pow(n2, L - 2);
-        return leaf2 + GENERIC_POINT_COST * std::max(0.0, pts - leaf2) + LEAF2_MID_COST * mids;
+        return leaf2 + cost_generic * std::max(0.0, pts - leaf2) + cost_mid * mids;
     };
 
     // ---- shard range in depth-1 rank space ----
