@@ -265,3 +265,9 @@ DD_DEV void dd_sincos(dd a, dd &s, dd &c) {
     }
 }
 #endif  // __CUDACC__
+
+// Out-of-line copies for the latency-bound K0 / head launches: one body per kernel however many call
+// sites (the factor entry and the base), so the cold launch fetches less code.
+__device__ __noinline__ dd dd_exp_ool(dd a) { return dd_exp(a); }
+__device__ __noinline__ void dd_sincos_ool(dd a, dd &s, dd &c) { dd_sincos(a, s, c); }
+__device__ __noinline__ dd dd_div_ool(dd a, dd b) { return dd_div(a, b); }

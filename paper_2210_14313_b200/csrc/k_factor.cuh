@@ -27,14 +27,14 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOu
     dd Er = {1.0, 0.0}, Ei = {0.0, 0.0};
     switch (KIND) {
     case SG_F_EXP_LINEAR:
-        Er = dd_exp(dd_mul_d(xm, ck));
+        Er = dd_exp_ool(dd_mul_d(xm, ck));
         break;
     case SG_F_OSCILLATORY: {
         // sincos of |a| with the sign applied afterwards: nodes placed symmetrically about 1/2 get
         // exactly conjugate factors (used by k_leaf2's symmetric-pair path)
         dd a = dd_mul_d(xm, ck), s, co;
         const bool neg = a.hi < 0.0;
-        dd_sincos(neg ? dd_neg(a) : a, s, co);
+        dd_sincos_ool(neg ? dd_neg(a) : a, s, co);
         Er = co;
         Ei = neg ? dd_neg(s) : s;
         break;
@@ -44,15 +44,15 @@ __device__ __forceinline__ void factor_entry(const DevPlan &P, int idx, FactorOu
         const double wk = P.w[k];
         dd xp = dd_add(dd_from_sum(x, 0.5), dd{-2.0 * wk, 0.0});
         dd arg = dd_mul(dd_mul(xm, xp), dd_from_prod(ck, ck));
-        Er = dd_exp(dd_neg(arg));
+        Er = dd_exp_ool(dd_neg(arg));
         break;
     }
     case SG_F_PRODUCT_PEAK: {
         // phi(x)/phi(1/2) = (c^-2 + (1/2-w)^2) / (c^-2 + (x-w)^2)
         const double wk = P.w[k];
-        dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+        dd ci2 = dd_div_ool(dd{1.0, 0.0}, dd_from_prod(ck, ck));
         dd a = dd_from_sum(x, -wk), bm = dd_from_sum(0.5, -wk);
-        Er = dd_div(dd_add(ci2, dd_mul(bm, bm)), dd_add(ci2, dd_mul(a, a)));
+        Er = dd_div_ool(dd_add(ci2, dd_mul(bm, bm)), dd_add(ci2, dd_mul(a, a)));
         break;
     }
     }
@@ -111,8 +111,8 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
         }
         case SG_F_PRODUCT_PEAK: {
             dd bm = dd_from_sum(0.5, -P.w[k]);
-            dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
-            acc = dd_mul(acc, dd_div(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
+            dd ci2 = dd_div_ool(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+            acc = dd_mul(acc, dd_div_ool(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
             break;
         }
         }
@@ -132,8 +132,8 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
         dd s = {sm[0].x, sm[0].y};
         dd Br = s, Bi = {0.0, 0.0};
         switch (KIND) {
-        case SG_F_EXP_LINEAR: Br = dd_exp(s); break;
-        case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(s)); break;
+        case SG_F_EXP_LINEAR: Br = dd_exp_ool(s); break;
+        case SG_F_GAUSSIAN: Br = dd_exp_ool(dd_neg(s)); break;
         case SG_F_PRODUCT_PEAK: Br = s; break;
         case SG_F_OSCILLATORY: {
             const double u = P.u[0];
@@ -141,7 +141,7 @@ __device__ __forceinline__ void base_body(const DevPlan &P) {
             th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
             th = dd_add(th, s);
             dd sn, cs;
-            dd_sincos(th, sn, cs);
+            dd_sincos_ool(th, sn, cs);
             Br = cs;
             Bi = sn;
             break;
@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             }
             case SG_F_PRODUCT_PEAK: {
                 dd bm = dd_from_sum(0.5, -P.w[k]);
-                dd ci2 = dd_div(dd{1.0, 0.0}, dd_from_prod(ck, ck));
-                acc = dd_mul(acc, dd_div(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
+                dd ci2 = dd_div_ool(dd{1.0, 0.0}, dd_from_prod(ck, ck));
+                acc = dd_mul(acc, dd_div_ool(dd{1.0, 0.0}, dd_add(ci2, dd_mul(bm, bm))));
                 break;
             }
             }
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             dd sv = {sm[0].x, sm[0].y};
             dd Br = sv, Bi = {0.0, 0.0};
             switch (KIND) {
-            case SG_F_EXP_LINEAR: Br = dd_exp(sv); break;
-            case SG_F_GAUSSIAN: Br = dd_exp(dd_neg(sv)); break;
+            case SG_F_EXP_LINEAR: Br = dd_exp_ool(sv); break;
+            case SG_F_GAUSSIAN: Br = dd_exp_ool(dd_neg(sv)); break;
             case SG_F_PRODUCT_PEAK: Br = sv; break;
             case SG_F_OSCILLATORY: {
                 const double u = P.u[0];
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
                 th = dd_add(th, dd{DD_2PI_2 * u, 0.0});
                 th = dd_add(th, sv);
                 dd sn, cs;
-                dd_sincos(th, sn, cs);
+                dd_sincos_ool(th, sn, cs);
                 Br = cs;
                 Bi = sn;
                 break;

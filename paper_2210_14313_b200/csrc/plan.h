@@ -22,11 +22,15 @@
 #define SG_MAX_D ((1 << 20) - 1)
 #define SG_META_KBITS 20
 #ifndef GENERIC_POINT_COST
-#define GENERIC_POINT_COST 1.8    // shard cost model: a point of a generic pass vs a k_leaf2 point
+#define GENERIC_POINT_COST 1.0    // shard cost model: a point of a generic pass vs a k_leaf2 point.  With
+                                  // pass L-2 concurrent with the fused pass (side stream) the generic
+                                  // points overlap the fused ones; A/B of the N = 8 projection (graph
+                                  // replays, r02l): config 5 1.8 -> 1.736 ms, 1.0 -> 1.692 ms (with
+                                  // LEAF2_MID_COST 0); config 4 0.2878 -> 0.2843 ms
 #endif
 #ifndef LEAF2_MID_COST
-#define LEAF2_MID_COST 5.0        // shard cost model: fixed cost of one k_leaf2 row run, in points
-                                  // (A/B of the N = 8 projection on config 5: 5 -> 0.903, 10 -> 0.891, 20 -> 0.892)
+#define LEAF2_MID_COST 0.0        // shard cost model: fixed cost of one k_leaf2 row run, in points
+                                  // (r02l A/B on config 5 with GENERIC 1.0: 0 -> 1.692, 5 -> 1.706, 10 -> 1.741 ms)
 #endif
 #ifndef LEAF2_PPL
 #define LEAF2_PPL 3   // parents per lane for a level-2 row that is one conjugate pair (k_leaf2_pairs;
