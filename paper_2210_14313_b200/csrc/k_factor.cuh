@@ -320,14 +320,14 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
                 const long long seg = (long long)b1 * P.d + k1;
                 const long long o = R.off1[seg] + fo.j - R.JS[seg];
-                R.dst_re[o] = make_double2(cr.hi, cr.lo);
-                if (CPLX) R.dst_im[o] = make_double2(ci.hi, ci.lo);
-                R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+                SG_DST(R, dst_re, o) = make_double2(cr.hi, cr.lo);
+                if (CPLX) SG_DST(R, dst_im, o) = make_double2(ci.hi, ci.lo);
+                SG_DST(R, dst_meta, o) = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
             }
         }
     }
     dd sblk = block_reduce_dd<K0_THREADS / 32>(tot);
-    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(sblk.hi, sblk.lo);
+    if (threadIdx.x == 0) SG_PART(R.partials, blockIdx.x) = make_double2(sblk.hi, sblk.lo);
     // block 0: analytic suffix bounds of every level
     if (blockIdx.x == 0) {
         const int d = P.d, chunk = (d + K0_THREADS - 1) / K0_THREADS;   // <= HEAD_MAX_D / K0_THREADS

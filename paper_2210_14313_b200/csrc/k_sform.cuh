@@ -152,13 +152,13 @@ __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs 
         if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
             const long long seg = (long long)b1 * P.d + k1;
             const long long o = R.off1[seg] + j1 - R.JS[seg];
-            R.dst_re[o] = wv;
-            R.dst_im[o] = av;
-            R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+            SG_DST(R, dst_re, o) = wv;
+            SG_DST(R, dst_im, o) = av;
+            SG_DST(R, dst_meta, o) = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
         }
     }
     dd s = block_reduce_dd<8>(tot);
-    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(R.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }
 
 template <bool DDS, bool WRITE>
@@ -175,10 +175,10 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
         int b = L, k = d;
         dd W = {0.0, 0.0}, delta = {0.0, 0.0};
         if (valid) {
-            const uint32_t m = A.src_meta[g];
+            const uint32_t m = SG_SRC(A, src_meta, g);
             b = (int)(m >> SG_META_KBITS);
             k = (int)(m & META_KMASK);
-            const double2 v = A.src_re[g], dv = A.src_im[g];
+            const double2 v = SG_SRC(A, src_re, g), dv = SG_SRC(A, src_im, g);
             W = dd{v.x, v.y};
             delta = dd{dv.x, dv.y};
         }
@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
                     acc_add(ah, al, p, e);
                     if (WRITE && wk) {
                         const long long o = tb + (long long)j * Nseg;
-                        A.dst_re[o] = make_double2(Wc.hi, Wc.lo);
-                        A.dst_im[o] = make_double2(dl.hi, dl.lo);
-                        A.dst_meta[o] = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                        SG_DST(A, dst_re, o) = make_double2(Wc.hi, Wc.lo);
+                        SG_DST(A, dst_im, o) = make_double2(dl.hi, dl.lo);
+                        SG_DST(A, dst_meta, o) = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
                     }
                 }
             }
@@ -235,6 +235,6 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const 
         }
     }
     dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(A.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }
 

@@ -37,9 +37,9 @@ __device__ __forceinline__ dd root_node(const DevPlan &P, const RootArgs &R, lon
         if (P.nfront >= 1 && b1 <= P.L - 1 && k1 <= P.d - 2) {
             const long long seg = (long long)b1 * P.d + k1;
             const long long o = R.off1[seg] + j1 - R.JS[seg];
-            R.dst_re[o] = make_double2(cr.hi, cr.lo);
-            if (CPLX) R.dst_im[o] = make_double2(ci.hi, ci.lo);
-            R.dst_meta[o] = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
+            SG_DST(R, dst_re, o) = make_double2(cr.hi, cr.lo);
+            if (CPLX) SG_DST(R, dst_im, o) = make_double2(ci.hi, ci.lo);
+            SG_DST(R, dst_meta, o) = ((uint32_t)b1 << SG_META_KBITS) | (uint32_t)k1;
         }
     }
     return tot;
@@ -49,7 +49,7 @@ template <bool CPLX>
 __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R) {
     const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     dd s = block_reduce_dd<8>(root_node<CPLX>(P, R, r1));
-    if (threadIdx.x == 0) R.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(R.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -186,17 +186,17 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
                 dd_mul_pe(er, dd{f.x, f.y}, p1, e1);
                 if (!CPLX) {
                     const dd ch = dd_norm(p1, e1);
-                    A.dst_re[o] = make_double2(ch.hi, ch.lo);
+                    SG_DST(A, dst_re, o) = make_double2(ch.hi, ch.lo);
                 } else {
                     double p2, e2, p3, e3, p4, e4;
                     dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
                     dd_mul_pe(er, dd{fi.x, fi.y}, p3, e3);
                     dd_mul_pe(ei, dd{f.x, f.y}, p4, e4);
                     const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
-                    A.dst_re[o] = make_double2(cre.hi, cre.lo);
-                    A.dst_im[o] = make_double2(cim.hi, cim.lo);
+                    SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+                    SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
                 }
-                A.dst_meta[o] = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
+                SG_DST(A, dst_meta, o) = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
             }
         }
         if (++nfold == FOLD) {
@@ -234,12 +234,12 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
                 cdd cu, cl;
                 cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
                 const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
-                A.dst_re[ou] = make_double2(cu.re.hi, cu.re.lo);
-                A.dst_im[ou] = make_double2(cu.im.hi, cu.im.lo);
-                A.dst_meta[ou] = meta;
-                A.dst_re[ol] = make_double2(cl.re.hi, cl.re.lo);
-                A.dst_im[ol] = make_double2(cl.im.hi, cl.im.lo);
-                A.dst_meta[ol] = meta;
+                SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
+                SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
+                SG_DST(A, dst_meta, ou) = meta;
+                SG_DST(A, dst_re, ol) = make_double2(cl.re.hi, cl.re.lo);
+                SG_DST(A, dst_im, ol) = make_double2(cl.im.hi, cl.im.lo);
+                SG_DST(A, dst_meta, ol) = meta;
             }
         }
         if constexpr (NJ % 2 == 1) {
@@ -248,9 +248,9 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
             if (WRITE && wk) {
                 const long long oc = tb + (long long)NP * V.Nseg;
                 const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
-                A.dst_re[oc] = make_double2(cr.hi, cr.lo);
-                A.dst_im[oc] = make_double2(ci.hi, ci.lo);
-                A.dst_meta[oc] = meta;
+                SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
+                SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
+                SG_DST(A, dst_meta, oc) = meta;
             }
         }
         if (++nfold == LEAF_SYM_FOLD) {
@@ -277,13 +277,13 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
         int b = L, k = d;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (valid) {
-            const uint32_t m = A.src_meta[g];
+            const uint32_t m = SG_SRC(A, src_meta, g);
             b = (int)(m >> SG_META_KBITS);
             k = (int)(m & META_KMASK);
-            const double2 v = A.src_re[g];
+            const double2 v = SG_SRC(A, src_re, g);
             pr = dd{v.x, v.y};
             if (CPLX) {
-                const double2 vi = A.src_im[g];
+                const double2 vi = SG_SRC(A, src_im, g);
                 pim = dd{vi.x, vi.y};
             }
         }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
         }
     }
     dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(A.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -471,13 +471,13 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
         int b = L, k = d;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (valid) {
-            const uint32_t m = A.src_meta[g];
+            const uint32_t m = SG_SRC(A, src_meta, g);
             b = (int)(m >> SG_META_KBITS);
             k = (int)(m & META_KMASK);
-            const double2 v = A.src_re[g];
+            const double2 v = SG_SRC(A, src_re, g);
             pr = dd{v.x, v.y};
             if (CPLX) {
-                const double2 vi = A.src_im[g];
+                const double2 vi = SG_SRC(A, src_im, g);
                 pim = dd{vi.x, vi.y};
             }
         }
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
         }
     }
     dd s = block_reduce_dd<WPB>(tot);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(A.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -589,11 +589,11 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
     int k = d;
     dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
     if (valid) {
-        k = (int)(A.src_meta[g] & META_KMASK);
-        const double2 v = A.src_re[g];
+        k = (int)(SG_SRC(A, src_meta, g) & META_KMASK);
+        const double2 v = SG_SRC(A, src_re, g);
         pr = dd{v.x, v.y};
         if (CPLX) {
-            const double2 vi = A.src_im[g];
+            const double2 vi = SG_SRC(A, src_im, g);
             pim = dd{vi.x, vi.y};
         }
     }
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPla
         dd v = warp_reduce_dd(leaf1_task<CPLX, NJ, SMEM>(P, A, (long long)task, Fr, Fi));
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);
-            A.partials[task] = make_double2(v.hi, v.lo);
+            SG_PART(A.partials, task) = make_double2(v.hi, v.lo);
         }
     }
 }
@@ -699,6 +699,7 @@ struct Leaf2Args {
     double2 *partials;             // one per task
     unsigned long long *counter;   // dynamic task counter, zeroed per launch
     int prefetch;                  // software-pipelined task fetch (>= 16 tasks per resident warp)
+    SG_CHK_FIELDS
 };
 
 #ifndef LEAF2_ROWS
@@ -878,10 +879,10 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         const long long i = first + plane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
-            const double2 v = A.src_re[A.base + i];
+            const double2 v = SG_SRC(A, src_re, A.base + i);
             pr = dd{v.x, v.y};
             if (CPLX) {
-                const double2 vi = A.src_im[A.base + i];
+                const double2 vi = SG_SRC(A, src_im, A.base + i);
                 pim = dd{vi.x, vi.y};
             }
         }
@@ -939,6 +940,8 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
                 bh[jm] = sg[jm];
                 bl[jm] = 0.0;
             }
+            SG_CHK(km, d - 1, 6);                               // mid row (its factors, Cmid, SA)
+            SG_CHK(kp1 - 1, d, 5);                              // last leaf row of the table slice
             int kp = max(km + 1, kp0);
             while (kp < kp1) {
                 const int ke = min(kp1, kp + FOLD);
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[P.L]);
-            A.partials[task] = make_double2(v.hi, v.lo);
+            SG_PART(A.partials, task) = make_double2(v.hi, v.lo);
         }
 #if LEAF2_PREFETCH
         if (!A.prefetch) {
@@ -1072,7 +1075,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
             pr[q] = dd{0.0, 0.0};
             pim[q] = dd{0.0, 0.0};
             if (ip[q] < cend) {
-                const double2 v = A.src_re[A.base + ip[q]], vi = A.src_im[A.base + ip[q]];
+                const double2 v = SG_SRC(A, src_re, A.base + ip[q]), vi = SG_SRC(A, src_im, A.base + ip[q]);
                 pr[q] = dd{v.x, v.y};
                 pim[q] = dd{vi.x, vi.y};
             }
@@ -1102,6 +1105,8 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
                 ah[m] = bh[m] = sg[m];   // biased accumulators (node 0 -> a, node 1 -> b)
                 al[m] = bl[m] = 0.0;
             }
+            SG_CHK(km, d - 1, 6);
+            SG_CHK(kp1 - 1, d, 5);
             int kp = max(km + 1, kp0);
             while (kp < kp1) {
                 const int ke = min(kp1, kp + FOLD);
@@ -1142,7 +1147,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(
     dd v = warp_reduce_dd_fast(lane_sum);
     if (lane == 0) {
         v = dd_mul_d(v, P.coef[P.L]);
-        A.partials[task] = make_double2(v.hi, v.lo);
+        SG_PART(A.partials, task) = make_double2(v.hi, v.lo);
     }
     if (!A.prefetch) {
         next = fetch();
@@ -1189,7 +1194,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
         pr[q] = dd{0.0, 0.0};
         pim[q] = dd{0.0, 0.0};
         if (ip[q] < cend) {
-            const double2 v = A.src_re[A.base + ip[q]], vi = A.src_im[A.base + ip[q]];
+            const double2 v = SG_SRC(A, src_re, A.base + ip[q]), vi = SG_SRC(A, src_im, A.base + ip[q]);
             pr[q] = dd{v.x, v.y};
             pim[q] = dd{vi.x, vi.y};
         }
@@ -1205,7 +1210,7 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
                 const int is = 32 * m + lane;
                 er[m] = ei[m] = dd{0.0, 0.0};
                 if (is < kb) {
-                    const double2 v = A.src_re[first + is], vi = A.src_im[first + is];
+                    const double2 v = SG_SRC(A, src_re, first + is), vi = SG_SRC(A, src_im, first + is);
                     er[m] = dd{v.x, v.y};
                     ei[m] = dd{vi.x, vi.y};
                 }
@@ -1234,6 +1239,8 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
             ah[m] = bh[m] = sg[m];   // biased accumulators (node 0 -> a, node 1 -> b)
             al[m] = bl[m] = 0.0;
         }
+        SG_CHK(km, d, 6);
+        SG_CHK(kp1 - 1, d, 5);
         int kp = max(km + 1, kp0);
         while (kp < kp1) {
             const int ke = min(kp1, kp + FOLD);
@@ -1385,7 +1392,7 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
         dd v = warp_reduce_dd_fast(lane_sum);
         if (lane == 0) {
             v = dd_mul_d(v, P.coef[SRC && (kb & SRC_CPREV) ? P.L - 1 : P.L]);
-            A.partials[task] = make_double2(v.hi, v.lo);
+            SG_PART(A.partials, task) = make_double2(v.hi, v.lo);
         }
         if (!A.prefetch) {
             next = fetch();

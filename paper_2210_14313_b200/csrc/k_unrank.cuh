@@ -146,5 +146,5 @@ __global__ void __launch_bounds__(256) k_plain(const DevPlan P, const UnrankTabs
         acc_add(ah, al, p, e);
     }
     const dd s = block_reduce_dd<8>(dd_norm(ah, al));
-    if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(s.hi, s.lo);
+    if (threadIdx.x == 0) SG_PART(partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }

@@ -31,6 +31,54 @@ struct DevPlan {
     double wabs[SG_MAX_L + 3];   // sum_j |w_j^l| (+ |lo|) per level: k_head's analytic suffix bounds
 };
 
+// ---------------------------------------------------------------------------------------------
+// Checked build (-DSG_CHECKS, tools/checked_run.py; compute-sanitizer is closed on this GPU pool):
+// every frontier read / write is bounds-checked against its buffer's capacity, every partial slot
+// write is counted (each slot must be written exactly once per step: a task claimed twice or never
+// shows up there), and the first violation is recorded.  The production build compiles the same
+// accessors to plain indexing (no fields, no code).
+// ---------------------------------------------------------------------------------------------
+#ifdef SG_CHECKS
+#define SG_CHK_FIELDS long long chk_src_cap, chk_dst_cap;
+struct ChkState {
+    unsigned long long viol;
+    long long first[4];   // code, index, bound, source line of the first violation
+    unsigned *writes;     // write count per partial slot
+    long long nslots;
+    const double2 *part_base;
+};
+__device__ ChkState g_chk;
+__device__ __noinline__ void chk_fail(int code, long long idx, long long bound, int line) {
+    if (atomicAdd(&g_chk.viol, 1ull) == 0) {
+        g_chk.first[0] = code;
+        g_chk.first[1] = idx;
+        g_chk.first[2] = bound;
+        g_chk.first[3] = line;
+    }
+}
+template <class T>
+__device__ __forceinline__ T *chk_at(T *p, long long i, long long cap, int code, int line) {
+    if (i < 0 || i >= cap) chk_fail(code, i, cap, line);
+    return p;
+}
+__device__ __forceinline__ double2 *chk_part(double2 *p, int line) {
+    const long long sl = (long long)(p - g_chk.part_base);
+    if (!g_chk.writes || sl < 0 || sl >= g_chk.nslots) chk_fail(3, sl, g_chk.nslots, line);
+    else atomicAdd(g_chk.writes + sl, 1u);
+    return p;
+}
+#define SG_SRC(A, f, i) (*chk_at(&(A).f[i], (long long)(i), (A).chk_src_cap, 1, __LINE__))
+#define SG_DST(A, f, i) (*chk_at(&(A).f[i], (long long)(i), (A).chk_dst_cap, 2, __LINE__))
+#define SG_PART(base, i) (*chk_part(&(base)[i], __LINE__))
+#define SG_CHK(i, cap, code) ((void)chk_at((const char *)nullptr, (long long)(i), (long long)(cap), code, __LINE__))
+#else
+#define SG_CHK_FIELDS
+#define SG_SRC(A, f, i) ((A).f[i])
+#define SG_DST(A, f, i) ((A).f[i])
+#define SG_PART(base, i) ((base)[i])
+#define SG_CHK(i, cap, code) ((void)0)
+#endif
+
 struct PassArgs {
     long long nsrc, ntasks;
     int nsplit;
@@ -42,6 +90,7 @@ struct PassArgs {
     const long long *offT, *NT, *CT, *TB;
     double2 *partials;
     unsigned long long *counter;   // dynamic task counter (persistent kernels), zeroed per launch
+    SG_CHK_FIELDS
 };
 
 struct RootArgs {
@@ -50,6 +99,7 @@ struct RootArgs {
     double2 *dst_re, *dst_im;
     uint32_t *dst_meta;
     double2 *partials;
+    SG_CHK_FIELDS
 };
 
 // Status words: status[0] is the live NonFiniteIntegrand flag of the running step (atomicOr by any

@@ -725,6 +725,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     R.JS = p->d_tabs + p->tab_JS;
     if (hp.nfront >= 1) front_ptrs(p, 1, R.dst_re, R.dst_im, R.dst_meta);
     R.partials = partials;
+#ifdef SG_CHECKS
+    R.chk_src_cap = 0;
+    R.chk_dst_cap = hp.ws_front_cap[1];
+#endif
     if (p->head) {
         // K0 + base + root pass + analytic suffix bounds in one launch (k_head, k_factor.cuh)
         launch_head(dp, R, (unsigned)hp.root_blocks, st);
@@ -782,6 +786,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.partials = partials + hp.pass_partial_off[t];
             B.counter = cnt_leaf;
             B.prefetch = B.ntasks >= (long long)p->prefetch_min * p->leaf1_grid * (p->leaf2_threads / 32) ? 1 : 0;
+#ifdef SG_CHECKS
+            B.chk_src_cap = hp.ws_front_cap[(t - 1) % 2];
+            B.chk_dst_cap = 0;
+#endif
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
                 else launch_leaf2<false>(p, B, hp.nl[2], st);
@@ -809,6 +817,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             S.partials = partials + hp.pass_partial_off[t];
             S.counter = cnt_src;
             S.prefetch = 0;
+#ifdef SG_CHECKS
+            S.chk_src_cap = hp.ws_front_cap[t % 2];
+            S.chk_dst_cap = 0;
+#endif
             if (S.ntasks > 0) launch_leaf2_src(p, S, sx);
         } else {
             PassArgs A;
@@ -831,6 +843,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             A.TB = write ? p->d_tabs + p->tab_TB[t] : nullptr;
             A.partials = partials + hp.pass_partial_off[t];
             A.counter = cnt_leaf;   // k_leaf1 (the last pass of an unfused plan)
+#ifdef SG_CHECKS
+            A.chk_src_cap = hp.ws_front_cap[t % 2];
+            A.chk_dst_cap = write ? hp.ws_front_cap[(t + 1) % 2] : 0;
+#endif
             const unsigned grid = (unsigned)hp.pass_blocks[t];
             // single-level last pass (every source has excess L-1): specialised k_leaf1
             const int n2 = hp.nl[2];
@@ -1141,6 +1157,48 @@ extern "C" int sg_eval_points(sg_plan_t p, sg_stream_t s, const unsigned long lo
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
 }
+
+#ifdef SG_CHECKS
+// Checked build only (not in include/sg_b200.h): arm the checks for the next sg_integrate / read them.
+static unsigned *g_chk_writes_host = nullptr;
+static long long g_chk_writes_cap = 0;
+extern "C" int sg_chk_begin(sg_plan_t p) {
+    if (!p || !p->ws) return SG_EINVAL;
+    const long long n = p->collapse ? 0 : p->plain ? p->plain_blocks : p->hp.total_partials;
+    if (n > g_chk_writes_cap) {
+        if (g_chk_writes_host) cudaFree(g_chk_writes_host);
+        if (cudaMalloc(&g_chk_writes_host, sizeof(unsigned) * (size_t)n) != cudaSuccess) return SG_ENOMEM;
+        g_chk_writes_cap = n;
+    }
+    if (n > 0 && cudaMemset(g_chk_writes_host, 0, sizeof(unsigned) * (size_t)n) != cudaSuccess) return SG_ECUDA;
+    ChkState st;
+    memset(&st, 0, sizeof st);
+    st.writes = g_chk_writes_host;
+    st.nslots = n;
+    st.part_base = (const double2 *)(p->ws + p->ws_part_off);
+    if (cudaMemcpyToSymbol(g_chk, &st, sizeof st) != cudaSuccess) return SG_ECUDA;
+    return SG_OK;
+}
+// out[0] = violations, out[1..4] = first (code, index, bound, line), out[5] = slots not written exactly
+// once, out[6] = slots checked
+extern "C" int sg_chk_end(sg_plan_t p, long long *out) {
+    if (!p || !out) return SG_EINVAL;
+    if (cudaDeviceSynchronize() != cudaSuccess) return SG_ECUDA;
+    ChkState st;
+    if (cudaMemcpyFromSymbol(&st, g_chk, sizeof st) != cudaSuccess) return SG_ECUDA;
+    std::vector<unsigned> w((size_t)st.nslots);
+    if (st.nslots > 0 && cudaMemcpy(w.data(), st.writes, sizeof(unsigned) * (size_t)st.nslots,
+                                    cudaMemcpyDeviceToHost) != cudaSuccess)
+        return SG_ECUDA;
+    long long bad = 0;
+    for (unsigned v : w) bad += (v != 1);
+    out[0] = (long long)st.viol;
+    for (int i = 0; i < 4; ++i) out[1 + i] = st.first[i];
+    out[5] = bad;
+    out[6] = st.nslots;
+    return SG_OK;
+}
+#endif
 
 extern "C" int sg_destroy(sg_plan_t p) {
     if (!p) return SG_EINVAL;
