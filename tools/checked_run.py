@@ -23,9 +23,9 @@ CHECKED = os.path.join(ROOT, "paper_2210_14313_b200", "libsg_b200_checked.so")
 
 def main():
     quick = "--quick" in sys.argv
+    os.environ["SG_B200_LIB"] = CHECKED   # before the package is imported (_lib reads it once)
     from paper_2210_14313_b200 import build as B
     B.build(defines=("SG_CHECKS",), out=CHECKED)
-    os.environ["SG_B200_LIB"] = CHECKED
     import mpmath as mp
     import torch
 
