@@ -176,8 +176,8 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
         const double2 *fi_row = CPLX ? V.Fi + (long long)kp * n : nullptr;
 #pragma unroll
         for (int j = 0; j < (NJ > 0 ? NJ : n); ++j) {
-            const double2 f = __ldg(fr_row + j);
-            const double2 fi = CPLX ? __ldg(fi_row + j) : make_double2(0.0, 0.0);
+            const double2 f = fr_row[j];
+            const double2 fi = CPLX ? fi_row[j] : make_double2(0.0, 0.0);
             leaf_term<CPLX>(er, ei, f, fi, acc);
             if (WRITE && wk) {
                 // the stored child product P F in dd (complex for the oscillatory kind)
@@ -228,7 +228,7 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
             const int ju = NJ - 1 - q;
-            const double2 f = __ldg(fr_row + ju), g = __ldg(fi_row + ju);
+            const double2 f = fr_row[ju], g = fi_row[ju];
             leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
             if (WRITE && wk) {
                 cdd cu, cl;
@@ -243,7 +243,7 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
             }
         }
         if constexpr (NJ % 2 == 1) {
-            const double2 w = __ldg(fr_row + NP);
+            const double2 w = fr_row[NP];
             leaf_real_factor_term<false>(er, w, acc.h, acc.l);
             if (WRITE && wk) {
                 const long long oc = tb + (long long)NP * V.Nseg;
@@ -265,6 +265,20 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
 #endif
 template <bool CPLX, bool WRITE>
 __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan P, const PassArgs A) {
+    // factor levels 2 .. A.stage_lmax staged in shared memory (same layout as the table: level l at
+    // tab_off[l] - tab_off[2]); the row loads of the level loop then cost shared-memory latency
+    // instead of an L1/L2 round trip per row (ncu r02p: long-scoreboard stalls on those loads were the
+    // first limiter of this kernel)
+    extern __shared__ double2 fsm[];
+    if (A.stage_lmax >= 2) {
+        const double2 *gr = P.Fre + P.tab_off[2];
+        const double2 *gi = CPLX ? P.Fim + P.tab_off[2] : nullptr;
+        for (int i = threadIdx.x; i < A.stage_entries; i += blockDim.x) {
+            fsm[i] = gr[i];
+            if (CPLX) fsm[A.stage_entries + i] = gi[i];
+        }
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
     dd tot = {0.0, 0.0};
@@ -304,8 +318,11 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             const bool lv = valid && (lp <= L + 1 - b);
             const int n = P.nl[lp];
             const int bp = b + lp - 1;
-            const double2 *Fr = P.Fre + P.tab_off[lp];
-            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            const bool staged = lp <= A.stage_lmax;
+            const double2 *Fr = staged ? fsm + (P.tab_off[lp] - P.tab_off[2]) : P.Fre + P.tab_off[lp];
+            const double2 *Fi = CPLX ? (staged ? fsm + A.stage_entries + (P.tab_off[lp] - P.tab_off[2])
+                                               : P.Fim + P.tab_off[lp])
+                                     : nullptr;
             const bool wr = WRITE && lv && (bp <= L - 1);
             const long long wbase = (long long)n * Cseg + iseg;
             // biased grid accumulator (leaf_term): sigma = 1.5 * 2^m > 2 * bound on the lane's

@@ -90,6 +90,8 @@ struct PassArgs {
     const long long *offT, *NT, *CT, *TB;
     double2 *partials;
     unsigned long long *counter;   // dynamic task counter (persistent kernels), zeroed per launch
+    int stage_lmax;                // k_pass: factor levels 2 .. stage_lmax staged in shared memory
+    int stage_entries;             // their table entries (d * sum nl)
     SG_CHK_FIELDS
 };
 

@@ -75,6 +75,8 @@ struct sg_plan_s {
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
     bool head = false;                  // K0 + base + root + suffix bounds as one k_head launch
+    size_t pass_smem_cap = 0;           // k_pass: bytes of factor levels staged in shared memory
+                                        // (SG_B200_PASS_SMEM: A/B runs)
     int prefetch_min = 16;              // fused kernel prefetches the next task with >= this many
                                         // tasks per resident warp (SG_B200_PREFETCH_MIN: A/B runs)
     std::vector<cudaEvent_t> ev;
@@ -312,6 +314,15 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         return SG_ECUDA;
     }
     if (const char *e = getenv("SG_B200_PREFETCH_MIN"); e && e[0]) p->prefetch_min = atoi(e);
+    if (const char *e = getenv("SG_B200_PASS_SMEM"); e && e[0]) p->pass_smem_cap = (size_t)atoll(e);
+    if (p->pass_smem_cap > 48 * 1024) {
+        if (cudaFuncSetAttribute(k_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+            cudaFuncSetAttribute(k_pass<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
+            cudaGetLastError();
+            p->pass_smem_cap = 48 * 1024;
+        }
+        p->pass_smem_cap = std::min<size_t>(p->pass_smem_cap, 200 * 1024);
+    }
     rc = (p->collapse || p->plain) ? SG_OK : setup_leaf1(p);
     if (rc) {
         cudaGetLastError();
@@ -848,6 +859,21 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             A.chk_dst_cap = write ? hp.ws_front_cap[(t + 1) % 2] : 0;
 #endif
             const unsigned grid = (unsigned)hp.pass_blocks[t];
+            size_t pass_smem = 0;
+            if (write && !p->sform) {
+                // stage factor levels 2 .. while they fit p->pass_smem_cap bytes (k_pass)
+                const size_t per = p->cplx ? 2 * sizeof(double2) : sizeof(double2);
+                int lmax = 1, ent = 0;
+                for (int l = 2; l <= hp.L + 1; ++l) {
+                    const int e = hp.d * hp.nl[l];
+                    if ((size_t)(ent + e) * per > p->pass_smem_cap) break;
+                    ent += e;
+                    lmax = l;
+                }
+                A.stage_lmax = lmax >= 2 ? lmax : 0;
+                A.stage_entries = ent;
+                pass_smem = (size_t)ent * per;
+            }
             // single-level last pass (every source has excess L-1): specialised k_leaf1
             const int n2 = hp.nl[2];
             const bool single = !write && t == p->leaf1_t;
@@ -860,11 +886,11 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                     else k_pass_s<false, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
                 }
             } else if (p->cplx) {
-                if (write) k_pass<true, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                if (write) k_pass<true, true><<<grid, PASS_THREADS, pass_smem, sx>>>(dp, A);
                 else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, sx); }
                 else k_leaf<true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
             } else {
-                if (write) k_pass<false, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                if (write) k_pass<false, true><<<grid, PASS_THREADS, pass_smem, sx>>>(dp, A);
                 else if (single) { if (A.ntasks > 0) launch_leaf1<false>(p, A, n2, sx); }
                 else k_leaf<false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
             }
