@@ -159,7 +159,17 @@ struct PassLevel {
     const double2 *Fr, *Fi;
 };
 
-template <bool CPLX, bool WRITE, int NJ>
+// WONLY (write-only pass of a split frontier pass): only the stored children (rows kp <= d-2 of the
+// levels with bp <= L-1, the caller restricts both); each child's term is the real part of its
+// stored dd product, added to the biased accumulator as a dd value (leaf_add_dd).
+__device__ __forceinline__ void leaf_add_dd(const dd &x, LeafAcc &a) {
+    const double a1 = a.h + x.hi;   // x.hi rounded once onto the grid of sigma
+    const double h = a1 - a.h;      // exact (Sterbenz)
+    a.h = a1;
+    a.l += (x.hi - h) + x.lo;       // x.hi - h exact: a multiple of ulp(x.hi), |.| <= ulp(sigma) / 2
+}
+
+template <bool CPLX, bool WRITE, int NJ, bool WONLY = false>
 __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
                                            const dd &pim, double sigma, LeafAcc &acc, int nrt = 0) {
     const int n = NJ > 0 ? NJ : nrt;
@@ -178,7 +188,7 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
         for (int j = 0; j < (NJ > 0 ? NJ : n); ++j) {
             const double2 f = fr_row[j];
             const double2 fi = CPLX ? fi_row[j] : make_double2(0.0, 0.0);
-            leaf_term<CPLX>(er, ei, f, fi, acc);
+            if (!WONLY) leaf_term<CPLX>(er, ei, f, fi, acc);
             if (WRITE && wk) {
                 // the stored child product P F in dd (complex for the oscillatory kind)
                 const long long o = tb + (long long)j * V.Nseg;
@@ -187,6 +197,7 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
                 if (!CPLX) {
                     const dd ch = dd_norm(p1, e1);
                     SG_DST(A, dst_re, o) = make_double2(ch.hi, ch.lo);
+                    if (WONLY) leaf_add_dd(ch, acc);
                 } else {
                     double p2, e2, p3, e3, p4, e4;
                     dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
@@ -195,6 +206,7 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
                     const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
                     SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
                     SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+                    if (WONLY) leaf_add_dd(cre, acc);
                 }
                 SG_DST(A, dst_meta, o) = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
             }
@@ -209,7 +221,7 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
 // Symmetric oscillatory row (P.symmask): conjugate node pairs share the products of their terms
 // (leaf_sym_pair_terms) and of their stored child products (cdd_mul_conj_pair); the midpoint
 // (odd NJ) has a real factor.
-template <bool WRITE, int NJ>
+template <bool WRITE, int NJ, bool WONLY = false>
 __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
                                                const dd &pim, double sigma, LeafAcc &acc) {
     constexpr int NP = NJ / 2;
@@ -229,10 +241,14 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
         for (int q = 0; q < NP; ++q) {
             const int ju = NJ - 1 - q;
             const double2 f = fr_row[ju], g = fi_row[ju];
-            leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
+            if (!WONLY) leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
             if (WRITE && wk) {
                 cdd cu, cl;
                 cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
+                if (WONLY) {
+                    leaf_add_dd(cu.re, acc);
+                    leaf_add_dd(cl.re, acc);
+                }
                 const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
                 SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
                 SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
@@ -244,10 +260,11 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
         }
         if constexpr (NJ % 2 == 1) {
             const double2 w = fr_row[NP];
-            leaf_real_factor_term<false>(er, w, acc.h, acc.l);
+            if (!WONLY) leaf_real_factor_term<false>(er, w, acc.h, acc.l);
             if (WRITE && wk) {
                 const long long oc = tb + (long long)NP * V.Nseg;
                 const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
+                if (WONLY) leaf_add_dd(cr, acc);
                 SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
                 SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
                 SG_DST(A, dst_meta, oc) = meta;
@@ -263,7 +280,10 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
 #ifndef PASS_MINB
 #define PASS_MINB 3   // CTAs/SM bound of k_pass
 #endif
-template <bool CPLX, bool WRITE>
+// WONLY: the write-only kernel of a split frontier pass (only the stored children: levels with
+// bp <= L-1, rows k' <= d-2; their terms from the stored products); the others are evaluated by
+// k_leaf<CPLX, true> concurrently.
+template <bool CPLX, bool WRITE, bool WONLY = false>
 __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan P, const PassArgs A) {
     // factor levels 2 .. A.stage_lmax staged in shared memory (same layout as the table: level l at
     // tab_off[l] - tab_off[2]); the row loads of the level loop then cost shared-memory latency
@@ -302,7 +322,8 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             }
         }
         const int ks0 = (int)((long long)split * d / A.nsplit);
-        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
+        const int ks1 = WONLY ? min((int)((long long)(split + 1) * d / A.nsplit), d - 1)
+                              : (int)((long long)(split + 1) * d / A.nsplit);
         const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
         const int bmin = __reduce_min_sync(0xffffffffu, b);
         long long iseg = 0, Nseg = 0, Cseg = 0;
@@ -314,8 +335,8 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
         }
         const double pabs = fabs(pr.hi) + (CPLX ? fabs(pim.hi) : 0.0);
         const int kb = max(ks0, kmin + 1);
-        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
-            const bool lv = valid && (lp <= L + 1 - b);
+        for (int lp = 2; lp <= (WONLY ? L - bmin : L + 1 - bmin); ++lp) {
+            const bool lv = valid && (lp <= (WONLY ? L - b : L + 1 - b));
             const int n = P.nl[lp];
             const int bp = b + lp - 1;
             const bool staged = lp <= A.stage_lmax;
@@ -332,14 +353,14 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             LeafAcc acc = {sigma, 0.0};
             PassLevel L0 = {kb, ks1, k, lv, wr, b, bp, wbase, Nseg, Fr, Fi};
             const bool sym = CPLX && ((P.symmask >> lp) & 1);
-            if (sym && n == 3) pass_level_sym<WRITE, 3>(P, A, L0, pr, pim, sigma, acc);
-            else if (sym && n == 5) pass_level_sym<WRITE, 5>(P, A, L0, pr, pim, sigma, acc);
-            else if (sym && n == 2) pass_level_sym<WRITE, 2>(P, A, L0, pr, pim, sigma, acc);
+            if (sym && n == 3) pass_level_sym<WRITE, 3, WONLY>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 5) pass_level_sym<WRITE, 5, WONLY>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 2) pass_level_sym<WRITE, 2, WONLY>(P, A, L0, pr, pim, sigma, acc);
             else switch (n) {
-            case 2: pass_level<CPLX, WRITE, 2>(P, A, L0, pr, pim, sigma, acc); break;
-            case 3: pass_level<CPLX, WRITE, 3>(P, A, L0, pr, pim, sigma, acc); break;
-            case 5: pass_level<CPLX, WRITE, 5>(P, A, L0, pr, pim, sigma, acc); break;
-            default: pass_level<CPLX, WRITE, 0>(P, A, L0, pr, pim, sigma, acc, n); break;
+            case 2: pass_level<CPLX, WRITE, 2, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
+            case 3: pass_level<CPLX, WRITE, 3, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
+            case 5: pass_level<CPLX, WRITE, 5, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
+            default: pass_level<CPLX, WRITE, 0, WONLY>(P, A, L0, pr, pim, sigma, acc, n); break;
             }
             if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(acc.h - sigma, acc.l), A.t + 1, bp));
         }
@@ -474,7 +495,10 @@ __device__ __forceinline__ dd leaf_level_sym(const double2 *Fr, const double2 *F
     return s;
 }
 
-template <bool CPLX>
+// SKIPW: the leaf-only kernel of a split frontier pass — the children the write-only k_pass stores
+// (levels with bp <= L-1, rows k' <= d-2) are skipped: for such a level a lane only walks the row
+// k' = d-1 (its effective last coordinate becomes max(k, d-2)).
+template <bool CPLX, bool SKIPW = false>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan P, const PassArgs A) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
@@ -503,7 +527,7 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
         const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
         const int kmax = __reduce_max_sync(0xffffffffu, valid ? k : -1);
         const int bmin = __reduce_min_sync(0xffffffffu, b);
-        const int kb = max(ks0, kmin + 1), kmain = kmax + 1;
+        const int kb0 = max(ks0, kmin + 1), kmain0 = kmax + 1, k0 = k;
         const double pabs = fabs(pr.hi) + (CPLX ? fabs(pim.hi) : 0.0);
         for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
             const bool lv = valid && (lp <= L + 1 - b);
@@ -515,6 +539,15 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan 
             const double sigma = grid_sigma(bound);
             const double2 *Fr = P.Fre + P.tab_off[lp];
             const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            int kb = kb0, kmain = kmain0, k = k0;
+            if (SKIPW) {
+                // stored children of this level belong to the write-only kernel
+                if (lv && b + lp - 1 <= L - 1) k = max(k0, d - 2);
+                const int kmn = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
+                const int kmx = __reduce_max_sync(0xffffffffu, valid ? k : -1);
+                kb = max(ks0, kmn + 1);
+                kmain = kmx + 1;
+            }
             dd s;
             const bool sym = CPLX && ((P.symmask >> lp) & 1);
             if (sym && n == 3) s = leaf_level_sym<3>(Fr, Fi, kb, kmain, ks1, k, er, ei, sigma);

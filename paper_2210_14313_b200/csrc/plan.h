@@ -46,6 +46,9 @@
 #ifndef LEAF2_SPLIT_SHARE
 #define LEAF2_SPLIT_SHARE 4   // split long tasks when one is > 1/SHARE of a resident warp's row share
 #endif
+#ifndef FRONT_SPLIT_MIN_BYTES
+#define FRONT_SPLIT_MIN_BYTES (64.0 * 1024 * 1024)   // split a frontier pass writing at least this much
+#endif
 #ifndef LEAF2_PIECES_PER_WARP
 #define LEAF2_PIECES_PER_WARP 2   // split pieces per resident warp on small shards (A/B on config 4 at N = 8:
                                   // 8 -> 0.314 ms, 4 -> 0.296, 2 -> 0.294, 1 -> 0.325; fewer, longer pieces
@@ -92,6 +95,9 @@ struct HostPlan {
     // launch geometry
     std::vector<int> pass_nsplit;      // index t
     std::vector<int64_t> pass_ntasks, pass_blocks, pass_partial_off;
+    // split frontier pass t (sg_kernels.cu, factor form, large frontiers): a write-only k_pass for the
+    // stored children and a concurrent leaf-only k_leaf for the others, pass_blocks[t] slots each
+    std::vector<char> pass_split;
     int64_t root_blocks = 0, total_partials = 0;
     size_t ws_front_bytes[2] = {0, 0}; // ping-pong frontier buffers (odd / even depth)
     int64_t ws_front_cap[2] = {0, 0};

@@ -91,6 +91,17 @@ struct sg_plan_s {
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
+static void layout_partials(HostPlan &hp) {
+    int64_t poff = hp.root_blocks;
+    for (int u = 1; u <= hp.nfront; ++u) {
+        hp.pass_partial_off[u] = poff;
+        const bool split = u < (int)hp.pass_split.size() && hp.pass_split[u];
+        poff += hp.pass_blocks[u] * (split ? 2 : 1);
+    }
+    hp.total_partials = poff;
+}
 static int setup_leaf1(sg_plan_s *p);
 static int build_unrank_tables(sg_plan_s *p);
 
@@ -314,6 +325,22 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         return SG_ECUDA;
     }
     if (const char *e = getenv("SG_B200_PREFETCH_MIN"); e && e[0]) p->prefetch_min = atoi(e);
+    {
+        // Split frontier passes (factor form): a pass that stores more than FRONT_SPLIT_MIN_BYTES of
+        // frontier records runs as a write-only k_pass (the stored children, their terms from the
+        // stored products) and, concurrently on the side stream, a leaf-only k_leaf (the other
+        // children).  SG_B200_FRONT_SPLIT=0/1 forces it off/on (A/B, tests).
+        const char *e = getenv("SG_B200_FRONT_SPLIT"), *nf = getenv("SG_B200_NOFORK");
+        const int force = (nf && nf[0] == '1') ? 0 : (e && e[0]) ? atoi(e) : -1;   // no side stream: no split
+        hp.pass_split.assign(hp.nfront + 1, 0);
+        const size_t rec = (p->cplx ? 32 : 16) + 4;
+        for (int t = 1; t < hp.nfront; ++t) {
+            const bool writes = !(hp.fuse && t + 1 == hp.nfront);
+            const bool big = (double)hp.pass_written[t] * rec >= FRONT_SPLIT_MIN_BYTES;
+            hp.pass_split[t] = (!p->sform && writes && (force == 1 || (force != 0 && big))) ? 1 : 0;
+        }
+        layout_partials(hp);
+    }
     if (const char *e = getenv("SG_B200_PASS_SMEM"); e && e[0]) p->pass_smem_cap = (size_t)atoll(e);
     if (p->pass_smem_cap > 48 * 1024) {
         if (cudaFuncSetAttribute(k_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
@@ -390,7 +417,10 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         const char *nh = getenv("SG_B200_NOHEAD");
         p->head = !p->sform && hp.d <= HEAD_MAX_D && !(nh && nh[0] == '1');
     }
-    if (p->leaf2 && hp.nfront >= 2 && !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
+    bool any_split = false;
+    for (size_t t = 0; t < hp.pass_split.size(); ++t) any_split = any_split || hp.pass_split[t];
+    if ((any_split || (p->leaf2 && hp.nfront >= 2)) &&
+        !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
         // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
         // fills the rest of the GPU and takes over the SMs the short pass frees (graph kernel nodes
@@ -577,12 +607,7 @@ static int setup_leaf1(sg_plan_s *p) {
     const long long ntasks = hp.pass_ntasks[t];
     p->leaf1_grid = std::max<long long>(1, std::min<long long>((ntasks + wpb - 1) / wpb, (long long)sms * per_sm));
     hp.pass_blocks[t] = ntasks;   // partial slots: one per task (0 tasks -> no slot, no launch)
-    int64_t poff = hp.root_blocks;
-    for (int u = 1; u <= hp.nfront; ++u) {
-        hp.pass_partial_off[u] = poff;
-        poff += hp.pass_blocks[u];
-    }
-    hp.total_partials = poff;
+    layout_partials(hp);
     p->leaf1_t = t;
     return SG_OK;
 }
@@ -770,11 +795,12 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
     // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).
     // The persistent fused kernel takes the SMs the shorter pass leaves or frees (its tail fill).
-    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2;
+    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2;   // passes nfront-1 || nfront
     int ev_fork = -1;
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
         cudaStream_t sx = st;
+        bool split_done = false;
         if (fork && t == hp.nfront - 1) {
             if (cudaEventRecord(p->ev_fork, st) != cudaSuccess) return SG_ECUDA;
             if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
@@ -885,6 +911,34 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                     if (write) k_pass_s<false, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
                     else k_pass_s<false, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
                 }
+            } else if (write && hp.pass_split[t] && p->side != nullptr) {
+                // split frontier pass: write-only k_pass here, leaf-only k_leaf on the side stream
+                // (both read frontier t; partial slots [0, grid) and [grid, 2 grid) of the pass)
+                PassArgs A2 = A;
+                A2.dst_re = A2.dst_im = nullptr;
+                A2.dst_meta = nullptr;
+                A2.TB = nullptr;
+                A2.partials = A.partials + grid;
+#ifdef SG_CHECKS
+                A2.chk_dst_cap = 0;
+#endif
+                if (cudaEventRecord(p->ev_fork, st) != cudaSuccess) return SG_ECUDA;
+                if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
+                if (p->cplx) {
+                    k_leaf<true, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    k_pass<true, true, true><<<grid, PASS_THREADS, pass_smem, st>>>(dp, A);
+                } else {
+                    k_leaf<false, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    k_pass<false, true, true><<<grid, PASS_THREADS, pass_smem, st>>>(dp, A);
+                }
+                // profile entry of the pass = the write-only kernel (fork -> its end on this stream);
+                // the leaf-only kernel overlaps it, the join wait falls into the next interval
+                split_done = true;
+                const int e = pr.rec(st);
+                pr.launch_done(pr.last, e);
+                pr.last = e;
+                if (cudaEventRecord(p->ev_join, p->side) != cudaSuccess) return SG_ECUDA;
+                if (cudaStreamWaitEvent(st, p->ev_join, 0) != cudaSuccess) return SG_ECUDA;
             } else if (p->cplx) {
                 if (write) k_pass<true, true><<<grid, PASS_THREADS, pass_smem, sx>>>(dp, A);
                 else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, sx); }
@@ -899,7 +953,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             const int e = pr.rec(sx);
             pr.launch_done(ev_fork, e);
             if (cudaEventRecord(p->ev_join, sx) != cudaSuccess) return SG_ECUDA;
-        } else {
+        } else if (!split_done) {
             pr.seq();
         }
     }

@@ -86,11 +86,15 @@ def main():
         ("collapse d=20 L=4", S.random_problem(66, 20, 4, S.RULE_CC, S.KIND_OSC), {"method": api.METHOD_COLLAPSE}, {}, [1], None),
         ("s-form dd corner d=8 L=4", S.random_problem(67, 8, 4, S.RULE_CC, S.KIND_CORNER), {"arith": api.ARITH_SFORM_DD}, {}, [1, 3], None),
         ("unfused osc d=30 L=4", S.random_problem(68, 30, 4, S.RULE_CC, S.KIND_OSC), {}, {"SG_B200_NOFUSE": "1"}, [1, 3], None),
+        ("split unfused osc d=30 L=4", S.random_problem(68, 30, 4, S.RULE_CC, S.KIND_OSC), {},
+         {"SG_B200_NOFUSE": "1", "SG_B200_FRONT_SPLIT": "1"}, [1, 3], None),
+        ("split exp d=12 L=6", S.random_problem(92, 12, 6, S.RULE_CC, S.KIND_EXP), {}, {"SG_B200_FRONT_SPLIT": "1"}, [1, 3], None),
+        ("c5 unfused (split 4.3 GB frontier)", S.baseline_config(5), {}, {"SG_B200_NOFUSE": "1"}, [1], None),
         ("trapezoid d=33 L=4", S.random_problem(74, 33, 4, S.RULE_TRAP, S.KIND_GAUSS), {}, {}, [1, 3], None),
         ("patterson d=8 L=5", S.random_problem(55, 8, 5, S.RULE_GP, S.KIND_OSC), {}, {}, [1, 3], None),
     ]
     if quick:
-        cases = [c for c in cases if c[0] not in ("c5", "c5 merged")]
+        cases = [c for c in cases if not c[0].startswith("c5")]
     print(f"checked build: {CHECKED}")
     worst = 0.0
     for name, p, kw, env, worlds, _ in cases:
