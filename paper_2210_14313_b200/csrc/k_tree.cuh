@@ -226,53 +226,82 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
                                                const dd &pim, double sigma, LeafAcc &acc) {
     constexpr int NP = NJ / 2;
     const int d = P.d, L = P.L;
+    const int lane = threadIdx.x & 31;
+    // rows are walked in chunks of 32: lane r loads row kc + r's factors and its TB offset once (one
+    // coalesced load each instead of a dependent global load per row), rows take them by shuffle
+    const bool tb_uniform = __all_sync(0xffffffffu, !V.wr || (V.b == __shfl_sync(0xffffffffu, V.b, 0) &&
+                                                                V.bp == __shfl_sync(0xffffffffu, V.bp, 0)));
+    const int b0 = __shfl_sync(0xffffffffu, V.b, 0), bp0 = __shfl_sync(0xffffffffu, V.bp, 0);
+    const bool any_wr = __any_sync(0xffffffffu, V.wr);
     int nfold = 0;
-    for (int kp = V.kb; kp < V.ks1; ++kp) {
-        const bool kv = V.lv && (kp > V.k);
-        const dd er = kv ? pr : dd{0.0, 0.0};
-        const dd ei = kv ? pim : dd{0.0, 0.0};
-        const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
-        long long tb = 0;
-        if (WRITE && wk) tb = A.TB[((long long)V.b * L + V.bp) * d + kp] + V.wbase;
-        const double2 *fr_row = V.Fr + (long long)kp * NJ;
-        const double2 *fi_row = V.Fi + (long long)kp * NJ;
-        const uint32_t meta = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
+    for (int kc = V.kb; kc < V.ks1; kc += 32) {
+        const int nrow = min(32, V.ks1 - kc), kr = kc + lane;
+        double2 pf[NP + 1], pg[NP + 1];
+        long long ptb = 0;
+        if (lane < nrow) {
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const int ju = NJ - 1 - q;
-            const double2 f = fr_row[ju], g = fi_row[ju];
-            if (!WONLY) leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
-            if (WRITE && wk) {
-                cdd cu, cl;
-                cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
-                if (WONLY) {
-                    leaf_add_dd(cu.re, acc);
-                    leaf_add_dd(cl.re, acc);
+            for (int q = 0; q < NP; ++q) {
+                pf[q] = V.Fr[(long long)kr * NJ + NJ - 1 - q];
+                pg[q] = V.Fi[(long long)kr * NJ + NJ - 1 - q];
+            }
+            if constexpr (NJ % 2 == 1) pf[NP] = V.Fr[(long long)kr * NJ + NP];
+            if (WRITE && any_wr && tb_uniform && kr <= d - 2) ptb = A.TB[((long long)b0 * L + bp0) * d + kr];
+        }
+        for (int r = 0; r < nrow; ++r) {
+            const int kp = kc + r;
+            const bool kv = V.lv && (kp > V.k);
+            const dd er = kv ? pr : dd{0.0, 0.0};
+            const dd ei = kv ? pim : dd{0.0, 0.0};
+            const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
+            long long tb = 0;
+            if (WRITE && any_wr) {
+                const long long tbs = __shfl_sync(0xffffffffu, ptb, r);
+                if (wk) tb = (tb_uniform ? tbs : A.TB[((long long)V.b * L + V.bp) * d + kp]) + V.wbase;
+            }
+            const uint32_t meta = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int ju = NJ - 1 - q;
+                double2 f, g;
+                f.x = __shfl_sync(0xffffffffu, pf[q].x, r);
+                f.y = __shfl_sync(0xffffffffu, pf[q].y, r);
+                g.x = __shfl_sync(0xffffffffu, pg[q].x, r);
+                g.y = __shfl_sync(0xffffffffu, pg[q].y, r);
+                if (!WONLY) leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
+                if (WRITE && wk) {
+                    cdd cu, cl;
+                    cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
+                    if (WONLY) {
+                        leaf_add_dd(cu.re, acc);
+                        leaf_add_dd(cl.re, acc);
+                    }
+                    const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
+                    SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
+                    SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
+                    SG_DST(A, dst_meta, ou) = meta;
+                    SG_DST(A, dst_re, ol) = make_double2(cl.re.hi, cl.re.lo);
+                    SG_DST(A, dst_im, ol) = make_double2(cl.im.hi, cl.im.lo);
+                    SG_DST(A, dst_meta, ol) = meta;
                 }
-                const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
-                SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
-                SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
-                SG_DST(A, dst_meta, ou) = meta;
-                SG_DST(A, dst_re, ol) = make_double2(cl.re.hi, cl.re.lo);
-                SG_DST(A, dst_im, ol) = make_double2(cl.im.hi, cl.im.lo);
-                SG_DST(A, dst_meta, ol) = meta;
             }
-        }
-        if constexpr (NJ % 2 == 1) {
-            const double2 w = fr_row[NP];
-            if (!WONLY) leaf_real_factor_term<false>(er, w, acc.h, acc.l);
-            if (WRITE && wk) {
-                const long long oc = tb + (long long)NP * V.Nseg;
-                const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
-                if (WONLY) leaf_add_dd(cr, acc);
-                SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
-                SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
-                SG_DST(A, dst_meta, oc) = meta;
+            if constexpr (NJ % 2 == 1) {
+                double2 w;
+                w.x = __shfl_sync(0xffffffffu, pf[NP].x, r);
+                w.y = __shfl_sync(0xffffffffu, pf[NP].y, r);
+                if (!WONLY) leaf_real_factor_term<false>(er, w, acc.h, acc.l);
+                if (WRITE && wk) {
+                    const long long oc = tb + (long long)NP * V.Nseg;
+                    const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
+                    if (WONLY) leaf_add_dd(cr, acc);
+                    SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
+                    SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
+                    SG_DST(A, dst_meta, oc) = meta;
+                }
             }
-        }
-        if (++nfold == LEAF_SYM_FOLD) {
-            nfold = 0;
-            leaf_fold(acc, sigma);
+            if (++nfold == LEAF_SYM_FOLD) {
+                nfold = 0;
+                leaf_fold(acc, sigma);
+            }
         }
     }
 }
