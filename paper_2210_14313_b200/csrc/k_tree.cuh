@@ -229,9 +229,9 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
     const int lane = threadIdx.x & 31;
     // rows are walked in chunks of 32: lane r loads row kc + r's factors and its TB offset once (one
     // coalesced load each instead of a dependent global load per row), rows take them by shuffle
-    const bool tb_uniform = __all_sync(0xffffffffu, !V.wr || (V.b == __shfl_sync(0xffffffffu, V.b, 0) &&
-                                                                V.bp == __shfl_sync(0xffffffffu, V.bp, 0)));
+    // (every lane executes every shuffle: no shuffle inside a short-circuited or divergent expression)
     const int b0 = __shfl_sync(0xffffffffu, V.b, 0), bp0 = __shfl_sync(0xffffffffu, V.bp, 0);
+    const bool tb_uniform = __all_sync(0xffffffffu, !V.wr || (V.b == b0 && V.bp == bp0));
     const bool any_wr = __any_sync(0xffffffffu, V.wr);
     int nfold = 0;
     for (int kc = V.kb; kc < V.ks1; kc += 32) {
