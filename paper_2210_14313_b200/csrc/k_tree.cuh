@@ -159,17 +159,7 @@ struct PassLevel {
     const double2 *Fr, *Fi;
 };
 
-// WONLY (write-only pass of a split frontier pass): only the stored children (rows kp <= d-2 of the
-// levels with bp <= L-1, the caller restricts both); each child's term is the real part of its
-// stored dd product, added to the biased accumulator as a dd value (leaf_add_dd).
-__device__ __forceinline__ void leaf_add_dd(const dd &x, LeafAcc &a) {
-    const double a1 = a.h + x.hi;   // x.hi rounded once onto the grid of sigma
-    const double h = a1 - a.h;      // exact (Sterbenz)
-    a.h = a1;
-    a.l += (x.hi - h) + x.lo;       // x.hi - h exact: a multiple of ulp(x.hi), |.| <= ulp(sigma) / 2
-}
-
-template <bool CPLX, bool WRITE, int NJ, bool WONLY = false>
+template <bool CPLX, bool WRITE, int NJ>
 __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
                                            const dd &pim, double sigma, LeafAcc &acc, int nrt = 0) {
     const int n = NJ > 0 ? NJ : nrt;
@@ -188,7 +178,7 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
         for (int j = 0; j < (NJ > 0 ? NJ : n); ++j) {
             const double2 f = fr_row[j];
             const double2 fi = CPLX ? fi_row[j] : make_double2(0.0, 0.0);
-            if (!WONLY) leaf_term<CPLX>(er, ei, f, fi, acc);
+            leaf_term<CPLX>(er, ei, f, fi, acc);
             if (WRITE && wk) {
                 // the stored child product P F in dd (complex for the oscillatory kind)
                 const long long o = tb + (long long)j * V.Nseg;
@@ -197,7 +187,6 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
                 if (!CPLX) {
                     const dd ch = dd_norm(p1, e1);
                     SG_DST(A, dst_re, o) = make_double2(ch.hi, ch.lo);
-                    if (WONLY) leaf_add_dd(ch, acc);
                 } else {
                     double p2, e2, p3, e3, p4, e4;
                     dd_mul_pe(ei, dd{fi.x, fi.y}, p2, e2);
@@ -206,7 +195,6 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
                     const dd cre = dd_combine_pe(p1, e1, -p2, -e2), cim = dd_combine_pe(p3, e3, p4, e4);
                     SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
                     SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
-                    if (WONLY) leaf_add_dd(cre, acc);
                 }
                 SG_DST(A, dst_meta, o) = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
             }
@@ -221,87 +209,53 @@ __device__ __forceinline__ void pass_level(const DevPlan &P, const PassArgs &A, 
 // Symmetric oscillatory row (P.symmask): conjugate node pairs share the products of their terms
 // (leaf_sym_pair_terms) and of their stored child products (cdd_mul_conj_pair); the midpoint
 // (odd NJ) has a real factor.
-template <bool WRITE, int NJ, bool WONLY = false>
+template <bool WRITE, int NJ>
 __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs &A, const PassLevel &V, const dd &pr,
                                                const dd &pim, double sigma, LeafAcc &acc) {
     constexpr int NP = NJ / 2;
     const int d = P.d, L = P.L;
-    const int lane = threadIdx.x & 31;
-    // rows are walked in chunks of 32: lane r loads row kc + r's factors and its TB offset once (one
-    // coalesced load each instead of a dependent global load per row), rows take them by shuffle
-    // (every lane executes every shuffle: no shuffle inside a short-circuited or divergent expression)
-    const int b0 = __shfl_sync(0xffffffffu, V.b, 0), bp0 = __shfl_sync(0xffffffffu, V.bp, 0);
-    const bool tb_uniform = __all_sync(0xffffffffu, !V.wr || (V.b == b0 && V.bp == bp0));
-    const bool any_wr = __any_sync(0xffffffffu, V.wr);
     int nfold = 0;
-    for (int kc = V.kb; kc < V.ks1; kc += 32) {
-        const int nrow = min(32, V.ks1 - kc), kr = kc + lane;
-        double2 pf[NP + 1], pg[NP + 1];
-        long long ptb = 0;
-        if (lane < nrow) {
+    for (int kp = V.kb; kp < V.ks1; ++kp) {
+        const bool kv = V.lv && (kp > V.k);
+        const dd er = kv ? pr : dd{0.0, 0.0};
+        const dd ei = kv ? pim : dd{0.0, 0.0};
+        const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
+        long long tb = 0;
+        if (WRITE && wk) tb = A.TB[((long long)V.b * L + V.bp) * d + kp] + V.wbase;
+        const double2 *fr_row = V.Fr + (long long)kp * NJ;
+        const double2 *fi_row = V.Fi + (long long)kp * NJ;
+        const uint32_t meta = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                pf[q] = V.Fr[(long long)kr * NJ + NJ - 1 - q];
-                pg[q] = V.Fi[(long long)kr * NJ + NJ - 1 - q];
+        for (int q = 0; q < NP; ++q) {
+            const int ju = NJ - 1 - q;
+            const double2 f = fr_row[ju], g = fi_row[ju];
+            leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
+            if (WRITE && wk) {
+                cdd cu, cl;
+                cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
+                const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
+                SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
+                SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
+                SG_DST(A, dst_meta, ou) = meta;
+                SG_DST(A, dst_re, ol) = make_double2(cl.re.hi, cl.re.lo);
+                SG_DST(A, dst_im, ol) = make_double2(cl.im.hi, cl.im.lo);
+                SG_DST(A, dst_meta, ol) = meta;
             }
-            if constexpr (NJ % 2 == 1) pf[NP] = V.Fr[(long long)kr * NJ + NP];
-            if (WRITE && any_wr && tb_uniform && kr <= d - 2) ptb = A.TB[((long long)b0 * L + bp0) * d + kr];
         }
-        for (int r = 0; r < nrow; ++r) {
-            const int kp = kc + r;
-            const bool kv = V.lv && (kp > V.k);
-            const dd er = kv ? pr : dd{0.0, 0.0};
-            const dd ei = kv ? pim : dd{0.0, 0.0};
-            const bool wk = WRITE && V.wr && kv && (kp <= d - 2);
-            long long tb = 0;
-            if (WRITE && any_wr) {
-                const long long tbs = __shfl_sync(0xffffffffu, ptb, r);
-                if (wk) tb = (tb_uniform ? tbs : A.TB[((long long)V.b * L + V.bp) * d + kp]) + V.wbase;
+        if constexpr (NJ % 2 == 1) {
+            const double2 w = fr_row[NP];
+            leaf_real_factor_term<false>(er, w, acc.h, acc.l);
+            if (WRITE && wk) {
+                const long long oc = tb + (long long)NP * V.Nseg;
+                const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
+                SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
+                SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
+                SG_DST(A, dst_meta, oc) = meta;
             }
-            const uint32_t meta = ((uint32_t)V.bp << SG_META_KBITS) | (uint32_t)kp;
-#pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                const int ju = NJ - 1 - q;
-                double2 f, g;
-                f.x = __shfl_sync(0xffffffffu, pf[q].x, r);
-                f.y = __shfl_sync(0xffffffffu, pf[q].y, r);
-                g.x = __shfl_sync(0xffffffffu, pg[q].x, r);
-                g.y = __shfl_sync(0xffffffffu, pg[q].y, r);
-                if (!WONLY) leaf_sym_pair_terms(er, ei, f, g, acc.h, acc.l);
-                if (WRITE && wk) {
-                    cdd cu, cl;
-                    cdd_mul_conj_pair(cdd{er, ei}, cdd{dd{f.x, f.y}, dd{g.x, g.y}}, cu, cl);
-                    if (WONLY) {
-                        leaf_add_dd(cu.re, acc);
-                        leaf_add_dd(cl.re, acc);
-                    }
-                    const long long ou = tb + (long long)ju * V.Nseg, ol = tb + (long long)q * V.Nseg;
-                    SG_DST(A, dst_re, ou) = make_double2(cu.re.hi, cu.re.lo);
-                    SG_DST(A, dst_im, ou) = make_double2(cu.im.hi, cu.im.lo);
-                    SG_DST(A, dst_meta, ou) = meta;
-                    SG_DST(A, dst_re, ol) = make_double2(cl.re.hi, cl.re.lo);
-                    SG_DST(A, dst_im, ol) = make_double2(cl.im.hi, cl.im.lo);
-                    SG_DST(A, dst_meta, ol) = meta;
-                }
-            }
-            if constexpr (NJ % 2 == 1) {
-                double2 w;
-                w.x = __shfl_sync(0xffffffffu, pf[NP].x, r);
-                w.y = __shfl_sync(0xffffffffu, pf[NP].y, r);
-                if (!WONLY) leaf_real_factor_term<false>(er, w, acc.h, acc.l);
-                if (WRITE && wk) {
-                    const long long oc = tb + (long long)NP * V.Nseg;
-                    const dd cr = dd_mul(er, dd{w.x, w.y}), ci = dd_mul(ei, dd{w.x, w.y});
-                    if (WONLY) leaf_add_dd(cr, acc);
-                    SG_DST(A, dst_re, oc) = make_double2(cr.hi, cr.lo);
-                    SG_DST(A, dst_im, oc) = make_double2(ci.hi, ci.lo);
-                    SG_DST(A, dst_meta, oc) = meta;
-                }
-            }
-            if (++nfold == LEAF_SYM_FOLD) {
-                nfold = 0;
-                leaf_fold(acc, sigma);
-            }
+        }
+        if (++nfold == LEAF_SYM_FOLD) {
+            nfold = 0;
+            leaf_fold(acc, sigma);
         }
     }
 }
@@ -309,10 +263,7 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
 #ifndef PASS_MINB
 #define PASS_MINB 3   // CTAs/SM bound of k_pass
 #endif
-// WONLY: the write-only kernel of a split frontier pass (only the stored children: levels with
-// bp <= L-1, rows k' <= d-2; their terms from the stored products); the others are evaluated by
-// k_leaf<CPLX, true> concurrently.
-template <bool CPLX, bool WRITE, bool WONLY = false>
+template <bool CPLX, bool WRITE>
 __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan P, const PassArgs A) {
     // factor levels 2 .. A.stage_lmax staged in shared memory (same layout as the table: level l at
     // tab_off[l] - tab_off[2]); the row loads of the level loop then cost shared-memory latency
@@ -351,8 +302,7 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             }
         }
         const int ks0 = (int)((long long)split * d / A.nsplit);
-        const int ks1 = WONLY ? min((int)((long long)(split + 1) * d / A.nsplit), d - 1)
-                              : (int)((long long)(split + 1) * d / A.nsplit);
+        const int ks1 = (int)((long long)(split + 1) * d / A.nsplit);
         const int kmin = __reduce_min_sync(0xffffffffu, valid ? k : INT_MAX);
         const int bmin = __reduce_min_sync(0xffffffffu, b);
         long long iseg = 0, Nseg = 0, Cseg = 0;
@@ -364,8 +314,8 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
         }
         const double pabs = fabs(pr.hi) + (CPLX ? fabs(pim.hi) : 0.0);
         const int kb = max(ks0, kmin + 1);
-        for (int lp = 2; lp <= (WONLY ? L - bmin : L + 1 - bmin); ++lp) {
-            const bool lv = valid && (lp <= (WONLY ? L - b : L + 1 - b));
+        for (int lp = 2; lp <= L + 1 - bmin; ++lp) {
+            const bool lv = valid && (lp <= L + 1 - b);
             const int n = P.nl[lp];
             const int bp = b + lp - 1;
             const bool staged = lp <= A.stage_lmax;
@@ -382,14 +332,14 @@ __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan 
             LeafAcc acc = {sigma, 0.0};
             PassLevel L0 = {kb, ks1, k, lv, wr, b, bp, wbase, Nseg, Fr, Fi};
             const bool sym = CPLX && ((P.symmask >> lp) & 1);
-            if (sym && n == 3) pass_level_sym<WRITE, 3, WONLY>(P, A, L0, pr, pim, sigma, acc);
-            else if (sym && n == 5) pass_level_sym<WRITE, 5, WONLY>(P, A, L0, pr, pim, sigma, acc);
-            else if (sym && n == 2) pass_level_sym<WRITE, 2, WONLY>(P, A, L0, pr, pim, sigma, acc);
+            if (sym && n == 3) pass_level_sym<WRITE, 3>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 5) pass_level_sym<WRITE, 5>(P, A, L0, pr, pim, sigma, acc);
+            else if (sym && n == 2) pass_level_sym<WRITE, 2>(P, A, L0, pr, pim, sigma, acc);
             else switch (n) {
-            case 2: pass_level<CPLX, WRITE, 2, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
-            case 3: pass_level<CPLX, WRITE, 3, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
-            case 5: pass_level<CPLX, WRITE, 5, WONLY>(P, A, L0, pr, pim, sigma, acc); break;
-            default: pass_level<CPLX, WRITE, 0, WONLY>(P, A, L0, pr, pim, sigma, acc, n); break;
+            case 2: pass_level<CPLX, WRITE, 2>(P, A, L0, pr, pim, sigma, acc); break;
+            case 3: pass_level<CPLX, WRITE, 3>(P, A, L0, pr, pim, sigma, acc); break;
+            case 5: pass_level<CPLX, WRITE, 5>(P, A, L0, pr, pim, sigma, acc); break;
+            default: pass_level<CPLX, WRITE, 0>(P, A, L0, pr, pim, sigma, acc, n); break;
             }
             if (lv) tot = dd_add(tot, coef_mul(P, dd_norm(acc.h - sigma, acc.l), A.t + 1, bp));
         }
@@ -1486,4 +1436,65 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
         kk = nkk;
         rr = nrr;
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_front: the write-only frontier kernel of a split pass (HBM-bound by design).  Frontier t+1 is a
+// concatenation of RUNS — for a stored child level (b' = b + l' - 1 <= L-1) and row k' <= d-2, the
+// children with node j' of all sources of segment (b, k < k') are N_t(b, k) consecutive records
+// (the layout of plan.h: TB[b][b'][k'] + n_l' C_t(b, k) + j' N_t(b, k) + i).  The host lists the runs
+// (FrontRun); CTA c takes runs c, c + G, ... in order and its threads walk a run's records: source
+// i read coalesced, the factor F[l'][k'][j'] broadcast, the dd (complex dd) product stored coalesced
+// (re, im, meta), and the product's real part — the stored child's own Smolyak term — accumulated
+// (per run, times its coefficient C(t+1, b')).  The other children of the pass are evaluated by
+// k_leaf<CPLX, true> concurrently.  Static run assignment: one partial per CTA, fixed order.
+// ---------------------------------------------------------------------------------------------
+struct FrontRun {
+    long long out0, src0;   // first output record, first source record
+    int len;                // records (= N_t(b, k))
+    int tab;                // factor table entry of (l', k', j')
+    int kp, bp;             // the children's last coordinate and excess
+};
+
+#ifndef FRONT_THREADS
+#define FRONT_THREADS 256
+#endif
+template <bool CPLX>
+__global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontRun *runs,
+                                                         long long nruns) {
+    dd tot = {0.0, 0.0};
+    for (long long r = blockIdx.x; r < nruns; r += gridDim.x) {
+        const FrontRun R = runs[r];
+        const double2 f = P.Fre[R.tab];
+        const double2 fi = CPLX ? P.Fim[R.tab] : make_double2(0.0, 0.0);
+        const uint32_t meta = ((uint32_t)R.bp << SG_META_KBITS) | (uint32_t)R.kp;
+        double ah = 0.0, al = 0.0;   // this thread's share of the run's terms (TwoSum on the high parts)
+        for (int i = threadIdx.x; i < R.len; i += FRONT_THREADS) {
+            const long long g = R.src0 + i, o = R.out0 + i;
+            const double2 v = SG_SRC(A, src_re, g);
+            const dd pr = {v.x, v.y};
+            dd cre;
+            if (!CPLX) {
+                cre = dd_mul(pr, dd{f.x, f.y});
+                SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+            } else {
+                const double2 vi = SG_SRC(A, src_im, g);
+                const dd pim = {vi.x, vi.y};
+                double p1, e1, p2, e2, p3, e3, p4, e4;
+                dd_mul_pe(pr, dd{f.x, f.y}, p1, e1);
+                dd_mul_pe(pim, dd{fi.x, fi.y}, p2, e2);
+                dd_mul_pe(pr, dd{fi.x, fi.y}, p3, e3);
+                dd_mul_pe(pim, dd{f.x, f.y}, p4, e4);
+                cre = dd_combine_pe(p1, e1, -p2, -e2);
+                const dd cim = dd_combine_pe(p3, e3, p4, e4);
+                SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+                SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+            }
+            SG_DST(A, dst_meta, o) = meta;
+            acc_add(ah, al, cre.hi, cre.lo);
+        }
+        tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, R.bp));
+    }
+    dd s = block_reduce_dd<FRONT_THREADS / 32>(tot);
+    if (threadIdx.x == 0) SG_PART(A.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }

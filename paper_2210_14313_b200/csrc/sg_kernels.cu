@@ -83,6 +83,10 @@ struct sg_plan_s {
     std::vector<std::pair<int, int>> prof_pairs;   // per launch of the last sg_integrate: (start, end) event
     // fused plans: pass nfront-1 runs on a plan-owned side stream, concurrently with the fused pass
     cudaStream_t side = nullptr;
+    // split frontier passes: the runs of the stored children (k_front), per pass t (plan-owned)
+    FrontRun *d_runs = nullptr;
+    std::vector<long long> runs_off, runs_n;   // per pass t: offset into d_runs, count
+    int front_grid = 0;                        // k_front CTAs (= its partial slots)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
     char *ws = nullptr;
@@ -93,14 +97,36 @@ struct sg_plan_s {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
+#define FRONT_GRID (148 * 8)   // k_front CTAs: its partial slots of a split pass come first
 static void layout_partials(HostPlan &hp) {
     int64_t poff = hp.root_blocks;
     for (int u = 1; u <= hp.nfront; ++u) {
         hp.pass_partial_off[u] = poff;
         const bool split = u < (int)hp.pass_split.size() && hp.pass_split[u];
-        poff += hp.pass_blocks[u] * (split ? 2 : 1);
+        poff += hp.pass_blocks[u] + (split ? FRONT_GRID : 0);
     }
     hp.total_partials = poff;
+}
+
+// Runs of the stored children of pass t (k_front): target segments (b', k') of frontier t+1 in
+// order, inside each the source segments (b < b', k < k') in (b, k) order, their nodes j'.
+static void build_front_runs(const HostPlan &hp, int t, std::vector<FrontRun> &runs) {
+    const int d = hp.d, L = hp.L;
+    for (int bp = t + 1; bp <= L - 1; ++bp)
+        for (int kp = 0; kp <= d - 2; ++kp)
+            for (int b = 0; b < bp; ++b) {
+                const int lp = bp - b + 1, n = hp.nl[lp];
+                if (lp < 2) continue;
+                const int64_t tb = hp.TB[t][((size_t)b * L + bp) * d + kp];
+                for (int k = 0; k < kp; ++k) {
+                    const int64_t N = hp.N[t][(size_t)b * d + k];
+                    if (N == 0) continue;
+                    const int64_t C = hp.C[t][(size_t)b * d + k], src0 = hp.off[t][(size_t)b * d + k];
+                    for (int j = 0; j < n; ++j)
+                        runs.push_back(FrontRun{tb + (int64_t)n * C + (int64_t)j * N, src0, (int)N,
+                                                hp.tab_off[lp] + kp * n + j, kp, bp});
+                }
+            }
 }
 static int setup_leaf1(sg_plan_s *p);
 static int build_unrank_tables(sg_plan_s *p);
@@ -419,6 +445,24 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     bool any_split = false;
     for (size_t t = 0; t < hp.pass_split.size(); ++t) any_split = any_split || hp.pass_split[t];
+    if (any_split) {
+        std::vector<FrontRun> runs;
+        p->runs_off.assign(hp.nfront + 1, 0);
+        p->runs_n.assign(hp.nfront + 1, 0);
+        for (int t = 1; t < hp.nfront; ++t) {
+            if (!hp.pass_split[t]) continue;
+            p->runs_off[t] = (long long)runs.size();
+            build_front_runs(hp, t, runs);
+            p->runs_n[t] = (long long)runs.size() - p->runs_off[t];
+        }
+        p->front_grid = FRONT_GRID;
+        if (cudaMalloc(&p->d_runs, sizeof(FrontRun) * std::max<size_t>(runs.size(), 1)) != cudaSuccess ||
+            cudaMemcpy(p->d_runs, runs.data(), sizeof(FrontRun) * runs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            sg_destroy(p);
+            return SG_ENOMEM;
+        }
+    }
     if ((any_split || (p->leaf2 && hp.nfront >= 2)) &&
         !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
@@ -918,18 +962,20 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 A2.dst_re = A2.dst_im = nullptr;
                 A2.dst_meta = nullptr;
                 A2.TB = nullptr;
-                A2.partials = A.partials + grid;
+                A2.partials = A.partials + p->front_grid;
 #ifdef SG_CHECKS
                 A2.chk_dst_cap = 0;
 #endif
                 if (cudaEventRecord(p->ev_fork, st) != cudaSuccess) return SG_ECUDA;
                 if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
+                const FrontRun *runs = p->d_runs + p->runs_off[t];
+                const long long nr = p->runs_n[t];
                 if (p->cplx) {
                     k_leaf<true, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
-                    k_pass<true, true, true><<<grid, PASS_THREADS, pass_smem, st>>>(dp, A);
+                    k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 } else {
                     k_leaf<false, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
-                    k_pass<false, true, true><<<grid, PASS_THREADS, pass_smem, st>>>(dp, A);
+                    k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 }
                 // profile entry of the pass = the write-only kernel (fork -> its end on this stream);
                 // the leaf-only kernel overlaps it, the join wait falls into the next interval
@@ -1286,6 +1332,7 @@ extern "C" int sg_destroy(sg_plan_t p) {
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->side) cudaStreamDestroy(p->side);
+    if (p->d_runs) cudaFree(p->d_runs);
     if (p->d_unrank) cudaFree(p->d_unrank);
     if (p->dev_block) cudaFree(p->dev_block);
     delete p;

@@ -1,5 +1,6 @@
-"""Split frontier passes (sg_kernels.cu: a write-only k_pass for the stored children — their terms from
-the stored products — and, concurrently on the side stream, a leaf-only k_leaf for the other children):
+"""Split frontier passes (sg_kernels.cu: the write-only run kernel k_front for the stored children — their
+terms from the stored products — and, concurrently on the side stream, a leaf-only k_leaf for the other
+children):
 parity against the __float128 oracle with the split forced on every writing pass (fused and unfused
 plans, all rules and kinds, sharded), and the full-size unfused config 5 (the 4.3 GB frontier) against
 the stored oracle value."""
