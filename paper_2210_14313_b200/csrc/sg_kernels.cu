@@ -87,6 +87,7 @@ struct sg_plan_s {
     FrontRun *d_runs = nullptr;
     std::vector<long long> runs_off, runs_n;   // per pass t: offset into d_runs, count
     int front_grid = 0;                        // k_front CTAs (= its partial slots)
+    bool split_serial = false;                 // A/B: leaf-only kernel after k_front, same stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
     char *ws = nullptr;
@@ -456,6 +457,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             p->runs_n[t] = (long long)runs.size() - p->runs_off[t];
         }
         p->front_grid = FRONT_GRID;
+        p->split_serial = getenv("SG_B200_SPLIT_SERIAL") && getenv("SG_B200_SPLIT_SERIAL")[0] == '1';
         if (cudaMalloc(&p->d_runs, sizeof(FrontRun) * std::max<size_t>(runs.size(), 1)) != cudaSuccess ||
             cudaMemcpy(p->d_runs, runs.data(), sizeof(FrontRun) * runs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaGetLastError();
@@ -970,12 +972,16 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
                 const FrontRun *runs = p->d_runs + p->runs_off[t];
                 const long long nr = p->runs_n[t];
+                // SG_B200_SPLIT_SERIAL=1 (A/B): the leaf-only kernel after k_front on this stream
+                cudaStream_t sl = p->split_serial ? st : p->side;
                 if (p->cplx) {
-                    k_leaf<true, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    if (!p->split_serial) k_leaf<true, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
                     k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
+                    if (p->split_serial) k_leaf<true, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
                 } else {
-                    k_leaf<false, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    if (!p->split_serial) k_leaf<false, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
                     k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
+                    if (p->split_serial) k_leaf<false, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
                 }
                 // profile entry of the pass = the write-only kernel (fork -> its end on this stream);
                 // the leaf-only kernel overlaps it, the join wait falls into the next interval
