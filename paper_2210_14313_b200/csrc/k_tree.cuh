@@ -1459,6 +1459,27 @@ struct FrontRun {
 #ifndef FRONT_THREADS
 #define FRONT_THREADS 256
 #endif
+#ifndef FRONT_UNROLL
+#define FRONT_UNROLL 4   // records per thread per iteration (their loads issued together)
+#endif
+template <bool CPLX>
+__device__ __forceinline__ dd front_product(const double2 v, const double2 vi, const double2 f, const double2 fi,
+                                            dd &cim) {
+    const dd pr = {v.x, v.y};
+    if (!CPLX) {
+        cim = dd{0.0, 0.0};
+        return dd_mul(pr, dd{f.x, f.y});
+    }
+    const dd pim = {vi.x, vi.y};
+    double p1, e1, p2, e2, p3, e3, p4, e4;
+    dd_mul_pe(pr, dd{f.x, f.y}, p1, e1);
+    dd_mul_pe(pim, dd{fi.x, fi.y}, p2, e2);
+    dd_mul_pe(pr, dd{fi.x, fi.y}, p3, e3);
+    dd_mul_pe(pim, dd{f.x, f.y}, p4, e4);
+    cim = dd_combine_pe(p3, e3, p4, e4);
+    return dd_combine_pe(p1, e1, -p2, -e2);
+}
+
 template <bool CPLX>
 __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontRun *runs,
                                                          long long nruns) {
@@ -1469,29 +1490,30 @@ __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const 
         const double2 fi = CPLX ? P.Fim[R.tab] : make_double2(0.0, 0.0);
         const uint32_t meta = ((uint32_t)R.bp << SG_META_KBITS) | (uint32_t)R.kp;
         double ah = 0.0, al = 0.0;   // this thread's share of the run's terms (TwoSum on the high parts)
-        for (int i = threadIdx.x; i < R.len; i += FRONT_THREADS) {
-            const long long g = R.src0 + i, o = R.out0 + i;
-            const double2 v = SG_SRC(A, src_re, g);
-            const dd pr = {v.x, v.y};
-            dd cre;
-            if (!CPLX) {
-                cre = dd_mul(pr, dd{f.x, f.y});
-                SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
-            } else {
-                const double2 vi = SG_SRC(A, src_im, g);
-                const dd pim = {vi.x, vi.y};
-                double p1, e1, p2, e2, p3, e3, p4, e4;
-                dd_mul_pe(pr, dd{f.x, f.y}, p1, e1);
-                dd_mul_pe(pim, dd{fi.x, fi.y}, p2, e2);
-                dd_mul_pe(pr, dd{fi.x, fi.y}, p3, e3);
-                dd_mul_pe(pim, dd{f.x, f.y}, p4, e4);
-                cre = dd_combine_pe(p1, e1, -p2, -e2);
-                const dd cim = dd_combine_pe(p3, e3, p4, e4);
-                SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
-                SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+        for (int i0 = threadIdx.x; i0 < R.len; i0 += FRONT_THREADS * FRONT_UNROLL) {
+            double2 v[FRONT_UNROLL], vi[FRONT_UNROLL];
+#pragma unroll
+            for (int u = 0; u < FRONT_UNROLL; ++u) {   // all loads first
+                const int i = i0 + u * FRONT_THREADS;
+                v[u] = vi[u] = make_double2(0.0, 0.0);
+                if (i < R.len) {
+                    v[u] = SG_SRC(A, src_re, R.src0 + i);
+                    if (CPLX) vi[u] = SG_SRC(A, src_im, R.src0 + i);
+                }
             }
-            SG_DST(A, dst_meta, o) = meta;
-            acc_add(ah, al, cre.hi, cre.lo);
+#pragma unroll
+            for (int u = 0; u < FRONT_UNROLL; ++u) {
+                const int i = i0 + u * FRONT_THREADS;
+                if (i < R.len) {
+                    const long long o = R.out0 + i;
+                    dd cim;
+                    const dd cre = front_product<CPLX>(v[u], vi[u], f, fi, cim);
+                    SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+                    if (CPLX) SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+                    SG_DST(A, dst_meta, o) = meta;
+                    acc_add(ah, al, cre.hi, cre.lo);
+                }
+            }
         }
         tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, R.bp));
     }

@@ -98,7 +98,7 @@ struct sg_plan_s {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
-#define FRONT_GRID (148 * 8)   // k_front CTAs: its partial slots of a split pass come first
+#define FRONT_GRID (148 * 4)   // k_front CTAs (one wave at its occupancy): its partial slots come first
 static void layout_partials(HostPlan &hp) {
     int64_t poff = hp.root_blocks;
     for (int u = 1; u <= hp.nfront; ++u) {
