@@ -78,6 +78,7 @@ k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int includ
         // passes finished before this launch)
         task_counters[0] = 0;
         task_counters[2] = 0;
+        task_counters[4] = 0;
         step_close_status(P, st);
     }
 }

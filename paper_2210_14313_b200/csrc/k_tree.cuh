@@ -1439,38 +1439,34 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
 }
 
 // ---------------------------------------------------------------------------------------------
-// k_front: the write-only frontier kernel of a split pass (HBM-bound by design).  Frontier t+1 is a
-// concatenation of RUNS — for a stored child level (b' = b + l' - 1 <= L-1) and row k' <= d-2, the
-// children with node j' of all sources of segment (b, k < k') are N_t(b, k) consecutive records
-// (the layout of plan.h: TB[b][b'][k'] + n_l' C_t(b, k) + j' N_t(b, k) + i).  The host lists the runs
-// (FrontRun); CTA c takes runs c, c + G, ... in order and its threads walk a run's records: source
-// i read coalesced, the factor F[l'][k'][j'] broadcast, the dd (complex dd) product stored coalesced
-// (re, im, meta), and the product's real part — the stored child's own Smolyak term — accumulated
-// (per run, times its coefficient C(t+1, b')).  The other children of the pass are evaluated by
-// k_leaf<CPLX, true> concurrently.  Static run assignment: one partial per CTA, fixed order.
+// k_front: the write-only frontier kernel of a split pass (HBM-bound by design).  A CTA takes a chunk
+// of up to FRONT_THREADS consecutive sources of one frontier-t segment (b, k) — one source per thread,
+// read once, coalesced — and writes all their stored children: for every child level l' with
+// b' = b + l' - 1 <= L-1, every row k' in (k, d-2] and node j', the chunk's children are consecutive
+// records at TB[b][b'][k'] + n_l' C_t(b, k) + j' N_t(b, k) + i (plan.h layout), so each (k', j')
+// store is one contiguous block of up to FRONT_THREADS records (re, im, meta).  The factor and the TB
+// offset of a row are CTA-uniform (broadcast loads).  Each stored child's own Smolyak term, the real
+// part of its product, is accumulated (times C(t+1, b')).  The other children of the pass are
+// evaluated by k_leaf<CPLX, true> concurrently.  Chunks are assigned dynamically (sorted
+// heavy-first, pulled from an atomic counter): one partial per chunk, fixed reduction order.
 // ---------------------------------------------------------------------------------------------
-struct FrontRun {
-    long long out0, src0;   // first output record, first source record
-    int len;                // records (= N_t(b, k))
-    int tab;                // factor table entry of (l', k', j')
-    int kp, bp;             // the children's last coordinate and excess
+struct FrontChunk {
+    long long src0;   // first source record (frontier t index)
+    int i0, cnt;      // index of the first source inside its segment, sources in the chunk
+    int b, k;         // the segment
+    long long C, N;   // C_t(b, k), N_t(b, k)
 };
 
 #ifndef FRONT_THREADS
 #define FRONT_THREADS 256
 #endif
-#ifndef FRONT_UNROLL
-#define FRONT_UNROLL 4   // records per thread per iteration (their loads issued together)
-#endif
 template <bool CPLX>
-__device__ __forceinline__ dd front_product(const double2 v, const double2 vi, const double2 f, const double2 fi,
+__device__ __forceinline__ dd front_product(const dd &pr, const dd &pim, const double2 f, const double2 fi,
                                             dd &cim) {
-    const dd pr = {v.x, v.y};
     if (!CPLX) {
         cim = dd{0.0, 0.0};
         return dd_mul(pr, dd{f.x, f.y});
     }
-    const dd pim = {vi.x, vi.y};
     double p1, e1, p2, e2, p3, e3, p4, e4;
     dd_mul_pe(pr, dd{f.x, f.y}, p1, e1);
     dd_mul_pe(pim, dd{fi.x, fi.y}, p2, e2);
@@ -1481,42 +1477,57 @@ __device__ __forceinline__ dd front_product(const double2 v, const double2 vi, c
 }
 
 template <bool CPLX>
-__global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontRun *runs,
-                                                         long long nruns) {
-    dd tot = {0.0, 0.0};
-    for (long long r = blockIdx.x; r < nruns; r += gridDim.x) {
-        const FrontRun R = runs[r];
-        const double2 f = P.Fre[R.tab];
-        const double2 fi = CPLX ? P.Fim[R.tab] : make_double2(0.0, 0.0);
-        const uint32_t meta = ((uint32_t)R.bp << SG_META_KBITS) | (uint32_t)R.kp;
-        double ah = 0.0, al = 0.0;   // this thread's share of the run's terms (TwoSum on the high parts)
-        for (int i0 = threadIdx.x; i0 < R.len; i0 += FRONT_THREADS * FRONT_UNROLL) {
-            double2 v[FRONT_UNROLL], vi[FRONT_UNROLL];
-#pragma unroll
-            for (int u = 0; u < FRONT_UNROLL; ++u) {   // all loads first
-                const int i = i0 + u * FRONT_THREADS;
-                v[u] = vi[u] = make_double2(0.0, 0.0);
-                if (i < R.len) {
-                    v[u] = SG_SRC(A, src_re, R.src0 + i);
-                    if (CPLX) vi[u] = SG_SRC(A, src_im, R.src0 + i);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < FRONT_UNROLL; ++u) {
-                const int i = i0 + u * FRONT_THREADS;
-                if (i < R.len) {
-                    const long long o = R.out0 + i;
-                    dd cim;
-                    const dd cre = front_product<CPLX>(v[u], vi[u], f, fi, cim);
-                    SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
-                    if (CPLX) SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
-                    SG_DST(A, dst_meta, o) = meta;
-                    acc_add(ah, al, cre.hi, cre.lo);
-                }
+__global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontChunk *chunks,
+                                                         long long nchunks) {
+    const int d = P.d, L = P.L;
+    __shared__ long long cnext;
+    for (;;) {
+        if (threadIdx.x == 0) cnext = (long long)atomicAdd(A.counter, 1ull);
+        __syncthreads();
+        const long long c = cnext;
+        __syncthreads();
+        if (c >= nchunks) break;
+        dd tot = {0.0, 0.0};
+        const FrontChunk C = chunks[c];
+        const bool on = (int)threadIdx.x < C.cnt;
+        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
+        if (on) {
+            const double2 v = SG_SRC(A, src_re, C.src0 + threadIdx.x);
+            pr = dd{v.x, v.y};
+            if (CPLX) {
+                const double2 vi = SG_SRC(A, src_im, C.src0 + threadIdx.x);
+                pim = dd{vi.x, vi.y};
             }
         }
-        tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, R.bp));
+        const long long i = C.i0 + threadIdx.x;
+        for (int lp = 2; lp <= L - C.b; ++lp) {   // stored child levels: b' = b + lp - 1 <= L - 1
+            const int bp = C.b + lp - 1, n = P.nl[lp];
+            const double2 *Fr = P.Fre + P.tab_off[lp];
+            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            const long long *tbrow = A.TB + ((long long)C.b * L + bp) * d;
+            const long long base = (long long)n * C.C + i;
+            double ah = 0.0, al = 0.0;
+            for (int kp = C.k + 1; kp <= d - 2; ++kp) {
+                const long long tb = tbrow[kp] + base;
+                const uint32_t meta = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+                for (int j = 0; j < n; ++j) {
+                    const double2 f = Fr[(long long)kp * n + j];
+                    const double2 fi = CPLX ? Fi[(long long)kp * n + j] : make_double2(0.0, 0.0);
+                    if (on) {
+                        const long long o = tb + (long long)j * C.N;
+                        dd cim;
+                        const dd cre = front_product<CPLX>(pr, pim, f, fi, cim);
+                        SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+                        if (CPLX) SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+                        SG_DST(A, dst_meta, o) = meta;
+                        acc_add(ah, al, cre.hi, cre.lo);
+                    }
+                }
+            }
+            if (on) tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, bp));
+        }
+        dd s = block_reduce_dd<FRONT_THREADS / 32>(tot);
+        if (threadIdx.x == 0) SG_PART(A.partials, c) = make_double2(s.hi, s.lo);
+        __syncthreads();   // block_reduce's shared scratch is reused by the next chunk
     }
-    dd s = block_reduce_dd<FRONT_THREADS / 32>(tot);
-    if (threadIdx.x == 0) SG_PART(A.partials, blockIdx.x) = make_double2(s.hi, s.lo);
 }

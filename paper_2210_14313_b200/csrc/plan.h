@@ -98,6 +98,7 @@ struct HostPlan {
     // split frontier pass t (sg_kernels.cu, factor form, large frontiers): a write-only k_pass for the
     // stored children and a concurrent leaf-only k_leaf for the others, pass_blocks[t] slots each
     std::vector<char> pass_split;
+    std::vector<int64_t> pass_front_slots;   // split pass t: k_front's chunks (one partial slot each)
     int64_t root_blocks = 0, total_partials = 0;
     size_t ws_front_bytes[2] = {0, 0}; // ping-pong frontier buffers (odd / even depth)
     int64_t ws_front_cap[2] = {0, 0};

@@ -84,9 +84,10 @@ struct sg_plan_s {
     // fused plans: pass nfront-1 runs on a plan-owned side stream, concurrently with the fused pass
     cudaStream_t side = nullptr;
     // split frontier passes: the runs of the stored children (k_front), per pass t (plan-owned)
-    FrontRun *d_runs = nullptr;
-    std::vector<long long> runs_off, runs_n;   // per pass t: offset into d_runs, count
-    int front_grid = 0;                        // k_front CTAs (= its partial slots)
+    FrontChunk *d_runs = nullptr;
+    std::vector<long long> runs_off, runs_n;   // per pass t: offset into d_runs (chunks), count
+    int front_grid = 0;                        // k_front CTAs (persistent)
+    std::vector<FrontChunk> front_chunks;      // host copy (built with the partial layout)
     bool split_serial = false;                 // A/B: leaf-only kernel after k_front, same stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
@@ -98,36 +99,30 @@ struct sg_plan_s {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
-#define FRONT_GRID (148 * 4)   // k_front CTAs (one wave at its occupancy): its partial slots come first
+#define FRONT_GRID (148 * 4)   // k_front CTAs (persistent; 4 per SM at its register count)
+// split pass t: slots [0, pass_split[t] - 1) for k_front's chunks, then pass_blocks[t] for k_leaf
 static void layout_partials(HostPlan &hp) {
     int64_t poff = hp.root_blocks;
     for (int u = 1; u <= hp.nfront; ++u) {
         hp.pass_partial_off[u] = poff;
-        const bool split = u < (int)hp.pass_split.size() && hp.pass_split[u];
-        poff += hp.pass_blocks[u] + (split ? FRONT_GRID : 0);
+        const int64_t fs = u < (int)hp.pass_front_slots.size() ? hp.pass_front_slots[u] : 0;
+        poff += hp.pass_blocks[u] + fs;
     }
     hp.total_partials = poff;
 }
 
-// Runs of the stored children of pass t (k_front): target segments (b', k') of frontier t+1 in
-// order, inside each the source segments (b < b', k < k') in (b, k) order, their nodes j'.
-static void build_front_runs(const HostPlan &hp, int t, std::vector<FrontRun> &runs) {
+// Source chunks of pass t for k_front: every segment (b <= L-2: it has stored children) of frontier t
+// cut into chunks of FRONT_THREADS consecutive sources.
+static void build_front_chunks(const HostPlan &hp, int t, std::vector<FrontChunk> &ch) {
     const int d = hp.d, L = hp.L;
-    for (int bp = t + 1; bp <= L - 1; ++bp)
-        for (int kp = 0; kp <= d - 2; ++kp)
-            for (int b = 0; b < bp; ++b) {
-                const int lp = bp - b + 1, n = hp.nl[lp];
-                if (lp < 2) continue;
-                const int64_t tb = hp.TB[t][((size_t)b * L + bp) * d + kp];
-                for (int k = 0; k < kp; ++k) {
-                    const int64_t N = hp.N[t][(size_t)b * d + k];
-                    if (N == 0) continue;
-                    const int64_t C = hp.C[t][(size_t)b * d + k], src0 = hp.off[t][(size_t)b * d + k];
-                    for (int j = 0; j < n; ++j)
-                        runs.push_back(FrontRun{tb + (int64_t)n * C + (int64_t)j * N, src0, (int)N,
-                                                hp.tab_off[lp] + kp * n + j, kp, bp});
-                }
-            }
+    for (int b = 0; b <= L - 2; ++b)
+        for (int k = 0; k <= d - 3; ++k) {   // a stored child needs a row k' in (k, d-2]
+            const int64_t N = hp.N[t][(size_t)b * d + k];
+            for (int64_t i0 = 0; i0 < N; i0 += FRONT_THREADS)
+                ch.push_back(FrontChunk{hp.off[t][(size_t)b * d + k] + i0, (int)i0,
+                                        (int)std::min<int64_t>(FRONT_THREADS, N - i0), b, k,
+                                        hp.C[t][(size_t)b * d + k], N});
+        }
 }
 static int setup_leaf1(sg_plan_s *p);
 static int build_unrank_tables(sg_plan_s *p);
@@ -366,6 +361,28 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             const bool big = (double)hp.pass_written[t] * rec >= FRONT_SPLIT_MIN_BYTES;
             hp.pass_split[t] = (!p->sform && writes && (force == 1 || (force != 0 && big))) ? 1 : 0;
         }
+        // k_front chunks of the split passes (heavy-first: work ~ sources x rows x stored nodes)
+        hp.pass_front_slots.assign(hp.nfront + 1, 0);
+        p->runs_off.assign(hp.nfront + 1, 0);
+        p->runs_n.assign(hp.nfront + 1, 0);
+        p->front_chunks.clear();
+        for (int t = 1; t < hp.nfront; ++t) {
+            if (!hp.pass_split[t]) continue;
+            std::vector<FrontChunk> ch;
+            build_front_chunks(hp, t, ch);
+            auto work = [&](const FrontChunk &c) {
+                int64_t nodes = 0;
+                for (int lp = 2; lp <= hp.L - c.b; ++lp) nodes += hp.nl[lp];
+                return (int64_t)c.cnt * (hp.d - 2 - c.k) * nodes;
+            };
+            std::stable_sort(ch.begin(), ch.end(), [&](const FrontChunk &a, const FrontChunk &b2) {
+                return work(a) > work(b2);
+            });
+            p->runs_off[t] = (long long)p->front_chunks.size();
+            p->runs_n[t] = (long long)ch.size();
+            hp.pass_front_slots[t] = (int64_t)ch.size();
+            p->front_chunks.insert(p->front_chunks.end(), ch.begin(), ch.end());
+        }
         layout_partials(hp);
     }
     if (const char *e = getenv("SG_B200_PASS_SMEM"); e && e[0]) p->pass_smem_cap = (size_t)atoll(e);
@@ -447,19 +464,11 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     bool any_split = false;
     for (size_t t = 0; t < hp.pass_split.size(); ++t) any_split = any_split || hp.pass_split[t];
     if (any_split) {
-        std::vector<FrontRun> runs;
-        p->runs_off.assign(hp.nfront + 1, 0);
-        p->runs_n.assign(hp.nfront + 1, 0);
-        for (int t = 1; t < hp.nfront; ++t) {
-            if (!hp.pass_split[t]) continue;
-            p->runs_off[t] = (long long)runs.size();
-            build_front_runs(hp, t, runs);
-            p->runs_n[t] = (long long)runs.size() - p->runs_off[t];
-        }
+        const std::vector<FrontChunk> &runs = p->front_chunks;
         p->front_grid = FRONT_GRID;
         p->split_serial = getenv("SG_B200_SPLIT_SERIAL") && getenv("SG_B200_SPLIT_SERIAL")[0] == '1';
-        if (cudaMalloc(&p->d_runs, sizeof(FrontRun) * std::max<size_t>(runs.size(), 1)) != cudaSuccess ||
-            cudaMemcpy(p->d_runs, runs.data(), sizeof(FrontRun) * runs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        if (cudaMalloc(&p->d_runs, sizeof(FrontChunk) * std::max<size_t>(runs.size(), 1)) != cudaSuccess ||
+            cudaMemcpy(p->d_runs, runs.data(), sizeof(FrontChunk) * runs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaGetLastError();
             sg_destroy(p);
             return SG_ENOMEM;
@@ -964,13 +973,15 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 A2.dst_re = A2.dst_im = nullptr;
                 A2.dst_meta = nullptr;
                 A2.TB = nullptr;
-                A2.partials = A.partials + p->front_grid;
+                A2.partials = A.partials + hp.pass_front_slots[t];
+                A.counter = p->d_counter + 4;   // k_front's chunk counter (zeroed per split pass)
+                if (cudaMemsetAsync(A.counter, 0, sizeof(unsigned long long), st) != cudaSuccess) return SG_ECUDA;
 #ifdef SG_CHECKS
                 A2.chk_dst_cap = 0;
 #endif
                 if (cudaEventRecord(p->ev_fork, st) != cudaSuccess) return SG_ECUDA;
                 if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
-                const FrontRun *runs = p->d_runs + p->runs_off[t];
+                const FrontChunk *runs = p->d_runs + p->runs_off[t];
                 const long long nr = p->runs_n[t];
                 // SG_B200_SPLIT_SERIAL=1 (A/B): the leaf-only kernel after k_front on this stream
                 cudaStream_t sl = p->split_serial ? st : p->side;
