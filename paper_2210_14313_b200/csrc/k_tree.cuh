@@ -1502,17 +1502,22 @@ __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const 
         const long long i = C.i0 + threadIdx.x;
         for (int lp = 2; lp <= L - C.b; ++lp) {   // stored child levels: b' = b + lp - 1 <= L - 1
             const int bp = C.b + lp - 1, n = P.nl[lp];
-            const double2 *Fr = P.Fre + P.tab_off[lp];
-            const double2 *Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
-            const long long *tbrow = A.TB + ((long long)C.b * L + bp) * d;
+            const double2 *__restrict__ Fr = P.Fre + P.tab_off[lp];
+            const double2 *__restrict__ Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
+            const long long *__restrict__ tbrow = A.TB + ((long long)C.b * L + bp) * d;
             const long long base = (long long)n * C.C + i;
             double ah = 0.0, al = 0.0;
+            // read-only table loads through the non-coherent path, the next row's issued ahead (the
+            // stores of this row cannot alias them)
+            long long tbn = __ldg(tbrow + C.k + 1);
             for (int kp = C.k + 1; kp <= d - 2; ++kp) {
-                const long long tb = tbrow[kp] + base;
+                const long long tb = tbn + base;
+                if (kp + 1 <= d - 2) tbn = __ldg(tbrow + kp + 1);
                 const uint32_t meta = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
+#pragma unroll 3
                 for (int j = 0; j < n; ++j) {
-                    const double2 f = Fr[(long long)kp * n + j];
-                    const double2 fi = CPLX ? Fi[(long long)kp * n + j] : make_double2(0.0, 0.0);
+                    const double2 f = __ldg(Fr + (long long)kp * n + j);
+                    const double2 fi = CPLX ? __ldg(Fi + (long long)kp * n + j) : make_double2(0.0, 0.0);
                     if (on) {
                         const long long o = tb + (long long)j * C.N;
                         dd cim;
