@@ -1476,6 +1476,9 @@ __device__ __forceinline__ dd front_product(const dd &pr, const dd &pim, const d
     return dd_combine_pe(p1, e1, -p2, -e2);
 }
 
+#ifndef FRONT_SPT
+#define FRONT_SPT 4   // sources per thread: a (row, node) store block is FRONT_THREADS * FRONT_SPT records
+#endif
 template <bool CPLX>
 __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontChunk *chunks,
                                                          long long nchunks) {
@@ -1489,47 +1492,51 @@ __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const 
         if (c >= nchunks) break;
         dd tot = {0.0, 0.0};
         const FrontChunk C = chunks[c];
-        const bool on = (int)threadIdx.x < C.cnt;
-        dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
-        if (on) {
-            const double2 v = SG_SRC(A, src_re, C.src0 + threadIdx.x);
-            pr = dd{v.x, v.y};
-            if (CPLX) {
-                const double2 vi = SG_SRC(A, src_im, C.src0 + threadIdx.x);
-                pim = dd{vi.x, vi.y};
+        // sources s = threadIdx.x + FRONT_THREADS u of the chunk (u < FRONT_SPT), loaded once
+        dd pr[FRONT_SPT], pim[FRONT_SPT];
+#pragma unroll
+        for (int u = 0; u < FRONT_SPT; ++u) {
+            const int sidx = threadIdx.x + FRONT_THREADS * u;
+            pr[u] = pim[u] = dd{0.0, 0.0};
+            if (sidx < C.cnt) {
+                const double2 v = SG_SRC(A, src_re, C.src0 + sidx);
+                pr[u] = dd{v.x, v.y};
+                if (CPLX) {
+                    const double2 vi = SG_SRC(A, src_im, C.src0 + sidx);
+                    pim[u] = dd{vi.x, vi.y};
+                }
             }
         }
-        const long long i = C.i0 + threadIdx.x;
         for (int lp = 2; lp <= L - C.b; ++lp) {   // stored child levels: b' = b + lp - 1 <= L - 1
             const int bp = C.b + lp - 1, n = P.nl[lp];
             const double2 *__restrict__ Fr = P.Fre + P.tab_off[lp];
             const double2 *__restrict__ Fi = CPLX ? P.Fim + P.tab_off[lp] : nullptr;
             const long long *__restrict__ tbrow = A.TB + ((long long)C.b * L + bp) * d;
-            const long long base = (long long)n * C.C + i;
+            const long long base = (long long)n * C.C + C.i0 + threadIdx.x;
             double ah = 0.0, al = 0.0;
-            // read-only table loads through the non-coherent path, the next row's issued ahead (the
-            // stores of this row cannot alias them)
             long long tbn = __ldg(tbrow + C.k + 1);
             for (int kp = C.k + 1; kp <= d - 2; ++kp) {
                 const long long tb = tbn + base;
                 if (kp + 1 <= d - 2) tbn = __ldg(tbrow + kp + 1);
                 const uint32_t meta = ((uint32_t)bp << SG_META_KBITS) | (uint32_t)kp;
-#pragma unroll 3
                 for (int j = 0; j < n; ++j) {
                     const double2 f = __ldg(Fr + (long long)kp * n + j);
                     const double2 fi = CPLX ? __ldg(Fi + (long long)kp * n + j) : make_double2(0.0, 0.0);
-                    if (on) {
-                        const long long o = tb + (long long)j * C.N;
-                        dd cim;
-                        const dd cre = front_product<CPLX>(pr, pim, f, fi, cim);
-                        SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
-                        if (CPLX) SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
-                        SG_DST(A, dst_meta, o) = meta;
-                        acc_add(ah, al, cre.hi, cre.lo);
+#pragma unroll
+                    for (int u = 0; u < FRONT_SPT; ++u) {
+                        if ((int)threadIdx.x + FRONT_THREADS * u < C.cnt) {
+                            const long long o = tb + (long long)j * C.N + FRONT_THREADS * u;
+                            dd cim;
+                            const dd cre = front_product<CPLX>(pr[u], pim[u], f, fi, cim);
+                            SG_DST(A, dst_re, o) = make_double2(cre.hi, cre.lo);
+                            if (CPLX) SG_DST(A, dst_im, o) = make_double2(cim.hi, cim.lo);
+                            SG_DST(A, dst_meta, o) = meta;
+                            acc_add(ah, al, cre.hi, cre.lo);
+                        }
                     }
                 }
             }
-            if (on) tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, bp));
+            tot = dd_add(tot, coef_mul(P, dd_norm(ah, al), A.t + 1, bp));
         }
         dd s = block_reduce_dd<FRONT_THREADS / 32>(tot);
         if (threadIdx.x == 0) SG_PART(A.partials, c) = make_double2(s.hi, s.lo);

@@ -112,15 +112,15 @@ static void layout_partials(HostPlan &hp) {
 }
 
 // Source chunks of pass t for k_front: every segment (b <= L-2: it has stored children) of frontier t
-// cut into chunks of FRONT_THREADS consecutive sources.
+// cut into chunks of FRONT_THREADS * FRONT_SPT consecutive sources.
 static void build_front_chunks(const HostPlan &hp, int t, std::vector<FrontChunk> &ch) {
     const int d = hp.d, L = hp.L;
     for (int b = 0; b <= L - 2; ++b)
         for (int k = 0; k <= d - 3; ++k) {   // a stored child needs a row k' in (k, d-2]
             const int64_t N = hp.N[t][(size_t)b * d + k];
-            for (int64_t i0 = 0; i0 < N; i0 += FRONT_THREADS)
+            for (int64_t i0 = 0; i0 < N; i0 += FRONT_THREADS * FRONT_SPT)
                 ch.push_back(FrontChunk{hp.off[t][(size_t)b * d + k] + i0, (int)i0,
-                                        (int)std::min<int64_t>(FRONT_THREADS, N - i0), b, k,
+                                        (int)std::min<int64_t>(FRONT_THREADS * FRONT_SPT, N - i0), b, k,
                                         hp.C[t][(size_t)b * d + k], N});
         }
 }
