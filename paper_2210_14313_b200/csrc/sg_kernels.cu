@@ -466,6 +466,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     if (any_split) {
         const std::vector<FrontChunk> &runs = p->front_chunks;
         p->front_grid = FRONT_GRID;
+        if (const char *e = getenv("SG_B200_FRONT_GRID"); e && e[0]) p->front_grid = std::max(1, atoi(e));   // A/B
         p->split_serial = getenv("SG_B200_SPLIT_SERIAL") && getenv("SG_B200_SPLIT_SERIAL")[0] == '1';
         if (cudaMalloc(&p->d_runs, sizeof(FrontChunk) * std::max<size_t>(runs.size(), 1)) != cudaSuccess ||
             cudaMemcpy(p->d_runs, runs.data(), sizeof(FrontChunk) * runs.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
