@@ -88,7 +88,7 @@ struct sg_plan_s {
     std::vector<long long> runs_off, runs_n;   // per pass t: offset into d_runs (chunks), count
     int front_grid = 0;                        // k_front CTAs (persistent)
     std::vector<FrontChunk> front_chunks;      // host copy (built with the partial layout)
-    bool split_serial = false;                 // A/B: leaf-only kernel after k_front, same stream
+    bool split_serial = false;                 // leaf-only kernel after k_front on the same stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
     char *ws = nullptr;
@@ -99,7 +99,7 @@ struct sg_plan_s {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
-#define FRONT_GRID (148 * 4)   // k_front CTAs (persistent; 4 per SM at its register count)
+#define FRONT_GRID 148   // k_front CTAs (persistent, one per SM: A/B r02z serial 148 -> 1.45 ms, 592 -> 1.65 ms)
 // split pass t: slots [0, pass_split[t] - 1) for k_front's chunks, then pass_blocks[t] for k_leaf
 static void layout_partials(HostPlan &hp) {
     int64_t poff = hp.root_blocks;
@@ -984,23 +984,24 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 if (cudaStreamWaitEvent(p->side, p->ev_fork, 0) != cudaSuccess) return SG_ECUDA;
                 const FrontChunk *runs = p->d_runs + p->runs_off[t];
                 const long long nr = p->runs_n[t];
-                // SG_B200_SPLIT_SERIAL=1 (A/B): the leaf-only kernel after k_front on this stream
-                cudaStream_t sl = p->split_serial ? st : p->side;
-                if (p->cplx) {
-                    if (!p->split_serial) k_leaf<true, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
-                    k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
-                    if (p->split_serial) k_leaf<true, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
-                } else {
-                    if (!p->split_serial) k_leaf<false, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
-                    k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
-                    if (p->split_serial) k_leaf<false, true><<<grid, PASS_THREADS, 0, sl>>>(dp, A2);
+                // profile entry of the pass = k_front (fork -> its end on this stream).  Concurrent
+                // (default): the leaf-only k_leaf overlaps it on the side stream.  Serial
+                // (SG_B200_SPLIT_SERIAL=1: the clean frontier-kernel time of bench.py's frontier leg):
+                // k_leaf follows on this stream and falls into the next launch's interval.
+                if (!p->split_serial) {
+                    if (p->cplx) k_leaf<true, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    else k_leaf<false, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
                 }
-                // profile entry of the pass = the write-only kernel (fork -> its end on this stream);
-                // the leaf-only kernel overlaps it, the join wait falls into the next interval
+                if (p->cplx) k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
+                else k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 split_done = true;
                 const int e = pr.rec(st);
                 pr.launch_done(pr.last, e);
                 pr.last = e;
+                if (p->split_serial) {
+                    if (p->cplx) k_leaf<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
+                    else k_leaf<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
+                }
                 if (cudaEventRecord(p->ev_join, p->side) != cudaSuccess) return SG_ECUDA;
                 if (cudaStreamWaitEvent(st, p->ev_join, 0) != cudaSuccess) return SG_ECUDA;
             } else if (p->cplx) {
