@@ -468,11 +468,16 @@ def main():
     # avoids.  Reports that launch's HBM bytes / time against MEASURED_PEAKS.json hbm_gbs.
     frontier = None
     if not args.no_frontier:
+        # the deepest frontier pass is split (sg_kernels.cu): k_front stores the 4.3 GB of records
+        # (HBM-bound, its own interval here: the serial split order) and k_leaf evaluates the other
+        # children after it
         os.environ["SG_B200_NOFUSE"] = "1"
+        os.environ["SG_B200_SPLIT_SERIAL"] = "1"
         try:
             fplan, _ = make_plan(p)
         finally:
             del os.environ["SG_B200_NOFUSE"]
+            del os.environ["SG_B200_SPLIT_SERIAL"]
         fplan.profile_enable(True)
         fpasses = fplan.passes()
         wpass = max(range(1, len(fpasses)), key=lambda i: fpasses[i].written) if len(fpasses) > 1 else 0
@@ -492,8 +497,10 @@ def main():
         gbs = (wbytes + rbytes) / (k_ms * 1e-3) / 1e9
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         ftraffic = json.load(open(tfile)).get(f"c{args.config}_frontier") if os.path.exists(tfile) else None
-        frontier = {"what": f"unfused step; pass {wpass} (k_pass WRITE) writes {fpasses[wpass].written} "
-                            f"frontier records of {rec} B and evaluates {fpasses[wpass].terms} points",
+        frontier = {"what": f"unfused step; pass {wpass}'s write-only frontier kernel k_front writes "
+                            f"{fpasses[wpass].written} frontier records of {rec} B (and accumulates their "
+                            f"terms; the pass's other children, {fpasses[wpass].terms} points in all, "
+                            f"follow in the leaf-only k_leaf)",
                     "step_ms": statistics.mean(f_times), "kernel_ms": k_ms,
                     "algorithmic_bytes": wbytes + rbytes, "achieved_gbs": gbs,
                     "peak_gbs": hbm, "frac": (gbs / hbm) if hbm else None, "traffic": ftraffic}
