@@ -22,6 +22,7 @@ ctr_runs() {   # plain run && the same command under ncu (FP64 counters of the d
 for s in $steps; do
   case $s in
     plain) bash $0 $tag test smoke bench plainruns ;;
+    full) bash $0 $tag test smoke bench nccl checked shards ;;
     test)  timeout 1800 python -m pytest tests -m gpu -q -x -rA 2>&1 | tail -60 > gpurun_out/${tag}_pytest_gpu.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1 ;;
     bench) timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err ;;
@@ -39,6 +40,8 @@ for s in $steps; do
         --log-file gpurun_out/${tag}_launches_c4.csv python tools/prof_step.py 4 2 > /dev/null 2>&1 ;;
     shards) for c in 4 5; do SHARD_PHASES=1 timeout 900 python tools/shard_times.py $c 2 4 8 > gpurun_out/${tag}_shards_c$c.txt 2>&1; done ;;
     pyt) timeout 1800 python -m pytest $PYT -q -x --tb=long 2>&1 | tail -150 > gpurun_out/${tag}_pyt.log ;;
+    nccl) NCCL_DEBUG=INFO timeout 900 python -m pytest tests/test_gpu_nccl.py -q -s 2>&1 | grep -E "NCCL INFO|passed|failed|Error" | head -80 > gpurun_out/${tag}_nccl.log ;;
+    checked) timeout 1500 python tools/checked_run.py > gpurun_out/${tag}_checked_run.txt 2>&1 ;;
     memcheck|racecheck|synccheck|initcheck)
       timeout 2400 compute-sanitizer --tool $s --error-exitcode 9 --print-limit 50 \
         python tools/sanitize_cases.py > gpurun_out/${tag}_san_$s.log 2>&1
