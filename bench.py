@@ -298,13 +298,14 @@ def main():
         else:
             plan.sg_finalize(part, 1, stream, result)
 
-    def graph_step(plan):
-        """The step as one CUDA-graph replay (sg_integrate, + sg_finalize at world 1; the launch
-        events are graph event-record nodes, so profile_read still times each launch); with a
-        process group the all-gather and sg_finalize follow the replay as in step()."""
+    def graph_step(plan, prof=2):
+        """The step as one CUDA-graph replay (sg_integrate, + sg_finalize at world 1); with prof = 2
+        the dominant pass's launch is bracketed by two graph event-record nodes (profile_read times it
+        on every replay), with 0 the step has no event nodes; with a process group the all-gather and
+        sg_finalize follow the replay as in step()."""
         if args.no_graph:
             return lambda: step(plan)
-        plan.profile_enable(True)
+        plan.profile_enable(prof)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             part = plan.sg_integrate()
@@ -348,19 +349,20 @@ def main():
         passes = plan.passes()
         return (max(range(1, len(passes)), key=lambda i: passes[i].terms) if len(passes) > 1 else 0), passes
 
-    def measure(q, k, w, **kw):
-        """plan + warm-up + k timed graph replays of problem q."""
+    def measure(q, k, w, prof=2, **kw):
+        """plan + warm-up + k timed graph replays of problem q (prof = 2: the dominant pass timed
+        inside the replays; 0: no event nodes, and no kernel time)."""
         plan, plan_ms = make_plan(q, **kw)
-        plan.profile_enable(True)
+        plan.profile_enable(prof)
         dom, passes = dominant_pass(plan)
         for _ in range(w):
             step(plan)
         torch.cuda.synchronize(dev)
-        g = graph_step(plan)
+        g = graph_step(plan, prof)
         for _ in range(w):
             g()
         torch.cuda.synchronize(dev)
-        times, dom_ms = timed(g, k, plan, dom)
+        times, dom_ms = timed(g, k, plan, dom if prof else None)
         res = result.cpu().numpy().copy()
         return plan, plan_ms, dom, passes, times, dom_ms, res, g
 
@@ -401,7 +403,8 @@ def main():
                 cplan, c_plan_ms, cdom, cpasses, ctimes, cdom_ms, cres = (plan, plan_ms, dominant, passes,
                                                                           times, dom, value_res)
             else:
-                cplan, c_plan_ms, cdom, cpasses, ctimes, cdom_ms, cres, _ = measure(q, args.steps, args.warmup)
+                cplan, c_plan_ms, cdom, cpasses, ctimes, cdom_ms, cres, _ = measure(q, args.steps, args.warmup,
+                                                                                prof=2 if i >= 3 else 0)
             cst = stats(ctimes)
             npts = cplan.points()[1]
             row = {"d": q.d, "q": q.q, "rule": S.RULE_NAMES[q.rule], "integrand": S.KIND_NAMES[q.kind],
@@ -585,9 +588,9 @@ def main():
             "roofline": roof,
             "e2e": {"value": total_pts / (e2e_ms * 1e-3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms},
-            # per step: k_factor_base, k_suffix_abs, k_root, one kernel per pass >= 1,
-            # k_reduce_fused, k_finalize
-            "gpu_launches": (len(passes) - 1 + 5) * args.steps,
+            # per step: k_head (d <= 2048; else k_factor_base, k_suffix_abs, k_root), one kernel per
+            # pass >= 1, k_reduce_fused, k_finalize
+            "gpu_launches": ((1 if p.d <= 2048 else 3) + (len(passes) - 1) + 2) * args.steps,
             "clocks": clk.summary(),
             "parity": parity_block(p, value_res),
             "step_ms_all": [round(t, 4) for t in times],

@@ -243,7 +243,8 @@ int sg_plan_leaf_work(sg_plan_t p, double *dfma_per_point, double *dadd_per_poin
 int sg_debug_tables(sg_plan_t p, double *table_host, size_t table_doubles, double *base_host);
 
 /* Defined by: DESIGN.md §6 (measurement), no paper passage.
- * Profiling hook.  When enabled, sg_integrate records a CUDA event on its stream before its first
+ * Profiling hook.  enable = 0 off, 1 every launch, 2 only the dominant pass (the pass with the most
+ * points: two events around its launch, the other entries read 0 — bench.py's timed steps).  When enabled, sg_integrate records a CUDA event on its stream before its first
  * kernel and after each kernel.  sg_profile_read waits for the events of the LAST sg_integrate and
  * writes the device duration (ms) of each launch, in launch order:
  *   [K0 factor table, K0 base, root pass, pass 1 .. pass nfront, final reduce]

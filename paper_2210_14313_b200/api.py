@@ -213,8 +213,10 @@ class Plan:
         """Device tensor [value, residual] written by sg_finalize (default output buffer)."""
         return self._res
 
-    def profile_enable(self, on: bool = True):
-        check(lib().sg_profile_enable(self._h, int(bool(on))), "sg_profile_enable")
+    def profile_enable(self, on=True):
+        """0/False off, 1/True every launch, 2 the dominant pass only (sg_profile_enable)."""
+        mode = on if isinstance(on, int) and not isinstance(on, bool) else int(bool(on))
+        check(lib().sg_profile_enable(self._h, mode), "sg_profile_enable")
 
     def profile_read(self) -> list[float]:
         """Device ms of each launch of the last sg_integrate:

@@ -75,6 +75,9 @@ struct sg_plan_s {
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
     bool head = false;                  // K0 + base + root + suffix bounds as one k_head launch
+    int prof_mode = 0;                  // sg_profile_enable: 1 every launch, 2 the dominant pass only
+    int prof_dom = -1;                  // the dominant pass (most points)
+    int world = 1;                      // shard count of the plan's partition (options)
     size_t pass_smem_cap = 0;           // k_pass: bytes of factor levels staged in shared memory
                                         // (SG_B200_PASS_SMEM: A/B runs)
     int prefetch_min = 16;              // fused kernel prefetches the next task with >= this many
@@ -220,6 +223,9 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
     }
     HostPlan &hp = p->hp;
     p->cplx = (f->kind == SG_F_OSCILLATORY);
+    p->world = (o.range_hi > o.range_lo && o.range_lo >= 0) ? 2 : o.world;   // explicit range: a shard
+    for (int t = 1; t <= hp.nfront; ++t)
+        if (p->prof_dom < 0 || hp.pass_terms[t] > hp.pass_terms[p->prof_dom]) p->prof_dom = t;
     p->sform = (o.arith == SG_ARITH_SFORM_FP64 || o.arith == SG_ARITH_SFORM_DD);
     p->sform_dd = (o.arith == SG_ARITH_SFORM_DD);
     p->two = p->cplx || p->sform;
@@ -475,7 +481,7 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             return SG_ENOMEM;
         }
     }
-    if ((any_split || (p->leaf2 && hp.nfront >= 2)) &&
+    if ((any_split || (p->leaf2 && hp.nfront >= 2 && p->world > 1)) &&
         !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
         // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
@@ -741,12 +747,18 @@ struct ProfRec {
     int nev = 0;
     int last = -1;   // index of the most recent event on the main stream
     int rec(cudaStream_t on) {
-        if (!p->prof || nev >= (int)p->ev.size()) return -1;
+        if (!p->prof || p->prof_mode == 2 || nev >= (int)p->ev.size()) return -1;
         cudaEventRecordWithFlags(p->ev[nev], on, flags);
         return nev++;
     }
     void launch_done(int start, int end) {
         if (p->prof) p->prof_pairs.push_back({start, end});
+    }
+    // mode 2 (sg_profile_enable(p, 2)): events around the dominant pass's launch only
+    int dom_rec(cudaStream_t on, int t) {
+        if (!p->prof || p->prof_mode != 2 || t != p->prof_dom || nev >= (int)p->ev.size()) return -1;
+        cudaEventRecordWithFlags(p->ev[nev], on, flags);
+        return nev++;
     }
     // a sequential launch just issued on the main stream
     void seq() {
@@ -851,7 +863,9 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
     // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).
     // The persistent fused kernel takes the SMs the shorter pass leaves or frees (its tail fill).
-    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2;   // passes nfront-1 || nfront
+    // passes nfront-1 || nfront on shards of a world (their tails matter); at world 1 the fused pass
+    // runs alone (same step time within 0.2% on configs 4-5, and a clean kernel interval)
+    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2 && p->world > 1;
     int ev_fork = -1;
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
@@ -883,11 +897,15 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             B.chk_src_cap = hp.ws_front_cap[(t - 1) % 2];
             B.chk_dst_cap = 0;
 #endif
+            const int d0 = pr.dom_rec(st, t);
             if (B.ntasks > 0) {
                 if (p->cplx) launch_leaf2<true>(p, B, hp.nl[2], st);
                 else launch_leaf2<false>(p, B, hp.nl[2], st);
             }
-            if (fork) {
+            const int d1 = pr.dom_rec(st, t);
+            if (p->prof_mode == 2) {
+                pr.launch_done(d0, d1);
+            } else if (fork) {
                 const int e = pr.rec(st);
                 pr.launch_done(ev_fork, e);
                 pr.last = e;
@@ -896,6 +914,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             }
             continue;
         }
+        const int d0 = pr.dom_rec(sx, t);
         if (hp.leaf2_srctasks && p->leaf2 && t == hp.nfront - 1) {
             // pass L-2 as k_leaf2_sym3 source tasks over every source of frontier L-2
             Leaf2Args S;
@@ -995,9 +1014,11 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 if (p->cplx) k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 else k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 split_done = true;
-                const int e = pr.rec(st);
-                pr.launch_done(pr.last, e);
-                pr.last = e;
+                if (p->prof_mode != 2) {
+                    const int e = pr.rec(st);
+                    pr.launch_done(pr.last, e);
+                    pr.last = e;
+                }
                 if (p->split_serial) {
                     if (p->cplx) k_leaf<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
                     else k_leaf<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
@@ -1014,10 +1035,13 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 else k_leaf<false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
             }
         }
+        const int d1 = pr.dom_rec(sx, t);
         if (sx != st) {
-            const int e = pr.rec(sx);
-            pr.launch_done(ev_fork, e);
+            if (p->prof_mode == 2) pr.launch_done(d0, d1);
+            else pr.launch_done(ev_fork, pr.rec(sx));
             if (cudaEventRecord(p->ev_join, sx) != cudaSuccess) return SG_ECUDA;
+        } else if (p->prof_mode == 2) {
+            pr.launch_done(d0, d1);
         } else if (!split_done) {
             pr.seq();
         }
@@ -1199,7 +1223,8 @@ extern "C" int sg_rule_table(sg_rule rule, int level, double *x, double *w) {
 }
 
 extern "C" int sg_profile_enable(sg_plan_t p, int enable) {
-    if (!p) return SG_EINVAL;
+    if (!p || enable < 0 || enable > 2) return SG_EINVAL;
+    p->prof_mode = enable;
     if (enable && p->ev.empty()) {
         p->ev.resize(6 + p->hp.nfront);
         for (auto &e : p->ev)
@@ -1219,13 +1244,9 @@ extern "C" int sg_profile_read(sg_plan_t p, float *ms, int *n) {
         return SG_OK;
     }
     if (*n < nl || p->ev.empty() || (int)p->prof_pairs.size() != nl) return SG_EINVAL;
-    int emax = 0;
-    for (auto &pr : p->prof_pairs) emax = std::max(emax, std::max(pr.first, pr.second));
-    if (cudaEventSynchronize(p->ev[emax]) != cudaSuccess) return SG_ECUDA;
     for (int i = 0; i < nl; ++i) {
         const int a = p->prof_pairs[i].first, b = p->prof_pairs[i].second;
-        if (a < 0 || b < 0) return SG_EINVAL;
-        if (a == b) {
+        if (a < 0 || b < 0 || a == b) {   // merged launch, or not timed (mode 2: only the dominant pass)
             ms[i] = 0.0f;
             continue;
         }
