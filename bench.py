@@ -265,6 +265,11 @@ def main():
     dist_on = world > 1 or args.force_dist
     if dist_on:
         if args.dist_backend == "nccl":
+            # NCCL's init lines (nRanks, NVLS / ring setup) on stderr, so a multi-GPU record can confirm
+            # the communicator; the JSON line stays the only stdout line of rank 0
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
@@ -583,6 +588,9 @@ def main():
                 "parallelism": f"dp{world} (depth-1 subtree shards)", "shard_points_rank0": shard_pts,
                 "collective": ("nccl all_gather_into_tensor" if dist_on and args.dist_backend == "nccl"
                                else "gloo (test aid)" if dist_on else "none (world 1)"),
+                "process_group": ({"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                                   "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                                   if args.dist_backend == "nccl" else None} if dist_on else None),
                 "launch": "stream launches" if args.no_graph else
                           "CUDA-graph replay of sg_integrate (+ sg_finalize)"}),
             "roofline": roof,

@@ -36,7 +36,8 @@ typedef enum {
     SG_OK = 0,
     SG_EINVAL = -1,        /* d < 1, q < d (BudgetTooSmall), NULL pointer, bad enum, non-finite
                               parameter, w missing for peak/gauss, rank/world/range inconsistent */
-    SG_EUNSUPPORTED = -2,  /* UnsupportedLevel: CC / trapezoidal max level L+1 > 12, GL n > 64,
+    SG_EUNSUPPORTED = -2,  /* UnsupportedLevel: CC max level L+1 > 12 (its weights cost O(n^2) quad
+                              cosines at plan time), trapezoidal L+1 > 20, GL n > 64,
                               Gauss-Patterson rule > 63 points, d > 2^20-1, L > 19 */
     SG_EOVERFLOW = -3,     /* a point or frontier count would reach 2^63 */
     SG_ENOMEM = -4,        /* device allocation failed, or workspace smaller than required */

@@ -269,7 +269,7 @@ int host_rule(int rule, int l, double *x, double *w) {
         if (l > SG_CC_MAX_LEVEL) return -1;
         cc_rule_q(n, x, w);
     } else if (rule == SG_RULE_TRAPEZOIDAL) {
-        if (l > SG_CC_MAX_LEVEL) return -1;
+        if (l > SG_TRAP_MAX_LEVEL) return -1;
         trap_rule_q(n, x, w);
     } else if (rule == SG_RULE_GAUSS_PATTERSON) {
         if (gp_index(l) > SG_GP_MAX_K) return -1;
@@ -309,8 +309,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
     hp.merge = merge;
     if (world < 1 || rank < 0 || rank >= world) return SG_EINVAL;
     if (d > SG_MAX_D || L > SG_MAX_L) return SG_EUNSUPPORTED;
-    if ((rule == SG_RULE_CLENSHAW_CURTIS || rule == SG_RULE_TRAPEZOIDAL) && L + 1 > SG_CC_MAX_LEVEL)
-        return SG_EUNSUPPORTED;
+    if (rule == SG_RULE_CLENSHAW_CURTIS && L + 1 > SG_CC_MAX_LEVEL) return SG_EUNSUPPORTED;
+    if (rule == SG_RULE_TRAPEZOIDAL && L + 1 > SG_TRAP_MAX_LEVEL) return SG_EUNSUPPORTED;
     if (rule == SG_RULE_GAUSS_PATTERSON && gp_index(L + 1) > SG_GP_MAX_K) return SG_EUNSUPPORTED;
     if (rule == SG_RULE_GAUSS_LEGENDRE && L + 1 > SG_GL_MAX_N) return SG_EUNSUPPORTED;
     hp.d = d;

@@ -16,7 +16,11 @@
 #include <vector>
 
 #define SG_MAX_L 19        // L + 1 <= 20 levels in the tables
-#define SG_CC_MAX_LEVEL 12 // CC weights are O(n^2) quad evaluations; n_12 = 2049
+#define SG_CC_MAX_LEVEL 12 // CC weights are O(n^2) quad cosines at plan time: level 12 (n = 2049)
+                           // takes ~2 s, level 13 ~8 s, level 20 (n = 524289) hours; the oracle's
+                           // independent generator has the same cost, so levels above 12 could
+                           // not be checked bit for bit either (SG_EUNSUPPORTED)
+#define SG_TRAP_MAX_LEVEL 20 // trapezoidal nodes / weights are exact dyadic rationals (O(n))
 #define SG_GL_MAX_N 64
 #define SG_GP_MAX_K 6      // Gauss-Patterson rules up to 2^6 - 1 = 63 points (levels <= 48)
 #define SG_MAX_D ((1 << 20) - 1)

@@ -43,7 +43,7 @@ def _rule(L, rule, level):
 
 
 @pytest.mark.parametrize("rule,levels", [(S.RULE_CC, range(1, 11)), (S.RULE_GL, range(1, 30)),
-                                         (S.RULE_TRAP, range(1, 13)), (S.RULE_GP, range(1, 30))])
+                                         (S.RULE_TRAP, range(1, 21)), (S.RULE_GP, range(1, 30))])
 def test_library_rules_bit_identical_to_oracle(L, rule, levels):
     for l in levels:
         rc, x, w = _rule(L, rule, l)
@@ -56,7 +56,8 @@ def test_library_rules_bit_identical_to_oracle(L, rule, levels):
 def test_rule_table_limits(L):
     assert _rule(L, S.RULE_CC, 13)[0] == -2    # SG_EUNSUPPORTED beyond CC level 12
     assert _rule(L, 5, 2)[0] == -1             # no rule 5: SG_EINVAL
-    assert _rule(L, S.RULE_TRAP, 13)[0] == -2  # trapezoid shares the CC level limit
+    assert _rule(L, S.RULE_TRAP, 20)[0] == (1 << 19) + 1   # trapezoid: exact dyadic tables to level 20
+    assert _rule(L, S.RULE_TRAP, 21)[0] == -2
     assert _rule(L, S.RULE_GP, 48)[0] == 63    # 63-point Patterson rule up to level 48
     assert _rule(L, S.RULE_GP, 49)[0] == -2
 

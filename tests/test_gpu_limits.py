@@ -75,3 +75,13 @@ def test_limits_rejected(api):
         with pytest.raises(SGError) as e:
             api.Plan(d, q, rule, S.KIND_EXP, np.full(d, 0.1))
         assert e.value.code == -2
+
+
+@pytest.mark.parametrize("d,L,kind", [(1, 19, S.KIND_OSC), (2, 15, S.KIND_GAUSS), (3, 12, S.KIND_EXP)])
+def test_trapezoid_up_to_level_20(api, d, L, kind):
+    """The trapezoidal rule's exact dyadic tables go to level 20 (n = 524289 nodes per row; the
+    Clenshaw-Curtis cap stays 12, include/sg_b200.h): tree and merged modes against the oracle."""
+    p = S.random_problem(120 + d, d, L, S.RULE_TRAP, kind)
+    ref = mp.mpf(oracle.integrate_problem(p, eval_mode=1).text)
+    assert rel(gpu(api, p), ref) <= HEALTH
+    assert rel(gpu(api, p, merge=api.MERGE_MIDPOINT), ref) <= HEALTH
