@@ -14,11 +14,7 @@ __device__ __forceinline__ int task_lo32(long long v) { return (int)(int32_t)(ui
 // may start while its predecessor in the stream finishes; it lets its own dependents launch at
 // once and waits for the predecessor's completion and memory before touching anything the
 // predecessor wrote.  Without the attribute both instructions are no-ops.
-#ifndef SG_NO_PDL_ENTRY
 #define SG_PDL_ENTRY() asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
-#else
-#define SG_PDL_ENTRY() ((void)0)
-#endif
 
 struct DevPlan {
     int d, L, kind, nfront;
