@@ -60,7 +60,6 @@ __device__ void collapse_tree(double2 *sre, double2 *sim, int L) {
 template <bool CPLX>
 __global__ void __launch_bounds__(COLLAPSE_THREADS) k_collapse_part(const DevPlan P, double2 *part_re,
                                                                      double2 *part_im) {
-    SG_PDL_ENTRY();
     extern __shared__ double2 csm[];
     const int L = P.L, n1 = L + 1, d = P.d;
     double2 *sre = csm, *sim = csm + COLLAPSE_THREADS * n1;
@@ -107,7 +106,6 @@ template <bool CPLX>
 __global__ void __launch_bounds__(COLLAPSE_THREADS) k_collapse_final(const DevPlan P, const double2 *part_re,
                                                                       const double2 *part_im, int nparts,
                                                                       int emit, double *out) {
-    SG_PDL_ENTRY();
     extern __shared__ double2 csm[];
     const int L = P.L, n1 = L + 1;
     double2 *sre = csm, *sim = csm + COLLAPSE_THREADS * n1;

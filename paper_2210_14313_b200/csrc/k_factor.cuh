@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(K0_THREADS) k_factor_base(const DevPlan P, int
 // turn is latency-bound; reverted.)
 #define SUFFIX_THREADS 1024
 __global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) {
-    SG_PDL_ENTRY();
     const int l = 2 + blockIdx.x;
     if (l > P.L + 1) return;
     const int d = P.d, n = P.nl[l];

@@ -5,7 +5,6 @@
 // One-block fixed-order reduction of per-block partials (+ the root point) -> out[0..1] (plain path).
 __global__ void __launch_bounds__(1024) k_reduce(const DevPlan P, const double2 *partials,
                                                  long long n, int include_root, double *out) {
-    SG_PDL_ENTRY();
     dd s = {0.0, 0.0};
     for (long long i = threadIdx.x; i < n; i += blockDim.x) s = dd_add(s, dd{partials[i].x, partials[i].y});
     s = block_reduce_dd<32>(s);
@@ -38,7 +37,6 @@ template <int SF>
 __global__ void __launch_bounds__(RED_THREADS)
 k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int include_root, double *out,
                double2 *l1, unsigned long long *ticket, unsigned long long *task_counters) {
-    SG_PDL_ENTRY();
     const long long b0 = (long long)blockIdx.x * RED_CHUNK2 + (long long)threadIdx.x * RED_PER_THREAD;
     double2 v[RED_PER_THREAD];
 #pragma unroll
@@ -87,7 +85,6 @@ k_reduce_fused(const DevPlan P, const double2 *partials, long long n, int includ
 
 // status = the plan's status words; status[1] holds the flag of the last completed sg_integrate
 __global__ void k_finalize(const double *gathered, int world, const int *status, double *result) {
-    SG_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     dd s = {0.0, 0.0};
     for (int r = 0; r < world; ++r) s = dd_add(s, dd{gathered[2 * r], gathered[2 * r + 1]});

@@ -131,7 +131,6 @@ __device__ __forceinline__ dd sform_value(const DevPlan &P, dd arg) {
 
 template <bool DDS>
 __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs R) {
-    SG_PDL_ENTRY();
     const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     dd tot = {0.0, 0.0};
     if (r1 < R.hi) {
@@ -164,7 +163,6 @@ __global__ void __launch_bounds__(256) k_root_s(const DevPlan P, const RootArgs 
 
 template <bool DDS, bool WRITE>
 __global__ void __launch_bounds__(PASS_THREADS) k_pass_s(const DevPlan P, const PassArgs A) {
-    SG_PDL_ENTRY();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
     dd tot = {0.0, 0.0};

@@ -47,7 +47,6 @@ __device__ __forceinline__ dd root_node(const DevPlan &P, const RootArgs &R, lon
 
 template <bool CPLX>
 __global__ void __launch_bounds__(256) k_root(const DevPlan P, const RootArgs R) {
-    SG_PDL_ENTRY();
     const long long r1 = R.lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     dd s = block_reduce_dd<8>(root_node<CPLX>(P, R, r1));
     if (threadIdx.x == 0) SG_PART(R.partials, blockIdx.x) = make_double2(s.hi, s.lo);
@@ -266,7 +265,6 @@ __device__ __forceinline__ void pass_level_sym(const DevPlan &P, const PassArgs 
 #endif
 template <bool CPLX, bool WRITE>
 __global__ void __launch_bounds__(PASS_THREADS, PASS_MINB) k_pass(const DevPlan P, const PassArgs A) {
-    SG_PDL_ENTRY();
     // factor levels 2 .. A.stage_lmax staged in shared memory (same layout as the table: level l at
     // tab_off[l] - tab_off[2]); the row loads of the level loop then cost shared-memory latency
     // instead of an L1/L2 round trip per row (ncu r02p: long-scoreboard stalls on those loads were the
@@ -481,7 +479,6 @@ __device__ __forceinline__ dd leaf_level_sym(const double2 *Fr, const double2 *F
 // k' = d-1 (its effective last coordinate becomes max(k, d-2)).
 template <bool CPLX, bool SKIPW = false>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF_MINB) k_leaf(const DevPlan P, const PassArgs A) {
-    SG_PDL_ENTRY();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * WPB + wib;
     dd tot = {0.0, 0.0};
@@ -683,7 +680,6 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
 // row loads are broadcast LDS instead of LDG through the L1 data path.
 template <bool CPLX, int NJ, bool SMEM>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPlan P, const PassArgs A) {
-    SG_PDL_ENTRY();
     extern __shared__ double2 fsm[];
     const int wib = threadIdx.x >> 5;
     const double2 *Fr = P.Fre + P.tab_off[2];
@@ -849,7 +845,6 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
 // fills its lanes.  G = 1 is the lane = parent mapping (every k_mid of the task on every lane).
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false, int G = 1>
 __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
-    SG_PDL_ENTRY();
     extern __shared__ double2 fsm[];
     static_assert(G == 1 || G == 2 || G == 4 || G == 8, "lane groups");
     constexpr int PCH = 32 / G;   // parents per task chunk
@@ -1060,7 +1055,6 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 #endif
 template <int PPL, bool SMEM>
 __global__ void __launch_bounds__(PASS_THREADS, LEAF2_PAIRS_MINB) k_leaf2_pairs(const DevPlan P, const Leaf2Args A) {
-    SG_PDL_ENTRY();
     constexpr int NM = 2 * PPL;   // mid prefixes per lane
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31;
@@ -1375,7 +1369,6 @@ __device__ __forceinline__ dd sym3_task(const DevPlan &P, const Leaf2Args &A, co
 // sharing one kernel slowed the fused tasks by 1.6-4% through code layout alone).
 template <int PPL, bool SMEM, bool CZ, bool SRC, int L3S = 0>
 __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const DevPlan P, const Leaf2Args A) {
-    SG_PDL_ENTRY();
     constexpr int NM = 3 * PPL;   // mid prefixes per lane
     extern __shared__ double2 fsm[];
     const int lane = threadIdx.x & 31;
@@ -1489,7 +1482,6 @@ __device__ __forceinline__ dd front_product(const dd &pr, const dd &pim, const d
 template <bool CPLX>
 __global__ void __launch_bounds__(FRONT_THREADS) k_front(const DevPlan P, const PassArgs A, const FrontChunk *chunks,
                                                          long long nchunks) {
-    SG_PDL_ENTRY();
     const int d = P.d, L = P.L;
     __shared__ long long cnext;
     for (;;) {

@@ -124,7 +124,6 @@ __global__ void __launch_bounds__(128) k_eval_points(const DevPlan P, const Unra
 // iteration): thread g handles the flat indices g, g + G, g + 2G, ... of the shard (fixed order),
 // unranks each one and forms its term from its t factors; dd accumulation, fixed CTA reduction.
 __global__ void __launch_bounds__(256) k_plain(const DevPlan P, const UnrankTabs U, double2 *partials) {
-    SG_PDL_ENTRY();
     const unsigned long long G = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long g0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     double ah = 0.0, al = 0.0;

@@ -10,12 +10,6 @@
 __device__ __forceinline__ int task_hi32(long long v) { return (int)(int32_t)(uint32_t)((unsigned long long)v >> 32); }
 __device__ __forceinline__ int task_lo32(long long v) { return (int)(int32_t)(uint32_t)((unsigned long long)v & 0xffffffffull); }
 
-// Programmatic dependent launch: a kernel launched with the PDL attribute (sg_kernels.cu klaunch)
-// may start while its predecessor in the stream finishes; it lets its own dependents launch at
-// once and waits for the predecessor's completion and memory before touching anything the
-// predecessor wrote.  Without the attribute both instructions are no-ops.
-#define SG_PDL_ENTRY() asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
-
 struct DevPlan {
     int d, L, kind, nfront;
     int nl[SG_MAX_L + 3];

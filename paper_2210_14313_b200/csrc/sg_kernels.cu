@@ -75,8 +75,6 @@ struct sg_plan_s {
     int leaf2_threads = PASS_THREADS;   // CTA size of the persistent leaf launch
     int leaf2_l3s = 0;                  // level-3 row symmetry for the source tasks (0 / 1 / 2)
     bool head = false;                  // K0 + base + root + suffix bounds as one k_head launch
-    bool pdl = true;                    // programmatic dependent launch for the step's later kernels
-                                        // (SG_B200_NOPDL=1: plain stream order, A/B)
     int prof_mode = 0;                  // sg_profile_enable: 1 every launch, 2 the dominant pass only
     int prof_dom = -1;                  // the dominant pass (most points)
     int world = 1;                      // shard count of the plan's partition (options)
@@ -102,37 +100,6 @@ struct sg_plan_s {
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-// Launch with the programmatic-dependent-launch attribute (pdl): the kernel may be scheduled while
-// its stream predecessor finishes; the kernel's SG_PDL_ENTRY waits for the predecessor's completion
-// before reading its results.  Used for every kernel of a step after the first.
-template <typename... KArgs, typename... Args>
-static void klaunch(bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = g;
-    cfg.blockDim = b;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = pdl ? at : nullptr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k, args...);
-}
-static void klaunch_fn(bool pdl, const void *fn, dim3 g, dim3 b, size_t smem, cudaStream_t st, void **args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = g;
-    cfg.blockDim = b;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = pdl ? at : nullptr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelExC(&cfg, fn, args);
-}
 
 // Partial slots: the root's, then per pass t its pass_blocks[t] (twice for a split frontier pass).
 #define FRONT_GRID 148   // k_front CTAs (persistent, one per SM: A/B r02z serial 148 -> 1.45 ms, 592 -> 1.65 ms)
@@ -386,7 +353,6 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         return SG_ECUDA;
     }
     if (const char *e = getenv("SG_B200_PREFETCH_MIN"); e && e[0]) p->prefetch_min = atoi(e);
-    if (const char *e = getenv("SG_B200_NOPDL"); e && e[0] == '1') p->pdl = false;
     {
         // Split frontier passes (factor form): a pass that stores more than FRONT_SPLIT_MIN_BYTES of
         // frontier records runs as a write-only k_pass (the stored children, their terms from the
@@ -717,7 +683,7 @@ static void launch_leaf2(sg_plan_s *p, const Leaf2Args &A, int nj, cudaStream_t 
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
-    klaunch_fn(p->pdl, fn, dim3(grid), dim3(p->leaf2_threads), sm, st, args);
+    cudaLaunchKernel(fn, dim3(grid), dim3(p->leaf2_threads), args, sm, st);
 }
 
 static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) {
@@ -727,7 +693,7 @@ static void launch_leaf2_src(sg_plan_s *p, const Leaf2Args &A, cudaStream_t st) 
     DevPlan dp = p->dp;
     Leaf2Args a = A;
     void *args[] = {&dp, &a};
-    klaunch_fn(p->pdl, fn, dim3(grid), dim3(SYM3_THREADS), sm, st, args);
+    cudaLaunchKernel(fn, dim3(grid), dim3(SYM3_THREADS), args, sm, st);
 }
 
 template <bool CPLX>
@@ -735,11 +701,11 @@ static void launch_leaf1(sg_plan_s *p, const PassArgs &A, int nj, cudaStream_t s
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
     if (nj == 3) {
-        if (sm) klaunch(p->pdl, k_leaf1<CPLX, 3, true>, grid, PASS_THREADS, sm, st, p->dp, A);
-        else klaunch(p->pdl, k_leaf1<CPLX, 3, false>, grid, PASS_THREADS, 0, st, p->dp, A);
+        if (sm) k_leaf1<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 3, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
     } else {
-        if (sm) klaunch(p->pdl, k_leaf1<CPLX, 2, true>, grid, PASS_THREADS, sm, st, p->dp, A);
-        else klaunch(p->pdl, k_leaf1<CPLX, 2, false>, grid, PASS_THREADS, 0, st, p->dp, A);
+        if (sm) k_leaf1<CPLX, 2, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 2, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
     }
 }
 
@@ -876,23 +842,21 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     } else {
         // K0 (factor table + base), then the suffix bounds of |F|
         if (p->sform) {
-            // the step's first kernel: never a programmatic launch (it would overlap the previous step)
             if (p->sform_dd) k_factor_base_s<true><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
             else k_factor_base_s<false><<<nfb + 1, K0_THREADS, 0, st>>>(dp, nfb);
         } else {
             launch_factor_base(dp, nfb, st);
-            if (hp.tab_entries > 0) klaunch(p->pdl, k_suffix_abs, dim3(hp.L), dim3(SUFFIX_THREADS), 0, st, dp);
+            if (hp.tab_entries > 0) k_suffix_abs<<<hp.L, SUFFIX_THREADS, 0, st>>>(dp);
         }
         pr.seq();
         pr.launch_done(pr.last, pr.last);   // K0 base: merged into the factor launch
         // root pass
         if (p->sform)
-            klaunch(p->pdl, p->sform_dd ? k_root_s<true> : k_root_s<false>, dim3((unsigned)hp.root_blocks), dim3(256), 0,
-                    st, dp, R);
+            (p->sform_dd ? k_root_s<true> : k_root_s<false>)<<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
         else if (p->cplx)
-            klaunch(p->pdl, k_root<true>, dim3((unsigned)hp.root_blocks), dim3(256), 0, st, dp, R);
+            k_root<true><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
         else
-            klaunch(p->pdl, k_root<false>, dim3((unsigned)hp.root_blocks), dim3(256), 0, st, dp, R);
+            k_root<false><<<(unsigned)hp.root_blocks, 256, 0, st>>>(dp, R);
         pr.seq();
     }
     // Fused plans: pass nfront-1 writes no frontier (its children are the fused kernel's business),
@@ -1016,11 +980,11 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
             const bool single = !write && t == p->leaf1_t;
             if (p->sform) {
                 if (p->sform_dd) {
-                    if (write) klaunch(p->pdl, k_pass_s<true, true>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
-                    else klaunch(p->pdl, k_pass_s<true, false>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
+                    if (write) k_pass_s<true, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                    else k_pass_s<true, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
                 } else {
-                    if (write) klaunch(p->pdl, k_pass_s<false, true>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
-                    else klaunch(p->pdl, k_pass_s<false, false>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
+                    if (write) k_pass_s<false, true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
+                    else k_pass_s<false, false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
                 }
             } else if (write && hp.pass_split[t] && p->side != nullptr) {
                 // split frontier pass: write-only k_pass here, leaf-only k_leaf on the side stream
@@ -1044,11 +1008,11 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                 // (SG_B200_SPLIT_SERIAL=1: the clean frontier-kernel time of bench.py's frontier leg):
                 // k_leaf follows on this stream and falls into the next launch's interval.
                 if (!p->split_serial) {
-                    if (p->cplx) klaunch(p->pdl, k_leaf<true, true>, dim3(grid), dim3(PASS_THREADS), 0, p->side, dp, A2);
-                    else klaunch(p->pdl, k_leaf<false, true>, dim3(grid), dim3(PASS_THREADS), 0, p->side, dp, A2);
+                    if (p->cplx) k_leaf<true, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
+                    else k_leaf<false, true><<<grid, PASS_THREADS, 0, p->side>>>(dp, A2);
                 }
-                if (p->cplx) klaunch(p->pdl, k_front<true>, dim3(p->front_grid), dim3(FRONT_THREADS), 0, st, dp, A, runs, nr);
-                else klaunch(p->pdl, k_front<false>, dim3(p->front_grid), dim3(FRONT_THREADS), 0, st, dp, A, runs, nr);
+                if (p->cplx) k_front<true><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
+                else k_front<false><<<p->front_grid, FRONT_THREADS, 0, st>>>(dp, A, runs, nr);
                 split_done = true;
                 if (p->prof_mode != 2) {
                     const int e = pr.rec(st);
@@ -1056,19 +1020,19 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
                     pr.last = e;
                 }
                 if (p->split_serial) {
-                    if (p->cplx) klaunch(p->pdl, k_leaf<true, true>, dim3(grid), dim3(PASS_THREADS), 0, st, dp, A2);
-                    else klaunch(p->pdl, k_leaf<false, true>, dim3(grid), dim3(PASS_THREADS), 0, st, dp, A2);
+                    if (p->cplx) k_leaf<true, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
+                    else k_leaf<false, true><<<grid, PASS_THREADS, 0, st>>>(dp, A2);
                 }
                 if (cudaEventRecord(p->ev_join, p->side) != cudaSuccess) return SG_ECUDA;
                 if (cudaStreamWaitEvent(st, p->ev_join, 0) != cudaSuccess) return SG_ECUDA;
             } else if (p->cplx) {
-                if (write) klaunch(p->pdl, k_pass<true, true>, dim3(grid), dim3(PASS_THREADS), pass_smem, sx, dp, A);
+                if (write) k_pass<true, true><<<grid, PASS_THREADS, pass_smem, sx>>>(dp, A);
                 else if (single) { if (A.ntasks > 0) launch_leaf1<true>(p, A, n2, sx); }
-                else klaunch(p->pdl, k_leaf<true>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
+                else k_leaf<true><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
             } else {
-                if (write) klaunch(p->pdl, k_pass<false, true>, dim3(grid), dim3(PASS_THREADS), pass_smem, sx, dp, A);
+                if (write) k_pass<false, true><<<grid, PASS_THREADS, pass_smem, sx>>>(dp, A);
                 else if (single) { if (A.ntasks > 0) launch_leaf1<false>(p, A, n2, sx); }
-                else klaunch(p->pdl, k_leaf<false>, dim3(grid), dim3(PASS_THREADS), 0, sx, dp, A);
+                else k_leaf<false><<<grid, PASS_THREADS, 0, sx>>>(dp, A);
             }
         }
         const int d1 = pr.dom_rec(sx, t);
@@ -1087,7 +1051,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
         const long long nl1 = std::max<long long>(1, (hp.total_partials + RED_CHUNK2 - 1) / RED_CHUNK2);
         double2 *l1 = (double2 *)(p->ws + p->ws_red_off);
         auto red = dp.sform == 2 ? k_reduce_fused<2> : dp.sform == 1 ? k_reduce_fused<1> : k_reduce_fused<0>;
-        klaunch(p->pdl, red, dim3((unsigned)nl1), dim3(RED_THREADS), 0, st, dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev,
+        red<<<(unsigned)nl1, RED_THREADS, 0, st>>>(dp, partials, hp.total_partials, hp.include_root ? 1 : 0, out_dev,
                                                   l1, p->d_counter + 1, p->d_counter);
     }
     {
@@ -1102,7 +1066,7 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
 extern "C" int sg_finalize(sg_plan_t p, sg_stream_t s, const double *gathered_dev, int world,
                            double *result_dev) {
     if (!p || !gathered_dev || !result_dev || world < 1) return SG_EINVAL;
-    klaunch(p->pdl, k_finalize, dim3(1), dim3(32), 0, (cudaStream_t)s, gathered_dev, world, p->dp.status, result_dev);
+    k_finalize<<<1, 32, 0, (cudaStream_t)s>>>(gathered_dev, world, p->dp.status, result_dev);
     if (cudaGetLastError() != cudaSuccess) return SG_ECUDA;
     return SG_OK;
 }
