@@ -63,3 +63,17 @@ def test_fuzz_vs_oracle(api, seed, d, L, rule, kind, mode):
     ref = mp.mpf(oracle.integrate_problem(p, eval_mode=1).text)
     r = rel(mp.mpf(hi) + mp.mpf(lo), ref)
     assert r <= HEALTH, (p.name, mode, float(r))
+
+
+def test_fuzz_all_paths_and_switches():
+    """tools/fuzz_all.py: 40 seeded cases over every rule, kind, form, merge / collapse / dd s-form,
+    shard world and plan switch (split frontier passes, lane groups, unfused, generic leaf, the
+    three-launch head) against the oracle at 1e-15 (the 300-case sweep: profiles/r02F_fuzz_all_300.txt)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_all.py"), "40", "3"], cwd=root,
+                         capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "failures=0" in out.stdout
