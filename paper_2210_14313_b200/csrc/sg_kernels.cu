@@ -365,6 +365,10 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
         for (int t = 1; t < hp.nfront; ++t) {
             const bool writes = !(hp.fuse && t + 1 == hp.nfront);
             const bool big = (double)hp.pass_written[t] * rec >= FRONT_SPLIT_MIN_BYTES;
+            // k_front indexes a source inside its segment with an int (FrontChunk::i0)
+            bool fits = true;
+            for (size_t q = 0; q < hp.N[t].size(); ++q) fits = fits && hp.N[t][q] < INT_MAX;
+            if (!fits) continue;
             hp.pass_split[t] = (!p->sform && writes && (force == 1 || (force != 0 && big))) ? 1 : 0;
         }
         // k_front chunks of the split passes (heavy-first: work ~ sources x rows x stored nodes)
