@@ -737,8 +737,16 @@ struct Leaf2Args {
 #ifndef LEAF2_ROWS_CPLX
 #define LEAF2_ROWS_CPLX 4   // rows per iteration, oscillatory (A/B on config 5: 4 = 6 = 8 > 2 > 1)
 #endif
+// Real kinds: ONE CTA of 24 warps per SM (80 registers), not three CTAs of 8.  With three, the warp
+// schedulers' age priority starves the youngest CTA of every SM (tools/tail_profile.py, config 4 at
+// N = 1: rows per warp 9925 / 2625 / 810 by CTA age) and its warps, still holding early-claimed tasks
+// when the list runs dry, finish alone over the last 8% (N = 1) to 20% (N = 8) of the launch; in one
+// CTA the 24 warps share the pipe evenly (rows per warp 4212-4756, warp-busy 0.947 -> 0.994).
 #ifndef LEAF2_MINB
-#define LEAF2_MINB 3        // CTAs/SM bound, real kinds (80 regs)
+#define LEAF2_MINB 1        // CTAs/SM bound, real kinds
+#endif
+#ifndef LEAF2_REAL_THREADS
+#define LEAF2_REAL_THREADS 768   // k_leaf2 CTA size, real kinds
 #endif
 #ifndef LEAF2_MINB_CPLX
 #define LEAF2_MINB_CPLX 2   // CTAs/SM bound, oscillatory (108 regs, 16 warps/SM: 26.14 ms vs 27.52)
@@ -843,8 +851,25 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
 // k_mid group lane / (32/G)); group g walks the task's k_mids ka + g, ka + g + G, ... < kb (rows
 // [max(k_mid + 1, kp0), kp1) each), so a shard with few parents (config 4 on 8 GPUs: 132 on rank 0)
 // fills its lanes.  G = 1 is the lane = parent mapping (every k_mid of the task on every lane).
+#ifdef SG_TAILPROF
+// experiment build only (-DSG_TAILPROF, tools/tail_profile.py): per-warp start / exit times (globaltimer,
+// ns), SM id and task count of the persistent fused kernel
+#define TAILPROF_MAX 16384
+__device__ unsigned long long g_tp_t0[TAILPROF_MAX], g_tp_t1[TAILPROF_MAX];
+__device__ unsigned g_tp_sm[TAILPROF_MAX], g_tp_n[TAILPROF_MAX], g_tp_rows[TAILPROF_MAX];
+__device__ __forceinline__ unsigned long long tp_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned tp_smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#endif
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false, int G = 1>
-__global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
+__global__ void __launch_bounds__(CPLX ? PASS_THREADS : LEAF2_REAL_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];
     static_assert(G == 1 || G == 2 || G == 4 || G == 8, "lane groups");
     constexpr int PCH = 32 / G;   // parents per task chunk
@@ -864,6 +889,11 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         Fi = CPLX ? fsm + n : nullptr;
     }
     (void)wib;
+#ifdef SG_TAILPROF
+    const int tp_w = (int)(blockIdx.x * (blockDim.x >> 5) + wib);
+    const unsigned long long tp_start = tp_now();
+    unsigned tp_tasks = 0, tp_rows = 0;
+#endif
 #if LEAF2_PREFETCH
     // software-pipelined task fetch: the next task's index and descriptor are requested before the
     // current task's rows run, so their latency (atomic + L2 loads) is hidden behind the FP64 work
@@ -905,6 +935,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
 #endif
         const int ka = task_hi32(kk), kb = task_lo32(kk);
         const int kp0 = task_hi32(rr), kp1 = task_lo32(rr);
+#ifdef SG_TAILPROF
+        ++tp_tasks;
+#endif
         const long long i = first + plane;
         dd pr = {0.0, 0.0}, pim = {0.0, 0.0};
         if (i < A.Cmid[kb - 1]) {   // Cmid is nondecreasing: valid for the last k_mid
@@ -972,6 +1005,9 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
             SG_CHK(km, d - 1, 6);                               // mid row (its factors, Cmid, SA)
             SG_CHK(kp1 - 1, d, 5);                              // last leaf row of the table slice
             int kp = max(km + 1, kp0);
+#ifdef SG_TAILPROF
+            tp_rows += (unsigned)max(0, kp1 - kp);
+#endif
             while (kp < kp1) {
                 const int ke = min(kp1, kp + FOLD);
                 constexpr int RW = CPLX ? LEAF2_ROWS_CPLX : LEAF2_ROWS;
@@ -1031,6 +1067,15 @@ __global__ void __launch_bounds__(PASS_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_M
         rr = nrr;
 #endif
     }
+#ifdef SG_TAILPROF
+    if (lane == 0 && tp_w < TAILPROF_MAX) {
+        g_tp_t0[tp_w] = tp_start;
+        g_tp_t1[tp_w] = tp_now();
+        g_tp_sm[tp_w] = tp_smid();
+        g_tp_n[tp_w] = tp_tasks;
+        g_tp_rows[tp_w] = tp_rows;
+    }
+#endif
 }
 
 
@@ -1385,6 +1430,10 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
         Fr = fsm;
         Fi = fsm + n;
     }
+#ifdef SG_TAILPROF
+    const unsigned long long tp_start = tp_now();
+    unsigned tp_tasks = 0;
+#endif
     auto fetch = [&]() -> long long {
         unsigned long long u = 0;
         if (lane == 0) u = atomicAdd(A.counter, 1ull);
@@ -1431,11 +1480,24 @@ __global__ void __launch_bounds__(SYM3_THREADS, SYM3_MINB) k_leaf2_sym3(const De
                 nrr = A.T2[3 * next + 2];
             }
         }
+#ifdef SG_TAILPROF
+        ++tp_tasks;
+#endif
         task = next;
         first = nfirst;
         kk = nkk;
         rr = nrr;
     }
+#ifdef SG_TAILPROF
+    const int tp_w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    if (!SRC && lane == 0 && tp_w < TAILPROF_MAX) {
+        g_tp_t0[tp_w] = tp_start;
+        g_tp_t1[tp_w] = tp_now();
+        g_tp_sm[tp_w] = tp_smid();
+        g_tp_n[tp_w] = tp_tasks;
+        g_tp_rows[tp_w] = 0;
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -861,6 +861,59 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             if (a.kp0 != b.kp0) return a.kp0 < b.kp0;
             return a.first < b.first;
         });
+        // Guided tail (guided self-scheduling on the fixed list): a task claimed when work W_rem
+        // (itself and everything after it) is left is cut to at most LEAF2_GUIDE x W_rem / resident
+        // warps rows (>= LEAF2_MIN_PIECE), so the tasks in flight when the list runs dry are short.
+        // Measured (tools/tail_profile.py, config 4): without it the warps exit over the last 8% of
+        // the launch at N = 1 and 25% at N = 8 — the youngest CTA of each SM is starved by the
+        // scheduler's age priority and still holds a full task when the list empties.  Single-k_mid
+        // tasks split by rows, grouped tasks by k_mid blocks; pieces stay in list order.
+        if (LEAF2_GUIDE > 0.0) {
+            double guide = LEAF2_GUIDE;
+            if (const char *e = getenv("SG_B200_GUIDE"); e && e[0]) guide = atof(e);   // A/B runs
+            // resident warps of the kernel that runs the list: 8 / SM (k_leaf2_sym3, k_leaf2_pairs:
+            // one 8-warp CTA), 16 (k_leaf2, oscillatory), 24 (k_leaf2, real kinds)
+            const double W = hp.leaf2_ppl > 1 ? 148.0 * 8 : kind == SG_F_OSCILLATORY ? 148.0 * 16 : 148.0 * 24;
+            std::vector<Task> rev;
+            rev.reserve(tasks.size() + tasks.size() / 4);
+            double rem = 0.0;
+            for (size_t ii = tasks.size(); ii-- > 0;) {
+                const Task &tk = tasks[ii];
+                rem += (double)tk.rows;
+                const int64_t cap = std::max<int64_t>(LEAF2_MIN_PIECE, (int64_t)(guide * rem / W));
+                if (guide <= 0.0 || tk.rows <= cap) {
+                    rev.push_back(tk);
+                    continue;
+                }
+                std::vector<Task> pcs;
+                if (tk.kb - tk.ka <= G) {
+                    // one k_mid block: rows [max(ka + 1, kp0), kp1) of its first group in pieces
+                    const int r0 = std::max(tk.ka + 1, tk.kp0), r1 = std::min(tk.kp1, d);
+                    const int nr = r1 - r0;
+                    const int pieces = (int)std::min<int64_t>(nr, (nr + cap - 1) / cap);
+                    for (int q = 0; q < pieces; ++q) {
+                        const int a = r0 + (int)((int64_t)nr * q / pieces);
+                        const int b = r0 + (int)((int64_t)nr * (q + 1) / pieces);
+                        pcs.push_back(Task{b - a, tk.first, tk.ka, tk.kb, a, b});
+                    }
+                } else {
+                    // k_mid blocks of G (the first group's rows d - 1 - km per block), cut greedily
+                    int ka = tk.ka;
+                    int64_t acc = 0;
+                    for (int km = tk.ka; km < tk.kb; km += G) {
+                        acc += d - 1 - km;
+                        const int nx = std::min(km + G, tk.kb);
+                        if (acc >= cap || nx >= tk.kb) {
+                            pcs.push_back(Task{acc, tk.first, ka, nx, tk.kp0, tk.kp1});
+                            acc = 0;
+                            ka = nx;
+                        }
+                    }
+                }
+                for (size_t q = pcs.size(); q-- > 0;) rev.push_back(pcs[q]);
+            }
+            tasks.assign(rev.rbegin(), rev.rend());
+        }
         if (const char *dbg = getenv("SG_B200_DEBUG_TASKS"); dbg && dbg[0] == '1') {
             // list schedule of the sorted tasks on the resident warps (cost = rows + 2 per k_mid of the
             // task's group for its prologue): makespan against the perfect balance (tail loss)

@@ -663,7 +663,9 @@ static int setup_leaf1(sg_plan_s *p) {
                              (int)p->leaf1_smem) != cudaSuccess)
         return SG_ECUDA;
     // k_leaf2_sym3 has its own CTA size; every other leaf kernel runs PASS_THREADS
-    p->leaf2_threads = (p->leaf2 && p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2) ? SYM3_THREADS : PASS_THREADS;
+    p->leaf2_threads = (p->leaf2 && p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2) ? SYM3_THREADS
+                       : (p->leaf2 && !p->cplx)                                       ? LEAF2_REAL_THREADS
+                                                                                      : PASS_THREADS;
     const int wpb = p->leaf2_threads / 32;
     int per_sm = 0, dev = 0, sms = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->leaf2_threads, p->leaf1_smem) != cudaSuccess ||
@@ -1366,6 +1368,21 @@ extern "C" int sg_chk_end(sg_plan_t p, long long *out) {
     for (int i = 0; i < 4; ++i) out[1 + i] = st.first[i];
     out[5] = bad;
     out[6] = st.nslots;
+    return SG_OK;
+}
+#endif
+
+#ifdef SG_TAILPROF
+// experiment build only: copy the per-warp records of the last k_leaf2 launch (n <= TAILPROF_MAX)
+extern "C" int sg_tailprof_read(unsigned long long *t0, unsigned long long *t1, unsigned *sm, unsigned *ntask,
+                                unsigned *kmids, int n) {
+    if (n > TAILPROF_MAX || cudaDeviceSynchronize() != cudaSuccess) return SG_EINVAL;
+    if (cudaMemcpyFromSymbol(t0, g_tp_t0, sizeof(unsigned long long) * n) != cudaSuccess ||
+        cudaMemcpyFromSymbol(t1, g_tp_t1, sizeof(unsigned long long) * n) != cudaSuccess ||
+        cudaMemcpyFromSymbol(sm, g_tp_sm, sizeof(unsigned) * n) != cudaSuccess ||
+        cudaMemcpyFromSymbol(ntask, g_tp_n, sizeof(unsigned) * n) != cudaSuccess ||
+        cudaMemcpyFromSymbol(kmids, g_tp_rows, sizeof(unsigned) * n) != cudaSuccess)
+        return SG_ECUDA;
     return SG_OK;
 }
 #endif
