@@ -581,8 +581,28 @@ __device__ __forceinline__ void leaf1_term(const dd &er, const dd &ei, const dou
     }
 }
 
+#ifdef SG_TAILPROF
+// experiment build only (-DSG_TAILPROF, tools/tail_profile.py): per-warp start / exit times (globaltimer,
+// ns), SM id and task count of the persistent fused kernel
+#define TAILPROF_MAX 16384
+__device__ unsigned long long g_tp_t0[TAILPROF_MAX], g_tp_t1[TAILPROF_MAX];
+__device__ unsigned g_tp_sm[TAILPROF_MAX], g_tp_n[TAILPROF_MAX], g_tp_rows[TAILPROF_MAX];
+__device__ __forceinline__ unsigned long long tp_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned tp_smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#endif
 #ifndef LEAF1_MINB
 #define LEAF1_MINB 4
+#endif
+#ifndef LEAF1_THREADS
+#define LEAF1_THREADS PASS_THREADS   // k_leaf1 CTA size
 #endif
 #ifndef LEAF1_PERJ
 #define LEAF1_PERJ 0   // 1 = one accumulator pair per node j of the row (measured slower)
@@ -679,7 +699,7 @@ __device__ __forceinline__ dd leaf1_task(const DevPlan &P, const PassArgs &A, lo
 // level-2 factor slice (d x NJ entries) is staged once per CTA in shared memory, so the warp-uniform
 // row loads are broadcast LDS instead of LDG through the L1 data path.
 template <bool CPLX, int NJ, bool SMEM>
-__global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPlan P, const PassArgs A) {
+__global__ void __launch_bounds__(LEAF1_THREADS, LEAF1_MINB) k_leaf1(const DevPlan P, const PassArgs A) {
     extern __shared__ double2 fsm[];
     const int wib = threadIdx.x >> 5;
     const double2 *Fr = P.Fre + P.tab_off[2];
@@ -698,6 +718,10 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPla
     const int lane = threadIdx.x & 31;
     // dynamic scheduling: warps pull tasks (sorted heavy-first) from a global counter; every task
     // writes its own partial, so the fixed-order reduction keeps results bitwise reproducible
+#ifdef SG_TAILPROF
+    const unsigned long long tp_start = tp_now();
+    unsigned tp_tasks = 0;
+#endif
     for (;;) {
         unsigned long long task = 0;
         if (lane == 0) task = atomicAdd(A.counter, 1ull);
@@ -708,7 +732,20 @@ __global__ void __launch_bounds__(PASS_THREADS, LEAF1_MINB) k_leaf1(const DevPla
             v = dd_mul_d(v, P.coef[P.L]);
             SG_PART(A.partials, task) = make_double2(v.hi, v.lo);
         }
+#ifdef SG_TAILPROF
+        ++tp_tasks;
+#endif
     }
+#ifdef SG_TAILPROF
+    const int tp_w = (int)(blockIdx.x * (blockDim.x >> 5) + wib);
+    if (lane == 0 && tp_w < TAILPROF_MAX) {
+        g_tp_t0[tp_w] = tp_start;
+        g_tp_t1[tp_w] = tp_now();
+        g_tp_sm[tp_w] = tp_smid();
+        g_tp_n[tp_w] = tp_tasks;
+        g_tp_rows[tp_w] = 0;
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -851,23 +888,6 @@ __device__ __forceinline__ void leaf2_row_multi(const double2 *__restrict__ Fr, 
 // k_mid group lane / (32/G)); group g walks the task's k_mids ka + g, ka + g + G, ... < kb (rows
 // [max(k_mid + 1, kp0), kp1) each), so a shard with few parents (config 4 on 8 GPUs: 132 on rank 0)
 // fills its lanes.  G = 1 is the lane = parent mapping (every k_mid of the task on every lane).
-#ifdef SG_TAILPROF
-// experiment build only (-DSG_TAILPROF, tools/tail_profile.py): per-warp start / exit times (globaltimer,
-// ns), SM id and task count of the persistent fused kernel
-#define TAILPROF_MAX 16384
-__device__ unsigned long long g_tp_t0[TAILPROF_MAX], g_tp_t1[TAILPROF_MAX];
-__device__ unsigned g_tp_sm[TAILPROF_MAX], g_tp_n[TAILPROF_MAX], g_tp_rows[TAILPROF_MAX];
-__device__ __forceinline__ unsigned long long tp_now() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned tp_smid() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-    return r;
-}
-#endif
 template <bool CPLX, int NJ, bool SMEM, int CJ, bool SYM = false, bool CZ = false, int G = 1>
 __global__ void __launch_bounds__(CPLX ? PASS_THREADS : LEAF2_REAL_THREADS, CPLX ? LEAF2_MINB_CPLX : LEAF2_MINB) k_leaf2(const DevPlan P, const Leaf2Args A) {
     extern __shared__ double2 fsm[];

@@ -665,7 +665,8 @@ static int setup_leaf1(sg_plan_s *p) {
     // k_leaf2_sym3 has its own CTA size; every other leaf kernel runs PASS_THREADS
     p->leaf2_threads = (p->leaf2 && p->cplx && sy && ct && nj == 3 && hp.leaf2_ppl >= 2) ? SYM3_THREADS
                        : (p->leaf2 && !p->cplx)                                       ? LEAF2_REAL_THREADS
-                                                                                      : PASS_THREADS;
+                       : p->leaf2                                                     ? PASS_THREADS
+                                                                                      : LEAF1_THREADS;
     const int wpb = p->leaf2_threads / 32;
     int per_sm = 0, dev = 0, sms = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->leaf2_threads, p->leaf1_smem) != cudaSuccess ||
@@ -707,11 +708,11 @@ static void launch_leaf1(sg_plan_s *p, const PassArgs &A, int nj, cudaStream_t s
     const unsigned grid = (unsigned)p->leaf1_grid;
     const size_t sm = p->leaf1_smem;
     if (nj == 3) {
-        if (sm) k_leaf1<CPLX, 3, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf1<CPLX, 3, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+        if (sm) k_leaf1<CPLX, 3, true><<<grid, LEAF1_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 3, false><<<grid, LEAF1_THREADS, 0, st>>>(p->dp, A);
     } else {
-        if (sm) k_leaf1<CPLX, 2, true><<<grid, PASS_THREADS, sm, st>>>(p->dp, A);
-        else k_leaf1<CPLX, 2, false><<<grid, PASS_THREADS, 0, st>>>(p->dp, A);
+        if (sm) k_leaf1<CPLX, 2, true><<<grid, LEAF1_THREADS, sm, st>>>(p->dp, A);
+        else k_leaf1<CPLX, 2, false><<<grid, LEAF1_THREADS, 0, st>>>(p->dp, A);
     }
 }
 
@@ -1374,6 +1375,12 @@ extern "C" int sg_chk_end(sg_plan_t p, long long *out) {
 
 #ifdef SG_TAILPROF
 // experiment build only: copy the per-warp records of the last k_leaf2 launch (n <= TAILPROF_MAX)
+extern "C" int sg_tailprof_reset() {
+    static unsigned long long z[TAILPROF_MAX];
+    if (cudaMemcpyToSymbol(g_tp_t0, z, sizeof z) != cudaSuccess || cudaMemcpyToSymbol(g_tp_t1, z, sizeof z) != cudaSuccess)
+        return SG_ECUDA;
+    return SG_OK;
+}
 extern "C" int sg_tailprof_read(unsigned long long *t0, unsigned long long *t1, unsigned *sm, unsigned *ntask,
                                 unsigned *kmids, int n) {
     if (n > TAILPROF_MAX || cudaDeviceSynchronize() != cudaSuccess) return SG_EINVAL;

@@ -38,6 +38,7 @@ def main():
         for _ in range(2):
             plan.sg_integrate()
         g = plan.capture_graph(finalize=False)
+        assert L.sg_tailprof_reset() == 0   # records of an earlier plan's launch
         for _ in range(3):
             flush.fill_(1.0)
             torch.cuda.synchronize()
