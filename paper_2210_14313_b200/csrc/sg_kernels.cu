@@ -92,6 +92,8 @@ struct sg_plan_s {
     int front_grid = 0;                        // k_front CTAs (persistent)
     std::vector<FrontChunk> front_chunks;      // host copy (built with the partial layout)
     bool split_serial = false;                 // leaf-only kernel after k_front on the same stream
+    bool fork1 = false;                        // passes L-2 || L-1 concurrent at world 1 too (see sg_integrate)
+    int resident_ctas = 0;                     // fused launch: SMs x CTAs per SM (setup_leaf1)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // workspace
     char *ws = nullptr;
@@ -485,7 +487,12 @@ extern "C" int sg_plan(int d, int q, sg_rule rule, const sg_integrand_desc *f, c
             return SG_ENOMEM;
         }
     }
-    if ((any_split || (p->leaf2 && hp.nfront >= 2 && p->world > 1)) &&
+    // world 1: fork only when the fused launch leaves SMs free (its grid is below the resident CTAs);
+    // a full persistent grid would have to wait for the concurrent pass's CTAs to drain on every SM
+    // they took (config 3: 0.085 -> 0.087 ms forked; configs 1-2: 0.038 -> 0.036, 0.109 -> 0.097 ms)
+    p->fork1 = p->leaf2 && p->leaf1_grid < p->resident_ctas;
+    if (const char *e = getenv("SG_B200_FORK1"); e && e[0]) p->fork1 = e[0] == '1';   // A/B
+    if ((any_split || (p->leaf2 && hp.nfront >= 2 && (p->world > 1 || p->fork1))) &&
         !(getenv("SG_B200_NOFORK") && getenv("SG_B200_NOFORK")[0] == '1')) {
         // side stream + fork/join events for the concurrent passes nfront-1 and nfront (sg_integrate)
         // highest priority: the shorter pass's blocks are scheduled first, the persistent fused kernel
@@ -675,6 +682,7 @@ static int setup_leaf1(sg_plan_s *p) {
         return SG_ECUDA;
     const long long ntasks = hp.pass_ntasks[t];
     p->leaf1_grid = std::max<long long>(1, std::min<long long>((ntasks + wpb - 1) / wpb, (long long)sms * per_sm));
+    p->resident_ctas = sms * per_sm;
     hp.pass_blocks[t] = ntasks;   // partial slots: one per task (0 tasks -> no slot, no launch)
     layout_partials(hp);
     p->leaf1_t = t;
@@ -870,9 +878,10 @@ extern "C" int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev) {
     // so it and the fused pass nfront both only read frontier nfront-1 — they run concurrently, pass
     // nfront-1 on the plan's side stream (fork/join through events; graph branches under capture).
     // The persistent fused kernel takes the SMs the shorter pass leaves or frees (its tail fill).
-    // passes nfront-1 || nfront on shards of a world (their tails matter); at world 1 the fused pass
-    // runs alone (same step time within 0.2% on configs 4-5, and a clean kernel interval)
-    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2 && p->world > 1;
+    // passes nfront-1 || nfront on shards of a world (their tails matter); at world 1 only when the
+    // fused grid leaves SMs free (fork1: configs 1-2); otherwise the fused pass runs alone (same step
+    // time within 0.2% on configs 4-5, and a clean kernel interval)
+    const bool fork = p->leaf2 && p->side != nullptr && hp.nfront >= 2 && (p->world > 1 || p->fork1);
     int ev_fork = -1;
     // level-synchronous passes
     for (int t = 1; t <= hp.nfront; ++t) {
