@@ -871,6 +871,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
         if (LEAF2_GUIDE > 0.0) {
             double guide = LEAF2_GUIDE;
             if (const char *e = getenv("SG_B200_GUIDE"); e && e[0]) guide = atof(e);   // A/B runs
+            int64_t gmin = LEAF2_GUIDE_MIN;
+            if (const char *e = getenv("SG_B200_GUIDE_MIN"); e && e[0]) gmin = std::max(1, atoi(e));   // A/B runs
             // resident warps of the kernel that runs the list: 8 / SM (k_leaf2_sym3, k_leaf2_pairs:
             // one 8-warp CTA), 16 (k_leaf2, oscillatory), 24 (k_leaf2, real kinds)
             const double W = hp.leaf2_ppl > 1 ? 148.0 * 8 : kind == SG_F_OSCILLATORY ? 148.0 * 16 : 148.0 * 24;
@@ -880,7 +882,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             for (size_t ii = tasks.size(); ii-- > 0;) {
                 const Task &tk = tasks[ii];
                 rem += (double)tk.rows;
-                const int64_t cap = std::max<int64_t>(LEAF2_MIN_PIECE, (int64_t)(guide * rem / W));
+                const int64_t cap = std::max<int64_t>(gmin, (int64_t)(guide * rem / W));
                 if (guide <= 0.0 || tk.rows <= cap) {
                     rev.push_back(tk);
                     continue;

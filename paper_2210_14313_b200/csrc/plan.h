@@ -67,6 +67,9 @@
 #ifndef LEAF2_GUIDE
 #define LEAF2_GUIDE 1.0           // guided tail: task rows <= GUIDE x remaining rows / resident warps (0: off)
 #endif
+#ifndef LEAF2_GUIDE_MIN
+#define LEAF2_GUIDE_MIN 32        // shortest guided-tail piece (rows)
+#endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 #endif
