@@ -223,21 +223,30 @@ __global__ void __launch_bounds__(SUFFIX_THREADS) k_suffix_abs(const DevPlan P) 
 // Replaces k_factor_base + k_suffix_abs + k_root (three graph nodes) for d <= HEAD_MAX_D, where the
 // redundant per-block base loop (d / 256 coordinates per thread) stays short.  Root partial slot =
 // the block (plan.cpp sizes root_blocks to the K0 grid).
+// CTA = K0_THREADS entry threads (warps 0-7, one factor entry each) + one helper warp.  B's
+// coordinate sum and CTA tree come first; then the helper's lane 0 evaluates B's dd exp / sincos
+// WHILE the entry threads evaluate their entries' (the two transcendental chains overlap instead of
+// following each other: configs 1-2 0.036 -> 0.032 ms, 0.096 -> 0.094 ms) and exits; the entry
+// threads then run the root pass, the block partial and (block 0) the suffix bounds, synchronised
+// by named barrier 1 over the K0_THREADS entry threads.  (The suffix bounds by the helper warp
+// alone, beside the root pass, were slower for d = 1000: 32 coordinates per lane.)
 // ---------------------------------------------------------------------------------------------
 #define HEAD_MAX_D 2048
+#define HEAD_THREADS (K0_THREADS + 32)
+
 template <int KIND>
-__global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const RootArgs R) {
+__global__ void __launch_bounds__(HEAD_THREADS) k_head(const DevPlan P, const RootArgs R) {
     constexpr bool CPLX = (KIND == SG_F_OSCILLATORY);
+    const bool helper = threadIdx.x >= K0_THREADS;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int idx = blockIdx.x * K0_THREADS + threadIdx.x;
-    FactorOut fo;
-    fo.l = -1;
-    factor_entry<KIND>(P, idx, &fo);
-    // B, block-wide (base_body's arithmetic; every thread gets the value through shared memory)
-    __shared__ double2 bsm[4];
-    {
-        const bool prod = (KIND == SG_F_PRODUCT_PEAK);
+    __shared__ double2 bsm[2];
+    __shared__ double2 sm[K0_THREADS];
+    // (1) B's coordinate sum (product for the peak kind): base_body's strided partials and CTA tree
+    constexpr bool prod = (KIND == SG_F_PRODUCT_PEAK);
+    if (!helper) {
         dd acc = prod ? dd{1.0, 0.0} : dd{0.0, 0.0};
-        for (int k = threadIdx.x; k < P.d; k += blockDim.x) {
+        for (int k = threadIdx.x; k < P.d; k += K0_THREADS) {
             const double ck = P.c[k];
             switch (KIND) {
             case SG_F_EXP_LINEAR:
@@ -257,18 +266,22 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             }
             }
         }
-        __shared__ double2 sm[K0_THREADS];
         sm[threadIdx.x] = make_double2(acc.hi, acc.lo);
-        __syncthreads();
-        for (int s2 = K0_THREADS / 2; s2 > 0; s2 >>= 1) {
-            if (threadIdx.x < s2) {
-                dd a = {sm[threadIdx.x].x, sm[threadIdx.x].y}, b = {sm[threadIdx.x + s2].x, sm[threadIdx.x + s2].y};
-                dd r = prod ? dd_mul(a, b) : dd_add(a, b);
-                sm[threadIdx.x] = make_double2(r.hi, r.lo);
-            }
-            __syncthreads();
+    }
+    __syncthreads();
+    for (int s2 = K0_THREADS / 2; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2) {
+            dd a = {sm[threadIdx.x].x, sm[threadIdx.x].y}, b = {sm[threadIdx.x + s2].x, sm[threadIdx.x + s2].y};
+            dd r = prod ? dd_mul(a, b) : dd_add(a, b);
+            sm[threadIdx.x] = make_double2(r.hi, r.lo);
         }
-        if (threadIdx.x == 0) {
+        __syncthreads();
+    }
+    // (2) helper lane 0: B from the sum; entry threads: their factor entries (concurrently)
+    FactorOut fo;
+    fo.l = -1;
+    if (helper) {
+        if (threadIdx.x == K0_THREADS) {
             dd sv = {sm[0].x, sm[0].y};
             dd Br = sv, Bi = {0.0, 0.0};
             switch (KIND) {
@@ -297,9 +310,12 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
                 if (!dd_finite(Br) || !dd_finite(Bi)) atomicOr(P.status, 1);
             }
         }
-        __syncthreads();
+    } else {
+        factor_entry<KIND>(P, idx, &fo);
     }
-    // root pass for this thread's entry (k_root's arithmetic)
+    __syncthreads();
+    if (helper) return;   // no further barrier 0: the entry threads use named barrier 1
+    // (3a) root pass for this thread's entry (k_root's arithmetic)
     dd tot = {0.0, 0.0};
     if (fo.l >= 2) {
         long long r1 = (long long)fo.k * P.M0 + fo.j;
@@ -326,9 +342,19 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             }
         }
     }
-    dd sblk = block_reduce_dd<K0_THREADS / 32>(tot);
-    if (threadIdx.x == 0) SG_PART(R.partials, blockIdx.x) = make_double2(sblk.hi, sblk.lo);
-    // block 0: analytic suffix bounds of every level
+    // block partial: block_reduce_dd's arithmetic over the entry warps, synchronised by named
+    // barrier 1 (K0_THREADS threads; the helper warp does not take part)
+    dd v = warp_reduce_dd(tot);
+    __shared__ double2 rsm[K0_THREADS / 32];
+    if (lane == 0) rsm[wid] = make_double2(v.hi, v.lo);
+    asm volatile("bar.sync 1, %0;" ::"r"(K0_THREADS) : "memory");
+    if (threadIdx.x == 0) {
+        dd sblk = {0.0, 0.0};
+        for (int i = 0; i < K0_THREADS / 32; ++i) sblk = dd_add(sblk, dd{rsm[i].x, rsm[i].y});
+        SG_PART(R.partials, blockIdx.x) = make_double2(sblk.hi, sblk.lo);
+    }
+    // block 0: analytic suffix bounds of every level (chunk sums, a Hillis-Steele suffix scan over
+    // the K0_THREADS chunks, then each thread writes its chunk's suffix values)
     if (blockIdx.x == 0) {
         const int d = P.d, chunk = (d + K0_THREADS - 1) / K0_THREADS;   // <= HEAD_MAX_D / K0_THREADS
         const int k0 = min(d, (int)threadIdx.x * chunk), k1 = min(d, k0 + chunk);
@@ -340,15 +366,14 @@ __global__ void __launch_bounds__(K0_THREADS) k_head(const DevPlan P, const Root
             cs += bk[c];
         }
         __shared__ double suf[K0_THREADS + 1];
-        __syncthreads();
         suf[threadIdx.x] = cs;
         if (threadIdx.x == 0) suf[K0_THREADS] = 0.0;
-        __syncthreads();
+        asm volatile("bar.sync 1, %0;" ::"r"(K0_THREADS) : "memory");
         for (int off = 1; off < K0_THREADS; off <<= 1) {   // suf[i] = sum of chunks i.. end
             const double t = (threadIdx.x + off < K0_THREADS) ? suf[threadIdx.x + off] : 0.0;
-            __syncthreads();
+            asm volatile("bar.sync 1, %0;" ::"r"(K0_THREADS) : "memory");
             suf[threadIdx.x] += t;
-            __syncthreads();
+            asm volatile("bar.sync 1, %0;" ::"r"(K0_THREADS) : "memory");
         }
         double sacc = suf[threadIdx.x + 1];
         double sk[HEAD_MAX_D / K0_THREADS];

@@ -736,10 +736,10 @@ static void launch_factor_base(const DevPlan &dp, int nfb, cudaStream_t st) {
 }
 static void launch_head(const DevPlan &dp, const RootArgs &R, unsigned grid, cudaStream_t st) {
     switch (dp.kind) {
-    case SG_F_EXP_LINEAR: k_head<SG_F_EXP_LINEAR><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
-    case SG_F_OSCILLATORY: k_head<SG_F_OSCILLATORY><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
-    case SG_F_PRODUCT_PEAK: k_head<SG_F_PRODUCT_PEAK><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
-    case SG_F_GAUSSIAN: k_head<SG_F_GAUSSIAN><<<grid, K0_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_EXP_LINEAR: k_head<SG_F_EXP_LINEAR><<<grid, HEAD_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_OSCILLATORY: k_head<SG_F_OSCILLATORY><<<grid, HEAD_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_PRODUCT_PEAK: k_head<SG_F_PRODUCT_PEAK><<<grid, HEAD_THREADS, 0, st>>>(dp, R); break;
+    case SG_F_GAUSSIAN: k_head<SG_F_GAUSSIAN><<<grid, HEAD_THREADS, 0, st>>>(dp, R); break;
     }
 }
 
