@@ -87,7 +87,7 @@ def parse(directory, tag):
             "flops_per_point": flops / pts, "fp64_inst_per_point": inst / pts,
             "dfma_per_point": dom["dfma"] / pts, "dadd_per_point": dom["dadd"] / pts,
             "dmul_per_point": dom.get("dmul", 0) / pts,
-            "source": f"{tag}: {os.path.basename(csvp)}"}
+            "source": f"{tag}: {os.path.relpath(csvp, ROOT)}"}
         print(key, json.dumps(data["launches"][key]))
     json.dump(data, open(OUT, "w"), indent=1)
 
