@@ -25,7 +25,8 @@ def time_plan(plan, flush, reps=5):
     g = plan.capture_graph(finalize=False)
     best = None
     for _ in range(reps):
-        flush.fill_(1.0)
+        if not os.environ.get("SHARD_NOFLUSH"):   # A/B: warm L2 (code and tables resident)
+            flush.fill_(1.0)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -43,7 +44,8 @@ def phases(plan, flush, reps=5):
     g = plan.capture_graph(finalize=False, profile=True)
     best = None
     for _ in range(reps):
-        flush.fill_(1.0)
+        if not os.environ.get("SHARD_NOFLUSH"):
+            flush.fill_(1.0)
         torch.cuda.synchronize()
         g.replay()
         ms = plan.profile_read()
