@@ -188,7 +188,11 @@ int sg_update_integrand(sg_plan_t p, sg_stream_t s, const sg_integrand_desc *f);
  * step").
  * Enqueue the whole hot path on stream s: factor tables (K0), root pass, level-synchronous
  * frontier/leaf passes (K2/K3), deterministic reduction (K4).  out_dev (device, 2 doubles) receives
- * this plan's partial sum as a double-double (hi, lo).  Bitwise reproducible for a fixed plan. */
+ * this plan's partial sum as a double-double (hi, lo).  Bitwise reproducible for a fixed plan.
+ * Some plans (sharded fused plans, small fused plans, split frontier passes) also run one pass on
+ * a plan-owned side stream: forked from s by an event recorded on s and joined back into s by an
+ * event before the reduction, so the call still behaves as ordered work on s (and captures into a
+ * CUDA graph on s as two branches).  Not safe to call concurrently for the same plan. */
 int sg_integrate(sg_plan_t p, sg_stream_t s, double *out_dev);
 
 /* Defined by: the outer sum of Eq 2.6 split over disjoint point sets (the shards of
