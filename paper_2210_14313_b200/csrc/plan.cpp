@@ -854,8 +854,15 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                     "lane_util %.4f groups %d\n", tasks.size(), (long long)total_rows, (long long)max_rows, (int)do_split,
                     hp.leaf2_ppl, (long long)cmid(d - 2), useful / slots, G);
         }
-        // heavy-first for the dynamic scheduler; ties in a fixed order (k_mid, rows, chunk)
-        std::stable_sort(tasks.begin(), tasks.end(), [](const Task &a, const Task &b) {
+        // task cost for the schedule: rows + LEAF2_PRO_COST per k_mid block (its prologue: the
+        // mid products, grid bounds and lane epilogue, about two rows' work)
+        auto tcost = [G](const Task &tk) -> int64_t {
+            return tk.rows + (int64_t)LEAF2_PRO_COST * ((tk.kb - tk.ka + G - 1) / G);
+        };
+        // heavy-first (by cost) for the dynamic scheduler; ties in a fixed order (k_mid, rows, chunk)
+        std::stable_sort(tasks.begin(), tasks.end(), [&tcost](const Task &a, const Task &b) {
+            const int64_t ca = tcost(a), cb = tcost(b);
+            if (ca != cb) return ca > cb;
             if (a.rows != b.rows) return a.rows > b.rows;
             if (a.ka != b.ka) return a.ka < b.ka;
             if (a.kp0 != b.kp0) return a.kp0 < b.kp0;
@@ -881,9 +888,9 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             double rem = 0.0;
             for (size_t ii = tasks.size(); ii-- > 0;) {
                 const Task &tk = tasks[ii];
-                rem += (double)tk.rows;
+                rem += (double)tcost(tk);
                 const int64_t cap = std::max<int64_t>(gmin, (int64_t)(guide * rem / W));
-                if (guide <= 0.0 || tk.rows <= cap) {
+                if (guide <= 0.0 || tcost(tk) <= cap) {
                     rev.push_back(tk);
                     continue;
                 }
@@ -892,7 +899,8 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                     // one k_mid block: rows [max(ka + 1, kp0), kp1) of its first group in pieces
                     const int r0 = std::max(tk.ka + 1, tk.kp0), r1 = std::min(tk.kp1, d);
                     const int nr = r1 - r0;
-                    const int pieces = (int)std::min<int64_t>(nr, (nr + cap - 1) / cap);
+                    const int64_t rcap = std::max<int64_t>(1, cap - LEAF2_PRO_COST);
+                    const int pieces = (int)std::min<int64_t>(nr, (nr + rcap - 1) / rcap);
                     for (int q = 0; q < pieces; ++q) {
                         const int a = r0 + (int)((int64_t)nr * q / pieces);
                         const int b = r0 + (int)((int64_t)nr * (q + 1) / pieces);
@@ -900,14 +908,37 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
                     }
                 } else {
                     // k_mid blocks of G (the first group's rows d - 1 - km per block), cut greedily
+                    // without overshooting the cap: a piece closes before the block that would take
+                    // it past the cap, and a block longer than the cap on its own is cut into row
+                    // pieces (every lane group walks the same row range [kp0, kp1))
                     int ka = tk.ka;
                     int64_t acc = 0;
+                    int64_t accc = 0;   // acc in cost units
                     for (int km = tk.ka; km < tk.kb; km += G) {
-                        acc += d - 1 - km;
+                        const int64_t r = d - 1 - km;
                         const int nx = std::min(km + G, tk.kb);
-                        if (acc >= cap || nx >= tk.kb) {
+                        if (acc > 0 && accc + r + LEAF2_PRO_COST > cap) {
+                            pcs.push_back(Task{acc, tk.first, ka, km, tk.kp0, tk.kp1});
+                            acc = accc = 0;
+                            ka = km;
+                        }
+                        if (r + LEAF2_PRO_COST > cap && tk.kp0 == 0 && tk.kp1 == d) {
+                            const int r0 = km + 1, nr = (int)r;
+                            const int64_t rcap = std::max<int64_t>(1, cap - LEAF2_PRO_COST);
+                            const int pieces = (int)std::min<int64_t>(nr, (nr + rcap - 1) / rcap);
+                            for (int q = 0; q < pieces; ++q) {
+                                const int a = r0 + (int)((int64_t)nr * q / pieces);
+                                const int b = r0 + (int)((int64_t)nr * (q + 1) / pieces);
+                                pcs.push_back(Task{b - a, tk.first, km, nx, a, b});
+                            }
+                            ka = nx;
+                            continue;
+                        }
+                        acc += r;
+                        accc += r + LEAF2_PRO_COST;
+                        if (accc >= cap || nx >= tk.kb) {
                             pcs.push_back(Task{acc, tk.first, ka, nx, tk.kp0, tk.kp1});
-                            acc = 0;
+                            acc = accc = 0;
                             ka = nx;
                         }
                     }
@@ -923,7 +954,7 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             std::make_heap(wq.begin(), wq.end(), std::greater<double>());
             double tot = 0.0;
             for (const Task &tk : tasks) {
-                const double c = (double)tk.rows + 2.0 * (double)((tk.kb - tk.ka + G - 1) / G);
+                const double c = (double)tcost(tk);
                 std::pop_heap(wq.begin(), wq.end(), std::greater<double>());
                 wq.back() += c;
                 std::push_heap(wq.begin(), wq.end(), std::greater<double>());
@@ -932,6 +963,14 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             const double mk = *std::max_element(wq.begin(), wq.end());
             fprintf(stderr, "leaf2 schedule: makespan %.0f avg %.0f efficiency %.4f\n", mk,
                     tot / LEAF2_RESIDENT_WARPS, tot / LEAF2_RESIDENT_WARPS / mk);
+            if (const char *fn = getenv("SG_B200_DUMP_TASKS"); fn && fn[0]) {
+                if (FILE *f = fopen(fn, "w")) {
+                    for (const Task &tk : tasks)
+                        fprintf(f, "%lld %lld %d %d %d %d\n", (long long)tk.rows, (long long)tk.first, tk.ka, tk.kb,
+                                tk.kp0, tk.kp1);
+                    fclose(f);
+                }
+            }
         }
         hp.T2.resize(3 * tasks.size());
         for (size_t i = 0; i < tasks.size(); ++i) {

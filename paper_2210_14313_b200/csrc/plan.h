@@ -70,6 +70,9 @@
 #ifndef LEAF2_GUIDE_MIN
 #define LEAF2_GUIDE_MIN 32        // shortest guided-tail piece (rows)
 #endif
+#ifndef LEAF2_PRO_COST
+#define LEAF2_PRO_COST 2          // schedule cost of one k_mid block's prologue, in rows (guided tail, sort)
+#endif
 #ifndef LEAF2_TASK_ROWS
 #define LEAF2_TASK_ROWS 128   // minimum rows per fused task (grouping of short k_mid rows)
 #endif
