@@ -963,13 +963,15 @@ int host_plan_build(HostPlan &hp, int d, int L, int rule, int kind, int form, in
             const double mk = *std::max_element(wq.begin(), wq.end());
             fprintf(stderr, "leaf2 schedule: makespan %.0f avg %.0f efficiency %.4f\n", mk,
                     tot / LEAF2_RESIDENT_WARPS, tot / LEAF2_RESIDENT_WARPS / mk);
-            if (const char *fn = getenv("SG_B200_DUMP_TASKS"); fn && fn[0]) {
-                if (FILE *f = fopen(fn, "w")) {
-                    for (const Task &tk : tasks)
-                        fprintf(f, "%lld %lld %d %d %d %d\n", (long long)tk.rows, (long long)tk.first, tk.ka, tk.kb,
-                                tk.kp0, tk.kp1);
-                    fclose(f);
-                }
+        }
+        if (const char *fn = getenv("SG_B200_DUMP_TASKS"); fn && fn[0]) {
+            // the fused task list in claim order (tests: coverage of every (chunk, k_mid, row) once)
+            if (FILE *f = fopen(fn, "w")) {
+                fprintf(f, "%d %d %d\n", G, d, (int)CH);
+                for (const Task &tk : tasks)
+                    fprintf(f, "%lld %lld %d %d %d %d\n", (long long)tk.rows, (long long)tk.first, tk.ka, tk.kb,
+                            tk.kp0, tk.kp1);
+                fclose(f);
             }
         }
         hp.T2.resize(3 * tasks.size());

@@ -246,3 +246,47 @@ def test_ctypes_structs_match_header(tmp_path):
         assert int(got[st]) == ctypes.sizeof(cls), st
         for f in fields[st]:
             assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
+
+
+@pytest.mark.parametrize("cfg,rank,world", [(4, 0, 1), (4, 0, 8), (4, 7, 8), (4, 3, 4), (5, 0, 1), (5, 5, 8),
+                                            (3, 0, 1), (3, 1, 2), (2, 0, 1)])
+def test_fused_task_list_tiles_every_row_once(L, tmp_path, cfg, rank, world):
+    """The fused pass's task list (plan.cpp: k_mid grouping, long-task row pieces, the guided tail's
+    cuts) covers every (parent chunk, k_mid, leaf row) of the shard exactly once: for each chunk the
+    k_mids form one contiguous range ending at d - 2, and each k_mid's row ranges, over all tasks and
+    lane groups, tile [k_mid + 1, d) without gap or overlap.  (A task lost or claimed twice changes
+    the integral; this pins the host side of it without a GPU.)"""
+    p = S.baseline_config(cfg)
+    fn = str(tmp_path / "tasks.txt")
+    os.environ["SG_B200_DUMP_TASKS"] = fn
+    try:
+        rc = _query(L, p.d, p.q, p.rule, p.kind, rank=rank, world=world)[0]
+    finally:
+        del os.environ["SG_B200_DUMP_TASKS"]
+    assert rc == 0
+    lines = open(fn).read().split("\n")
+    G, d, CH = map(int, lines[0].split())
+    cover = {}   # (chunk first, k_mid) -> list of row intervals
+    ntask = 0
+    for ln in lines[1:]:
+        if not ln:
+            continue
+        rows, first, ka, kb, kp0, kp1 = map(int, ln.split())
+        assert first % CH == 0 and 0 <= ka < kb <= d - 1 and 0 <= kp0 < kp1 <= d
+        ntask += 1
+        for g in range(G):
+            for km in range(ka + g, kb, G):
+                r0, r1 = max(km + 1, kp0), min(kp1, d)
+                if r1 > r0:
+                    cover.setdefault((first, km), []).append((r0, r1))
+    assert ntask > 0
+    kms = {}
+    for (first, km), iv in cover.items():
+        iv.sort()
+        assert iv[0][0] == km + 1 and iv[-1][1] == d, (first, km, iv[:3])
+        for a, b in zip(iv, iv[1:]):
+            assert a[1] == b[0], (first, km, a, b)   # no gap, no overlap
+        kms.setdefault(first, []).append(km)
+    for first, ks in kms.items():
+        ks.sort()
+        assert ks == list(range(ks[0], d - 1)), (first, ks[0], len(ks))
