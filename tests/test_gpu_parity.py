@@ -319,3 +319,63 @@ def test_parameter_extremes(api, name, d, L, rule, kind, c, w, u):
     for kw in ({}, {"merge": api.MERGE_MIDPOINT}, {"method": api.METHOD_COLLAPSE}):
         v, _ = gpu_value(api, p, **kw)
         assert rel(v, ref) <= HEALTH, (name, kw, float(rel(v, ref)))
+
+
+@pytest.mark.parametrize("name,d,L,rule,kind,c,w,u,tol", [
+    # exp arguments c (x - 1/2) up to +-160 (m up to ~230 in the 2^m exp(j/64) exp(s) reduction); the
+    # integrand's largest value e^470 stays finite
+    ("exp_wide", 5, 3, S.RULE_CC, S.KIND_EXP, [320.0, -320.0, 150.0, -1.5, 0.0], None, 0.0, 1e-28),
+    # phases up to 5e3 (the one pi/64 reduction: N up to 1e5, every quadrant and table index) and a
+    # base phase 2 pi u of ~7.8e5
+    ("osc_wide", 4, 3, S.RULE_CC, S.KIND_OSC, [1.0e4, -3.0e3, 77.7, 0.5], None, 123456.789, 1e-26),
+    # Gaussian exponents c^2 (x - 1/2)(x + 1/2 - 2 w) up to ~+-310, w at the ends of [0, 1]
+    ("gauss_wide", 3, 3, S.RULE_TRAP, S.KIND_GAUSS, [25.0, 20.0, 0.1], [0.0, 1.0, 0.5], 0.0, 1e-28),
+    ("peak_wide", 3, 3, S.RULE_GL, S.KIND_PEAK, [100.0, 1e-3, 3.0], [0.5, 0.0, 1.0], 0.0, 1e-29),
+])
+def test_factor_table_and_base_wide_arguments(api, name, d, L, rule, kind, c, w, u, tol):
+    """K0 element by element at wide arguments (the table-driven dd exp / sincos of csrc/dd.cuh over
+    their whole reduction ranges): every F[l][k][j] = w_j E_k(x_j) and the base B against 50-digit
+    mpmath, to `tol` relative (absolute x |w_j| for the unit-modulus oscillatory factors)."""
+    p = S.Problem(name, d, L, rule, kind, np.array(c, dtype=float),
+                  None if w is None else np.array(w, dtype=float), u)
+    plan = api.Plan(p.d, p.q, p.rule, p.kind, p.c, p.w, p.u)
+    plan.integrate_host()
+    tab, base = plan.debug_tables()
+    ck = [mp.mpf(v) for v in p.c]
+    wk = [mp.mpf(v) for v in p.w] if p.w is not None else None
+    idx = 0
+    for l in range(2, p.L + 2):
+        x, wt = pins.mp_rule(p.rule, l)
+        for k in range(p.d):
+            for j in range(len(x)):
+                xm = mp.mpf(x[j]) - mp.mpf(0.5)
+                if kind == S.KIND_EXP:
+                    e = mp.exp(ck[k] * xm)
+                elif kind == S.KIND_OSC:
+                    e = mp.expj(ck[k] * xm)
+                elif kind == S.KIND_GAUSS:
+                    e = mp.exp(-ck[k] ** 2 * ((mp.mpf(x[j]) - wk[k]) ** 2 - (mp.mpf(0.5) - wk[k]) ** 2))
+                else:
+                    e = (1 / ck[k] ** 2 + (mp.mpf(0.5) - wk[k]) ** 2) / (1 / ck[k] ** 2 + (mp.mpf(x[j]) - wk[k]) ** 2)
+                ref = mp.mpf(wt[j]) * e
+                scale = abs(mp.mpf(wt[j])) if kind == S.KIND_OSC else abs(ref)
+                got = mp.mpf(tab[idx, 0]) + mp.mpf(tab[idx, 1])
+                assert abs(got - mp.re(ref)) <= tol * scale, (name, l, k, j, float(abs(got - mp.re(ref)) / scale))
+                if kind == S.KIND_OSC:
+                    goti = mp.mpf(tab[idx, 2]) + mp.mpf(tab[idx, 3])
+                    assert abs(goti - mp.im(ref)) <= tol * scale, (name, l, k, j)
+                idx += 1
+    half = mp.mpf(0.5)
+    if kind == S.KIND_EXP:
+        B = mp.exp(sum(ck) * half)
+    elif kind == S.KIND_OSC:
+        B = mp.expj(2 * mp.pi * mp.mpf(p.u) + sum(ck) * half)
+    elif kind == S.KIND_GAUSS:
+        B = mp.exp(-sum(ck[k] ** 2 * (half - wk[k]) ** 2 for k in range(p.d)))
+    else:
+        B = mp.fprod(1 / (1 / ck[k] ** 2 + (half - wk[k]) ** 2) for k in range(p.d))
+    gb = mp.mpf(base[0]) + mp.mpf(base[1])
+    assert abs(gb - mp.re(B)) <= 10 * tol * abs(B), (name, float(abs(gb - mp.re(B)) / abs(B)))
+    if kind == S.KIND_OSC:
+        assert abs(mp.mpf(base[2]) + mp.mpf(base[3]) - mp.im(B)) <= 10 * tol * abs(B)
+    plan.close()
